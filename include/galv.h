@@ -1,0 +1,162 @@
+/*
+ * galv.h -- C ABI of the B200 (sm_100a) kernel library behind the hybrid-parallel
+ * runtime (paper_2504_21411_b200/csrc, built into libgalv_b200.so).
+ *
+ * The reference planner (/root/reference/pkg/src/hybridplan) stops at the Plan
+ * boundary: its "runtime" is the simulator pipesim.py and the paper's
+ * get_hybrid_parallel_configs / construct_hybrid_parallel_model (PAPER.md:82,
+ * SPEC.md:10) have no reference code.  Each entry point below realizes one term
+ * of the reference cost model (costmodel.py:90-213); the comment on each names it.
+ *
+ * Conventions
+ *   - status: 0 ok; < 0 invalid argument; > 0 CUDA error code.  galv_last_error()
+ *     returns a thread-local message for the last failure on the calling thread.
+ *   - all pointers are device pointers owned by the caller (PyTorch caching
+ *     allocator); kernels never allocate.  Row-major, strides in elements.
+ *   - dtype: GALV_F32 = 0, GALV_BF16 = 1.
+ *   - every call is asynchronous on `stream` (a cudaStream_t passed as void*);
+ *     no host synchronization, callable from any host thread.
+ */
+#ifndef GALV_H_
+#define GALV_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GALV_ABI_VERSION 1
+#define GALV_F32 0
+#define GALV_BF16 1
+
+int32_t galv_abi_version(void);
+const char* galv_last_error(void);
+/* number of SMs / sm major.minor of the current device (for host-side heuristics) */
+int32_t galv_device_info(int32_t* sm_count, int32_t* cc_major, int32_t* cc_minor);
+
+/*
+ * C[M,N] = alpha * op(A) @ op(B) (+ bias[N]) (+ C if accumulate)
+ * op(A) is [M,K]: A stored [M,K] (trans_a = 0, lda >= K) or [K,M] (trans_a = 1, lda >= M).
+ * op(B) is [K,N]: B stored [N,K] (trans_b = 1, the nn.Linear weight layout) or [K,N]
+ * (trans_b = 0).  bf16 inputs run on tcgen05 (TMA -> smem -> UMMA -> TMEM), fp32
+ * inputs on the exact SIMT FP32 path.  c_dtype may differ from ab_dtype (fp32
+ * accumulation buffers for bf16 GEMMs).  Realizes fwd_compute / bwd_compute
+ * (costmodel.py:104-106): column/row-parallel forward, dgrad and wgrad.
+ */
+int32_t galv_gemm(const void* A, const void* B, void* C, const void* bias,
+                  int64_t M, int64_t N, int64_t K, int64_t lda, int64_t ldb, int64_t ldc,
+                  int32_t trans_a, int32_t trans_b, float alpha, int32_t accumulate,
+                  int32_t ab_dtype, int32_t c_dtype, int32_t bias_dtype, void* stream);
+
+/*
+ * Batched strided GEMM (same op semantics), `batch` problems at element offsets
+ * stride_a/b/c.  Used by the small-head attention path and tests.
+ */
+int32_t galv_gemm_batched(const void* A, const void* B, void* C, int64_t batch,
+                          int64_t stride_a, int64_t stride_b, int64_t stride_c,
+                          int64_t M, int64_t N, int64_t K, int64_t lda, int64_t ldb,
+                          int64_t ldc, int32_t trans_a, int32_t trans_b, float alpha,
+                          int32_t accumulate, int32_t ab_dtype, int32_t c_dtype, void* stream);
+
+/*
+ * Causal/non-causal attention over q,k,v laid out [B, S, H, D] (token-major, the
+ * layout the QKV GEMM produces; strides given in elements for token and head).
+ * o: [B, S, H, D]; lse: fp32 [B, H, S] (natural-log logsumexp of scaled scores).
+ * Realizes the flops_per_token_sq term (costmodel.py:104; flash assumption,
+ * profiles.py:207-208: no S^2 memory).
+ */
+int32_t galv_attn_fwd(const void* q, const void* k, const void* v, void* o, float* lse,
+                      int64_t B, int64_t S, int64_t H, int64_t D,
+                      int64_t stride_tok, int64_t stride_head, int64_t o_stride_tok,
+                      float scale, int32_t causal, int32_t dtype, void* stream);
+/* dq/dk/dv same layout as q/k/v; ws: fp32 workspace of galv_attn_bwd_workspace bytes. */
+int64_t galv_attn_bwd_workspace(int64_t B, int64_t S, int64_t H, int64_t D, int32_t dtype);
+int32_t galv_attn_bwd(const void* q, const void* k, const void* v, const void* o,
+                      const void* dout, const float* lse, void* dq, void* dk, void* dv,
+                      int64_t B, int64_t S, int64_t H, int64_t D, int64_t stride_tok,
+                      int64_t stride_head, int64_t o_stride_tok, float scale, int32_t causal,
+                      int32_t dtype, void* ws, void* stream);
+
+/* y = norm(x (+ residual)) * gamma (+ beta).  rows x cols; residual/res_out optional:
+ * when residual != NULL, res_out = x + residual is written and normalized.
+ * rstd/mean: fp32 [rows] saved for backward (mean unused for RMSNorm). */
+int32_t galv_rmsnorm_fwd(const void* x, const void* residual, void* res_out,
+                         const void* gamma, void* y, float* rstd, int64_t rows, int64_t cols,
+                         float eps, int32_t dtype, void* stream);
+/* dx = d(norm)/dx^T dy (+ dres_in if not NULL); dgamma accumulated into fp32 dgamma_acc. */
+int32_t galv_rmsnorm_bwd(const void* x, const void* gamma, const float* rstd, const void* dy,
+                         const void* dres_in, void* dx, float* dgamma_acc, int64_t rows,
+                         int64_t cols, int32_t dtype, void* ws, void* stream);
+int32_t galv_layernorm_fwd(const void* x, const void* residual, void* res_out,
+                           const void* gamma, const void* beta, void* y, float* mean,
+                           float* rstd, int64_t rows, int64_t cols, float eps, int32_t dtype,
+                           void* stream);
+int32_t galv_layernorm_bwd(const void* x, const void* gamma, const float* mean,
+                           const float* rstd, const void* dy, const void* dres_in, void* dx,
+                           float* dgamma_acc, float* dbeta_acc, int64_t rows, int64_t cols,
+                           int32_t dtype, void* ws, void* stream);
+int64_t galv_norm_bwd_workspace(int64_t rows, int64_t cols);
+
+/* Rotary embedding in place on x [T, H, D] (rows of stride_tok), positions pos0 + t % S.
+ * inverse = 1 applies the transpose rotation (backward). theta base e.g. 10000. */
+int32_t galv_rope(void* x, int64_t T, int64_t S, int64_t H, int64_t D, int64_t stride_tok,
+                  int64_t stride_head, int64_t pos0, float theta, int32_t inverse,
+                  int32_t dtype, void* stream);
+
+/* SwiGLU on a fused [T, 2F] gate|up tensor -> h [T, F]; backward -> d(gate|up). */
+int32_t galv_swiglu_fwd(const void* gu, void* h, int64_t T, int64_t F, int32_t dtype,
+                        void* stream);
+int32_t galv_swiglu_bwd(const void* gu, const void* dh, void* dgu, int64_t T, int64_t F,
+                        int32_t dtype, void* stream);
+/* GeLU(tanh) with bias: y = gelu(x + b); backward dx = dy * gelu'(x + b). */
+int32_t galv_bias_gelu_fwd(const void* x, const void* bias, void* y, int64_t T, int64_t F,
+                           int32_t dtype, void* stream);
+int32_t galv_bias_gelu_bwd(const void* x, const void* bias, const void* dy, void* dx,
+                           int64_t T, int64_t F, int32_t dtype, void* stream);
+/* column sums: out[c] (+)= sum_r x[r, c] (fp32 out, for bias gradients) */
+int32_t galv_colsum(const void* x, float* out, int64_t rows, int64_t cols, int32_t accumulate,
+                    int32_t dtype, void* ws, void* stream);
+
+/* Embedding gather/scatter-add over a vocab shard [vocab_lo, vocab_lo + V_local). */
+int32_t galv_embed_fwd(const int64_t* ids, const void* table, void* out, int64_t T,
+                       int64_t V_local, int64_t vocab_lo, int64_t Hd, int32_t dtype,
+                       void* stream);
+int32_t galv_embed_bwd(const int64_t* ids, const void* dout, float* dtable_acc, int64_t T,
+                       int64_t V_local, int64_t vocab_lo, int64_t Hd, int32_t dtype,
+                       void* stream);
+
+/* Vocab-parallel cross entropy over a logits shard [T, V_local].
+ *  stage 0: row max -> stats[T*3+0] ; (caller all-reduces MAX over tp)
+ *  stage 1: sum exp(x - max) -> stats[1], target logit -> stats[2] ; (caller all-reduces SUM)
+ *  stage 2: loss[T] = log(sum) + max - target; dlogits = (softmax - onehot) * grad_scale
+ *  (in place over logits when dlogits == logits). ignore_index rows give 0. */
+int32_t galv_xent(void* logits, const int64_t* labels, float* stats, float* loss,
+                  void* dlogits, int64_t T, int64_t V_local, int64_t vocab_lo,
+                  float grad_scale, int64_t ignore_index, int32_t stage, int32_t dtype,
+                  void* stream);
+
+/* Fused AdamW over flat fp32 master/m/v shards; grad in `grad_dtype` scaled by
+ * grad_scale; writes the updated param copy (bf16 or fp32) to param_out (may be NULL). */
+int32_t galv_adamw(float* master, float* m, float* v, const void* grad, void* param_out,
+                   int64_t n, float lr, float beta1, float beta2, float eps,
+                   float weight_decay, float grad_scale, int64_t step, int32_t grad_dtype,
+                   int32_t param_dtype, void* stream);
+
+/* Reshard pack/unpack: dst[i] = src[idx[i]] row gather (rows of `row_bytes`). */
+int32_t galv_gather_rows(const void* src, void* dst, const int64_t* idx, int64_t n_rows,
+                         int64_t row_bytes, void* stream);
+/* dst[idx[i]] = src[i] row scatter. */
+int32_t galv_scatter_rows(const void* src, void* dst, const int64_t* idx, int64_t n_rows,
+                          int64_t row_bytes, void* stream);
+
+/* Elementwise helpers: y = a*x + b*y (axpby, any of f32/bf16 in/out), cast, fill. */
+int32_t galv_axpby(const void* x, void* y, int64_t n, float a, float b, int32_t x_dtype,
+                   int32_t y_dtype, void* stream);
+int32_t galv_sumsq(const void* x, int64_t n, float* out, int32_t dtype, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GALV_H_ */

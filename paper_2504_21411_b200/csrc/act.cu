@@ -1,0 +1,246 @@
+// Elementwise activation kernels (HBM-bound, 16-byte vectors, grid-stride):
+//   SwiGLU (Llama MLP) on the fused gate|up GEMM output, bias+GeLU(tanh) (GPT MLP),
+//   column sums for bias gradients, axpby / cast, sum of squares (grad-norm).
+#include "common.cuh"
+
+namespace galv {
+namespace act {
+
+__device__ __forceinline__ float silu(float x) { return x / (1.f + expf(-x)); }
+
+// gu: [T, 2F] (gate | up), h: [T, F]
+template <typename T>
+__global__ void swiglu_fwd(const T* __restrict__ gu, T* __restrict__ h, int64_t T_, int64_t F) {
+  constexpr int V = 16 / sizeof(T);
+  const int64_t nvec = T_ * F / V;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nvec;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = i * V, t = e / F, f = e - t * F;
+    float g[V], u[V], o[V];
+    load16(gu + t * 2 * F + f, g);
+    load16(gu + t * 2 * F + F + f, u);
+#pragma unroll
+    for (int k = 0; k < V; ++k) o[k] = silu(g[k]) * u[k];
+    store16(h + e, o);
+  }
+}
+
+template <typename T>
+__global__ void swiglu_bwd(const T* __restrict__ gu, const T* __restrict__ dh,
+                           T* __restrict__ dgu, int64_t T_, int64_t F) {
+  constexpr int V = 16 / sizeof(T);
+  const int64_t nvec = T_ * F / V;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nvec;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = i * V, t = e / F, f = e - t * F;
+    float g[V], u[V], d[V], dg[V], du[V];
+    load16(gu + t * 2 * F + f, g);
+    load16(gu + t * 2 * F + F + f, u);
+    load16(dh + e, d);
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      const float s = 1.f / (1.f + expf(-g[k]));
+      du[k] = d[k] * g[k] * s;
+      dg[k] = d[k] * u[k] * s * (1.f + g[k] * (1.f - s));
+    }
+    store16(dgu + t * 2 * F + f, dg);
+    store16(dgu + t * 2 * F + F + f, du);
+  }
+}
+
+__device__ __forceinline__ float gelu_tanh(float x) {
+  const float k0 = 0.7978845608028654f, k1 = 0.044715f;
+  return 0.5f * x * (1.f + tanhf(k0 * (x + k1 * x * x * x)));
+}
+__device__ __forceinline__ float gelu_tanh_grad(float x) {
+  const float k0 = 0.7978845608028654f, k1 = 0.044715f;
+  const float u = k0 * (x + k1 * x * x * x);
+  const float th = tanhf(u);
+  return 0.5f * (1.f + th) + 0.5f * x * (1.f - th * th) * k0 * (1.f + 3.f * k1 * x * x);
+}
+
+template <typename T>
+__global__ void bias_gelu_fwd(const T* __restrict__ x, const T* __restrict__ b, T* __restrict__ y,
+                              int64_t T_, int64_t F) {
+  constexpr int V = 16 / sizeof(T);
+  const int64_t nvec = T_ * F / V;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nvec;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = i * V, f = e % F;
+    float v[V], bb[V];
+    load16(x + e, v);
+    if (b) load16(b + f, bb);
+#pragma unroll
+    for (int k = 0; k < V; ++k) v[k] = gelu_tanh(v[k] + (b ? bb[k] : 0.f));
+    store16(y + e, v);
+  }
+}
+
+template <typename T>
+__global__ void bias_gelu_bwd(const T* __restrict__ x, const T* __restrict__ b,
+                              const T* __restrict__ dy, T* __restrict__ dx, int64_t T_,
+                              int64_t F) {
+  constexpr int V = 16 / sizeof(T);
+  const int64_t nvec = T_ * F / V;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nvec;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = i * V, f = e % F;
+    float v[V], bb[V], d[V];
+    load16(x + e, v);
+    load16(dy + e, d);
+    if (b) load16(b + f, bb);
+#pragma unroll
+    for (int k = 0; k < V; ++k) v[k] = d[k] * gelu_tanh_grad(v[k] + (b ? bb[k] : 0.f));
+    store16(dx + e, v);
+  }
+}
+
+// out[c] (+)= sum_r x[r, c]: CTA handles a 32-column strip over a row range; fp32 atomics.
+template <typename T>
+__global__ void colsum_kernel(const T* __restrict__ x, float* __restrict__ out, int64_t rows,
+                              int64_t cols, int64_t rows_per_cta) {
+  __shared__ float part[8][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t c = blockIdx.x * 32 + lane;
+  const int64_t r0 = blockIdx.y * rows_per_cta;
+  const int64_t r1 = min(rows, r0 + rows_per_cta);
+  float s = 0.f;
+  if (c < cols)
+    for (int64_t r = r0 + w; r < r1; r += 8) s += to_f(x[r * cols + c]);
+  part[w][lane] = s;
+  __syncthreads();
+  if (w == 0) {
+    float t = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) t += part[k][lane];
+    if (c < cols) atomicAdd(&out[c], t);
+  }
+}
+
+template <typename TX, typename TY>
+__global__ void axpby_kernel(const TX* __restrict__ x, TY* __restrict__ y, int64_t n, float a,
+                             float b) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float yv = b != 0.f ? to_f(y[i]) : 0.f;
+    y[i] = from_f<TY>(a * to_f(x[i]) + b * yv);
+  }
+}
+
+template <typename T>
+__global__ void sumsq_kernel(const T* __restrict__ x, int64_t n, float* out) {
+  __shared__ float red[33];
+  float s = 0.f;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float v = to_f(x[i]);
+    s += v * v;
+  }
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) atomicAdd(out, s);
+}
+
+inline unsigned grid_for(int64_t n, int threads) {
+  int64_t g = (n + threads - 1) / threads;
+  int64_t cap = (int64_t)sm_count() * 8;
+  return (unsigned)std::max<int64_t>(1, std::min(g, cap));
+}
+
+}  // namespace act
+}  // namespace galv
+
+using namespace galv;
+
+extern "C" {
+
+int32_t galv_swiglu_fwd(const void* gu, void* h, int64_t T_, int64_t F, int32_t dtype,
+                        void* stream) {
+  GALV_CHECK_ARG(gu && h && T_ > 0 && F > 0 && F % 8 == 0, "bad arguments");
+  GALV_DISPATCH(dtype, T, {
+    const int64_t nvec = T_ * F / (16 / sizeof(T));
+    act::swiglu_fwd<T><<<act::grid_for(nvec, 256), 256, 0, as_stream(stream)>>>(
+        (const T*)gu, (T*)h, T_, F);
+  });
+  GALV_LAUNCH_CHECK();
+  return 0;
+}
+
+int32_t galv_swiglu_bwd(const void* gu, const void* dh, void* dgu, int64_t T_, int64_t F,
+                        int32_t dtype, void* stream) {
+  GALV_CHECK_ARG(gu && dh && dgu && T_ > 0 && F % 8 == 0, "bad arguments");
+  GALV_DISPATCH(dtype, T, {
+    const int64_t nvec = T_ * F / (16 / sizeof(T));
+    act::swiglu_bwd<T><<<act::grid_for(nvec, 256), 256, 0, as_stream(stream)>>>(
+        (const T*)gu, (const T*)dh, (T*)dgu, T_, F);
+  });
+  GALV_LAUNCH_CHECK();
+  return 0;
+}
+
+int32_t galv_bias_gelu_fwd(const void* x, const void* bias, void* y, int64_t T_, int64_t F,
+                           int32_t dtype, void* stream) {
+  GALV_CHECK_ARG(x && y && T_ > 0 && F % 8 == 0, "bad arguments");
+  GALV_DISPATCH(dtype, T, {
+    const int64_t nvec = T_ * F / (16 / sizeof(T));
+    act::bias_gelu_fwd<T><<<act::grid_for(nvec, 256), 256, 0, as_stream(stream)>>>(
+        (const T*)x, (const T*)bias, (T*)y, T_, F);
+  });
+  GALV_LAUNCH_CHECK();
+  return 0;
+}
+
+int32_t galv_bias_gelu_bwd(const void* x, const void* bias, const void* dy, void* dx, int64_t T_,
+                           int64_t F, int32_t dtype, void* stream) {
+  GALV_CHECK_ARG(x && dy && dx && T_ > 0 && F % 8 == 0, "bad arguments");
+  GALV_DISPATCH(dtype, T, {
+    const int64_t nvec = T_ * F / (16 / sizeof(T));
+    act::bias_gelu_bwd<T><<<act::grid_for(nvec, 256), 256, 0, as_stream(stream)>>>(
+        (const T*)x, (const T*)bias, (const T*)dy, (T*)dx, T_, F);
+  });
+  GALV_LAUNCH_CHECK();
+  return 0;
+}
+
+int32_t galv_colsum(const void* x, float* out, int64_t rows, int64_t cols, int32_t accumulate,
+                    int32_t dtype, void* ws, void* stream) {
+  (void)ws;
+  GALV_CHECK_ARG(x && out && rows > 0 && cols > 0, "bad arguments");
+  if (!accumulate) GALV_CUDA_RET(cudaMemsetAsync(out, 0, sizeof(float) * cols, as_stream(stream)));
+  const int64_t strips = (cols + 31) / 32;
+  int64_t ychunks = std::max<int64_t>(1, std::min<int64_t>((rows + 255) / 256,
+                                                           sm_count() * 8 / std::max<int64_t>(1, strips) + 1));
+  const int64_t rpc = (rows + ychunks - 1) / ychunks;
+  dim3 grid((unsigned)strips, (unsigned)ychunks);
+  GALV_DISPATCH(dtype, T, {
+    act::colsum_kernel<T><<<grid, 256, 0, as_stream(stream)>>>((const T*)x, out, rows, cols, rpc);
+  });
+  GALV_LAUNCH_CHECK();
+  return 0;
+}
+
+int32_t galv_axpby(const void* x, void* y, int64_t n, float a, float b, int32_t x_dtype,
+                   int32_t y_dtype, void* stream) {
+  GALV_CHECK_ARG(x && y && n >= 0, "bad arguments");
+  if (n == 0) return 0;
+  const unsigned g = act::grid_for(n, 256);
+  GALV_DISPATCH(x_dtype, TX, {
+    GALV_DISPATCH(y_dtype, TY, {
+      act::axpby_kernel<TX, TY><<<g, 256, 0, as_stream(stream)>>>((const TX*)x, (TY*)y, n, a, b);
+    });
+  });
+  GALV_LAUNCH_CHECK();
+  return 0;
+}
+
+int32_t galv_sumsq(const void* x, int64_t n, float* out, int32_t dtype, void* stream) {
+  GALV_CHECK_ARG(x && out && n >= 0, "bad arguments");
+  if (n == 0) return 0;
+  GALV_DISPATCH(dtype, T, {
+    act::sumsq_kernel<T><<<act::grid_for(n, 256), 256, 0, as_stream(stream)>>>((const T*)x, n,
+                                                                                out);
+  });
+  GALV_LAUNCH_CHECK();
+  return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,341 @@
+"""ctypes bindings to libgalv_b200.so (the C ABI in include/galv.h).
+
+Thin, typed wrappers taking torch CUDA tensors: they pass raw device pointers,
+sizes and the *current* CUDA stream, and raise ``RuntimeError`` with the
+library's thread-local message on a non-zero status.  There is deliberately no
+fallback: if the shared library is missing or the tensors are not on a CUDA
+device the call fails loudly.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+import torch
+
+LIB_PATH = Path(__file__).resolve().parent / "libgalv_b200.so"
+F32, BF16 = 0, 1
+_DT = {torch.float32: F32, torch.bfloat16: BF16}
+
+_lib = None
+
+_P, _I64, _I32, _F = C.c_void_p, C.c_int64, C.c_int32, C.c_float
+_SIGS = {
+    "galv_abi_version": ([], _I32),
+    "galv_last_error": ([], C.c_char_p),
+    "galv_device_info": ([_P, _P, _P], _I32),
+    "galv_gemm": ([_P, _P, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I32, _I32, _F, _I32,
+                   _I32, _I32, _I32, _P], _I32),
+    "galv_gemm_batched": ([_P, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _I64,
+                           _I64, _I32, _I32, _F, _I32, _I32, _I32, _P], _I32),
+    "galv_attn_fwd": ([_P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _F, _I32,
+                       _I32, _P], _I32),
+    "galv_attn_bwd_workspace": ([_I64, _I64, _I64, _I64, _I32], _I64),
+    "galv_attn_bwd": ([_P, _P, _P, _P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64,
+                       _I64, _F, _I32, _I32, _P, _P], _I32),
+    "galv_rmsnorm_fwd": ([_P, _P, _P, _P, _P, _P, _I64, _I64, _F, _I32, _P], _I32),
+    "galv_rmsnorm_bwd": ([_P, _P, _P, _P, _P, _P, _P, _I64, _I64, _I32, _P, _P], _I32),
+    "galv_layernorm_fwd": ([_P, _P, _P, _P, _P, _P, _P, _P, _I64, _I64, _F, _I32, _P], _I32),
+    "galv_layernorm_bwd": ([_P, _P, _P, _P, _P, _P, _P, _P, _P, _I64, _I64, _I32, _P, _P],
+                           _I32),
+    "galv_norm_bwd_workspace": ([_I64, _I64], _I64),
+    "galv_rope": ([_P, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _F, _I32, _I32, _P], _I32),
+    "galv_swiglu_fwd": ([_P, _P, _I64, _I64, _I32, _P], _I32),
+    "galv_swiglu_bwd": ([_P, _P, _P, _I64, _I64, _I32, _P], _I32),
+    "galv_bias_gelu_fwd": ([_P, _P, _P, _I64, _I64, _I32, _P], _I32),
+    "galv_bias_gelu_bwd": ([_P, _P, _P, _P, _I64, _I64, _I32, _P], _I32),
+    "galv_colsum": ([_P, _P, _I64, _I64, _I32, _I32, _P, _P], _I32),
+    "galv_embed_fwd": ([_P, _P, _P, _I64, _I64, _I64, _I64, _I32, _P], _I32),
+    "galv_embed_bwd": ([_P, _P, _P, _I64, _I64, _I64, _I64, _I32, _P], _I32),
+    "galv_xent": ([_P, _P, _P, _P, _P, _I64, _I64, _I64, _F, _I64, _I32, _I32, _P], _I32),
+    "galv_adamw": ([_P, _P, _P, _P, _P, _I64, _F, _F, _F, _F, _F, _F, _I64, _I32, _I32, _P],
+                   _I32),
+    "galv_gather_rows": ([_P, _P, _P, _I64, _I64, _P], _I32),
+    "galv_scatter_rows": ([_P, _P, _P, _I64, _I64, _P], _I32),
+    "galv_axpby": ([_P, _P, _I64, _F, _F, _I32, _I32, _P], _I32),
+    "galv_sumsq": ([_P, _I64, _P, _I32, _P], _I32),
+}
+EXPORTED = tuple(_SIGS)
+
+
+def load_library(path: str | os.PathLike | None = None):
+    """Load (once) and type the C ABI; raises if the library or a symbol is missing."""
+    global _lib
+    if _lib is not None and path is None:
+        return _lib
+    p = Path(path) if path is not None else LIB_PATH
+    if not p.exists():
+        raise RuntimeError(f"{p} not built: run `python -m paper_2504_21411_b200.build` "
+                           "(there is no CPU fallback)")
+    lib = C.CDLL(str(p))
+    missing = []
+    for name, (args, res) in _SIGS.items():
+        try:
+            fn = getattr(lib, name)
+        except AttributeError:
+            missing.append(name)
+            continue
+        fn.argtypes = args
+        fn.restype = res
+    lib.galv_missing = tuple(missing)
+    if lib.galv_abi_version() != 1:
+        raise RuntimeError("libgalv_b200 ABI version mismatch")
+    if path is None:
+        _lib = lib
+    return lib
+
+
+def _call(name: str, *args) -> None:
+    rc = getattr(load_library(), name)(*args)
+    if rc != 0:
+        msg = load_library().galv_last_error().decode(errors="replace")
+        raise RuntimeError(f"{name} failed (status {rc}): {msg}")
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise RuntimeError("galv kernels need CUDA tensors (no CPU fallback)")
+    return t.data_ptr()
+
+
+def _stream():
+    return torch.cuda.current_stream().cuda_stream
+
+
+def dtype_code(dt) -> int:
+    try:
+        return _DT[dt]
+    except KeyError:
+        raise RuntimeError(f"unsupported dtype {dt}") from None
+
+
+# ---------------------------------------------------------------------------- GEMM
+
+
+def gemm(a, b, out=None, *, trans_a=False, trans_b=False, alpha=1.0, accumulate=False,
+         bias=None, out_dtype=None):
+    """out[M,N] (+)= alpha * op(a) @ op(b) (+ bias).
+
+    op(a): a is [M,K] (trans_a False) or [K,M] (True); op(b): b is [K,N] (trans_b
+    False) or [N,K] (True, the nn.Linear weight layout).  Inputs must have unit
+    stride in their last dim; leading dims are taken from stride(0).
+    """
+    if a.dim() != 2 or b.dim() != 2:
+        raise RuntimeError("gemm expects 2-D operands")
+    if a.stride(1) != 1 or b.stride(1) != 1:
+        raise RuntimeError("gemm operands need a contiguous last dim")
+    M, K = (a.shape[1], a.shape[0]) if trans_a else (a.shape[0], a.shape[1])
+    N, K2 = (b.shape[0], b.shape[1]) if trans_b else (b.shape[1], b.shape[0])
+    if K != K2:
+        raise RuntimeError(f"gemm K mismatch {K} vs {K2}")
+    if a.dtype != b.dtype:
+        raise RuntimeError("gemm operands must share a dtype")
+    if out is None:
+        out = torch.empty(M, N, device=a.device, dtype=out_dtype or a.dtype)
+    if out.shape != (M, N) or out.stride(1) != 1:
+        raise RuntimeError("bad gemm output")
+    _call("galv_gemm", _ptr(a), _ptr(b), _ptr(out), _ptr(bias), M, N, K, a.stride(0),
+          b.stride(0), out.stride(0), int(trans_a), int(trans_b), float(alpha),
+          int(accumulate), dtype_code(a.dtype), dtype_code(out.dtype),
+          dtype_code(bias.dtype) if bias is not None else F32, _stream())
+    return out
+
+
+def gemm_batched(a, b, out, *, trans_a=False, trans_b=False, alpha=1.0, accumulate=False):
+    """Strided batched GEMM over the leading dim of 3-D operands."""
+    Bt = a.shape[0]
+    M, K = (a.shape[2], a.shape[1]) if trans_a else (a.shape[1], a.shape[2])
+    N = b.shape[1] if trans_b else b.shape[2]
+    _call("galv_gemm_batched", _ptr(a), _ptr(b), _ptr(out), Bt, a.stride(0), b.stride(0),
+          out.stride(0), M, N, K, a.stride(1), b.stride(1), out.stride(1), int(trans_a),
+          int(trans_b), float(alpha), int(accumulate), dtype_code(a.dtype),
+          dtype_code(out.dtype), _stream())
+    return out
+
+
+# ---------------------------------------------------------------------------- attention
+
+
+def _attn_geometry(q, o):
+    # q/k/v: [B, S, H, D] views (possibly strided slices of a fused qkv buffer)
+    B, S, H, D = q.shape
+    if q.stride(3) != 1 or o.stride(3) != 1:
+        raise RuntimeError("attention needs unit stride in head_dim")
+    if q.stride(0) != S * q.stride(1) or o.stride(0) != S * o.stride(1):
+        raise RuntimeError("attention needs [B, S] token-major packing")
+    if o.stride(2) != q.stride(2):
+        raise RuntimeError("q and o must share the head stride")
+    return B, S, H, D, q.stride(1), q.stride(2), o.stride(1)
+
+
+def attn_fwd(q, k, v, o, lse, *, scale, causal=True):
+    B, S, H, D, st, sh, ost = _attn_geometry(q, o)
+    if k.stride() != q.stride() or v.stride() != q.stride():
+        raise RuntimeError("q, k, v must share strides")
+    _call("galv_attn_fwd", _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse), B, S, H, D, st, sh,
+          ost, float(scale), int(causal), dtype_code(q.dtype), _stream())
+
+
+def attn_bwd(q, k, v, o, dout, lse, dq, dk, dv, *, scale, causal=True, workspace=None):
+    B, S, H, D, st, sh, ost = _attn_geometry(q, o)
+    if dout.stride() != o.stride() or dq.stride() != q.stride():
+        raise RuntimeError("dout must match o's layout and dq/dk/dv q's layout")
+    need = load_library().galv_attn_bwd_workspace(B, S, H, D, dtype_code(q.dtype))
+    if workspace is None or workspace.numel() * workspace.element_size() < need:
+        workspace = torch.empty(need, dtype=torch.uint8, device=q.device)
+    _call("galv_attn_bwd", _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(dout), _ptr(lse), _ptr(dq),
+          _ptr(dk), _ptr(dv), B, S, H, D, st, sh, ost, float(scale), int(causal),
+          dtype_code(q.dtype), _ptr(workspace), _stream())
+
+
+# ---------------------------------------------------------------------------- norms
+
+
+def rmsnorm_fwd(x, gamma, eps, *, residual=None, res_out=None):
+    rows, cols = x.numel() // x.shape[-1], x.shape[-1]
+    y = torch.empty_like(x)
+    rstd = torch.empty(rows, device=x.device, dtype=torch.float32)
+    _call("galv_rmsnorm_fwd", _ptr(x), _ptr(residual), _ptr(res_out), _ptr(gamma), _ptr(y),
+          _ptr(rstd), rows, cols, float(eps), dtype_code(x.dtype), _stream())
+    return y, rstd
+
+
+def rmsnorm_bwd(x, gamma, rstd, dy, dgamma_acc, *, dres=None, dx=None):
+    rows, cols = x.numel() // x.shape[-1], x.shape[-1]
+    dx = torch.empty_like(x) if dx is None else dx
+    _call("galv_rmsnorm_bwd", _ptr(x), _ptr(gamma), _ptr(rstd), _ptr(dy), _ptr(dres), _ptr(dx),
+          _ptr(dgamma_acc), rows, cols, dtype_code(x.dtype), None, _stream())
+    return dx
+
+
+def layernorm_fwd(x, gamma, beta, eps, *, residual=None, res_out=None):
+    rows, cols = x.numel() // x.shape[-1], x.shape[-1]
+    y = torch.empty_like(x)
+    mean = torch.empty(rows, device=x.device, dtype=torch.float32)
+    rstd = torch.empty(rows, device=x.device, dtype=torch.float32)
+    _call("galv_layernorm_fwd", _ptr(x), _ptr(residual), _ptr(res_out), _ptr(gamma),
+          _ptr(beta), _ptr(y), _ptr(mean), _ptr(rstd), rows, cols, float(eps),
+          dtype_code(x.dtype), _stream())
+    return y, mean, rstd
+
+
+def layernorm_bwd(x, gamma, mean, rstd, dy, dgamma_acc, dbeta_acc, *, dres=None, dx=None):
+    rows, cols = x.numel() // x.shape[-1], x.shape[-1]
+    dx = torch.empty_like(x) if dx is None else dx
+    _call("galv_layernorm_bwd", _ptr(x), _ptr(gamma), _ptr(mean), _ptr(rstd), _ptr(dy),
+          _ptr(dres), _ptr(dx), _ptr(dgamma_acc), _ptr(dbeta_acc), rows, cols,
+          dtype_code(x.dtype), None, _stream())
+    return dx
+
+
+# ---------------------------------------------------------------------------- pointwise
+
+
+def rope_(x, seq_len, *, theta=10000.0, inverse=False, pos0=0):
+    """In place on a [T, H, D] view (T = B*S tokens, token-major)."""
+    T, H, D = x.shape
+    if x.stride(2) != 1:
+        raise RuntimeError("rope needs unit stride in head_dim")
+    _call("galv_rope", _ptr(x), T, seq_len, H, D, x.stride(0), x.stride(1), pos0, float(theta),
+          int(inverse), dtype_code(x.dtype), _stream())
+    return x
+
+
+def swiglu_fwd(gu, out=None):
+    T, F2 = gu.shape
+    out = torch.empty(T, F2 // 2, device=gu.device, dtype=gu.dtype) if out is None else out
+    _call("galv_swiglu_fwd", _ptr(gu), _ptr(out), T, F2 // 2, dtype_code(gu.dtype), _stream())
+    return out
+
+
+def swiglu_bwd(gu, dh, dgu=None):
+    T, F2 = gu.shape
+    dgu = torch.empty_like(gu) if dgu is None else dgu
+    _call("galv_swiglu_bwd", _ptr(gu), _ptr(dh), _ptr(dgu), T, F2 // 2, dtype_code(gu.dtype),
+          _stream())
+    return dgu
+
+
+def bias_gelu_fwd(x, bias, out=None):
+    T, F = x.shape
+    out = torch.empty_like(x) if out is None else out
+    _call("galv_bias_gelu_fwd", _ptr(x), _ptr(bias), _ptr(out), T, F, dtype_code(x.dtype),
+          _stream())
+    return out
+
+
+def bias_gelu_bwd(x, bias, dy, dx=None):
+    T, F = x.shape
+    dx = torch.empty_like(x) if dx is None else dx
+    _call("galv_bias_gelu_bwd", _ptr(x), _ptr(bias), _ptr(dy), _ptr(dx), T, F,
+          dtype_code(x.dtype), _stream())
+    return dx
+
+
+def colsum(x, out, *, accumulate=True):
+    rows, cols = x.shape
+    _call("galv_colsum", _ptr(x), _ptr(out), rows, cols, int(accumulate), dtype_code(x.dtype),
+          None, _stream())
+    return out
+
+
+def embed_fwd(ids, table, vocab_lo=0, out=None):
+    T = ids.numel()
+    V, Hd = table.shape
+    out = torch.empty(T, Hd, device=table.device, dtype=table.dtype) if out is None else out
+    _call("galv_embed_fwd", _ptr(ids), _ptr(table), _ptr(out), T, V, vocab_lo, Hd,
+          dtype_code(table.dtype), _stream())
+    return out
+
+
+def embed_bwd(ids, dout, dtable_acc, vocab_lo=0):
+    T = ids.numel()
+    V, Hd = dtable_acc.shape
+    _call("galv_embed_bwd", _ptr(ids), _ptr(dout), _ptr(dtable_acc), T, V, vocab_lo, Hd,
+          dtype_code(dout.dtype), _stream())
+
+
+def xent(logits, labels, stats, stage, *, loss=None, dlogits=None, vocab_lo=0, grad_scale=1.0,
+         ignore_index=-100):
+    T, V = logits.shape
+    _call("galv_xent", _ptr(logits), _ptr(labels), _ptr(stats), _ptr(loss), _ptr(dlogits), T,
+          V, vocab_lo, float(grad_scale), int(ignore_index), int(stage),
+          dtype_code(logits.dtype), _stream())
+
+
+def adamw(master, m, v, grad, param_out, *, lr, beta1, beta2, eps, weight_decay, step,
+          grad_scale=1.0):
+    n = master.numel()
+    _call("galv_adamw", _ptr(master), _ptr(m), _ptr(v), _ptr(grad), _ptr(param_out), n,
+          float(lr), float(beta1), float(beta2), float(eps), float(weight_decay),
+          float(grad_scale), int(step), dtype_code(grad.dtype),
+          dtype_code(param_out.dtype) if param_out is not None else F32, _stream())
+
+
+def gather_rows(src, idx, dst):
+    row_bytes = src.stride(0) * src.element_size()
+    _call("galv_gather_rows", _ptr(src), _ptr(dst), _ptr(idx), idx.numel(), row_bytes,
+          _stream())
+    return dst
+
+
+def scatter_rows(src, idx, dst):
+    row_bytes = src.stride(0) * src.element_size()
+    _call("galv_scatter_rows", _ptr(src), _ptr(dst), _ptr(idx), idx.numel(), row_bytes,
+          _stream())
+    return dst
+
+
+def axpby(x, y, a, b):
+    _call("galv_axpby", _ptr(x), _ptr(y), x.numel(), float(a), float(b), dtype_code(x.dtype),
+          dtype_code(y.dtype), _stream())
+    return y
+
+
+def sumsq(x, out):
+    _call("galv_sumsq", _ptr(x), x.numel(), _ptr(out), dtype_code(x.dtype), _stream())
+    return out
