@@ -115,6 +115,8 @@ int32_t galv_bias_gelu_fwd(const void* x, const void* bias, void* y, int64_t T, 
                            int32_t dtype, void* stream);
 int32_t galv_bias_gelu_bwd(const void* x, const void* bias, const void* dy, void* dx,
                            int64_t T, int64_t F, int32_t dtype, void* stream);
+/* x[T, F] += bias[F] (row broadcast) */
+int32_t galv_bias_add(void* x, const void* bias, int64_t T, int64_t F, int32_t dtype, void* stream);
 /* column sums: out[c] (+)= sum_r x[r, c] (fp32 out, for bias gradients) */
 int32_t galv_colsum(const void* x, float* out, int64_t rows, int64_t cols, int32_t accumulate,
                     int32_t dtype, void* ws, void* stream);

@@ -244,3 +244,36 @@ int32_t galv_sumsq(const void* x, int64_t n, float* out, int32_t dtype, void* st
 }
 
 }  // extern "C"
+
+namespace galv {
+namespace act {
+template <typename T>
+__global__ void bias_add_kernel(T* __restrict__ x, const T* __restrict__ b, int64_t T_,
+                                int64_t F) {
+  constexpr int V = 16 / sizeof(T);
+  const int64_t nvec = T_ * F / V;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nvec;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = i * V, f = e % F;
+    float v[V], bb[V];
+    load16(x + e, v);
+    load16(b + f, bb);
+#pragma unroll
+    for (int k = 0; k < V; ++k) v[k] += bb[k];
+    store16(x + e, v);
+  }
+}
+}  // namespace act
+}  // namespace galv
+
+extern "C" int32_t galv_bias_add(void* x, const void* bias, int64_t T_, int64_t F, int32_t dtype,
+                                 void* stream) {
+  GALV_CHECK_ARG(x && bias && T_ > 0 && F % 8 == 0, "bad arguments");
+  GALV_DISPATCH(dtype, T, {
+    const int64_t nvec = T_ * F / (16 / sizeof(T));
+    act::bias_add_kernel<T><<<act::grid_for(nvec, 256), 256, 0, as_stream(stream)>>>(
+        (T*)x, (const T*)bias, T_, F);
+  });
+  GALV_LAUNCH_CHECK();
+  return 0;
+}

@@ -46,6 +46,7 @@ _SIGS = {
     "galv_swiglu_bwd": ([_P, _P, _P, _I64, _I64, _I32, _P], _I32),
     "galv_bias_gelu_fwd": ([_P, _P, _P, _I64, _I64, _I32, _P], _I32),
     "galv_bias_gelu_bwd": ([_P, _P, _P, _P, _I64, _I64, _I32, _P], _I32),
+    "galv_bias_add": ([_P, _P, _I64, _I64, _I32, _P], _I32),
     "galv_colsum": ([_P, _P, _I64, _I64, _I32, _I32, _P, _P], _I32),
     "galv_embed_fwd": ([_P, _P, _P, _I64, _I64, _I64, _I64, _I32, _P], _I32),
     "galv_embed_bwd": ([_P, _P, _P, _I64, _I64, _I64, _I64, _I32, _P], _I32),
@@ -339,3 +340,9 @@ def axpby(x, y, a, b):
 def sumsq(x, out):
     _call("galv_sumsq", _ptr(x), x.numel(), _ptr(out), dtype_code(x.dtype), _stream())
     return out
+
+
+def bias_add_(x, bias):
+    T, F = x.shape
+    _call("galv_bias_add", _ptr(x), _ptr(bias), T, F, dtype_code(x.dtype), _stream())
+    return x

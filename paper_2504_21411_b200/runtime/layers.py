@@ -1,0 +1,442 @@
+"""Decoder layers, embedding and LM head with explicit forward/backward on galv kernels.
+
+Each layer realizes its ``ParallelStrategy`` (reference strategy.py:20-60):
+  * tp: Megatron column-parallel QKV / fc1 / gate_up and row-parallel proj / fc2 / down
+    (heads and FFN columns split over the contiguous tp group)
+  * sp: the residual stream is token-sharded over the tp group; all-gather before the
+    column GEMMs, reduce-scatter after the row GEMMs (same volume as the AR pair,
+    costmodel.py:7-10)
+  * dp / zero_stage: see params.ParamStore
+  * recompute: forward keeps only the layer input; backward replays the forward
+    (including its tp traffic, costmodel.py:122-126) and then runs backward.
+
+Activations are 2-D [tokens, hidden] in token-major [b, s] order.  Tokens of a
+microbatch are split into dp replicas (contiguous sample ranges) and, under sp, into
+tp chunks of contiguous tokens (per-token ops do not care which tokens a rank owns;
+attention runs on the gathered full sequences).
+"""
+
+from __future__ import annotations
+
+import math
+
+import torch
+
+from .. import kernels as K
+from . import comm
+from .params import ParamStore
+
+SMALL_SUFFIXES = ("norm.weight", "norm.bias", ".bias")
+
+
+def _is_small(name: str) -> bool:
+    return name.endswith(SMALL_SUFFIXES)
+
+
+# ---------------------------------------------------------------------------- TP slicing
+
+
+def tp_slice(cfg, name: str, full: torch.Tensor, tp: int, r: int) -> torch.Tensor:
+    """Local shard of a logical tensor for tp rank r (Megatron layout)."""
+    if tp == 1:
+        return full
+    leaf = name.split(".", 2)[-1] if name.startswith("layers.") else name
+    h, f = cfg.hidden, cfg.ffn
+    if leaf in ("qkv.weight", "qkv.bias"):
+        hl = h // tp
+        parts = [full[j * h + r * hl: j * h + (r + 1) * hl] for j in range(3)]
+        return torch.cat(parts, 0)
+    if leaf in ("fc1.weight", "fc1.bias"):
+        fl = f // tp
+        return full[r * fl:(r + 1) * fl]
+    if leaf == "gate_up.weight":
+        fl = f // tp
+        return torch.cat([full[r * fl:(r + 1) * fl], full[f + r * fl: f + (r + 1) * fl]], 0)
+    if leaf in ("proj.weight",):
+        hl = h // tp
+        return full[:, r * hl:(r + 1) * hl]
+    if leaf in ("fc2.weight", "down.weight"):
+        fl = f // tp
+        return full[:, r * fl:(r + 1) * fl]
+    if leaf in ("embed.weight", "lm_head.weight"):
+        vl = cfg.vocab // tp
+        return full[r * vl:(r + 1) * vl]
+    return full  # norms, row-parallel output biases, positional embedding: replicated
+
+
+def tp_unslice(cfg, name: str, parts: list) -> torch.Tensor:
+    """Inverse of tp_slice over the tp ranks' shards (tests / checkpoint export)."""
+    tp = len(parts)
+    if tp == 1:
+        return parts[0]
+    leaf = name.split(".", 2)[-1] if name.startswith("layers.") else name
+    if leaf in ("qkv.weight", "qkv.bias"):
+        hl = cfg.hidden // tp
+        return torch.cat([p[j * hl:(j + 1) * hl] for j in range(3) for p in parts], 0)
+    if leaf == "gate_up.weight":
+        fl = cfg.ffn // tp
+        return torch.cat([p[:fl] for p in parts] + [p[fl:] for p in parts], 0)
+    if leaf in ("fc1.weight", "fc1.bias", "embed.weight", "lm_head.weight"):
+        return torch.cat(parts, 0)
+    if leaf in ("proj.weight", "fc2.weight", "down.weight"):
+        return torch.cat(parts, 1)
+    return parts[0]
+
+
+# ---------------------------------------------------------------------------- helpers
+
+
+def _linear(x, w, out=None, bias=None):
+    """x [T, K] @ w[N, K]^T (+bias) -> [T, N]."""
+    return K.gemm(x, w, out, trans_b=True, bias=bias)
+
+
+def _dgrad(dy, w, out=None):
+    """dy [T, N] @ w [N, K] -> [T, K]."""
+    return K.gemm(dy, w, out)
+
+
+def _wgrad(dy, x, gw):
+    """gw [N, K] += dy^T [N, T] @ x [T, K]."""
+    K.gemm(dy, x, gw, trans_a=True, accumulate=True)
+
+
+class _Ctx:
+    __slots__ = ("saved", "x")
+
+    def __init__(self):
+        self.saved = None
+        self.x = None
+
+
+# ---------------------------------------------------------------------------- decoder layer
+
+
+class DecoderLayer:
+    def __init__(self, cfg, index: int, strategy, topo, *, dtype, grad_dtype, device):
+        self.cfg, self.index, self.s = cfg, index, strategy
+        self.dtype, self.device = dtype, device
+        self.tpg = topo.tp(strategy.tp)
+        self.dpg = topo.dp(strategy.tp)
+        self.tp, self.tpr = strategy.tp, self.tpg.index
+        h, f = cfg.hidden, cfg.ffn
+        self.hl, self.fl, self.Hl = h // self.tp, f // self.tp, cfg.heads // self.tp
+        from .init import layer_param_shapes
+        shapes = layer_param_shapes(cfg)
+        local = {}
+        for n, shp in shapes.items():
+            local[n] = tuple(tp_slice(cfg, n, torch.empty(shp, device="meta"), self.tp,
+                                      self.tpr).shape)
+        self.names = list(shapes)
+        self.store = ParamStore([(n, local[n]) for n in self.names], dtype=dtype,
+                                grad_dtype=grad_dtype, device=device, dp=self.dpg,
+                                zero=strategy.zero_stage,
+                                small_names=[n for n in self.names if _is_small(n)])
+        # replicated params whose grads are token-partial under sp
+        self.tp_partial = [n for n in self.names if _is_small(n) and strategy.sp and
+                           n not in ("qkv.bias", "fc1.bias")]
+        self.scale = 1.0 / math.sqrt(cfg.head_dim)
+        self._ws = None
+
+    def param_prefix(self) -> str:
+        return f"layers.{self.index}."
+
+    # -------------------------------------------------------------- forward
+    def _gather_seq(self, t):
+        return comm.all_gather(t, self.tpg) if self.s.sp else t
+
+    def _reduce_out(self, t):
+        if self.tp == 1:
+            return t
+        if self.s.sp:
+            return comm.reduce_scatter(t, self.tpg)
+        return comm.all_reduce(t, self.tpg)
+
+    def _norm_fwd(self, x, w, prefix, residual=None):
+        res_out = torch.empty_like(x) if residual is not None else None
+        if self.cfg.arch == "gpt":
+            y, mean, rstd = K.layernorm_fwd(x, w[prefix + ".weight"], w[prefix + ".bias"],
+                                            self.cfg.norm_eps, residual=residual,
+                                            res_out=res_out)
+        else:
+            y, rstd = K.rmsnorm_fwd(x, w[prefix + ".weight"], self.cfg.norm_eps,
+                                    residual=residual, res_out=res_out)
+            mean = None
+        return y, (mean, rstd), res_out
+
+    def _norm_bwd(self, x, w, stats, dy, prefix, sg, dres=None):
+        mean, rstd = stats
+        if self.cfg.arch == "gpt":
+            return K.layernorm_bwd(x, w[prefix + ".weight"], mean, rstd, dy,
+                                   sg[prefix + ".weight"], sg[prefix + ".bias"], dres=dres)
+        return K.rmsnorm_bwd(x, w[prefix + ".weight"], rstd, dy, sg[prefix + ".weight"],
+                             dres=dres)
+
+    def _attn_views(self, qkv, B, S):
+        hl, D = self.hl, self.cfg.head_dim
+        st = qkv.stride(0)
+        base = qkv.storage_offset()
+        mk = lambda j: qkv.as_strided((B, S, self.Hl, D), (S * st, st, D, 1), base + j * hl)
+        return mk(0), mk(1), mk(2)
+
+    def forward_impl(self, x, B, save: bool):
+        """x: [T_in, h] in this layer's layout; B = samples in this dp replica."""
+        cfg = self.cfg
+        S = cfg.seq_len
+        flat = self.store.materialize()
+        w = self.store.views(flat)
+        gpt = cfg.arch == "gpt"
+        n1, st1, _ = self._norm_fwd(x, w, "attn_norm")
+        n1f = self._gather_seq(n1)
+        T = n1f.shape[0]
+        qkv = _linear(n1f, w["qkv.weight"], bias=w["qkv.bias"] if gpt else None)
+        q, k, v = self._attn_views(qkv, B, S)
+        if not gpt:
+            for j in (0, 1):
+                K.rope_(qkv.as_strided((T, self.Hl, cfg.head_dim),
+                                       (qkv.stride(0), cfg.head_dim, 1),
+                                       qkv.storage_offset() + j * self.hl),
+                        S, theta=cfg.rope_theta)
+        o = torch.empty(T, self.hl, device=x.device, dtype=x.dtype)
+        lse = torch.empty(B, self.Hl, S, device=x.device, dtype=torch.float32)
+        K.attn_fwd(q, k, v, o.view(B, S, self.Hl, cfg.head_dim), lse, scale=self.scale,
+                   causal=True)
+        fuse_bias = gpt and self.tp == 1
+        a = _linear(o, w["proj.weight"], bias=w["proj.bias"] if fuse_bias else None)
+        a = self._reduce_out(a)
+        if gpt and not fuse_bias:
+            K.bias_add_(a, w["proj.bias"])
+        # h1 = x + a ; n2 = norm(h1)
+        n2, st2, h1 = self._norm_fwd(a, w, "mlp_norm", residual=x)
+        n2f = self._gather_seq(n2)
+        if gpt:
+            f1 = _linear(n2f, w["fc1.weight"])           # pre-activation (bias in gelu)
+            act = K.bias_gelu_fwd(f1, w["fc1.bias"])
+            m = _linear(act, w["fc2.weight"], bias=w["fc2.bias"] if fuse_bias else None)
+        else:
+            gu = _linear(n2f, w["gate_up.weight"])
+            act = K.swiglu_fwd(gu)
+            m = _linear(act, w["down.weight"])
+        m = self._reduce_out(m)
+        if gpt and not fuse_bias:
+            K.bias_add_(m, w["fc2.bias"])
+        y = K.axpby(h1, m, 1.0, 1.0)
+        if save:
+            saved = dict(x=x, st1=st1, n1f=n1f, qkv=qkv, o=o, lse=lse, h1=h1, st2=st2, n2f=n2f,
+                         act=act, B=B)
+            saved["pre"] = f1 if gpt else gu
+            return y, saved
+        return y, None
+
+    def forward(self, x, B):
+        ctx = _Ctx()
+        if self.s.recompute:
+            y, _ = self.forward_impl(x, B, save=False)
+            ctx.x, ctx.saved = (x, B), None
+        else:
+            y, ctx.saved = self.forward_impl(x, B, save=True)
+        self.store.release()
+        return y, ctx
+
+    # -------------------------------------------------------------- backward
+    def backward(self, dy, ctx):
+        cfg = self.cfg
+        if ctx.saved is None:
+            x, B = ctx.x
+            _, sv = self.forward_impl(x, B, save=True)
+        else:
+            sv = ctx.saved
+        ctx.saved = ctx.x = None
+        S = cfg.seq_len
+        gpt = cfg.arch == "gpt"
+        flat = self.store.materialize()
+        w = self.store.views(flat)
+        gflat = self.store.grad_target()
+        gw = self.store.views(gflat)
+        sg = self.store.small_grads()
+        B = sv["B"]
+        # ---- MLP
+        dmf = self._gather_seq(dy)
+        if gpt:
+            K.colsum(dy, sg["fc2.bias"])
+            dact = _dgrad(dmf, w["fc2.weight"])
+            _wgrad(dmf, sv["act"], gw["fc2.weight"])
+            dpre = K.bias_gelu_bwd(sv["pre"], w["fc1.bias"], dact)
+            del dact
+            K.colsum(dpre, sg["fc1.bias"])
+            dn2f = _dgrad(dpre, w["fc1.weight"])
+            _wgrad(dpre, sv["n2f"], gw["fc1.weight"])
+        else:
+            dact = _dgrad(dmf, w["down.weight"])
+            _wgrad(dmf, sv["act"], gw["down.weight"])
+            dpre = K.swiglu_bwd(sv["pre"], dact)
+            del dact
+            dn2f = _dgrad(dpre, w["gate_up.weight"])
+            _wgrad(dpre, sv["n2f"], gw["gate_up.weight"])
+        del dpre, dmf
+        dn2 = self._reduce_out(dn2f)
+        dh1 = self._norm_bwd(sv["h1"], w, sv["st2"], dn2, "mlp_norm", sg, dres=dy)
+        del dn2, dn2f
+        # ---- attention
+        daf = self._gather_seq(dh1)
+        if gpt:
+            K.colsum(dh1, sg["proj.bias"])
+        do = _dgrad(daf, w["proj.weight"])
+        _wgrad(daf, sv["o"], gw["proj.weight"])
+        del daf
+        qkv = sv["qkv"]
+        T = qkv.shape[0]
+        dqkv = torch.empty_like(qkv)
+        q, k, v = self._attn_views(qkv, B, S)
+        dq, dk, dv = self._attn_views(dqkv, B, S)
+        if self._ws is None:
+            self._ws = torch.empty(B * self.Hl * S, dtype=torch.float32, device=qkv.device)
+        K.attn_bwd(q, k, v, sv["o"].view(B, S, self.Hl, cfg.head_dim),
+                   do.view(B, S, self.Hl, cfg.head_dim), sv["lse"], dq, dk, dv,
+                   scale=self.scale, causal=True, workspace=self._ws)
+        del do
+        if not gpt:
+            for j in (0, 1):
+                K.rope_(dqkv.as_strided((T, self.Hl, cfg.head_dim),
+                                        (dqkv.stride(0), cfg.head_dim, 1),
+                                        dqkv.storage_offset() + j * self.hl),
+                        S, theta=cfg.rope_theta, inverse=True)
+        if gpt:
+            K.colsum(dqkv, sg["qkv.bias"])
+        dn1f = _dgrad(dqkv, w["qkv.weight"])
+        _wgrad(dqkv, sv["n1f"], gw["qkv.weight"])
+        del dqkv
+        dn1 = self._reduce_out(dn1f)
+        dx = self._norm_bwd(sv["x"], w, sv["st1"], dn1, "attn_norm", sg, dres=dh1)
+        self.store.release()
+        self.store.finish_microbatch(gflat, self.tp_partial, self.tpg)
+        return dx
+
+
+# ---------------------------------------------------------------------------- embedding
+
+
+class Embedding:
+    """Vocab-parallel token embedding (+ learned positions for GPT) in layer 0's layout."""
+
+    def __init__(self, cfg, strategy, topo, *, dtype, grad_dtype, device):
+        self.cfg, self.s, self.dtype = cfg, strategy, dtype
+        self.tpg, self.dpg = topo.tp(strategy.tp), topo.dp(strategy.tp)
+        self.tp, self.tpr = strategy.tp, self.tpg.index
+        self.vl = cfg.vocab // self.tp
+        entries = [("embed.weight", (self.vl, cfg.hidden))]
+        if cfg.arch == "gpt":
+            entries.append(("pos_embed.weight", (cfg.seq_len, cfg.hidden)))
+        self.store = ParamStore(entries, dtype=dtype, grad_dtype=grad_dtype, device=device,
+                                dp=self.dpg, zero=0)
+        self.dtable = None
+
+    def forward(self, ids):
+        """ids: [T_rep] int64 (this dp replica's tokens) -> [T_in, h] in layer-0 layout."""
+        w = self.store.views(self.store.materialize())
+        x = K.embed_fwd(ids, w["embed.weight"], vocab_lo=self.tpr * self.vl)
+        if self.tp > 1:
+            x = comm.reduce_scatter(x, self.tpg) if self.s.sp else comm.all_reduce(x, self.tpg)
+        if self.cfg.arch == "gpt":
+            S = self.cfg.seq_len
+            T = x.shape[0]
+            lo = self.tpr * T if (self.s.sp and self.tp > 1) else 0
+            pos = w["pos_embed.weight"]
+            rows = (torch.arange(lo, lo + T, device=x.device) % S)
+            x.add_(pos.index_select(0, rows))
+        return x
+
+    def backward(self, ids, dx):
+        cfg = self.cfg
+        dxf = comm.all_gather(dx, self.tpg) if (self.s.sp and self.tp > 1) else dx
+        gflat = self.store.grad_target()
+        gw = self.store.views(gflat)
+        if self.dtable is None:
+            self.dtable = torch.zeros(self.vl, cfg.hidden, dtype=torch.float32, device=dx.device)
+        K.embed_bwd(ids, dxf, self.dtable, vocab_lo=self.tpr * self.vl)
+        K.axpby(self.dtable, gw["embed.weight"], 1.0, 1.0)
+        self.dtable.zero_()
+        if cfg.arch == "gpt":
+            S = cfg.seq_len
+            T = dx.shape[0]
+            lo = self.tpr * T if (self.s.sp and self.tp > 1) else 0
+            rows = torch.arange(lo, lo + T, device=dx.device) % S
+            acc = torch.zeros(S, cfg.hidden, dtype=torch.float32, device=dx.device)
+            acc.index_add_(0, rows, dx.float())
+            if self.s.sp and self.tp > 1:
+                comm.all_reduce(acc, self.tpg)
+            K.axpby(acc, gw["pos_embed.weight"], 1.0, 1.0)
+        self.store.finish_microbatch(gflat)
+
+
+# ---------------------------------------------------------------------------- head
+
+
+class Head:
+    """Final norm + vocab-parallel LM head + fused cross-entropy (last layer's layout)."""
+
+    def __init__(self, cfg, strategy, topo, *, dtype, grad_dtype, device):
+        self.cfg, self.s, self.dtype = cfg, strategy, dtype
+        self.tpg, self.dpg = topo.tp(strategy.tp), topo.dp(strategy.tp)
+        self.tp, self.tpr = strategy.tp, self.tpg.index
+        self.vl = cfg.vocab // self.tp
+        entries = [("final_norm.weight", (cfg.hidden,))]
+        if cfg.arch == "gpt":
+            entries.append(("final_norm.bias", (cfg.hidden,)))
+        entries.append(("lm_head.weight", (self.vl, cfg.hidden)))
+        self.store = ParamStore(entries, dtype=dtype, grad_dtype=grad_dtype, device=device,
+                                dp=self.dpg, zero=0,
+                                small_names=("final_norm.weight", "final_norm.bias"))
+        self.tp_partial = ["final_norm.weight", "final_norm.bias"] if strategy.sp else []
+
+    def forward_backward(self, x, labels, grad_scale):
+        """x [T_in, h], labels [T_rep] -> (sum of token losses (fp32 tensor), dx)."""
+        cfg = self.cfg
+        w = self.store.views(self.store.materialize())
+        gflat = self.store.grad_target()
+        gw = self.store.views(gflat)
+        sg = self.store.small_grads()
+        gpt = cfg.arch == "gpt"
+        if gpt:
+            n, mean, rstd = K.layernorm_fwd(x, w["final_norm.weight"], w["final_norm.bias"],
+                                            cfg.norm_eps)
+        else:
+            n, rstd = K.rmsnorm_fwd(x, w["final_norm.weight"], cfg.norm_eps)
+            mean = None
+        sp = self.s.sp and self.tp > 1
+        nf = comm.all_gather(n, self.tpg) if sp else n
+        T = nf.shape[0]
+        logits = _linear(nf, w["lm_head.weight"])
+        stats = torch.empty(T, 3, dtype=torch.float32, device=x.device)
+        loss = torch.empty(T, dtype=torch.float32, device=x.device)
+        lo = self.tpr * self.vl
+        if self.tp == 1:
+            K.xent(logits, labels, stats, 3, loss=loss, dlogits=logits, vocab_lo=lo,
+                   grad_scale=grad_scale)
+        else:
+            import torch.distributed as dist
+            K.xent(logits, labels, stats, 0, vocab_lo=lo)
+            mx = stats[:, 0].contiguous()
+            comm.all_reduce(mx, self.tpg, op=dist.ReduceOp.MAX)
+            stats[:, 0] = mx
+            K.xent(logits, labels, stats, 1, vocab_lo=lo)
+            part = stats[:, 1:3].contiguous()
+            comm.all_reduce(part, self.tpg)
+            stats[:, 1:3] = part
+            K.xent(logits, labels, stats, 2, loss=loss, dlogits=logits, vocab_lo=lo,
+                   grad_scale=grad_scale)
+        dlogits = logits
+        dnf = _dgrad(dlogits, w["lm_head.weight"])
+        _wgrad(dlogits, nf, gw["lm_head.weight"])
+        del logits, dlogits
+        if self.tp > 1:
+            dn = comm.reduce_scatter(dnf, self.tpg) if sp else comm.all_reduce(dnf, self.tpg)
+        else:
+            dn = dnf
+        if gpt:
+            dx = K.layernorm_bwd(x, w["final_norm.weight"], mean, rstd, dn,
+                                 sg["final_norm.weight"], sg["final_norm.bias"])
+        else:
+            dx = K.rmsnorm_bwd(x, w["final_norm.weight"], rstd, dn, sg["final_norm.weight"])
+        self.store.finish_microbatch(gflat, self.tp_partial, self.tpg)
+        return loss.sum(), dx

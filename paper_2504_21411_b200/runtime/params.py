@@ -1,0 +1,183 @@
+"""Flat per-layer parameter / gradient / optimizer storage with ZeRO-0..3 on the dp axis.
+
+One ``ParamStore`` per decoder layer (and one each for the embedding and the head)
+holds the layer's TP-local tensors packed into one flat buffer (each entry 64-element
+aligned so every GEMM operand is TMA-aligned), padded so it splits into ``dp`` equal
+contiguous shards.  Memory per device follows the reference cost model exactly
+(costmodel.py:157-160): params bpp*P/tp (/dp if z3), grads bpg*P/tp (/dp if z>=2),
+fp32 master + Adam moments 12*P/tp (/dp if z>=1).
+
+Communication (costmodel.py:114-118, 199-213):
+  z0: grad all-reduce over dp at sync
+  z1: grad reduce-scatter at sync, param all-gather after the step
+  z2: grad reduce-scatter after every microbatch (shard accumulators), param AG after step
+  z3: as z2, params live sharded and are all-gathered before each fwd and each bwd
+"""
+
+from __future__ import annotations
+
+import math
+
+import torch
+
+from .. import kernels as K
+from . import comm
+
+ALIGN = 64
+
+
+def _roundup(x: int, m: int) -> int:
+    return (x + m - 1) // m * m
+
+
+class ParamStore:
+    def __init__(self, entries, *, dtype, grad_dtype, device, dp, zero: int,
+                 small_names=()):
+        """entries: ordered list of (name, local_shape)."""
+        self.dtype, self.grad_dtype, self.device = dtype, grad_dtype, device
+        self.dp = dp                          # GroupHandle or None
+        self.ndp = dp.size if dp is not None else 1
+        self.rank_dp = dp.index if dp is not None else 0
+        self.zero = zero if self.ndp > 1 else 0
+        self.layout = {}
+        off = 0
+        for name, shape in entries:
+            n = math.prod(shape)
+            self.layout[name] = (off, tuple(shape))
+            off = _roundup(off + n, ALIGN)
+        self.numel = sum(math.prod(s) for _, s in self.layout.values())
+        self.total = _roundup(max(off, 1), self.ndp * ALIGN)
+        self.shard = self.total // self.ndp
+        self.lo = self.rank_dp * self.shard
+        kw = dict(device=device)
+        if self.zero == 3:
+            self.p_shard = torch.zeros(self.shard, dtype=dtype, **kw)
+            self.p_full = None
+        else:
+            self.p_full = torch.zeros(self.total, dtype=dtype, **kw)
+        if self.zero >= 2:
+            self.g_shard = torch.zeros(self.shard, dtype=grad_dtype, **kw)
+            self.g_full = None
+        else:
+            self.g_full = torch.zeros(self.total, dtype=grad_dtype, **kw)
+            self.g_shard = None
+        # fp32 accumulators for small (1-D) entries: norms and biases
+        self.small = [n for n in small_names if n in self.layout]
+        self.small_layout = {}
+        soff = 0
+        for n in self.small:
+            size = math.prod(self.layout[n][1])
+            self.small_layout[n] = (soff, self.layout[n][1])
+            soff += size
+        self.acc32 = torch.zeros(max(soff, 1), dtype=torch.float32, **kw)
+        self.master = self.m = self.v = None
+        self._gathered = None
+        self._owned_grad = None
+
+    # ------------------------------------------------------------------ values
+    def views(self, flat: torch.Tensor) -> dict:
+        return {n: flat[o:o + math.prod(s)].view(s) for n, (o, s) in self.layout.items()}
+
+    def small_grads(self) -> dict:
+        return {n: self.acc32[o:o + math.prod(s)].view(s) for n, (o, s) in
+                self.small_layout.items()}
+
+    def load(self, tensors: dict) -> None:
+        """Fill parameters (and the fp32 master copy) from local tensors (any device)."""
+        full = torch.zeros(self.total, dtype=torch.float32, device=self.device)
+        for n, (o, s) in self.layout.items():
+            t = tensors[n]
+            if tuple(t.shape) != s:
+                raise RuntimeError(f"{n}: expected {s}, got {tuple(t.shape)}")
+            full[o:o + t.numel()] = t.reshape(-1).to(self.device, torch.float32)
+        cast = full.to(self.dtype)
+        if self.zero == 3:
+            self.p_shard.copy_(cast[self.lo:self.lo + self.shard])
+        else:
+            self.p_full.copy_(cast)
+        self._init_master(cast.float())
+
+    def _init_master(self, full32: torch.Tensor) -> None:
+        owned = full32 if self.zero == 0 else full32[self.lo:self.lo + self.shard]
+        self.master = owned.clone()
+        self.m = torch.zeros_like(owned)
+        self.v = torch.zeros_like(owned)
+
+    def materialize(self) -> torch.Tensor:
+        """Full flat parameters (z3: all-gather into a transient buffer)."""
+        if self.zero < 3:
+            return self.p_full
+        if self._gathered is None:
+            self._gathered = comm.all_gather(self.p_shard, self.dp)
+        return self._gathered
+
+    def release(self) -> None:
+        self._gathered = None
+
+    # ------------------------------------------------------------------ grads
+    def grad_target(self) -> torch.Tensor:
+        if self.zero >= 2:
+            return torch.zeros(self.total, dtype=self.grad_dtype, device=self.device)
+        return self.g_full
+
+    def finish_microbatch(self, target: torch.Tensor, tp_partial=(), tp_group=None) -> None:
+        """Fold the fp32 small-entry grads in, and (z>=2) reduce-scatter into the shard."""
+        sg = self.small_grads()
+        for n in tp_partial:
+            if n in sg:
+                comm.all_reduce(sg[n], tp_group)
+        views = self.views(target)
+        for n, g in sg.items():
+            K.axpby(g, views[n], 1.0, 1.0)
+        self.acc32.zero_()
+        if self.zero >= 2:
+            part = comm.reduce_scatter(target, self.dp)
+            K.axpby(part, self.g_shard, 1.0, 1.0)
+
+    def sync(self) -> None:
+        """End of the accumulation window: dp reduction of the gradients."""
+        if self.zero == 0:
+            comm.all_reduce(self.g_full, self.dp)
+            self._owned_grad = self.g_full
+        elif self.zero == 1:
+            self._owned_grad = comm.reduce_scatter(self.g_full, self.dp)
+        else:
+            self._owned_grad = self.g_shard
+
+    def owned_grad(self) -> torch.Tensor:
+        return self._owned_grad
+
+    def zero_grads(self) -> None:
+        if self.g_full is not None:
+            self.g_full.zero_()
+        if self.g_shard is not None:
+            self.g_shard.zero_()
+        self.acc32.zero_()
+        self._owned_grad = None
+
+    def full_grad(self) -> torch.Tensor:
+        """(tests) full flat gradient after sync, gathered across dp shards if needed."""
+        if self.zero == 0:
+            return self.g_full
+        return comm.all_gather(self._owned_grad.contiguous(), self.dp)
+
+    # ------------------------------------------------------------------ optimizer
+    def step(self, *, lr, beta1, beta2, eps, weight_decay, step, grad_scale=1.0) -> None:
+        g = self._owned_grad
+        if self.zero == 3:
+            out = self.p_shard
+        elif self.zero == 0:
+            out = self.p_full
+        else:
+            out = self.p_full[self.lo:self.lo + self.shard]
+        K.adamw(self.master, self.m, self.v, g, out, lr=lr, beta1=beta1, beta2=beta2, eps=eps,
+                weight_decay=weight_decay, step=step, grad_scale=grad_scale)
+        if self.zero in (1, 2):
+            comm.all_gather(out.clone(), self.dp, out=self.p_full)
+
+    def memory_bytes(self) -> dict:
+        def nb(t):
+            return 0 if t is None else t.numel() * t.element_size()
+        return {"param": nb(self.p_full) + nb(getattr(self, "p_shard", None)),
+                "grad": nb(self.g_full) + nb(self.g_shard),
+                "optimizer": nb(self.master) + nb(self.m) + nb(self.v)}
