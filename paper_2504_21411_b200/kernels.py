@@ -88,7 +88,49 @@ def load_library(path: str | os.PathLike | None = None):
     return lib
 
 
+# kernels launched per C-ABI call (for the bench's gpu_launches count)
+KERNELS_PER_CALL = {"galv_attn_bwd": 3}
+
+
+class KernelStats:
+    """Launch counter + optional CUDA-event timing of every GEMM (bench instrumentation)."""
+
+    def __init__(self, time_gemm: bool = False):
+        self.calls: dict = {}
+        self.time_gemm = time_gemm
+        self.gemm_events: list = []   # (flops, start_event, end_event, shape)
+
+    @property
+    def launches(self) -> int:
+        return sum(n * KERNELS_PER_CALL.get(k, 1) for k, n in self.calls.items())
+
+    def gemm_summary(self) -> dict:
+        torch.cuda.synchronize()
+        flops = sum(f for f, _, _, _ in self.gemm_events)
+        ms = sum(a.elapsed_time(b) for _, a, b, _ in self.gemm_events)
+        n = len(self.gemm_events)
+        return {"launches": n, "flops": flops, "ms": ms,
+                "tflops": flops / (ms * 1e-3) / 1e12 if ms else 0.0}
+
+
+_stats: KernelStats | None = None
+
+
+def start_stats(time_gemm: bool = False) -> KernelStats:
+    global _stats
+    _stats = KernelStats(time_gemm)
+    return _stats
+
+
+def stop_stats() -> KernelStats | None:
+    global _stats
+    s, _stats = _stats, None
+    return s
+
+
 def _call(name: str, *args) -> None:
+    if _stats is not None:
+        _stats.calls[name] = _stats.calls.get(name, 0) + 1
     rc = getattr(load_library(), name)(*args)
     if rc != 0:
         msg = load_library().galv_last_error().decode(errors="replace")
@@ -139,10 +181,17 @@ def gemm(a, b, out=None, *, trans_a=False, trans_b=False, alpha=1.0, accumulate=
         out = torch.empty(M, N, device=a.device, dtype=out_dtype or a.dtype)
     if out.shape != (M, N) or out.stride(1) != 1:
         raise RuntimeError("bad gemm output")
+    timed = _stats is not None and _stats.time_gemm
+    if timed:
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record()
     _call("galv_gemm", _ptr(a), _ptr(b), _ptr(out), _ptr(bias), M, N, K, a.stride(0),
           b.stride(0), out.stride(0), int(trans_a), int(trans_b), float(alpha),
           int(accumulate), dtype_code(a.dtype), dtype_code(out.dtype),
           dtype_code(bias.dtype) if bias is not None else F32, _stream())
+    if timed:
+        ev1.record()
+        _stats.gemm_events.append((2.0 * M * N * K, ev0, ev1, (M, N, K)))
     return out
 
 
