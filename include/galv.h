@@ -105,6 +105,11 @@ int32_t galv_rope(void* x, int64_t T, int64_t S, int64_t H, int64_t D, int64_t s
                   int64_t stride_head, int64_t pos0, float theta, int32_t inverse,
                   int32_t dtype, void* stream);
 
+/* Same rotation from a precomputed fp32 table [2][S][D/2] (cos plane, then sin plane). */
+int32_t galv_rope_table(void* x, const float* table, int64_t T, int64_t S, int64_t H, int64_t D,
+                        int64_t stride_tok, int64_t stride_head, int64_t pos0, int32_t inverse,
+                        int32_t dtype, void* stream);
+
 /* SwiGLU on a fused [T, 2F] gate|up tensor -> h [T, F]; backward -> d(gate|up). */
 int32_t galv_swiglu_fwd(const void* gu, void* h, int64_t T, int64_t F, int32_t dtype,
                         void* stream);

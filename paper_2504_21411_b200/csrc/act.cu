@@ -127,6 +127,26 @@ __global__ void axpby_kernel(const TX* __restrict__ x, TY* __restrict__ y, int64
   }
 }
 
+// vectorized variant: 8 elements per thread-iteration (n % 8 == 0, 16B-aligned pointers)
+template <typename TX, typename TY>
+__global__ void axpby_vec8(const TX* __restrict__ x, TY* __restrict__ y, int64_t n8, float a,
+                           float b) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n8;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float xv[8], yv[8];
+#pragma unroll
+    for (int h = 0; h < 8; h += 16 / (int)sizeof(TX)) load16(x + i * 8 + h, xv + h);
+    if (b != 0.f) {
+#pragma unroll
+      for (int h = 0; h < 8; h += 16 / (int)sizeof(TY)) load16(y + i * 8 + h, yv + h);
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) yv[k] = a * xv[k] + (b != 0.f ? b * yv[k] : 0.f);
+#pragma unroll
+    for (int h = 0; h < 8; h += 16 / (int)sizeof(TY)) store16(y + i * 8 + h, yv + h);
+  }
+}
+
 template <typename T>
 __global__ void sumsq_kernel(const T* __restrict__ x, int64_t n, float* out) {
   __shared__ float red[33];
@@ -222,10 +242,15 @@ int32_t galv_axpby(const void* x, void* y, int64_t n, float a, float b, int32_t 
                    int32_t y_dtype, void* stream) {
   GALV_CHECK_ARG(x && y && n >= 0, "bad arguments");
   if (n == 0) return 0;
-  const unsigned g = act::grid_for(n, 256);
+  const bool vec = (n % 8 == 0) && ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15) == 0;
   GALV_DISPATCH(x_dtype, TX, {
     GALV_DISPATCH(y_dtype, TY, {
-      act::axpby_kernel<TX, TY><<<g, 256, 0, as_stream(stream)>>>((const TX*)x, (TY*)y, n, a, b);
+      if (vec)
+        act::axpby_vec8<TX, TY><<<act::grid_for(n / 8, 256), 256, 0, as_stream(stream)>>>(
+            (const TX*)x, (TY*)y, n / 8, a, b);
+      else
+        act::axpby_kernel<TX, TY><<<act::grid_for(n, 256), 256, 0, as_stream(stream)>>>(
+            (const TX*)x, (TY*)y, n, a, b);
     });
   });
   GALV_LAUNCH_CHECK();

@@ -26,6 +26,39 @@ __global__ void adamw_kernel(float* __restrict__ master, float* __restrict__ m,
   }
 }
 
+// 4 parameters per thread-iteration with 16B master/m/v accesses (n % 4 == 0)
+template <typename TG, typename TP>
+__global__ void adamw_vec4(float* __restrict__ master, float* __restrict__ m,
+                           float* __restrict__ v, const TG* __restrict__ g,
+                           TP* __restrict__ pout, int64_t n4, float lr, float b1, float b2,
+                           float eps, float wd, float gscale, float bc1, float bc2) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float4 p4 = reinterpret_cast<float4*>(master)[i];
+    float4 m4 = reinterpret_cast<float4*>(m)[i];
+    float4 v4 = reinterpret_cast<float4*>(v)[i];
+    float gr[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) gr[k] = to_f(g[i * 4 + k]) * gscale;
+    float* pp = &p4.x;
+    float* mm = &m4.x;
+    float* vv = &v4.x;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      mm[k] = b1 * mm[k] + (1.f - b1) * gr[k];
+      vv[k] = b2 * vv[k] + (1.f - b2) * gr[k] * gr[k];
+      pp[k] = pp[k] - lr * ((mm[k] / bc1) / (sqrtf(vv[k] / bc2) + eps) + wd * pp[k]);
+    }
+    reinterpret_cast<float4*>(master)[i] = p4;
+    reinterpret_cast<float4*>(m)[i] = m4;
+    reinterpret_cast<float4*>(v)[i] = v4;
+    if (pout) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) pout[i * 4 + k] = from_f<TP>(pp[k]);
+    }
+  }
+}
+
 }  // namespace opt
 
 namespace rs {
@@ -66,9 +99,14 @@ int32_t galv_adamw(float* master, float* m, float* v, const void* grad, void* pa
   const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, sm_count() * 8);
   GALV_DISPATCH(grad_dtype, TG, {
     GALV_DISPATCH(param_dtype, TP, {
-      opt::adamw_kernel<TG, TP><<<grid, 256, 0, as_stream(stream)>>>(
-          master, m, v, (const TG*)grad, (TP*)param_out, n, lr, beta1, beta2, eps, weight_decay,
-          grad_scale, bc1, bc2);
+      if (n % 4 == 0)
+        opt::adamw_vec4<TG, TP><<<grid, 256, 0, as_stream(stream)>>>(
+            master, m, v, (const TG*)grad, (TP*)param_out, n / 4, lr, beta1, beta2, eps,
+            weight_decay, grad_scale, bc1, bc2);
+      else
+        opt::adamw_kernel<TG, TP><<<grid, 256, 0, as_stream(stream)>>>(
+            master, m, v, (const TG*)grad, (TP*)param_out, n, lr, beta1, beta2, eps,
+            weight_decay, grad_scale, bc1, bc2);
     });
   });
   GALV_LAUNCH_CHECK();

@@ -42,6 +42,7 @@ _SIGS = {
                            _I32),
     "galv_norm_bwd_workspace": ([_I64, _I64], _I64),
     "galv_rope": ([_P, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _F, _I32, _I32, _P], _I32),
+    "galv_rope_table": ([_P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _I32, _I32, _P], _I32),
     "galv_swiglu_fwd": ([_P, _P, _I64, _I64, _I32, _P], _I32),
     "galv_swiglu_bwd": ([_P, _P, _P, _I64, _I64, _I32, _P], _I32),
     "galv_bias_gelu_fwd": ([_P, _P, _P, _I64, _I64, _I32, _P], _I32),
@@ -285,13 +286,29 @@ def layernorm_bwd(x, gamma, mean, rstd, dy, dgamma_acc, dbeta_acc, *, dres=None,
 # ---------------------------------------------------------------------------- pointwise
 
 
+_ROPE_TABLES: dict = {}
+
+
+def rope_table(seq_len, head_dim, theta, device):
+    """fp32 [2, S, D/2] cos/sin planes, computed like the CPU restatement (fp32)."""
+    key = (seq_len, head_dim, float(theta), str(device))
+    t = _ROPE_TABLES.get(key)
+    if t is None:
+        inv = 1.0 / theta ** (torch.arange(0, head_dim, 2, dtype=torch.float32) / head_dim)
+        ang = torch.arange(seq_len, dtype=torch.float32)[:, None] * inv[None, :]
+        t = torch.stack([ang.cos(), ang.sin()]).contiguous().to(device)
+        _ROPE_TABLES[key] = t
+    return t
+
+
 def rope_(x, seq_len, *, theta=10000.0, inverse=False, pos0=0):
     """In place on a [T, H, D] view (T = B*S tokens, token-major)."""
     T, H, D = x.shape
     if x.stride(2) != 1:
         raise RuntimeError("rope needs unit stride in head_dim")
-    _call("galv_rope", _ptr(x), T, seq_len, H, D, x.stride(0), x.stride(1), pos0, float(theta),
-          int(inverse), dtype_code(x.dtype), _stream())
+    table = rope_table(seq_len, D, theta, x.device)
+    _call("galv_rope_table", _ptr(x), _ptr(table), T, seq_len, H, D, x.stride(0), x.stride(1),
+          pos0, int(inverse), dtype_code(x.dtype), _stream())
     return x
 
 

@@ -1,0 +1,84 @@
+"""torchrun worker: multi-GPU runtime parity scenarios vs the CPU oracle.
+
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 tests/mp_parity.py SCENARIO...
+
+Every rank checks the loss and the logical gradients of its own stage's parameters
+against oracle/model_ref.py (fp64) and prints one PASS/FAIL line per scenario.
+"""
+
+import os
+import sys
+
+import torch
+import torch.distributed as dist
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(HERE))
+sys.path.insert(0, HERE)
+
+from parity_harness import run_parity  # noqa: E402
+from paper_2504_21411_b200.planner.search import near_equal_split  # noqa: E402
+from paper_2504_21411_b200.planner.strategy import ParallelStrategy as PS  # noqa: E402
+from paper_2504_21411_b200.runtime.config import HybridConfig  # noqa: E402
+
+
+def hc(strats, *, pp=1, mb=2, m=2):
+    return HybridConfig(pp=pp, microbatch=mb, n_microbatches=m,
+                        stage_ranges=near_equal_split(len(strats), pp),
+                        layer_strategies=tuple(strats))
+
+
+F32, BF16 = torch.float32, torch.bfloat16
+# name -> (world, model, hybrid config, dtype, tolerance)
+SCENARIOS = {
+    "dp2_z0": (2, "micro-llama", hc([PS(1, 2, 0, False, False)] * 2), F32, 1e-5),
+    "dp2_z1": (2, "micro-llama", hc([PS(1, 2, 1, False, False)] * 2), F32, 1e-5),
+    "dp2_z2": (2, "micro-llama", hc([PS(1, 2, 2, False, False)] * 2), F32, 1e-5),
+    "dp2_z3_rc": (2, "micro-llama", hc([PS(1, 2, 3, False, True)] * 2), F32, 1e-5),
+    "tp2": (2, "micro-llama", hc([PS(2, 1, 0, False, False)] * 2), F32, 1e-5),
+    "tp2_sp": (2, "micro-llama", hc([PS(2, 1, 0, True, False)] * 2), F32, 1e-5),
+    "tp2_gpt": (2, "micro-gpt", hc([PS(2, 1, 0, False, False)] * 2), F32, 1e-5),
+    "tp2_sp_gpt_rc": (2, "micro-gpt", hc([PS(2, 1, 0, True, True)] * 2), F32, 1e-5),
+    "pp2": (2, "micro-llama", hc([PS(1, 1, 0, False, False)] * 2, pp=2, m=4), F32, 1e-5),
+    "pp2_gpt": (2, "micro-gpt", hc([PS(1, 1, 0, False, True)] * 2, pp=2, m=3), F32, 1e-5),
+    "mixed2": (2, "tiny-llama", hc([PS(2, 1, 0, True, False), PS(1, 2, 1, False, False),
+                                    PS(2, 1, 0, False, True), PS(1, 2, 3, False, False)]),
+               F32, 1e-5),
+    "mixed2_bf16": (2, "tiny-llama", hc([PS(2, 1, 0, True, False), PS(1, 2, 2, False, True),
+                                         PS(2, 1, 0, False, False), PS(1, 2, 0, False, False)]),
+                    BF16, 2e-2),
+    "tp2dp2": (4, "micro-llama", hc([PS(2, 2, 1, True, False)] * 2, mb=2), F32, 1e-5),
+    "pp2_tp2": (4, "tiny-llama", hc([PS(2, 1, 0, False, False), PS(1, 2, 2, False, False),
+                                     PS(2, 1, 0, True, True), PS(2, 1, 0, False, False)],
+                                    pp=2, m=4), F32, 1e-5),
+    "alt4": (4, "tiny-gpt", hc([PS(4, 1, 0, False, False), PS(1, 4, 3, False, False),
+                                PS(2, 2, 0, True, False), PS(4, 1, 0, True, True)],
+                               mb=4, m=1), F32, 1e-5),
+}
+
+
+def main():
+    local = int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    world = dist.get_world_size()
+    ok = True
+    cache = {}
+    for name in sys.argv[1:]:
+        need, model, cfg_hc, dtype, tol = SCENARIOS[name]
+        if need != world:
+            continue
+        gb = 4 if model.startswith("tiny") else None
+        lerr, errs = run_parity(model, cfg_hc, dtype, grad_bytes=4, oracle_cache=cache)
+        worst = max(errs.items(), key=lambda kv: kv[1]) if errs else ("-", 0.0)
+        good = lerr <= tol and worst[1] <= tol
+        ok &= good
+        print(f"[rank {dist.get_rank()}] {name}: {'PASS' if good else 'FAIL'} loss_err={lerr:.2e} "
+              f"worst={worst[0]}:{worst[1]:.2e} n_params={len(errs)}", flush=True)
+        dist.barrier()
+    dist.destroy_process_group()
+    sys.exit(0 if ok else 1)
+
+
+if __name__ == "__main__":
+    main()

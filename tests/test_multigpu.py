@@ -1,0 +1,35 @@
+"""Multi-GPU runtime parity (torchrun over NCCL) -- needs >= 2 / 4 B200s (gpurun --gpus N)."""
+
+import os
+import subprocess
+import sys
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+TWO = ["dp2_z0", "dp2_z1", "dp2_z2", "dp2_z3_rc", "tp2", "tp2_sp", "tp2_gpt", "tp2_sp_gpt_rc",
+       "pp2", "pp2_gpt", "mixed2", "mixed2_bf16"]
+FOUR = ["tp2dp2", "pp2_tp2", "alt4"]
+
+
+def _run(n, scenarios, port):
+    if torch.cuda.device_count() < n:
+        pytest.skip(f"needs {n} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.join(HERE, "mp_parity.py"), *scenarios]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
+    print(r.stdout[-6000:])
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
+    assert "FAIL" not in r.stdout
+
+
+def test_two_gpu_strategies():
+    _run(2, TWO, 29511)
+
+
+def test_four_gpu_strategies():
+    _run(4, FOUR, 29512)
