@@ -1,0 +1,151 @@
+"""CPU tests of the runtime's host-side logic: C-ABI exports, rank topology, reshard
+plans (pure and executed over a gloo world of 2/4 processes), the 1F1B op order."""
+
+import itertools
+import os
+import re
+import socket
+from pathlib import Path
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2504_21411_b200.planner.pipesim import one_f_one_b_order
+from paper_2504_21411_b200.runtime.reshard import Layout, index_tensors, plan_transition
+from paper_2504_21411_b200.runtime.topology import dp_members, tp_members
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def test_library_exports_every_header_symbol():
+    import ctypes
+    from paper_2504_21411_b200 import kernels
+    lib_path = kernels.LIB_PATH
+    if not lib_path.exists():
+        from paper_2504_21411_b200.build import build
+        build()
+    header = (ROOT / "include" / "galv.h").read_text()
+    declared = sorted(set(re.findall(r"\b(galv_[a-z0-9_]+)\s*\(", header)))
+    assert len(declared) >= 25
+    lib = ctypes.CDLL(str(lib_path))
+    missing = [s for s in declared if not hasattr(lib, s)]
+    assert not missing, missing
+    assert set(declared) <= set(kernels.EXPORTED), set(declared) - set(kernels.EXPORTED)
+    lib.galv_abi_version.restype = ctypes.c_int32
+    assert lib.galv_abi_version() == 1
+
+
+def test_kernels_refuse_cpu_tensors():
+    from paper_2504_21411_b200 import kernels as K
+    with pytest.raises(RuntimeError):
+        K.gemm(torch.zeros(8, 8), torch.zeros(8, 8))
+
+
+def test_topology_members_contiguous():
+    # stage 1 of a 2-stage, 8-device-per-stage layout, tp=2
+    assert tp_members(1, 8, 2, 3) == [14, 15]
+    assert dp_members(1, 8, 2, 1) == [9, 11, 13, 15]
+    assert dp_members(0, 4, 4, 2) == [2]
+
+
+LAYOUTS = {n: [Layout(tp, n // tp, sp) for tp in (1, 2, 4, 8) if tp <= n
+               for sp in (False, True) if not (sp and tp == 1)] for n in (1, 2, 4, 8)}
+
+
+@pytest.mark.parametrize("n", [2, 4, 8])
+def test_reshard_plans_cover_every_row_exactly(n):
+    T = 64
+    data = torch.arange(T)
+    for src, dst in itertools.product(LAYOUTS[n], LAYOUTS[n]):
+        plan = plan_transition(src, dst, T)
+        held = [data[slice(*src.token_range(i, T))] for i in range(n)]
+        for j in range(n):
+            lo, hi = dst.token_range(j, T)
+            out = torch.full((hi - lo,), -1)
+            for i in range(n):
+                s, r = plan.send_rows[i][j], plan.recv_rows[j][i]
+                assert s[1] - s[0] == r[1] - r[0]
+                out[r[0]:r[1]] = held[i][s[0]:s[1]]
+            assert torch.equal(out, data[lo:hi]), (src, dst, j)
+        # replicas -> their own slices never need the network
+        if src.tp == dst.tp * dst.dp and not src.sp and src.dp == 1:
+            assert not plan.moves_data
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _reshard_worker(rank, world, port, pairs, T, h):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    full = torch.arange(T * h, dtype=torch.float32).view(T, h)
+    for src, dst in pairs:
+        plan = plan_transition(src, dst, T)
+        sidx, ss, ridx, rs = index_tensors(plan, rank, "cpu")
+        x = full[slice(*src.token_range(rank, T))]
+        send = x.index_select(0, sidx)                    # pack (galv_gather_rows on GPU)
+        recv = torch.empty(sum(rs), h)
+        dist.all_to_all_single(recv, send, rs, ss)        # the single collective
+        lo, hi = dst.token_range(rank, T)
+        out = torch.empty(hi - lo, h)
+        out.index_copy_(0, ridx, recv)                    # unpack (galv_scatter_rows on GPU)
+        assert torch.equal(out, full[lo:hi]), (rank, src, dst)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_reshard_over_gloo(world):
+    pairs = list(itertools.product(LAYOUTS[world], LAYOUTS[world]))
+    mp.spawn(_reshard_worker, args=(world, _free_port(), pairs, 32, 8), nprocs=world, join=True)
+
+
+def _topology_worker(rank, world, port):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2504_21411_b200.planner.strategy import ParallelStrategy as PS
+    from paper_2504_21411_b200.runtime.config import HybridConfig
+    from paper_2504_21411_b200.runtime.topology import Topology
+    hc = HybridConfig(pp=1, microbatch=2, n_microbatches=1, stage_ranges=((0, 2),),
+                      layer_strategies=(PS(2, 1, 0, False, False), PS(1, 2, 1, False, False)))
+    topo = Topology(hc)
+    t = torch.tensor([float(rank + 1)])
+    from paper_2504_21411_b200.runtime import comm
+    comm.all_reduce(t, topo.tp(2))
+    assert t.item() == 3.0
+    u = torch.tensor([float(rank + 1)])
+    comm.all_reduce(u, topo.dp(1))
+    assert u.item() == 3.0
+    assert topo.tp(1).size == 1 and topo.dp(2).size == 1
+    dist.destroy_process_group()
+
+
+def test_topology_groups_over_gloo():
+    mp.spawn(_topology_worker, args=(2, _free_port()), nprocs=2, join=True)
+
+
+@pytest.mark.parametrize("pp,m", [(1, 4), (2, 4), (4, 8), (4, 2)])
+def test_1f1b_order_is_complete_and_causal(pp, m):
+    for stage in range(pp):
+        ops = one_f_one_b_order(pp, stage, m)
+        assert sorted(k for kind, k in ops if kind == "fwd") == list(range(1, m + 1))
+        assert sorted(k for kind, k in ops if kind == "bwd") == list(range(1, m + 1))
+        seen_f = set()
+        live = 0
+        for kind, k in ops:
+            if kind == "fwd":
+                seen_f.add(k)
+                live += 1
+            else:
+                assert k in seen_f
+                live -= 1
+            assert live <= min(m, pp - stage)
