@@ -1,0 +1,173 @@
+"""B200 profiler: measures this box and writes the planner's profile JSON.
+
+The reference ingests profiles (SPEC.md:8 puts measurement out of scope); this module
+is the paper's "Profiler" for B200, writing exactly the reference
+schema (profiles.py:233-422) so the unchanged search consumes it:
+
+* ``device_flops``: the *effective* rate at which the runtime executes a decoder
+  layer's cost-model FLOPs.  One layer of the target model is run fwd+bwd on galv
+  kernels at the given microbatch, and device_flops = 3 * fwd_flops / t(fwd+bwd),
+  with fwd_flops = flops_per_token * t + flops_per_token_sq * b * s^2 exactly as the
+  cost model counts them (costmodel.py:104-106).  Calibration happens only through
+  this profile input; the cost model itself is unchanged.
+* ``bandwidth_table``: NCCL bus bandwidth per group size g (all-reduce busbw
+  convention 2(g-1)/g * V / t, all-gather (g-1)/g * V / t; the table keeps the
+  smaller of the two so the model's ring passes are not optimistic) and an alpha fitted
+  from a small message so lat*(g-1) reproduces it (collectives.py:49-57).
+  Requires torchrun with >= 2 ranks; on one GPU the table is left to the caller.
+* ``device_memory_bytes``: total HBM; ``memory_reserve_fraction`` covers the CUDA
+  context, allocator fragmentation, logits and transient buffers the model ignores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import time
+
+import torch
+import torch.distributed as dist
+
+from .planner import profiles as P
+from .planner.strategy import ParallelStrategy
+
+
+def _time_cuda(fn, iters: int = 5, warmup: int = 2) -> float:
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(iters):
+        fn()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / iters / 1e3
+
+
+def measure_layer_flops(cfg, microbatch: int, *, iters: int = 3) -> dict:
+    """Effective FLOP/s of one decoder layer fwd+bwd (tp=1, dp=1) on this GPU."""
+    from .runtime.config import HybridConfig, profile_for
+    from .runtime.layers import DecoderLayer
+    from .runtime.topology import Topology
+    one = cfg.with_(n_layers=1)
+    s = ParallelStrategy(1, 1, 0, False, False)
+    hc = HybridConfig(pp=1, microbatch=microbatch, n_microbatches=1, stage_ranges=((0, 1),),
+                      layer_strategies=(s,))
+    topo = Topology(hc, rank=0, world=1)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    layer = DecoderLayer(one, 0, s, topo, dtype=torch.bfloat16, grad_dtype=torch.bfloat16,
+                         device=dev)
+    from .runtime.init import layer_param_shapes
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(0)
+    layer.store.load({n: 0.02 * torch.randn(shp, generator=gen, device=dev)
+                      if not n.endswith("norm.weight") else torch.ones(shp, device=dev)
+                      for n, shp in layer_param_shapes(one).items()})
+    T = microbatch * cfg.seq_len
+    x = torch.randn(T, cfg.hidden, device=dev, dtype=torch.bfloat16)
+    dy = torch.randn_like(x) * 1e-3
+
+    def step():
+        y, ctx = layer.forward(x, microbatch)
+        layer.backward(dy, ctx)
+
+    t = _time_cuda(step, iters=iters)
+    lp = profile_for(cfg).layers[0]
+    fwd_flops = lp.flops_per_token * T + lp.flops_per_token_sq * microbatch * cfg.seq_len ** 2
+    return {"seconds_fwd_bwd": t, "fwd_flops": fwd_flops,
+            "device_flops": 3.0 * fwd_flops / t}
+
+
+def measure_collectives(sizes=(2 ** 20, 2 ** 24, 2 ** 28)) -> dict:
+    """busbw (bytes/s) and alpha per contiguous group size; rank 0 returns the table."""
+    world = dist.get_world_size()
+    rank = dist.get_rank()
+    out = {}
+    g = 2
+    while g <= world:
+        members = [list(range(s, s + g)) for s in range(0, world, g)]
+        groups = [dist.new_group(m) for m in members]
+        grp = groups[rank // g]
+        res = {}
+        for nbytes in sizes:
+            n = nbytes // 2
+            x = torch.ones(n, dtype=torch.bfloat16, device="cuda")
+            y = torch.empty(n * 1, dtype=torch.bfloat16, device="cuda")
+            t_ar = _time_cuda(lambda: dist.all_reduce(x, group=grp), iters=10)
+            chunk = torch.ones(n // g, dtype=torch.bfloat16, device="cuda")
+            t_ag = _time_cuda(lambda: dist.all_gather_into_tensor(y, chunk, group=grp), iters=10)
+            res[nbytes] = (t_ar, t_ag)
+        big = sizes[-1]
+        t_ar, t_ag = res[big]
+        bw_ar = 2 * (g - 1) / g * big / t_ar
+        bw_ag = (g - 1) / g * big / t_ag
+        bw = min(bw_ar, bw_ag)
+        small_t = res[sizes[0]][1]
+        lat = max(small_t - (g - 1) / g * sizes[0] / bw, 0.0) / (g - 1)
+        out[g] = {"bus_bandwidth": bw, "latency": lat, "ar_busbw": bw_ar, "ag_busbw": bw_ag}
+        g *= 2
+    return out
+
+
+def build_cluster(n_devices: int, device_flops: float, table: dict, *,
+                  reserve: float = 0.1) -> P.ClusterProfile:
+    mem = torch.cuda.get_device_properties(0).total_memory if torch.cuda.is_available() \
+        else 180_000_000_000
+    entries = tuple(P.BandwidthEntry("intra_node", g, v["bus_bandwidth"], v["latency"])
+                    for g, v in sorted(table.items()))
+    c = P.ClusterProfile(n_devices, min(n_devices, 8), float(device_flops), int(mem), reserve,
+                         entries)
+    c.validate()
+    return c
+
+
+def main(argv=None) -> int:
+    ap = argparse.ArgumentParser(prog="galv-profile")
+    ap.add_argument("-o", "--output", required=True)
+    ap.add_argument("--model", default="llama2-7b")
+    ap.add_argument("--microbatch", type=int, default=2)
+    ap.add_argument("--devices", type=int, default=8, help="n_devices written to the profile")
+    ap.add_argument("--reserve", type=float, default=0.1)
+    ap.add_argument("--table-from", default=None, help="reuse the bandwidth table of a profile")
+    args = ap.parse_args(argv)
+    from .runtime.config import MODEL_PRESETS
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    table = {}
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        table = measure_collectives()
+    elif args.table_from:
+        c = P.load_cluster_profile(args.table_from)
+        table = {e.group_size: {"bus_bandwidth": e.bus_bandwidth, "latency": e.latency}
+                 for e in c.bandwidth_table if e.span == "intra_node"}
+    rank = dist.get_rank() if world > 1 else 0
+    if rank == 0:
+        lay = measure_layer_flops(MODEL_PRESETS[args.model], args.microbatch)
+        if not table:  # single GPU: NVLink table from the pool's published measurements
+            table = {g: {"bus_bandwidth": 725e9, "latency": 5e-6} for g in (2, 4, 8)}
+        cluster = build_cluster(args.devices, lay["device_flops"], table, reserve=args.reserve)
+        P.save_profiles(args.output, cluster=cluster)
+        meta = {"layer": lay, "table": {str(k): v for k, v in table.items()},
+                "model": args.model, "microbatch": args.microbatch, "world": world}
+        with open(os.path.splitext(args.output)[0] + ".meta.json", "w") as fh:
+            json.dump(meta, fh, indent=1)
+        print(json.dumps(meta))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def run_profile_cli(args) -> int:
+    """``hybridplan profile`` -> measure this GPU (and NCCL when under torchrun)."""
+    return main(["-o", args.output, "--model", {"llama": "llama2-7b", "gpt": "gpt2-medium"}
+                 [args.arch], "--devices", str(args.devices)])
+
+
+if __name__ == "__main__":
+    sys.exit(main())
