@@ -6,6 +6,8 @@
 // Backward is two deterministic kernels (no fp32 atomics): dK/dV per key block and dQ
 // per query block, each recomputing P from the saved logsumexp.
 // fp32 path: exact SIMT kernels (thread per row) for the fp32 parity configuration.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace galv {
@@ -668,6 +670,17 @@ static int32_t set_smem(K kernel, size_t bytes) {
   return 0;
 }
 
+namespace galv {
+int32_t attn_fwd_sm100(const void* q, const void* k, const void* v, void* o, float* lse,
+                       int64_t B, int64_t S, int64_t H, int64_t D, int64_t st, int64_t sh,
+                       int64_t ost, float scale, int32_t causal, cudaStream_t stream);
+int64_t attn_bwd_ws_sm100(int64_t B, int64_t S, int64_t H);
+int32_t attn_bwd_sm100(const void* q, const void* k, const void* v, const void* o,
+                       const void* dout, const float* lse, void* dq, void* dk, void* dv,
+                       int64_t B, int64_t S, int64_t H, int64_t D, int64_t st, int64_t sh,
+                       int64_t ost, float scale, int32_t causal, void* ws, cudaStream_t stream);
+}
+
 extern "C" {
 
 int32_t galv_attn_fwd(const void* q, const void* k, const void* v, void* o, float* lse, int64_t B,
@@ -679,6 +692,8 @@ int32_t galv_attn_fwd(const void* q, const void* k, const void* v, void* o, floa
   cudaStream_t s = as_stream(stream);
   if (dtype == GALV_BF16) {
     GALV_CHECK_ARG(st % 8 == 0 && sh % 8 == 0 && ost % 8 == 0, "strides must be multiples of 8");
+    if (getenv("GALV_ATTN_MMA_SYNC") == nullptr)  // tcgen05 path (default)
+      return attn_fwd_sm100(q, k, v, o, lse, B, S, H, D, st, sh, ost, scale, causal, s);
     const size_t smem = 5 * attn::BLK * D * 2;
     if (D == 64) {
       if (int32_t rc = set_smem(attn::fwd_bf16<64>, smem)) return rc;
@@ -706,7 +721,7 @@ int32_t galv_attn_fwd(const void* q, const void* k, const void* v, void* o, floa
 
 int64_t galv_attn_bwd_workspace(int64_t B, int64_t S, int64_t H, int64_t D, int32_t dtype) {
   (void)D;
-  (void)dtype;
+  if (dtype == GALV_BF16) return galv::attn_bwd_ws_sm100(B, S, H);
   return B * H * S * (int64_t)sizeof(float);
 }
 
@@ -722,6 +737,9 @@ int32_t galv_attn_bwd(const void* q, const void* k, const void* v, const void* o
   const dim3 gdot((unsigned)((S * H + 3) / 4), (unsigned)B);
   if (dtype == GALV_BF16) {
     GALV_CHECK_ARG(st % 8 == 0 && sh % 8 == 0 && ost % 8 == 0, "strides must be multiples of 8");
+    if (getenv("GALV_ATTN_MMA_SYNC") == nullptr)  // tcgen05 path (default)
+      return attn_bwd_sm100(q, k, v, o, dout, lse, dq, dk, dv, B, S, H, D, st, sh, ost, scale,
+                            causal, ws, s);
     attn::bwd_dot<__nv_bfloat16><<<gdot, 128, 0, s>>>(
         (const __nv_bfloat16*)o, (const __nv_bfloat16*)dout, dvec, (int)S, (int)H, (int)D, ost, sh);
     const size_t smem_kv = 6 * attn::BLK * D * 2 + 4 * attn::BLK * sizeof(float);

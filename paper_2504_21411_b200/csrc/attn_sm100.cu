@@ -1,0 +1,862 @@
+// tcgen05 flash-attention forward for sm_100a (bf16 in, fp32 softmax/accumulate).
+//
+// CTA = 128 queries of one (batch, head); K/V streamed in 128-key blocks by TMA into a
+// 2-stage ring; S = Q K^T and O += P V on the 5th-gen tensor cores with accumulators in
+// TMEM (S double-buffered: cols [0,128) and [128,256); O at cols [256, 256+D)).
+//   warp 0   : TMA producer (Q once, K/V ring; 3-D maps over [tokens, heads, head_dim])
+//   warp 1   : MMA issuer; issues S_{j+1} before PV_j so QK^T overlaps the softmax
+//   warp 2   : TMEM allocator
+//   warps 4-7: softmax -- thread = query row = TMEM lane; online softmax with a lazy
+//              rescale (O in TMEM is rescaled only when a row max grows by > 2^8),
+//              P written to smem as a 128B-swizzled K-major bf16 operand, epilogue.
+#include "common.cuh"
+#include "sm100.cuh"
+
+namespace galv {
+namespace fa {
+using namespace sm100;
+
+constexpr int BQ = 128, BKV = 128;
+constexpr float LOG2E = 1.4426950408889634f;
+constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 units
+
+template <int D>
+struct Smem {
+  static constexpr int TILE = D * BQ * 2;        // one [128 rows][D] bf16 tile
+  static constexpr int Q = 0;
+  static constexpr int K0 = Q + TILE;
+  static constexpr int V0 = K0 + 2 * TILE;
+  static constexpr int P = V0 + 2 * TILE;
+  static constexpr int BAR = P + BQ * BKV * 2;   // 32 KB of P
+  static constexpr int BYTES = BAR + 128 + 3 * 1024 + 1024;  // barriers, xch, slack
+};
+
+struct FwdParams {
+  int S, H, n_qblocks;
+  int causal;
+  float scale_log2;
+  __nv_bfloat16* o;
+  float* lse;
+  long long o_st;  // o token stride (elements)
+  long long sh;    // head stride (elements)
+};
+
+// 2^x on the FMA/ALU pipes (Cody-Waite split + degree-4 minimax, rel err 5e-6): used for
+// half of the softmax exponentials so the MUFU (XU) pipe is not the bottleneck.
+__device__ __forceinline__ float exp2_fma(float x) {
+  const float xc = fmaxf(x, -125.f);
+  const float magic = 12582912.f;  // 1.5 * 2^23: rounds to an integer in the low bits
+  const float r = xc + magic;
+  const float n = r - magic;
+  const float f = xc - n;  // [-0.5, 0.5]
+  float p = fmaf(0.009554105163799703f, f, 0.05587040851370001f);
+  p = fmaf(p, f, 0.24024696601651352f);
+  p = fmaf(p, f, 0.6931280281735204f);
+  p = fmaf(p, f, 0.9999994397927999f);
+  const int bits = __float_as_int(p) + (__float_as_int(r) << 23);
+  return x < -125.f ? 0.f : __int_as_float(bits);
+}
+__device__ __forceinline__ float exp2_mufu(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__device__ __forceinline__ uint32_t pack2(float a, float b) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+template <int D>
+__global__ void __launch_bounds__(384, 1)
+    fwd_tc(const __grid_constant__ CUtensorMap mq, const __grid_constant__ CUtensorMap mk,
+           const __grid_constant__ CUtensorMap mv, const FwdParams p) {
+  using L = Smem<D>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                           ~uintptr_t(1023));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::BAR);
+  uint64_t* q_full = bar + 0;
+  uint64_t* k_full = bar + 1;    // [2]
+  uint64_t* v_full = bar + 3;    // [2]
+  uint64_t* kv_empty = bar + 5;  // [2]
+  uint64_t* s_full = bar + 7;    // [2]
+  uint64_t* s_empty = bar + 9;   // [2]
+  uint64_t* p_full = bar + 11;
+  uint64_t* o_done = bar + 12;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 14);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int qb = p.n_qblocks - 1 - blockIdx.x;  // heavy causal blocks first
+  const int bh = blockIdx.y, b = bh / p.H, h = bh % p.H;
+  const int q0 = qb * BQ;
+  const int n_kv = p.causal ? min(qb + 1, (p.S + BKV - 1) / BKV) : (p.S + BKV - 1) / BKV;
+  const int tok0 = b * p.S;
+
+  if (threadIdx.x == 0) {
+    mbar_init(q_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&k_full[i], 1);
+      mbar_init(&v_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+      mbar_init(&s_full[i], 1);
+      mbar_init(&s_empty[i], 256);
+    }
+    mbar_init(p_full, 256);
+    mbar_init(o_done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    fence_async_smem();
+    prefetch_map(&mq);
+    prefetch_map(&mk);
+    prefetch_map(&mv);
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t t_s = tmem, t_o = tmem + 256;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      constexpr uint32_t TILE_BYTES = L::TILE;
+      mbar_expect_tx(q_full, TILE_BYTES);
+#pragma unroll
+      for (int c = 0; c < D / 64; ++c)
+        tma_load_3d(&mq, q_full, sm + L::Q + c * 16384, c * 64, h, tok0 + q0);
+      for (int j = 0; j < n_kv; ++j) {
+        const int st = j & 1;
+        mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
+        mbar_expect_tx(&k_full[st], TILE_BYTES);
+#pragma unroll
+        for (int c = 0; c < D / 64; ++c)
+          tma_load_3d(&mk, &k_full[st], sm + L::K0 + st * L::TILE + c * 16384, c * 64, h,
+                      tok0 + j * BKV);
+        mbar_expect_tx(&v_full[st], TILE_BYTES);
+#pragma unroll
+        for (int c = 0; c < D / 64; ++c)
+          tma_load_3d(&mv, &v_full[st], sm + L::V0 + st * L::TILE + c * 16384, c * 64, h,
+                      tok0 + j * BKV);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t id_s = make_idesc(BQ, BKV, 0, 0);  // Q (K-major) x K (K-major)
+      const uint32_t id_o = make_idesc(BQ, D, 0, 1);    // P (K-major) x V (MN-major)
+      const uint32_t a_q = smem_u32(sm + L::Q), a_p = smem_u32(sm + L::P);
+      mbar_wait(q_full, 0);
+      auto issue_pv = [&](int j) {
+        const int st = j & 1;
+        mbar_wait(p_full, j & 1);
+        mbar_wait(&v_full[st], (j >> 1) & 1);
+        tc_fence_after();
+        const uint32_t b_v = smem_u32(sm + L::V0 + st * L::TILE);
+#pragma unroll
+        for (int k = 0; k < BKV / 16; ++k) {
+          const uint64_t ad = sdesc(a_p + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024);
+          const uint64_t bd = sdesc(b_v + k * 2048, 16384, 1024);
+          umma_bf16(t_o, ad, bd, id_o, (j | k) != 0);
+        }
+        umma_commit(o_done);
+        umma_commit(&kv_empty[st]);
+      };
+      for (int j = 0; j < n_kv; ++j) {
+        const int st = j & 1;
+        mbar_wait(&k_full[st], (j >> 1) & 1);
+        mbar_wait(&s_empty[st], ((j >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t b_k = smem_u32(sm + L::K0 + st * L::TILE);
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k) {
+          const uint32_t off = (k >> 2) * 16384 + (k & 3) * 32;
+          umma_bf16(t_s + st * BKV, sdesc(a_q + off, 16, 1024), sdesc(b_k + off, 16, 1024),
+                    id_s, k != 0);
+        }
+        umma_commit(&s_full[st]);
+        if (j > 0) issue_pv(j - 1);
+      }
+      issue_pv(n_kv - 1);
+    }
+  } else if (warp >= 4) {
+    // softmax: warps 4..11; quarter q = warp % 4 owns TMEM lanes (rows) [32q, 32q+32),
+    // half = (warp - 4) / 4 owns key columns [64*half, 64*half + 64) of every S block and
+    // O columns [half*D/2, half*D/2 + D/2).  Row maxima are exchanged through smem.
+    const int q = warp & 3, half = (warp - 4) >> 2;
+    const int r = q * 32 + lane;
+    const int qi = q0 + r;
+    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    float* xch = reinterpret_cast<float*>(bar + 16);  // [2][128] partial maxima / sums
+    float m_used = -INFINITY, l = 0.f;
+    uint8_t* prow = sm + L::P + half * 16384 + r * 128;
+    constexpr int HC = BKV / 2;  // columns per half
+    for (int j = 0; j < n_kv; ++j) {
+      const int st = j & 1;
+      mbar_wait(&s_full[st], (j >> 1) & 1);
+      tc_fence_after();
+      float s[HC];
+#pragma unroll
+      for (int c = 0; c < HC / 32; ++c)
+        tmem_ld32_nowait(t_s + st * BKV + half * HC + c * 32 + lane_off,
+                         reinterpret_cast<uint32_t*>(s) + c * 32);
+      tmem_wait_ld();
+      tc_fence_before();
+      mbar_arrive(&s_empty[st]);
+      const int k0 = j * BKV + half * HC;
+      const bool mask = (k0 + HC > p.S) || (p.causal && k0 + HC - 1 > q0);
+      float mx = -INFINITY;
+#pragma unroll
+      for (int i = 0; i < HC; ++i) {
+        if (mask && (k0 + i >= p.S || (p.causal && k0 + i > qi))) s[i] = -INFINITY;
+        mx = fmaxf(mx, s[i]);
+      }
+      // combine the two halves' row maxima (pair barrier: 64 threads of this quarter)
+      xch[(j & 1) * 256 + half * 128 + r] = mx;
+      asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
+      mx = fmaxf(mx, xch[(j & 1) * 256 + (half ^ 1) * 128 + r]);
+      mx *= p.scale_log2;
+      float alpha = 1.f;
+      if ((mx > m_used + RESCALE_THRESHOLD || m_used == -INFINITY) && mx != -INFINITY) {
+        alpha = (m_used == -INFINITY) ? 0.f : exp2f(m_used - mx);
+        m_used = mx;
+      }
+      const float mu = (m_used == -INFINITY) ? 0.f : m_used;
+      float rs = 0.f;
+      uint32_t pk[HC / 2];
+#pragma unroll
+      for (int i = 0; i < HC; i += 2) {
+        const float p0 = exp2_mufu(fmaf(s[i], p.scale_log2, -mu));
+        const float p1 = exp2_mufu(fmaf(s[i + 1], p.scale_log2, -mu));
+        rs += p0 + p1;
+        pk[i / 2] = pack2(p0, p1);
+      }
+      l = l * alpha + rs;
+      if (j > 0) mbar_wait(o_done, (j - 1) & 1);
+      tc_fence_after();
+      if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
+#pragma unroll 1
+        for (int c = 0; c < D / 64; ++c) {
+          uint32_t ov[32];
+          const uint32_t ta = t_o + half * (D / 2) + c * 32 + lane_off;
+          tmem_ld32(ta, ov);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * alpha);
+          tmem_st32(ta, ov);
+        }
+      }
+      // P half-row -> smem chunk `half` (keys 64*half..), K-major SW128
+#pragma unroll
+      for (int u = 0; u < HC / 8; ++u) {
+        const int unit = u ^ (r & 7);
+        uint4 v4 = make_uint4(pk[u * 4], pk[u * 4 + 1], pk[u * 4 + 2], pk[u * 4 + 3]);
+        *reinterpret_cast<uint4*>(prow + unit * 16) = v4;
+      }
+      fence_async_smem();
+      tc_fence_before();
+      mbar_arrive(p_full);
+    }
+    // full row sum = both halves
+    xch[512 + half * 128 + r] = l;
+    asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
+    l += xch[512 + (half ^ 1) * 128 + r];
+    mbar_wait(o_done, (n_kv - 1) & 1);
+    tc_fence_after();
+    const float inv_l = l > 0.f ? 1.f / l : 0.f;
+    __nv_bfloat16* orow = p.o + (long long)(tok0 + qi) * p.o_st + (long long)h * p.sh + half * (D / 2);
+#pragma unroll 1
+    for (int c = 0; c < D / 64; ++c) {
+      uint32_t ov[32];
+      tmem_ld32(t_o + half * (D / 2) + c * 32 + lane_off, ov);
+      if (qi < p.S) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          uint4 w;
+          w.x = pack2(__uint_as_float(ov[u * 8 + 0]) * inv_l, __uint_as_float(ov[u * 8 + 1]) * inv_l);
+          w.y = pack2(__uint_as_float(ov[u * 8 + 2]) * inv_l, __uint_as_float(ov[u * 8 + 3]) * inv_l);
+          w.z = pack2(__uint_as_float(ov[u * 8 + 4]) * inv_l, __uint_as_float(ov[u * 8 + 5]) * inv_l);
+          w.w = pack2(__uint_as_float(ov[u * 8 + 6]) * inv_l, __uint_as_float(ov[u * 8 + 7]) * inv_l);
+          *reinterpret_cast<uint4*>(orow + c * 32 + u * 8) = w;
+        }
+      }
+    }
+    if (qi < p.S && half == 0)
+      p.lse[((long long)b * p.H + h) * p.S + qi] =
+          (m_used + log2f(l)) * 0.6931471805599453f;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+// ---------------------------------------------------------------- backward
+// Two deterministic kernels (no atomics), both on tcgen05 with 8 math warps:
+//   dkdv: CTA = 128 keys; per 64-query step  S^T = K Q^T, dP^T = V dO^T (TMEM, double
+//         buffered), P^T / dS^T -> smem (bf16, K-major), dV += P^T dO, dK += dS^T Q (TMEM)
+//   dq:   CTA = 128 queries; per 64-key step S = Q K^T, dP = dO V^T, dS -> smem,
+//         dQ += dS K (TMEM)
+// Q/dO (resp. K/V) tiles are loaded once by TMA and read as K-major operands for the
+// score GEMMs and as MN-major operands for the gradient GEMMs (same bytes).
+// lse*log2(e) and D = rowsum(dO*O) come from a padded workspace written by bwd_prep
+// (padded rows: lse2 = +inf so their P is exactly 0).
+
+__global__ void bwd_prep(const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ dout,
+                         const float* __restrict__ lse, float* __restrict__ lse2,
+                         float* __restrict__ dvec, int S, int S_pad, int H, int D, long long ost,
+                         long long sh) {
+  const long long row = (long long)blockIdx.x * 4 + (threadIdx.x >> 5);  // over B*H*S_pad
+  const int lane = threadIdx.x & 31;
+  const int bh = (int)(row / S_pad), i = (int)(row % S_pad);
+  const int b = bh / H, h = bh % H;
+  float s = 0.f;
+  if (i < S) {
+    const __nv_bfloat16* orow = o + ((long long)b * S + i) * ost + (long long)h * sh;
+    const __nv_bfloat16* drow = dout + ((long long)b * S + i) * ost + (long long)h * sh;
+    for (int d = lane * 8; d < D; d += 256) {
+      float a[8], c[8];
+      load16(orow + d, a);
+      load16(drow + d, c);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) s += a[e] * c[e];
+    }
+  }
+  s = warp_sum(s);
+  if (lane == 0) {
+    dvec[row] = i < S ? s : 0.f;
+    lse2[row] = i < S ? lse[(long long)bh * S + i] * LOG2E : INFINITY;
+  }
+}
+
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes,
+                                          uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+
+struct BwdParams {
+  int S, S_pad, H;
+  int causal;
+  float scale, scale_log2;
+  const float* lse2;
+  const float* dvec;
+  __nv_bfloat16* g0;   // dkdv: dk ; dq: dq
+  __nv_bfloat16* g1;   // dkdv: dv
+  long long st, sh;    // output (q layout) strides
+};
+
+template <int D>
+struct SmemKV {
+  static constexpr int KT = D * 128 * 2, QT = D * 64 * 2;
+  static constexpr int K = 0, V = KT, Q0 = 2 * KT, O0 = Q0 + 2 * QT;
+  static constexpr int PT = O0 + 2 * QT, DST = PT + 128 * 64 * 2;
+  static constexpr int LSE = DST + 128 * 64 * 2, DV = LSE + 2 * 64 * 4;
+  static constexpr int BAR = DV + 2 * 64 * 4;
+  static constexpr int BYTES = BAR + 256 + 1024;
+};
+
+// rows of a half-row (32 values) -> bf16 into a K-major SW128 [rows][64] tile
+__device__ __forceinline__ void store_half_row(uint8_t* tile, int r, int half, const float* v) {
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    uint4 w = make_uint4(pack2(v[u * 8 + 0], v[u * 8 + 1]), pack2(v[u * 8 + 2], v[u * 8 + 3]),
+                         pack2(v[u * 8 + 4], v[u * 8 + 5]), pack2(v[u * 8 + 6], v[u * 8 + 7]));
+    *reinterpret_cast<uint4*>(tile + r * 128 + (((half * 4 + u) ^ (r & 7)) * 16)) = w;
+  }
+}
+
+__device__ __forceinline__ void store_row_out(__nv_bfloat16* dst, uint32_t taddr, float mul,
+                                              bool write) {
+  uint32_t ov[32];
+  tmem_ld32(taddr, ov);  // warp-collective: every lane loads, only valid rows store
+  if (!write) return;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    uint4 w;
+    w.x = pack2(__uint_as_float(ov[u * 8 + 0]) * mul, __uint_as_float(ov[u * 8 + 1]) * mul);
+    w.y = pack2(__uint_as_float(ov[u * 8 + 2]) * mul, __uint_as_float(ov[u * 8 + 3]) * mul);
+    w.z = pack2(__uint_as_float(ov[u * 8 + 4]) * mul, __uint_as_float(ov[u * 8 + 5]) * mul);
+    w.w = pack2(__uint_as_float(ov[u * 8 + 6]) * mul, __uint_as_float(ov[u * 8 + 7]) * mul);
+    *reinterpret_cast<uint4*>(dst + u * 8) = w;
+  }
+}
+
+template <int D>
+__global__ void __launch_bounds__(384, 1)
+    bwd_dkdv_tc(const __grid_constant__ CUtensorMap mq, const __grid_constant__ CUtensorMap mk,
+                const __grid_constant__ CUtensorMap mv, const __grid_constant__ CUtensorMap mdo,
+                const BwdParams p) {
+  using L = SmemKV<D>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                           ~uintptr_t(1023));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::BAR);
+  uint64_t* kv_full = bar + 0;
+  uint64_t* q_full = bar + 1;    // [2]
+  uint64_t* q_empty = bar + 3;   // [2]
+  uint64_t* st_full = bar + 5;   // [2]
+  uint64_t* st_empty = bar + 7;  // [2]
+  uint64_t* p_full = bar + 9;
+  uint64_t* mm_done = bar + 10;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 12);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kb = blockIdx.x;
+  const int bh = blockIdx.y, b = bh / p.H, h = bh % p.H;
+  const int k0 = kb * 128, tok0 = b * p.S;
+  const int n_qb = (p.S + 63) / 64;
+  const int i0 = p.causal ? (k0 / 64) : 0;
+  const int n_it = n_qb - i0;
+  if (threadIdx.x == 0) {
+    mbar_init(kv_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&q_full[i], 1);
+      mbar_init(&q_empty[i], 1);
+      mbar_init(&st_full[i], 1);
+      mbar_init(&st_empty[i], 256);
+    }
+    mbar_init(p_full, 256);
+    mbar_init(mm_done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    fence_async_smem();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t t_dv = tmem + 256, t_dk = tmem + 384;
+  const float* lse2_g = p.lse2 + (long long)bh * p.S_pad;
+  const float* dv_g = p.dvec + (long long)bh * p.S_pad;
+
+  if (warp == 0) {
+    if (lane == 0 && n_it > 0) {
+      mbar_expect_tx(kv_full, 2 * L::KT);
+#pragma unroll
+      for (int c = 0; c < D / 64; ++c) {
+        tma_load_3d(&mk, kv_full, sm + L::K + c * 16384, c * 64, h, tok0 + k0);
+        tma_load_3d(&mv, kv_full, sm + L::V + c * 16384, c * 64, h, tok0 + k0);
+      }
+      for (int it = 0; it < n_it; ++it) {
+        const int st = it & 1, q0 = (i0 + it) * 64;
+        mbar_wait(&q_empty[st], ((it >> 1) & 1) ^ 1);
+        mbar_expect_tx(&q_full[st], 2 * L::QT + 512);
+#pragma unroll
+        for (int c = 0; c < D / 64; ++c) {
+          tma_load_3d(&mq, &q_full[st], sm + L::Q0 + st * L::QT + c * 8192, c * 64, h, tok0 + q0);
+          tma_load_3d(&mdo, &q_full[st], sm + L::O0 + st * L::QT + c * 8192, c * 64, h, tok0 + q0);
+        }
+        bulk_load(sm + L::LSE + st * 256, lse2_g + q0, 256, &q_full[st]);
+        bulk_load(sm + L::DV + st * 256, dv_g + q0, 256, &q_full[st]);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && n_it > 0) {
+      const uint32_t id_st = make_idesc(128, 64, 0, 0);
+      const uint32_t id_g = make_idesc(128, D, 0, 1);
+      const uint32_t a_k = smem_u32(sm + L::K), a_v = smem_u32(sm + L::V);
+      const uint32_t a_pt = smem_u32(sm + L::PT), a_ds = smem_u32(sm + L::DST);
+      mbar_wait(kv_full, 0);
+      auto grads = [&](int it) {
+        const int st = it & 1;
+        mbar_wait(p_full, it & 1);
+        tc_fence_after();
+        const uint32_t b_do = smem_u32(sm + L::O0 + st * L::QT);
+        const uint32_t b_q = smem_u32(sm + L::Q0 + st * L::QT);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          umma_bf16(t_dv, sdesc(a_pt + k * 32, 16, 1024), sdesc(b_do + k * 2048, 8192, 1024), id_g,
+                    (it | k) != 0);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          umma_bf16(t_dk, sdesc(a_ds + k * 32, 16, 1024), sdesc(b_q + k * 2048, 8192, 1024), id_g,
+                    (it | k) != 0);
+        umma_commit(mm_done);
+        umma_commit(&q_empty[st]);
+      };
+      for (int it = 0; it < n_it; ++it) {
+        const int st = it & 1;
+        mbar_wait(&q_full[st], (it >> 1) & 1);
+        mbar_wait(&st_empty[st], ((it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t b_q = smem_u32(sm + L::Q0 + st * L::QT);
+        const uint32_t b_do = smem_u32(sm + L::O0 + st * L::QT);
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k) {
+          const uint32_t oa = (k >> 2) * 16384 + (k & 3) * 32, ob = (k >> 2) * 8192 + (k & 3) * 32;
+          umma_bf16(tmem + st * 128, sdesc(a_k + oa, 16, 1024), sdesc(b_q + ob, 16, 1024), id_st,
+                    k != 0);
+        }
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k) {
+          const uint32_t oa = (k >> 2) * 16384 + (k & 3) * 32, ob = (k >> 2) * 8192 + (k & 3) * 32;
+          umma_bf16(tmem + st * 128 + 64, sdesc(a_v + oa, 16, 1024), sdesc(b_do + ob, 16, 1024),
+                    id_st, k != 0);
+        }
+        umma_commit(&st_full[st]);
+        if (it > 0) grads(it - 1);
+      }
+      grads(n_it - 1);
+    }
+  } else if (warp >= 4) {
+    const int q = warp & 3, half = (warp - 4) >> 2;
+    const int r = q * 32 + lane, key = k0 + r;
+    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    for (int it = 0; it < n_it; ++it) {
+      const int st = it & 1, q0 = (i0 + it) * 64;
+      mbar_wait(&st_full[st], (it >> 1) & 1);
+      tc_fence_after();
+      float s[32], dp[32];
+      tmem_ld32_nowait(tmem + st * 128 + half * 32 + lane_off, reinterpret_cast<uint32_t*>(s));
+      tmem_ld32_nowait(tmem + st * 128 + 64 + half * 32 + lane_off, reinterpret_cast<uint32_t*>(dp));
+      tmem_wait_ld();
+      tc_fence_before();
+      mbar_arrive(&st_empty[st]);
+      const float* l2 = reinterpret_cast<const float*>(sm + L::LSE + st * 256) + half * 32;
+      const float* dd = reinterpret_cast<const float*>(sm + L::DV + st * 256) + half * 32;
+      const int qbase = q0 + half * 32;
+      const bool need_mask = p.causal && (key > qbase);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        float pv = exp2_mufu(fmaf(s[i], p.scale_log2, -l2[i]));
+        if (need_mask && key > qbase + i) pv = 0.f;
+        s[i] = pv;
+        dp[i] = pv * (dp[i] - dd[i]);
+      }
+      if (it > 0) mbar_wait(mm_done, (it - 1) & 1);
+      store_half_row(sm + L::PT, r, half, s);
+      store_half_row(sm + L::DST, r, half, dp);
+      fence_async_smem();
+      tc_fence_before();
+      mbar_arrive(p_full);
+    }
+    if (n_it > 0) {
+      mbar_wait(mm_done, (n_it - 1) & 1);
+      tc_fence_after();
+      const bool ok = key < p.S;
+      const long long off =
+          (long long)(tok0 + (ok ? key : 0)) * p.st + (long long)h * p.sh + half * (D / 2);
+#pragma unroll 1
+      for (int c = 0; c < D / 64; ++c) {
+        store_row_out(p.g1 + off + c * 32, t_dv + half * (D / 2) + c * 32 + lane_off, 1.f, ok);
+        store_row_out(p.g0 + off + c * 32, t_dk + half * (D / 2) + c * 32 + lane_off, p.scale, ok);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+template <int D>
+struct SmemQ {
+  static constexpr int QT = D * 128 * 2, KT = D * 64 * 2;
+  static constexpr int Q = 0, O = QT, K0 = 2 * QT, V0 = K0 + 2 * KT;
+  static constexpr int DS = V0 + 2 * KT;
+  static constexpr int BAR = DS + 128 * 64 * 2;
+  static constexpr int BYTES = BAR + 256 + 1024;
+};
+
+template <int D>
+__global__ void __launch_bounds__(384, 1)
+    bwd_dq_tc(const __grid_constant__ CUtensorMap mq, const __grid_constant__ CUtensorMap mk,
+              const __grid_constant__ CUtensorMap mv, const __grid_constant__ CUtensorMap mdo,
+              const BwdParams p) {
+  using L = SmemQ<D>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                           ~uintptr_t(1023));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::BAR);
+  uint64_t* qo_full = bar + 0;
+  uint64_t* kv_full = bar + 1;   // [2]
+  uint64_t* kv_empty = bar + 3;  // [2]
+  uint64_t* st_full = bar + 5;   // [2]
+  uint64_t* st_empty = bar + 7;  // [2]
+  uint64_t* ds_full = bar + 9;
+  uint64_t* dq_done = bar + 10;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 12);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_q = (p.S + 127) / 128;
+  const int qb = n_q - 1 - blockIdx.x;
+  const int bh = blockIdx.y, b = bh / p.H, h = bh % p.H;
+  const int q0 = qb * 128, tok0 = b * p.S;
+  const int n_kb = (p.S + 63) / 64;
+  const int n_it = p.causal ? min(n_kb, (q0 + 128) / 64) : n_kb;
+  if (threadIdx.x == 0) {
+    mbar_init(qo_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+      mbar_init(&st_full[i], 1);
+      mbar_init(&st_empty[i], 256);
+    }
+    mbar_init(ds_full, 256);
+    mbar_init(dq_done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    fence_async_smem();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t t_dq = tmem + 256;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_expect_tx(qo_full, 2 * L::QT);
+#pragma unroll
+      for (int c = 0; c < D / 64; ++c) {
+        tma_load_3d(&mq, qo_full, sm + L::Q + c * 16384, c * 64, h, tok0 + q0);
+        tma_load_3d(&mdo, qo_full, sm + L::O + c * 16384, c * 64, h, tok0 + q0);
+      }
+      for (int it = 0; it < n_it; ++it) {
+        const int st = it & 1;
+        mbar_wait(&kv_empty[st], ((it >> 1) & 1) ^ 1);
+        mbar_expect_tx(&kv_full[st], 2 * L::KT);
+#pragma unroll
+        for (int c = 0; c < D / 64; ++c) {
+          tma_load_3d(&mk, &kv_full[st], sm + L::K0 + st * L::KT + c * 8192, c * 64, h, tok0 + it * 64);
+          tma_load_3d(&mv, &kv_full[st], sm + L::V0 + st * L::KT + c * 8192, c * 64, h, tok0 + it * 64);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t id_s = make_idesc(128, 64, 0, 0);
+      const uint32_t id_g = make_idesc(128, D, 0, 1);
+      const uint32_t a_q = smem_u32(sm + L::Q), a_o = smem_u32(sm + L::O);
+      const uint32_t a_ds = smem_u32(sm + L::DS);
+      mbar_wait(qo_full, 0);
+      auto grads = [&](int it) {
+        const int st = it & 1;
+        mbar_wait(ds_full, it & 1);
+        tc_fence_after();
+        const uint32_t b_k = smem_u32(sm + L::K0 + st * L::KT);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          umma_bf16(t_dq, sdesc(a_ds + k * 32, 16, 1024), sdesc(b_k + k * 2048, 8192, 1024), id_g,
+                    (it | k) != 0);
+        umma_commit(dq_done);
+        umma_commit(&kv_empty[st]);
+      };
+      for (int it = 0; it < n_it; ++it) {
+        const int st = it & 1;
+        mbar_wait(&kv_full[st], (it >> 1) & 1);
+        mbar_wait(&st_empty[st], ((it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t b_k = smem_u32(sm + L::K0 + st * L::KT);
+        const uint32_t b_v = smem_u32(sm + L::V0 + st * L::KT);
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k) {
+          const uint32_t oa = (k >> 2) * 16384 + (k & 3) * 32, ob = (k >> 2) * 8192 + (k & 3) * 32;
+          umma_bf16(tmem + st * 128, sdesc(a_q + oa, 16, 1024), sdesc(b_k + ob, 16, 1024), id_s,
+                    k != 0);
+        }
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k) {
+          const uint32_t oa = (k >> 2) * 16384 + (k & 3) * 32, ob = (k >> 2) * 8192 + (k & 3) * 32;
+          umma_bf16(tmem + st * 128 + 64, sdesc(a_o + oa, 16, 1024), sdesc(b_v + ob, 16, 1024),
+                    id_s, k != 0);
+        }
+        umma_commit(&st_full[st]);
+        if (it > 0) grads(it - 1);
+      }
+      grads(n_it - 1);
+    }
+  } else if (warp >= 4) {
+    const int q = warp & 3, half = (warp - 4) >> 2;
+    const int r = q * 32 + lane, qi = q0 + r;
+    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    const float l2 = p.lse2[(long long)bh * p.S_pad + qi];
+    const float dd = p.dvec[(long long)bh * p.S_pad + qi];
+    for (int it = 0; it < n_it; ++it) {
+      const int st = it & 1;
+      mbar_wait(&st_full[st], (it >> 1) & 1);
+      tc_fence_after();
+      float s[32], dp[32];
+      tmem_ld32_nowait(tmem + st * 128 + half * 32 + lane_off, reinterpret_cast<uint32_t*>(s));
+      tmem_ld32_nowait(tmem + st * 128 + 64 + half * 32 + lane_off, reinterpret_cast<uint32_t*>(dp));
+      tmem_wait_ld();
+      tc_fence_before();
+      mbar_arrive(&st_empty[st]);
+      const int kbase = it * 64 + half * 32;
+      const bool need_mask = (kbase + 32 > p.S) || (p.causal && kbase + 31 > qi);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        float pv = exp2_mufu(fmaf(s[i], p.scale_log2, -l2));
+        if (need_mask && (kbase + i >= p.S || (p.causal && kbase + i > qi))) pv = 0.f;
+        dp[i] = pv * (dp[i] - dd);
+      }
+      if (it > 0) mbar_wait(dq_done, (it - 1) & 1);
+      store_half_row(sm + L::DS, r, half, dp);
+      fence_async_smem();
+      tc_fence_before();
+      mbar_arrive(ds_full);
+    }
+    mbar_wait(dq_done, (n_it - 1) & 1);
+    tc_fence_after();
+    const bool ok = qi < p.S;
+    const long long off =
+        (long long)(tok0 + (ok ? qi : 0)) * p.st + (long long)h * p.sh + half * (D / 2);
+#pragma unroll 1
+    for (int c = 0; c < D / 64; ++c)
+      store_row_out(p.g0 + off + c * 32, t_dq + half * (D / 2) + c * 32 + lane_off, p.scale, ok);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+// ---------------------------------------------------------------- host
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+            cudaSuccess && q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(ptr);
+  }
+  return fn;
+}
+
+// 3-D map over [tokens, heads, head_dim] with box [128 tokens, 1 head, 64 dims]
+static bool qkv_map(CUtensorMap* m, const void* base, int64_t tokens, int64_t H, int64_t D,
+                    int64_t st, int64_t sh, uint32_t rows = 128) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)D, (cuuint64_t)H, (cuuint64_t)tokens};
+  cuuint64_t strides[2] = {(cuuint64_t)sh * 2, (cuuint64_t)st * 2};
+  cuuint32_t box[3] = {64, 1, rows};
+  cuuint32_t es[3] = {1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box,
+            es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace fa
+
+int32_t attn_fwd_sm100(const void* q, const void* k, const void* v, void* o, float* lse,
+                       int64_t B, int64_t S, int64_t H, int64_t D, int64_t st, int64_t sh,
+                       int64_t ost, float scale, int32_t causal, cudaStream_t stream) {
+  using namespace fa;
+  CUtensorMap mq, mk, mv;
+  const int64_t tokens = B * S;
+  bool ok = qkv_map(&mq, q, tokens, H, D, st, sh) && qkv_map(&mk, k, tokens, H, D, st, sh) &&
+            qkv_map(&mv, v, tokens, H, D, st, sh);
+  GALV_CHECK_ARG(ok, "tensor map encode failed (alignment?)");
+  FwdParams p;
+  p.S = (int)S;
+  p.H = (int)H;
+  p.n_qblocks = (int)((S + BQ - 1) / BQ);
+  p.causal = causal;
+  p.scale_log2 = scale * LOG2E;
+  p.o = (__nv_bfloat16*)o;
+  p.lse = lse;
+  p.o_st = ost;
+  p.sh = sh;
+  const dim3 grid((unsigned)p.n_qblocks, (unsigned)(B * H));
+  if (D == 128) {
+    static bool set = false;
+    if (!set) {
+      GALV_CUDA_RET(cudaFuncSetAttribute(fwd_tc<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         Smem<128>::BYTES));
+      set = true;
+    }
+    fwd_tc<128><<<grid, 384, Smem<128>::BYTES, stream>>>(mq, mk, mv, p);
+  } else {
+    static bool set = false;
+    if (!set) {
+      GALV_CUDA_RET(cudaFuncSetAttribute(fwd_tc<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         Smem<64>::BYTES));
+      set = true;
+    }
+    fwd_tc<64><<<grid, 384, Smem<64>::BYTES, stream>>>(mq, mk, mv, p);
+  }
+  GALV_LAUNCH_CHECK();
+  return 0;
+}
+
+
+int64_t attn_bwd_ws_sm100(int64_t B, int64_t S, int64_t H) {
+  const int64_t S_pad = (S + 127) / 128 * 128;
+  return 2 * B * H * S_pad * (int64_t)sizeof(float);
+}
+
+int32_t attn_bwd_sm100(const void* q, const void* k, const void* v, const void* o,
+                       const void* dout, const float* lse, void* dq, void* dk, void* dv,
+                       int64_t B, int64_t S, int64_t H, int64_t D, int64_t st, int64_t sh,
+                       int64_t ost, float scale, int32_t causal, void* ws, cudaStream_t stream) {
+  using namespace fa;
+  const int64_t S_pad = (S + 127) / 128 * 128;
+  float* lse2 = reinterpret_cast<float*>(ws);
+  float* dvec = lse2 + B * H * S_pad;
+  bwd_prep<<<(unsigned)(B * H * S_pad / 4), 128, 0, stream>>>(
+      (const __nv_bfloat16*)o, (const __nv_bfloat16*)dout, lse, lse2, dvec, (int)S, (int)S_pad,
+      (int)H, (int)D, ost, sh);
+  GALV_LAUNCH_CHECK();
+  const int64_t tokens = B * S;
+  CUtensorMap mq64, mdo64, mk128, mv128, mq128, mdo128, mk64, mv64;
+  bool ok = qkv_map(&mq64, q, tokens, H, D, st, sh, 64) &&
+            qkv_map(&mdo64, dout, tokens, H, D, ost, sh, 64) &&
+            qkv_map(&mk128, k, tokens, H, D, st, sh, 128) &&
+            qkv_map(&mv128, v, tokens, H, D, st, sh, 128) &&
+            qkv_map(&mq128, q, tokens, H, D, st, sh, 128) &&
+            qkv_map(&mdo128, dout, tokens, H, D, ost, sh, 128) &&
+            qkv_map(&mk64, k, tokens, H, D, st, sh, 64) &&
+            qkv_map(&mv64, v, tokens, H, D, st, sh, 64);
+  GALV_CHECK_ARG(ok, "tensor map encode failed (alignment?)");
+  BwdParams p;
+  p.S = (int)S;
+  p.S_pad = (int)S_pad;
+  p.H = (int)H;
+  p.causal = causal;
+  p.scale = scale;
+  p.scale_log2 = scale * LOG2E;
+  p.lse2 = lse2;
+  p.dvec = dvec;
+  p.st = st;
+  p.sh = sh;
+  const dim3 g_kv((unsigned)((S + 127) / 128), (unsigned)(B * H));
+  const dim3 g_q((unsigned)((S + 127) / 128), (unsigned)(B * H));
+#define GALV_FA_BWD(DD)                                                                          \
+  do {                                                                                           \
+    static bool set = false;                                                                     \
+    if (!set) {                                                                                  \
+      GALV_CUDA_RET(cudaFuncSetAttribute(bwd_dkdv_tc<DD>,                                        \
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,            \
+                                         SmemKV<DD>::BYTES));                                    \
+      GALV_CUDA_RET(cudaFuncSetAttribute(bwd_dq_tc<DD>,                                          \
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,            \
+                                         SmemQ<DD>::BYTES));                                     \
+      set = true;                                                                                \
+    }                                                                                            \
+    p.g0 = (__nv_bfloat16*)dk;                                                                   \
+    p.g1 = (__nv_bfloat16*)dv;                                                                   \
+    bwd_dkdv_tc<DD><<<g_kv, 384, SmemKV<DD>::BYTES, stream>>>(mq64, mk128, mv128, mdo64, p);     \
+    GALV_LAUNCH_CHECK();                                                                         \
+    p.g0 = (__nv_bfloat16*)dq;                                                                   \
+    p.g1 = nullptr;                                                                              \
+    bwd_dq_tc<DD><<<g_q, 384, SmemQ<DD>::BYTES, stream>>>(mq128, mk64, mv64, mdo128, p);         \
+    GALV_LAUNCH_CHECK();                                                                         \
+  } while (0)
+  if (D == 128)
+    GALV_FA_BWD(128);
+  else
+    GALV_FA_BWD(64);
+#undef GALV_FA_BWD
+  return 0;
+}
+
+}  // namespace galv

@@ -231,6 +231,10 @@ def attn_fwd(q, k, v, o, lse, *, scale, causal=True):
           ost, float(scale), int(causal), dtype_code(q.dtype), _stream())
 
 
+def attn_bwd_workspace_bytes(B, S, H, D, dtype) -> int:
+    return int(load_library().galv_attn_bwd_workspace(B, S, H, D, dtype_code(dtype)))
+
+
 def attn_bwd(q, k, v, o, dout, lse, dq, dk, dv, *, scale, causal=True, workspace=None):
     B, S, H, D, st, sh, ost = _attn_geometry(q, o)
     if dout.stride() != o.stride() or dq.stride() != q.stride():

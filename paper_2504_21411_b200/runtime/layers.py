@@ -289,8 +289,9 @@ class DecoderLayer:
         dqkv = torch.empty_like(qkv)
         q, k, v = self._attn_views(qkv, B, S)
         dq, dk, dv = self._attn_views(dqkv, B, S)
-        if self._ws is None:
-            self._ws = torch.empty(B * self.Hl * S, dtype=torch.float32, device=qkv.device)
+        need = K.attn_bwd_workspace_bytes(B, S, self.Hl, cfg.head_dim, qkv.dtype)
+        if self._ws is None or self._ws.numel() < need:
+            self._ws = torch.empty(need, dtype=torch.uint8, device=qkv.device)
         K.attn_bwd(q, k, v, sv["o"].view(B, S, self.Hl, cfg.head_dim),
                    do.view(B, S, self.Hl, cfg.head_dim), sv["lse"], dq, dk, dv,
                    scale=self.scale, causal=True, workspace=self._ws)
