@@ -70,19 +70,24 @@ __global__ void __launch_bounds__(WARPS * 32) fwd_kernel(
 }
 
 // dx = rstd * (g*dy - xhat * mean(g*dy*xhat) [- mean(g*dy) for LayerNorm]) (+ dres)
+// dgamma/dbeta partials are accumulated in warp-private shared-memory rows (no atomics),
+// summed per CTA at the end and flushed with one global atomic per column per CTA.
+constexpr int BWD_WARPS = 4;
 template <typename T, bool LAYER>
-__global__ void __launch_bounds__(WARPS * 32) bwd_kernel(
+__global__ void __launch_bounds__(BWD_WARPS * 32) bwd_kernel(
     const T* __restrict__ x, const T* __restrict__ gamma, const float* __restrict__ mean,
     const float* __restrict__ rstd, const T* __restrict__ dy, const T* __restrict__ dres,
     T* __restrict__ dx, float* __restrict__ dgamma, float* __restrict__ dbeta, int64_t rows,
     int cols) {
   constexpr int V = 16 / sizeof(T);
-  extern __shared__ float sacc[];  // [cols] dgamma partial (+ [cols] dbeta partial)
-  for (int c = threadIdx.x; c < cols * (LAYER ? 2 : 1); c += blockDim.x) sacc[c] = 0.f;
+  extern __shared__ float sacc[];  // [BWD_WARPS][(LAYER ? 2 : 1) * cols]
+  const int per = cols * (LAYER ? 2 : 1);
+  for (int c = threadIdx.x; c < per * BWD_WARPS; c += blockDim.x) sacc[c] = 0.f;
   __syncthreads();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (int64_t row = (int64_t)blockIdx.x * WARPS + w; row < rows;
-       row += (int64_t)gridDim.x * WARPS) {
+  float* mine = sacc + w * per;
+  for (int64_t row = (int64_t)blockIdx.x * BWD_WARPS + w; row < rows;
+       row += (int64_t)gridDim.x * BWD_WARPS) {
     const T* xr = x + row * cols;
     const T* dyr = dy + row * cols;
     const float mu = LAYER ? mean[row] : 0.f, rs = rstd[row];
@@ -98,8 +103,8 @@ __global__ void __launch_bounds__(WARPS * 32) bwd_kernel(
         const float gd = g[i] * d[i];
         a1 += gd * xh;
         a2 += gd;
-        atomicAdd(&sacc[c + i], d[i] * xh);
-        if (LAYER) atomicAdd(&sacc[cols + c + i], d[i]);
+        mine[c + i] += d[i] * xh;
+        if (LAYER) mine[cols + c + i] += d[i];
       }
     }
     a1 = warp_sum(a1) / cols;
@@ -123,9 +128,14 @@ __global__ void __launch_bounds__(WARPS * 32) bwd_kernel(
     }
   }
   __syncthreads();
-  for (int c = threadIdx.x; c < cols; c += blockDim.x) {
-    atomicAdd(&dgamma[c], sacc[c]);
-    if (LAYER) atomicAdd(&dbeta[c], sacc[cols + c]);
+  for (int c = threadIdx.x; c < per; c += blockDim.x) {
+    float t = 0.f;
+#pragma unroll
+    for (int k = 0; k < BWD_WARPS; ++k) t += sacc[k * per + c];
+    if (c < cols)
+      atomicAdd(&dgamma[c], t);
+    else
+      atomicAdd(&dbeta[c - cols], t);
   }
 }
 
@@ -164,16 +174,16 @@ static int32_t norm_bwd(const void* x, const void* gamma, const float* mean, con
   GALV_CHECK_ARG(x && gamma && rstd && dy && dx && dgamma && rows > 0, "bad arguments");
   GALV_CHECK_ARG(!LAYER || (mean && dbeta), "layernorm needs mean and dbeta");
   GALV_CHECK_ARG(cols % 8 == 0, "cols must be a multiple of 8");
-  const size_t smem = sizeof(float) * cols * (LAYER ? 2 : 1);
-  GALV_CHECK_ARG(smem <= 200 * 1024, "cols too large for the dgamma reduction");
-  int64_t want = (rows + norm::WARPS - 1) / norm::WARPS;
-  const unsigned grid = (unsigned)std::min<int64_t>(want, (int64_t)sm_count() * 2);
+  const size_t smem = sizeof(float) * cols * (LAYER ? 2 : 1) * norm::BWD_WARPS;
+  GALV_CHECK_ARG(smem <= 220 * 1024, "cols too large for the dgamma reduction");
+  int64_t want = (rows + norm::BWD_WARPS - 1) / norm::BWD_WARPS;
+  const unsigned grid = (unsigned)std::min<int64_t>(want, (int64_t)sm_count());
   GALV_DISPATCH(dtype, T, {
     auto k = norm::bwd_kernel<T, LAYER>;
     if (smem > 48 * 1024)
       GALV_CUDA_RET(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem));
-    k<<<grid, norm::WARPS * 32, smem, as_stream(stream)>>>(
+    k<<<grid, norm::BWD_WARPS * 32, smem, as_stream(stream)>>>(
         (const T*)x, (const T*)gamma, mean, rstd, (const T*)dy, (const T*)dres, (T*)dx, dgamma,
         dbeta, rows, (int)cols);
   });
