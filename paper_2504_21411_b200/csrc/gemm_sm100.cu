@@ -9,6 +9,7 @@
 // Operands may be K-major or MN-major independently (idesc bits 15/16), which covers
 // forward (X W^T), dgrad (dY W) and wgrad (dY^T X) without transposes.
 #include <cuda.h>
+#include <cstdlib>
 #include <mutex>
 
 #include "common.cuh"
@@ -47,6 +48,65 @@ __device__ __forceinline__ void tile_coords(const Params& p, int t, int& mt, int
   const int r = t - group * per_group;
   mt = first_m + r % gm;
   nt = r / gm;
+}
+
+// Epilogue of one 128-lane accumulator slice: this thread owns output row `row` and
+// the BN columns starting at `col_base`; alpha, bias and accumulate-into-C fused.
+__device__ __forceinline__ void epilogue_tile(const Params& p, uint32_t taddr, int row,
+                                              int col_base, bool vec_ok) {
+  const bool row_ok = row < p.M;
+#pragma unroll 1
+  for (int cc = 0; cc < BN; cc += 32) {
+    uint32_t r[32];
+    tmem_ld32(taddr + cc, r);
+    const int col0 = col_base + cc;
+    if (!row_ok || col0 >= p.N) continue;
+        float v[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]) * p.alpha;
+    const int ncol = min(32, p.N - col0);
+    if (p.bias) {
+      for (int i = 0; i < ncol; ++i)
+        v[i] += p.bias_bf16 ? __bfloat162float(
+                                  reinterpret_cast<const __nv_bfloat16*>(p.bias)[col0 + i])
+                            : reinterpret_cast<const float*>(p.bias)[col0 + i];
+    }
+    const long long off = (long long)row * p.ldc + col0;
+    if (p.c_bf16) {
+      __nv_bfloat16* c = reinterpret_cast<__nv_bfloat16*>(p.C) + off;
+      if (ncol == 32 && vec_ok) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          float tmp[8];
+          if (p.accumulate) load16(c + j * 8, tmp);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) tmp[e] = p.accumulate ? tmp[e] + v[j * 8 + e] : v[j * 8 + e];
+          store16(c + j * 8, tmp);
+        }
+      } else {
+        for (int i = 0; i < ncol; ++i) {
+          float o = v[i];
+          if (p.accumulate) o += __bfloat162float(c[i]);
+          c[i] = __float2bfloat16_rn(o);
+        }
+      }
+    } else {
+      float* c = reinterpret_cast<float*>(p.C) + off;
+      if (ncol == 32 && (p.ldc % 4) == 0) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          float4 o = make_float4(v[j * 4], v[j * 4 + 1], v[j * 4 + 2], v[j * 4 + 3]);
+          if (p.accumulate) {
+            float4 old = *reinterpret_cast<const float4*>(c + j * 4);
+            o.x += old.x; o.y += old.y; o.z += old.z; o.w += old.w;
+          }
+          *reinterpret_cast<float4*>(c + j * 4) = o;
+        }
+      } else {
+        for (int i = 0; i < ncol; ++i) c[i] = p.accumulate ? c[i] + v[i] : v[i];
+      }
+    }
+  }
 }
 
 __global__ void __launch_bounds__(256, 1)
@@ -168,60 +228,8 @@ __global__ void __launch_bounds__(256, 1)
       tile_coords(p, t, mt, nt);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const int row = mt * BM + q * 32 + lane;
-      const bool row_ok = row < p.M;
-#pragma unroll 1
-      for (int cc = 0; cc < BN; cc += 32) {
-        uint32_t r[32];
-        tmem_ld32(tmem + acc * BN + cc + ((uint32_t)(q * 32) << 16), r);
-        const int col0 = nt * BN + cc;
-        if (!row_ok || col0 >= p.N) continue;
-        float v[32];
-#pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]) * p.alpha;
-        const int ncol = min(32, p.N - col0);
-        if (p.bias) {
-          for (int i = 0; i < ncol; ++i)
-            v[i] += p.bias_bf16 ? __bfloat162float(
-                                      reinterpret_cast<const __nv_bfloat16*>(p.bias)[col0 + i])
-                                : reinterpret_cast<const float*>(p.bias)[col0 + i];
-        }
-        const long long off = (long long)row * p.ldc + col0;
-        if (p.c_bf16) {
-          __nv_bfloat16* c = reinterpret_cast<__nv_bfloat16*>(p.C) + off;
-          if (ncol == 32 && vec_ok) {
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              float tmp[8];
-              if (p.accumulate) load16(c + j * 8, tmp);
-#pragma unroll
-              for (int e = 0; e < 8; ++e) tmp[e] = p.accumulate ? tmp[e] + v[j * 8 + e] : v[j * 8 + e];
-              store16(c + j * 8, tmp);
-            }
-          } else {
-            for (int i = 0; i < ncol; ++i) {
-              float o = v[i];
-              if (p.accumulate) o += __bfloat162float(c[i]);
-              c[i] = __float2bfloat16_rn(o);
-            }
-          }
-        } else {
-          float* c = reinterpret_cast<float*>(p.C) + off;
-          if (ncol == 32 && (p.ldc % 4) == 0) {
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              float4 o = make_float4(v[j * 4], v[j * 4 + 1], v[j * 4 + 2], v[j * 4 + 3]);
-              if (p.accumulate) {
-                float4 old = *reinterpret_cast<const float4*>(c + j * 4);
-                o.x += old.x; o.y += old.y; o.z += old.z; o.w += old.w;
-              }
-              *reinterpret_cast<float4*>(c + j * 4) = o;
-            }
-          } else {
-            for (int i = 0; i < ncol; ++i) c[i] = p.accumulate ? c[i] + v[i] : v[i];
-          }
-        }
-      }
+      epilogue_tile(p, tmem + acc * BN + ((uint32_t)(q * 32) << 16), mt * BM + q * 32 + lane,
+                    nt * BN, vec_ok);
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
       if (++acc == 2) {
@@ -237,6 +245,155 @@ __global__ void __launch_bounds__(256, 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
                  "r"(TMEM_COLS)
                  : "memory");
+  }
+}
+
+
+// ---------------------------------------------------------------- 2-CTA variant
+// CTA pair (cluster of 2 on one TPC) computes a 256x256 tile with tcgen05.mma.cta_group::2:
+// each CTA stages its 128 rows of A and 128 rows (N) of B, so per-SM shared-memory
+// operand traffic is halved relative to the 1-CTA 128x256 kernel.  Only the leader CTA
+// issues MMAs; TMA bytes of both CTAs complete on the leader's `full` barriers; MMA
+// completion is multicast to both CTAs' `empty` / `tfull` barriers; both CTAs' epilogues
+// release the accumulator by arriving remotely on the leader's `tempty` barrier.
+constexpr int STAGES2 = 6;
+constexpr int HALF_STAGE = 128 * BK * 2;  // 16 KB: 128 rows of A (or of B)
+constexpr int SMEM2_BYTES = STAGES2 * 2 * HALF_STAGE + 1024 + 256;
+
+__device__ __forceinline__ void tile_coords2(const Params& p, int t, int& mt, int& nt) {
+  // pair tiles are 256 x 256; p.tiles_m counts 256-row tiles here
+  tile_coords(p, t, mt, nt);
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
+    gemm_bf16_tc2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                  const Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES2 * HALF_STAGE;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES2 * 2 * HALF_STAGE);
+  uint64_t* empty = full + STAGES2;
+  uint64_t* tfull = empty + STAGES2;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t cr = cluster_ctarank();
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES2; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 256);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    fence_async_smem();
+    prefetch_map(&tmA);
+    prefetch_map(&tmB);
+  }
+  if (warp == 2) tmem_alloc_2sm(tmem_slot, TMEM_COLS);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = pair; t < p.num_tiles; t += npairs) {
+        int mt, nt;
+        tile_coords2(p, t, mt, nt);
+        const int m0 = mt * 256 + (int)cr * 128, n0 = nt * 256 + (int)cr * 128;
+        for (int kb = 0; kb < p.k_blocks; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          if (cr == 0) mbar_expect_tx(&full[stage], 4 * HALF_STAGE);
+          uint8_t* a_dst = sA + stage * HALF_STAGE;
+          uint8_t* b_dst = sB + stage * HALF_STAGE;
+          if (!p.a_mn) {
+            tma_load_2d_2sm(&tmA, &full[stage], a_dst, kb * BK, m0);
+          } else {
+            tma_load_2d_2sm(&tmA, &full[stage], a_dst, m0, kb * BK);
+            tma_load_2d_2sm(&tmA, &full[stage], a_dst + 8192, m0 + 64, kb * BK);
+          }
+          if (!p.b_mn) {
+            tma_load_2d_2sm(&tmB, &full[stage], b_dst, kb * BK, n0);
+          } else {
+            tma_load_2d_2sm(&tmB, &full[stage], b_dst, n0, kb * BK);
+            tma_load_2d_2sm(&tmB, &full[stage], b_dst + 8192, n0 + 64, kb * BK);
+          }
+          if (++stage == STAGES2) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && cr == 0) {
+      const uint32_t idesc = make_idesc(256, 256, p.a_mn, p.b_mn);
+      int stage = 0, acc = 0;
+      uint32_t phase = 0, acc_phase = 0;
+      for (int t = pair; t < p.num_tiles; t += npairs) {
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + acc * BN;
+        for (int kb = 0; kb < p.k_blocks; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_base = smem_u32(sA + stage * HALF_STAGE);
+          const uint32_t b_base = smem_u32(sB + stage * HALF_STAGE);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t ad = p.a_mn ? sdesc(a_base + k * 2048, 8192, 1024)
+                                       : sdesc(a_base + k * 32, 16, 1024);
+            const uint64_t bd = p.b_mn ? sdesc(b_base + k * 2048, 8192, 1024)
+                                       : sdesc(b_base + k * 32, 16, 1024);
+            umma_bf16_2sm(d, ad, bd, idesc, (kb | k) != 0);
+          }
+          umma_commit_2sm(&empty[stage], 0x3);
+          if (++stage == STAGES2) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit_2sm(&tfull[acc], 0x3);
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    const int q = warp & 3;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    const bool vec_ok = (p.ldc % 8) == 0;
+    for (int t = pair; t < p.num_tiles; t += npairs) {
+      int mt, nt;
+      tile_coords2(p, t, mt, nt);
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      epilogue_tile(p, tmem + acc * BN + ((uint32_t)(q * 32) << 16),
+                    mt * 256 + (int)cr * 128 + q * 32 + lane, nt * BN, vec_ok);
+      tc_fence_before();
+      mbar_arrive_remote(&tempty[acc], 0);
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  }
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc_2sm(tmem, TMEM_COLS);
   }
 }
 
@@ -317,6 +474,26 @@ int32_t gemm_bf16_sm100(const void* A, const void* B, void* C, const void* bias,
     GALV_CUDA_RET(cudaFuncSetAttribute(gemm_bf16_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        SMEM_BYTES));
     attr_set = true;
+  }
+  if (M > 128 && getenv("GALV_GEMM_1CTA") == nullptr) {
+    // 2-CTA path: 256x256 pair tiles, per-CTA boxes of 128 rows
+    CUtensorMap ma2, mb2;
+    bool ok2 = a_mn ? make_map(&ma2, A, M, K, lda, 64, 64) : make_map(&ma2, A, K, M, lda, 64, 128);
+    ok2 = ok2 && (b_mn ? make_map(&mb2, B, N, K, ldb, 64, 64) : make_map(&mb2, B, K, N, ldb, 64, 128));
+    GALV_CHECK_ARG(ok2, "cuTensorMapEncodeTiled failed");
+    Params p2 = p;
+    p2.tiles_m = (int)((M + 255) / 256);
+    p2.num_tiles = p2.tiles_m * p2.tiles_n;
+    static bool attr2 = false;
+    if (!attr2) {
+      GALV_CUDA_RET(cudaFuncSetAttribute(gemm_bf16_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         SMEM2_BYTES));
+      attr2 = true;
+    }
+    const int pairs = min(p2.num_tiles, sm_count() / 2);
+    gemm_bf16_tc2<<<2 * pairs, 256, SMEM2_BYTES, stream>>>(ma2, mb2, p2);
+    GALV_LAUNCH_CHECK();
+    return 0;
   }
   const int grid = min(p.num_tiles, sm_count());
   gemm_bf16_tc<<<grid, 256, SMEM_BYTES, stream>>>(ma, mb, p);
