@@ -301,19 +301,21 @@ __global__ void __launch_bounds__(384, 1)
 // lse*log2(e) and D = rowsum(dO*O) come from a padded workspace written by bwd_prep
 // (padded rows: lse2 = +inf so their P is exactly 0).
 
+// one warp handles 2 rows of D <= 128 (16 lanes x 8 elements per row, 16-byte loads)
 __global__ void bwd_prep(const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ dout,
                          const float* __restrict__ lse, float* __restrict__ lse2,
                          float* __restrict__ dvec, int S, int S_pad, int H, int D, long long ost,
                          long long sh) {
-  const long long row = (long long)blockIdx.x * 4 + (threadIdx.x >> 5);  // over B*H*S_pad
   const int lane = threadIdx.x & 31;
+  const long long row = ((long long)blockIdx.x * 4 + (threadIdx.x >> 5)) * 2 + (lane >> 4);
+  const int sub = lane & 15;
   const int bh = (int)(row / S_pad), i = (int)(row % S_pad);
   const int b = bh / H, h = bh % H;
   float s = 0.f;
   if (i < S) {
     const __nv_bfloat16* orow = o + ((long long)b * S + i) * ost + (long long)h * sh;
     const __nv_bfloat16* drow = dout + ((long long)b * S + i) * ost + (long long)h * sh;
-    for (int d = lane * 8; d < D; d += 256) {
+    for (int d = sub * 8; d < D; d += 128) {
       float a[8], c[8];
       load16(orow + d, a);
       load16(drow + d, c);
@@ -321,8 +323,9 @@ __global__ void bwd_prep(const __nv_bfloat16* __restrict__ o, const __nv_bfloat1
       for (int e = 0; e < 8; ++e) s += a[e] * c[e];
     }
   }
-  s = warp_sum(s);
-  if (lane == 0) {
+#pragma unroll
+  for (int off = 8; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+  if (sub == 0) {
     dvec[row] = i < S ? s : 0.f;
     lse2[row] = i < S ? lse[(long long)bh * S + i] * LOG2E : INFINITY;
   }
@@ -802,7 +805,7 @@ int32_t attn_bwd_sm100(const void* q, const void* k, const void* v, const void* 
   const int64_t S_pad = (S + 127) / 128 * 128;
   float* lse2 = reinterpret_cast<float*>(ws);
   float* dvec = lse2 + B * H * S_pad;
-  bwd_prep<<<(unsigned)(B * H * S_pad / 4), 128, 0, stream>>>(
+  bwd_prep<<<(unsigned)(B * H * S_pad / 8), 128, 0, stream>>>(
       (const __nv_bfloat16*)o, (const __nv_bfloat16*)dout, lse, lse2, dvec, (int)S, (int)S_pad,
       (int)H, (int)D, ost, sh);
   GALV_LAUNCH_CHECK();

@@ -69,73 +69,88 @@ __global__ void __launch_bounds__(WARPS * 32) fwd_kernel(
   }
 }
 
-// dx = rstd * (g*dy - xhat * mean(g*dy*xhat) [- mean(g*dy) for LayerNorm]) (+ dres)
-// dgamma/dbeta partials are accumulated in warp-private shared-memory rows (no atomics),
-// summed per CTA at the end and flushed with one global atomic per column per CTA.
-constexpr int BWD_WARPS = 4;
+// dx = rstd * (g*dy - xhat * mean(g*dy*xhat) [- mean(g*dy) for LayerNorm]) (+ dres):
+// warp per row, 8 warps per CTA, full occupancy (HBM-bound, 16-byte vectors).
 template <typename T, bool LAYER>
-__global__ void __launch_bounds__(BWD_WARPS * 32) bwd_kernel(
+__global__ void __launch_bounds__(WARPS * 32) bwd_dx_kernel(
     const T* __restrict__ x, const T* __restrict__ gamma, const float* __restrict__ mean,
     const float* __restrict__ rstd, const T* __restrict__ dy, const T* __restrict__ dres,
-    T* __restrict__ dx, float* __restrict__ dgamma, float* __restrict__ dbeta, int64_t rows,
-    int cols) {
+    T* __restrict__ dx, int64_t rows, int cols) {
   constexpr int V = 16 / sizeof(T);
-  extern __shared__ float sacc[];  // [BWD_WARPS][(LAYER ? 2 : 1) * cols]
-  const int per = cols * (LAYER ? 2 : 1);
-  for (int c = threadIdx.x; c < per * BWD_WARPS; c += blockDim.x) sacc[c] = 0.f;
-  __syncthreads();
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  float* mine = sacc + w * per;
-  for (int64_t row = (int64_t)blockIdx.x * BWD_WARPS + w; row < rows;
-       row += (int64_t)gridDim.x * BWD_WARPS) {
-    const T* xr = x + row * cols;
-    const T* dyr = dy + row * cols;
-    const float mu = LAYER ? mean[row] : 0.f, rs = rstd[row];
-    float a1 = 0.f, a2 = 0.f;  // sum(g*dy*xhat), sum(g*dy)
-    for (int c = lane * V; c < cols; c += 32 * V) {
-      float v[V], d[V], g[V];
-      load16(xr + c, v);
-      load16(dyr + c, d);
-      load16(gamma + c, g);
+  const int lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * WARPS + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  const T* xr = x + row * cols;
+  const T* dyr = dy + row * cols;
+  const float mu = LAYER ? mean[row] : 0.f, rs = rstd[row];
+  float a1 = 0.f, a2 = 0.f;
+  for (int c = lane * V; c < cols; c += 32 * V) {
+    float v[V], d[V], g[V];
+    load16(xr + c, v);
+    load16(dyr + c, d);
+    load16(gamma + c, g);
 #pragma unroll
-      for (int i = 0; i < V; ++i) {
-        const float xh = (v[i] - mu) * rs;
-        const float gd = g[i] * d[i];
-        a1 += gd * xh;
-        a2 += gd;
-        mine[c + i] += d[i] * xh;
-        if (LAYER) mine[cols + c + i] += d[i];
-      }
-    }
-    a1 = warp_sum(a1) / cols;
-    a2 = warp_sum(a2) / cols;
-    T* dxr = dx + row * cols;
-    const T* drr = dres ? dres + row * cols : nullptr;
-    for (int c = lane * V; c < cols; c += 32 * V) {
-      float v[V], d[V], g[V], r[V];
-      load16(xr + c, v);
-      load16(dyr + c, d);
-      load16(gamma + c, g);
-      if (drr) load16(drr + c, r);
-#pragma unroll
-      for (int i = 0; i < V; ++i) {
-        const float xh = (v[i] - mu) * rs;
-        float o = rs * (g[i] * d[i] - xh * a1 - (LAYER ? a2 : 0.f));
-        if (drr) o += r[i];
-        v[i] = o;
-      }
-      store16(dxr + c, v);
+    for (int i = 0; i < V; ++i) {
+      const float gd = g[i] * d[i];
+      a1 += gd * (v[i] - mu) * rs;
+      a2 += gd;
     }
   }
-  __syncthreads();
-  for (int c = threadIdx.x; c < per; c += blockDim.x) {
-    float t = 0.f;
+  a1 = warp_sum(a1) / cols;
+  a2 = warp_sum(a2) / cols;
+  T* dxr = dx + row * cols;
+  const T* drr = dres ? dres + row * cols : nullptr;
+  for (int c = lane * V; c < cols; c += 32 * V) {
+    float v[V], d[V], g[V], r[V];
+    load16(xr + c, v);
+    load16(dyr + c, d);
+    load16(gamma + c, g);
+    if (drr) load16(drr + c, r);
 #pragma unroll
-    for (int k = 0; k < BWD_WARPS; ++k) t += sacc[k * per + c];
-    if (c < cols)
-      atomicAdd(&dgamma[c], t);
-    else
-      atomicAdd(&dbeta[c - cols], t);
+    for (int i = 0; i < V; ++i) {
+      const float xh = (v[i] - mu) * rs;
+      float o = rs * (g[i] * d[i] - xh * a1 - (LAYER ? a2 : 0.f));
+      if (drr) o += r[i];
+      v[i] = o;
+    }
+    store16(dxr + c, v);
+  }
+}
+
+// dgamma[c] += sum_r dy[r,c] * xhat[r,c] (and dbeta[c] += sum_r dy[r,c]): column strips of
+// 2*blockDim columns (bf16x2 / float2 loads, coalesced), row chunks across blockIdx.y.
+template <typename T, bool LAYER>
+__global__ void __launch_bounds__(128) bwd_dgamma_kernel(
+    const T* __restrict__ x, const float* __restrict__ mean, const float* __restrict__ rstd,
+    const T* __restrict__ dy, float* __restrict__ dgamma, float* __restrict__ dbeta,
+    int64_t rows, int cols, int64_t rows_per_cta) {
+  const int c = (blockIdx.x * 128 + threadIdx.x) * 2;
+  if (c >= cols) return;
+  const int64_t r0 = blockIdx.y * rows_per_cta, r1 = min(rows, r0 + rows_per_cta);
+  float g0 = 0.f, g1 = 0.f, b0 = 0.f, b1 = 0.f;
+  for (int64_t r = r0; r < r1; ++r) {
+    const float mu = LAYER ? mean[r] : 0.f, rs = rstd[r];
+    float xv0, xv1, d0, d1;
+    if constexpr (sizeof(T) == 2) {
+      const __nv_bfloat162 xx = *reinterpret_cast<const __nv_bfloat162*>(x + r * cols + c);
+      const __nv_bfloat162 dd = *reinterpret_cast<const __nv_bfloat162*>(dy + r * cols + c);
+      xv0 = __bfloat162float(xx.x); xv1 = __bfloat162float(xx.y);
+      d0 = __bfloat162float(dd.x); d1 = __bfloat162float(dd.y);
+    } else {
+      const float2 xx = *reinterpret_cast<const float2*>(x + r * cols + c);
+      const float2 dd = *reinterpret_cast<const float2*>(dy + r * cols + c);
+      xv0 = xx.x; xv1 = xx.y; d0 = dd.x; d1 = dd.y;
+    }
+    g0 += d0 * (xv0 - mu) * rs;
+    g1 += d1 * (xv1 - mu) * rs;
+    b0 += d0;
+    b1 += d1;
+  }
+  atomicAdd(&dgamma[c], g0);
+  atomicAdd(&dgamma[c + 1], g1);
+  if (LAYER) {
+    atomicAdd(&dbeta[c], b0);
+    atomicAdd(&dbeta[c + 1], b1);
   }
 }
 
@@ -174,18 +189,18 @@ static int32_t norm_bwd(const void* x, const void* gamma, const float* mean, con
   GALV_CHECK_ARG(x && gamma && rstd && dy && dx && dgamma && rows > 0, "bad arguments");
   GALV_CHECK_ARG(!LAYER || (mean && dbeta), "layernorm needs mean and dbeta");
   GALV_CHECK_ARG(cols % 8 == 0, "cols must be a multiple of 8");
-  const size_t smem = sizeof(float) * cols * (LAYER ? 2 : 1) * norm::BWD_WARPS;
-  GALV_CHECK_ARG(smem <= 220 * 1024, "cols too large for the dgamma reduction");
-  int64_t want = (rows + norm::BWD_WARPS - 1) / norm::BWD_WARPS;
-  const unsigned grid = (unsigned)std::min<int64_t>(want, (int64_t)sm_count());
+  const unsigned grid = (unsigned)((rows + norm::WARPS - 1) / norm::WARPS);
+  const int64_t strips = (cols / 2 + 127) / 128;
+  const int64_t chunks = std::max<int64_t>(1, std::min<int64_t>(rows / 32 + 1,
+                                                                (int64_t)sm_count() * 8 / strips + 1));
+  const int64_t rpc = (rows + chunks - 1) / chunks;
   GALV_DISPATCH(dtype, T, {
-    auto k = norm::bwd_kernel<T, LAYER>;
-    if (smem > 48 * 1024)
-      GALV_CUDA_RET(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem));
-    k<<<grid, norm::BWD_WARPS * 32, smem, as_stream(stream)>>>(
-        (const T*)x, (const T*)gamma, mean, rstd, (const T*)dy, (const T*)dres, (T*)dx, dgamma,
-        dbeta, rows, (int)cols);
+    norm::bwd_dx_kernel<T, LAYER><<<grid, norm::WARPS * 32, 0, as_stream(stream)>>>(
+        (const T*)x, (const T*)gamma, mean, rstd, (const T*)dy, (const T*)dres, (T*)dx, rows,
+        (int)cols);
+    norm::bwd_dgamma_kernel<T, LAYER><<<dim3((unsigned)strips, (unsigned)chunks), 128, 0,
+                                        as_stream(stream)>>>(
+        (const T*)x, mean, rstd, (const T*)dy, dgamma, dbeta, rows, (int)cols, rpc);
   });
   GALV_LAUNCH_CHECK();
   return 0;
