@@ -351,11 +351,12 @@ struct BwdParams {
 
 template <int D>
 struct SmemKV {
+  static constexpr int NST = 3;  // Q/dO pipeline depth
   static constexpr int KT = D * 128 * 2, QT = D * 64 * 2;
-  static constexpr int K = 0, V = KT, Q0 = 2 * KT, O0 = Q0 + 2 * QT;
-  static constexpr int PT = O0 + 2 * QT, DST = PT + 128 * 64 * 2;
-  static constexpr int LSE = DST + 128 * 64 * 2, DV = LSE + 2 * 64 * 4;
-  static constexpr int BAR = DV + 2 * 64 * 4;
+  static constexpr int K = 0, V = KT, Q0 = 2 * KT, O0 = Q0 + NST * QT;
+  static constexpr int PT = O0 + NST * QT, DST = PT + 128 * 64 * 2;
+  static constexpr int LSE = DST + 128 * 64 * 2, DV = LSE + NST * 64 * 4;
+  static constexpr int BAR = DV + NST * 64 * 4;
   static constexpr int BYTES = BAR + 256 + 1024;
 };
 
@@ -395,14 +396,15 @@ __global__ void __launch_bounds__(384, 1)
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                            ~uintptr_t(1023));
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::BAR);
+  constexpr int NST = L::NST;
   uint64_t* kv_full = bar + 0;
-  uint64_t* q_full = bar + 1;    // [2]
-  uint64_t* q_empty = bar + 3;   // [2]
-  uint64_t* st_full = bar + 5;   // [2]
-  uint64_t* st_empty = bar + 7;  // [2]
-  uint64_t* p_full = bar + 9;
-  uint64_t* mm_done = bar + 10;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 12);
+  uint64_t* q_full = bar + 1;          // [NST]
+  uint64_t* q_empty = q_full + NST;    // [NST]
+  uint64_t* st_full = q_empty + NST;   // [2]
+  uint64_t* st_empty = st_full + 2;    // [2]
+  uint64_t* p_full = st_empty + 2;
+  uint64_t* mm_done = p_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mm_done + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int kb = blockIdx.x;
   const int bh = blockIdx.y, b = bh / p.H, h = bh % p.H;
@@ -412,9 +414,11 @@ __global__ void __launch_bounds__(384, 1)
   const int n_it = n_qb - i0;
   if (threadIdx.x == 0) {
     mbar_init(kv_full, 1);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < NST; ++i) {
       mbar_init(&q_full[i], 1);
       mbar_init(&q_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
       mbar_init(&st_full[i], 1);
       mbar_init(&st_empty[i], 256);
     }
@@ -441,8 +445,8 @@ __global__ void __launch_bounds__(384, 1)
         tma_load_3d(&mv, kv_full, sm + L::V + c * 16384, c * 64, h, tok0 + k0);
       }
       for (int it = 0; it < n_it; ++it) {
-        const int st = it & 1, q0 = (i0 + it) * 64;
-        mbar_wait(&q_empty[st], ((it >> 1) & 1) ^ 1);
+        const int st = it % NST, q0 = (i0 + it) * 64;
+        mbar_wait(&q_empty[st], ((it / NST) & 1) ^ 1);
         mbar_expect_tx(&q_full[st], 2 * L::QT + 512);
 #pragma unroll
         for (int c = 0; c < D / 64; ++c) {
@@ -461,7 +465,7 @@ __global__ void __launch_bounds__(384, 1)
       const uint32_t a_pt = smem_u32(sm + L::PT), a_ds = smem_u32(sm + L::DST);
       mbar_wait(kv_full, 0);
       auto grads = [&](int it) {
-        const int st = it & 1;
+        const int st = it % NST;
         mbar_wait(p_full, it & 1);
         tc_fence_after();
         const uint32_t b_do = smem_u32(sm + L::O0 + st * L::QT);
@@ -478,25 +482,25 @@ __global__ void __launch_bounds__(384, 1)
         umma_commit(&q_empty[st]);
       };
       for (int it = 0; it < n_it; ++it) {
-        const int st = it & 1;
-        mbar_wait(&q_full[st], (it >> 1) & 1);
-        mbar_wait(&st_empty[st], ((it >> 1) & 1) ^ 1);
+        const int st = it % NST, sb = it & 1;
+        mbar_wait(&q_full[st], (it / NST) & 1);
+        mbar_wait(&st_empty[sb], ((it >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t b_q = smem_u32(sm + L::Q0 + st * L::QT);
         const uint32_t b_do = smem_u32(sm + L::O0 + st * L::QT);
 #pragma unroll
         for (int k = 0; k < D / 16; ++k) {
           const uint32_t oa = (k >> 2) * 16384 + (k & 3) * 32, ob = (k >> 2) * 8192 + (k & 3) * 32;
-          umma_bf16(tmem + st * 128, sdesc(a_k + oa, 16, 1024), sdesc(b_q + ob, 16, 1024), id_st,
+          umma_bf16(tmem + sb * 128, sdesc(a_k + oa, 16, 1024), sdesc(b_q + ob, 16, 1024), id_st,
                     k != 0);
         }
 #pragma unroll
         for (int k = 0; k < D / 16; ++k) {
           const uint32_t oa = (k >> 2) * 16384 + (k & 3) * 32, ob = (k >> 2) * 8192 + (k & 3) * 32;
-          umma_bf16(tmem + st * 128 + 64, sdesc(a_v + oa, 16, 1024), sdesc(b_do + ob, 16, 1024),
+          umma_bf16(tmem + sb * 128 + 64, sdesc(a_v + oa, 16, 1024), sdesc(b_do + ob, 16, 1024),
                     id_st, k != 0);
         }
-        umma_commit(&st_full[st]);
+        umma_commit(&st_full[sb]);
         if (it > 0) grads(it - 1);
       }
       grads(n_it - 1);
@@ -506,15 +510,15 @@ __global__ void __launch_bounds__(384, 1)
     const int r = q * 32 + lane, key = k0 + r;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     for (int it = 0; it < n_it; ++it) {
-      const int st = it & 1, q0 = (i0 + it) * 64;
-      mbar_wait(&st_full[st], (it >> 1) & 1);
+      const int st = it % NST, sb = it & 1, q0 = (i0 + it) * 64;
+      mbar_wait(&st_full[sb], (it >> 1) & 1);
       tc_fence_after();
       float s[32], dp[32];
-      tmem_ld32_nowait(tmem + st * 128 + half * 32 + lane_off, reinterpret_cast<uint32_t*>(s));
-      tmem_ld32_nowait(tmem + st * 128 + 64 + half * 32 + lane_off, reinterpret_cast<uint32_t*>(dp));
+      tmem_ld32_nowait(tmem + sb * 128 + half * 32 + lane_off, reinterpret_cast<uint32_t*>(s));
+      tmem_ld32_nowait(tmem + sb * 128 + 64 + half * 32 + lane_off, reinterpret_cast<uint32_t*>(dp));
       tmem_wait_ld();
       tc_fence_before();
-      mbar_arrive(&st_empty[st]);
+      mbar_arrive(&st_empty[sb]);
       const float* l2 = reinterpret_cast<const float*>(sm + L::LSE + st * 256) + half * 32;
       const float* dd = reinterpret_cast<const float*>(sm + L::DV + st * 256) + half * 32;
       const int qbase = q0 + half * 32;
@@ -556,9 +560,10 @@ __global__ void __launch_bounds__(384, 1)
 
 template <int D>
 struct SmemQ {
+  static constexpr int NST = 4;  // K/V pipeline depth
   static constexpr int QT = D * 128 * 2, KT = D * 64 * 2;
-  static constexpr int Q = 0, O = QT, K0 = 2 * QT, V0 = K0 + 2 * KT;
-  static constexpr int DS = V0 + 2 * KT;
+  static constexpr int Q = 0, O = QT, K0 = 2 * QT, V0 = K0 + NST * KT;
+  static constexpr int DS = V0 + NST * KT;
   static constexpr int BAR = DS + 128 * 64 * 2;
   static constexpr int BYTES = BAR + 256 + 1024;
 };
@@ -573,14 +578,15 @@ __global__ void __launch_bounds__(384, 1)
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                            ~uintptr_t(1023));
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::BAR);
+  constexpr int NST = L::NST;
   uint64_t* qo_full = bar + 0;
-  uint64_t* kv_full = bar + 1;   // [2]
-  uint64_t* kv_empty = bar + 3;  // [2]
-  uint64_t* st_full = bar + 5;   // [2]
-  uint64_t* st_empty = bar + 7;  // [2]
-  uint64_t* ds_full = bar + 9;
-  uint64_t* dq_done = bar + 10;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 12);
+  uint64_t* kv_full = bar + 1;          // [NST]
+  uint64_t* kv_empty = kv_full + NST;   // [NST]
+  uint64_t* st_full = kv_empty + NST;   // [2]
+  uint64_t* st_empty = st_full + 2;     // [2]
+  uint64_t* ds_full = st_empty + 2;
+  uint64_t* dq_done = ds_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dq_done + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_q = (p.S + 127) / 128;
   const int qb = n_q - 1 - blockIdx.x;
@@ -590,9 +596,11 @@ __global__ void __launch_bounds__(384, 1)
   const int n_it = p.causal ? min(n_kb, (q0 + 128) / 64) : n_kb;
   if (threadIdx.x == 0) {
     mbar_init(qo_full, 1);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < NST; ++i) {
       mbar_init(&kv_full[i], 1);
       mbar_init(&kv_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
       mbar_init(&st_full[i], 1);
       mbar_init(&st_empty[i], 256);
     }
@@ -617,8 +625,8 @@ __global__ void __launch_bounds__(384, 1)
         tma_load_3d(&mdo, qo_full, sm + L::O + c * 16384, c * 64, h, tok0 + q0);
       }
       for (int it = 0; it < n_it; ++it) {
-        const int st = it & 1;
-        mbar_wait(&kv_empty[st], ((it >> 1) & 1) ^ 1);
+        const int st = it % NST;
+        mbar_wait(&kv_empty[st], ((it / NST) & 1) ^ 1);
         mbar_expect_tx(&kv_full[st], 2 * L::KT);
 #pragma unroll
         for (int c = 0; c < D / 64; ++c) {
@@ -635,7 +643,7 @@ __global__ void __launch_bounds__(384, 1)
       const uint32_t a_ds = smem_u32(sm + L::DS);
       mbar_wait(qo_full, 0);
       auto grads = [&](int it) {
-        const int st = it & 1;
+        const int st = it % NST;
         mbar_wait(ds_full, it & 1);
         tc_fence_after();
         const uint32_t b_k = smem_u32(sm + L::K0 + st * L::KT);
@@ -647,25 +655,25 @@ __global__ void __launch_bounds__(384, 1)
         umma_commit(&kv_empty[st]);
       };
       for (int it = 0; it < n_it; ++it) {
-        const int st = it & 1;
-        mbar_wait(&kv_full[st], (it >> 1) & 1);
-        mbar_wait(&st_empty[st], ((it >> 1) & 1) ^ 1);
+        const int st = it % NST, sb = it & 1;
+        mbar_wait(&kv_full[st], (it / NST) & 1);
+        mbar_wait(&st_empty[sb], ((it >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t b_k = smem_u32(sm + L::K0 + st * L::KT);
         const uint32_t b_v = smem_u32(sm + L::V0 + st * L::KT);
 #pragma unroll
         for (int k = 0; k < D / 16; ++k) {
           const uint32_t oa = (k >> 2) * 16384 + (k & 3) * 32, ob = (k >> 2) * 8192 + (k & 3) * 32;
-          umma_bf16(tmem + st * 128, sdesc(a_q + oa, 16, 1024), sdesc(b_k + ob, 16, 1024), id_s,
+          umma_bf16(tmem + sb * 128, sdesc(a_q + oa, 16, 1024), sdesc(b_k + ob, 16, 1024), id_s,
                     k != 0);
         }
 #pragma unroll
         for (int k = 0; k < D / 16; ++k) {
           const uint32_t oa = (k >> 2) * 16384 + (k & 3) * 32, ob = (k >> 2) * 8192 + (k & 3) * 32;
-          umma_bf16(tmem + st * 128 + 64, sdesc(a_o + oa, 16, 1024), sdesc(b_v + ob, 16, 1024),
+          umma_bf16(tmem + sb * 128 + 64, sdesc(a_o + oa, 16, 1024), sdesc(b_v + ob, 16, 1024),
                     id_s, k != 0);
         }
-        umma_commit(&st_full[st]);
+        umma_commit(&st_full[sb]);
         if (it > 0) grads(it - 1);
       }
       grads(n_it - 1);
