@@ -46,7 +46,12 @@ def parse():
     ap.add_argument("--cluster-profile", default=os.path.join(ROOT, "profiles", "b200_cluster.json"))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--plan-out", default=None)
-    ap.add_argument("--trace-out", default=None)
+    ap.add_argument("--trace-out", default=None,
+                    help="write the measured step timeline (pipesim JSONL schema) + sim diff")
+    ap.add_argument("--layer-pattern", default=None,
+                    help="explicit per-layer strategies instead of the search, cycled over "
+                         "layers, e.g. 'tp8,dp8z3,tp4dp2' (BASELINE config 4)")
+    ap.add_argument("--microbatch", type=int, default=None, help="with --layer-pattern")
     return ap.parse_args()
 
 
@@ -145,6 +150,33 @@ def plan_for(cfg, n: int, global_batch: int, cluster):
     return plan, get_hybrid_parallel_configs(plan, cfg), training
 
 
+def parse_pattern(text: str, n: int):
+    """'tp8,dp8z3,tp4dp2sp,tp1dp8rc' -> [ParallelStrategy] (tp*dp must equal n)."""
+    import re
+    from paper_2504_21411_b200.planner.strategy import ParallelStrategy
+    out = []
+    for tok in text.split(","):
+        m = re.fullmatch(r"(?:tp(\d+))?(?:dp(\d+))?(?:z(\d))?(sp)?(rc)?", tok.strip())
+        if not m:
+            raise SystemExit(f"bad strategy token {tok!r}")
+        tp = int(m.group(1) or (n // int(m.group(2)) if m.group(2) else 1))
+        dp = int(m.group(2) or n // tp)
+        out.append(ParallelStrategy(tp, dp, int(m.group(3) or 0), bool(m.group(4)),
+                                    bool(m.group(5))))
+    return out
+
+
+def explicit_plan(cfg, n, global_batch, cluster, pattern, microbatch):
+    from paper_2504_21411_b200.planner.profiles import TrainingConfig
+    from paper_2504_21411_b200.planner.search import make_plan
+    from paper_2504_21411_b200.runtime.config import get_hybrid_parallel_configs, profile_for
+    strats = parse_pattern(pattern, n)
+    layers = [strats[i % len(strats)] for i in range(cfg.n_layers)]
+    training = TrainingConfig(global_batch=global_batch)
+    plan = make_plan(profile_for(cfg), cluster, training, 1, microbatch, layers)
+    return plan, get_hybrid_parallel_configs(plan, cfg), training
+
+
 def describe(hc) -> str:
     kinds = []
     for s in hc.layer_strategies:
@@ -153,7 +185,14 @@ def describe(hc) -> str:
             kinds.append([k, 1])
         else:
             kinds[-1][1] += 1
-    layers = "+".join(f"{k}x{c}" for k, c in kinds)
+    names = [k for k, c in kinds for _ in range(c)]
+    for period in range(1, len(names) // 2 + 1):
+        if len(names) % period == 0 and names == names[:period] * (len(names) // period) \
+                and period > 1:
+            layers = "(" + "+".join(names[:period]) + f")x{len(names) // period}"
+            break
+    else:
+        layers = "+".join(f"{k}x{c}" for k, c in kinds)
     return f"pp{hc.pp} mb{hc.microbatch}x{hc.n_microbatches} [{layers}]"
 
 
@@ -233,7 +272,11 @@ def main():
     from paper_2504_21411_b200.runtime.init import synthetic_tokens
 
     cluster, cluster_src = cluster_profile(n, args.cluster_profile)
-    plan, hc, training = plan_for(cfg, n, gb, cluster)
+    if args.layer_pattern:
+        plan, hc, training = explicit_plan(cfg, n, gb, cluster, args.layer_pattern,
+                                           args.microbatch or max(n, 1))
+    else:
+        plan, hc, training = plan_for(cfg, n, gb, cluster)
     if args.plan_out and rank == 0:
         from paper_2504_21411_b200.planner.serialize import dumps_canonical
         with open(args.plan_out, "w") as fh:
@@ -327,6 +370,30 @@ def main():
                 "d2h_bytes_per_step": 4},
         "clocks": clk, "loss": loss_val, "peak_mem_gb": mem,
     }
+    if args.trace_out:
+        model.record_trace = True
+        model.trace.clear()
+        model.train_step(tokens_dev)
+        model.record_trace = False
+        measured = model.measured_trace()
+        from paper_2504_21411_b200.planner.pipesim import simulate, trace_to_jsonl, SimResult
+        from paper_2504_21411_b200.runtime.config import profile_for
+        sim = simulate(plan, profile_for(cfg), cluster, training)
+        def per_kind(events):
+            acc = {}
+            for e in events:
+                acc.setdefault(e.kind, []).append(e.duration)
+            return {k: {"n": len(v), "mean_s": sum(v) / len(v)} for k, v in acc.items()}
+        diff = {"measured": per_kind(measured),
+                "simulated": per_kind([e for e in sim.trace if e.device_stage == model.stage]),
+                "measured_makespan_s": sum(e.duration for e in measured),
+                "simulated_makespan_s": sim.makespan}
+        if rank == 0 or model.stage > 0:
+            with open(f"{args.trace_out}.rank{rank}.jsonl", "w") as fh:
+                fh.write(trace_to_jsonl(SimResult(0.0, (), tuple(measured), 0.0)))
+            with open(f"{args.trace_out}.rank{rank}.diff.json", "w") as fh:
+                json.dump(diff, fh, indent=1)
+        line["trace_diff"] = diff
     if rank == 0 and n == 1 and not args.no_cpu_baseline:
         tok_s, t1, cores, sample = cpu_reference(cfg, 1, 0)
         line["cpu_baseline"] = {"value": tok_s, "unit": "tokens/s", "cores": cores,
