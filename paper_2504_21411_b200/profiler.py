@@ -47,7 +47,7 @@ def _time_cuda(fn, iters: int = 5, warmup: int = 2) -> float:
     return a.elapsed_time(b) / iters / 1e3
 
 
-def measure_layer_flops(cfg, microbatch: int, *, iters: int = 3) -> dict:
+def measure_layer_flops(cfg, microbatch: int, *, iters: int = 3, sustain_s: float = 6.0) -> dict:
     """Effective FLOP/s of one decoder layer fwd+bwd (tp=1, dp=1) on this GPU."""
     from .runtime.config import HybridConfig, profile_for
     from .runtime.layers import DecoderLayer
@@ -74,7 +74,19 @@ def measure_layer_flops(cfg, microbatch: int, *, iters: int = 3) -> dict:
         y, ctx = layer.forward(x, microbatch)
         layer.backward(dy, ctx)
 
-    t = _time_cuda(step, iters=iters)
+    # sustained rate: the GPU runs at ~1 kW cap under a long training step, so time the
+    # layer back to back for `sustain_s` seconds and keep the steady-state second half
+    for _ in range(2):
+        step()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    n_runs = 0
+    while time.perf_counter() - t0 < sustain_s / 2:
+        step()
+        n_runs += 1
+        if n_runs % 4 == 0:
+            torch.cuda.synchronize()
+    t = _time_cuda(step, iters=max(iters, n_runs), warmup=0)
     lp = profile_for(cfg).layers[0]
     fwd_flops = lp.flops_per_token * T + lp.flops_per_token_sq * microbatch * cfg.seq_len ** 2
     return {"seconds_fwd_bwd": t, "fwd_flops": fwd_flops,
