@@ -100,6 +100,13 @@ class HybridConfig:
     stage_ranges: tuple
     layer_strategies: tuple
     predicted_iteration_time: float = float("nan")
+    # "megatron": sp=True layers run Megatron-SP (weights tp-sharded, AG/RS around GEMMs).
+    # "ulysses": sp=True layers run DeepSpeed-Ulysses over the same rank group: weights
+    #   replicated in the group (grads all-reduced over it), tokens sequence-sharded, two
+    #   all-to-alls (sequence <-> heads) around attention.  Runtime extension outside the
+    #   reference strategy space: the cost model's param/tp memory term
+    #   does not describe it.
+    sp_mode: str = "megatron"
 
     @property
     def global_batch(self) -> int:
@@ -124,6 +131,8 @@ class HybridConfig:
         if len(self.layer_strategies) != cfg.n_layers:
             raise ValidationError("one strategy per decoder layer required")
         width = self.devices_per_stage
+        if self.sp_mode not in ("megatron", "ulysses"):
+            raise ValidationError(f"unknown sp_mode {self.sp_mode!r}")
         for i, s in enumerate(self.layer_strategies):
             s.validate(width)
             if self.microbatch % s.dp:
@@ -135,7 +144,8 @@ class HybridConfig:
                 raise ValidationError(f"layer {i}: sp needs tokens divisible by tp")
 
 
-def get_hybrid_parallel_configs(plan, model_cfg: ModelConfig | None = None) -> HybridConfig:
+def get_hybrid_parallel_configs(plan, model_cfg: ModelConfig | None = None, *,
+                                sp_mode: str = "megatron") -> HybridConfig:
     """Plan object, Plan dict, or path to a Plan JSON -> HybridConfig (validated)."""
     if isinstance(plan, (str, bytes)) or hasattr(plan, "__fspath__"):
         with open(plan, "r", encoding="utf-8") as fh:
@@ -148,7 +158,7 @@ def get_hybrid_parallel_configs(plan, model_cfg: ModelConfig | None = None) -> H
                       n_microbatches=plan.n_microbatches,
                       stage_ranges=tuple(tuple(r) for r in plan.stage_ranges),
                       layer_strategies=tuple(plan.layer_strategies),
-                      predicted_iteration_time=plan.predicted_iteration_time)
+                      predicted_iteration_time=plan.predicted_iteration_time, sp_mode=sp_mode)
     if model_cfg is not None:
         hc.validate(model_cfg)
     return hc

@@ -79,7 +79,7 @@ class HybridParallelModel:
     def _init_params(self, seed, mode, perturb, weights):
         cfg = self.cfg
         for prefix, store, owner in self.stores():
-            tp, r = owner.tp, owner.tpr
+            tp, r = getattr(owner, "wtp", owner.tp), getattr(owner, "wtpr", owner.tpr)
             local = {}
             for name, (_, shape) in store.layout.items():
                 full_name = prefix + name
@@ -291,7 +291,7 @@ class HybridParallelModel:
             views = store.views(flat)
             for name, v in views.items():
                 parts = [v]
-                if owner.tp > 1:
+                if getattr(owner, "wtp", owner.tp) > 1:
                     g = torch.empty((owner.tp,) + tuple(v.shape), dtype=v.dtype, device=v.device)
                     dist.all_gather_into_tensor(g, v.contiguous(), group=owner.tpg.group)
                     parts = list(g.unbind(0))

@@ -119,22 +119,30 @@ class DecoderLayer:
         self.tpg = topo.tp(strategy.tp)
         self.dpg = topo.dp(strategy.tp)
         self.tp, self.tpr = strategy.tp, self.tpg.index
+        # Ulysses: sp layers keep full weights in the group and shard only the sequence
+        self.uly = bool(strategy.sp and strategy.tp > 1 and topo.hc.sp_mode == "ulysses")
+        self.wtp, self.wtpr = (1, 0) if self.uly else (self.tp, self.tpr)
         h, f = cfg.hidden, cfg.ffn
-        self.hl, self.fl, self.Hl = h // self.tp, f // self.tp, cfg.heads // self.tp
+        self.hl, self.fl = h // self.wtp, f // self.wtp       # GEMM widths
+        self.Hl = cfg.heads // self.tp                        # attention heads per rank
+        self.ahl = self.Hl * cfg.head_dim                     # attention width per rank
         from .init import layer_param_shapes
         shapes = layer_param_shapes(cfg)
         local = {}
         for n, shp in shapes.items():
-            local[n] = tuple(tp_slice(cfg, n, torch.empty(shp, device="meta"), self.tp,
-                                      self.tpr).shape)
+            local[n] = tuple(tp_slice(cfg, n, torch.empty(shp, device="meta"), self.wtp,
+                                      self.wtpr).shape)
         self.names = list(shapes)
         self.store = ParamStore([(n, local[n]) for n in self.names], dtype=dtype,
                                 grad_dtype=grad_dtype, device=device, dp=self.dpg,
                                 zero=strategy.zero_stage,
-                                small_names=[n for n in self.names if _is_small(n)])
-        # replicated params whose grads are token-partial under sp
-        self.tp_partial = [n for n in self.names if _is_small(n) and strategy.sp and
-                           n not in ("qkv.bias", "fc1.bias")]
+                                small_names=[n for n in self.names if _is_small(n)],
+                                extra_allreduce=self.tpg if self.uly else None)
+        # replicated params whose grads are token-partial under Megatron-SP
+        self.tp_partial = [] if self.uly else [
+            n for n in self.names if _is_small(n) and strategy.sp and
+            n not in ("qkv.bias", "fc1.bias")]
+        self._uly_idx = {}
         self.scale = 1.0 / math.sqrt(cfg.head_dim)
         self._ws = None
 
@@ -143,10 +151,10 @@ class DecoderLayer:
 
     # -------------------------------------------------------------- forward
     def _gather_seq(self, t):
-        return comm.all_gather(t, self.tpg) if self.s.sp else t
+        return comm.all_gather(t, self.tpg) if (self.s.sp and not self.uly) else t
 
     def _reduce_out(self, t):
-        if self.tp == 1:
+        if self.tp == 1 or self.uly:
             return t
         if self.s.sp:
             return comm.reduce_scatter(t, self.tpg)
@@ -172,8 +180,78 @@ class DecoderLayer:
         return K.rmsnorm_bwd(x, w[prefix + ".weight"], rstd, dy, sg[prefix + ".weight"],
                              dres=dres)
 
+    # ------------------------------------------------------------- Ulysses all-to-alls
+    def _uly_maps(self, Tl):
+        """Row-index maps (rows = one head vector) for the sequence<->head all-to-alls."""
+        key = Tl
+        if key not in self._uly_idx:
+            u, H, Hl = self.tp, self.cfg.heads, self.Hl
+            dev = self.device
+            j = torch.arange(u).view(u, 1, 1, 1)
+            t = torch.arange(Tl).view(1, Tl, 1, 1)
+            p = torch.arange(3).view(1, 1, 3, 1)
+            hh = torch.arange(Hl).view(1, 1, 1, Hl)
+            # pack for qkv: local [Tl, 3, H] rows -> (dest j, t, p, hl)
+            qkv_pack = (t * (3 * H) + p * H + j * Hl + hh).reshape(-1)
+            jj = torch.arange(u).view(u, 1, 1)
+            tt = torch.arange(Tl).view(1, Tl, 1)
+            h2 = torch.arange(Hl).view(1, 1, Hl)
+            # o: received (src r, t, hl) -> local [Tl, H] row t*H + r*Hl + hl
+            o_unpack = (tt * H + jj * Hl + h2).reshape(-1)
+            self._uly_idx[key] = (qkv_pack.to(dev), o_unpack.to(dev))
+        return self._uly_idx[key]
+
+    def _uly_qkv_to_heads(self, qkv_local):
+        """[Tl, 3h] (all heads, local tokens) -> [T, 3*Hl*D] (local heads, all tokens)."""
+        Tl, D = qkv_local.shape[0], self.cfg.head_dim
+        pack, _ = self._uly_maps(Tl)
+        rows = qkv_local.view(-1, D)
+        send = torch.empty(pack.numel(), D, dtype=qkv_local.dtype, device=qkv_local.device)
+        K.gather_rows(rows, pack, send)
+        out = torch.empty(Tl * self.tp, 3 * self.ahl, dtype=qkv_local.dtype,
+                          device=qkv_local.device)
+        n = send.shape[0] // self.tp
+        comm.all_to_all(out.view(-1, D), send, [n] * self.tp, [n] * self.tp, self.tpg)
+        return out
+
+    def _uly_heads_to_qkv(self, dqkv_full):
+        """inverse of _uly_qkv_to_heads (gradient direction)."""
+        T, D = dqkv_full.shape[0], self.cfg.head_dim
+        Tl = T // self.tp
+        pack, _ = self._uly_maps(Tl)
+        recv = torch.empty(pack.numel(), D, dtype=dqkv_full.dtype, device=dqkv_full.device)
+        n = recv.shape[0] // self.tp
+        comm.all_to_all(recv, dqkv_full.view(-1, D), [n] * self.tp, [n] * self.tp, self.tpg)
+        out = torch.empty(Tl, 3 * self.cfg.hidden, dtype=dqkv_full.dtype,
+                          device=dqkv_full.device)
+        K.scatter_rows(recv, pack, out.view(-1, D))
+        return out
+
+    def _uly_o_to_tokens(self, o_full):
+        """[T, Hl*D] -> [Tl, h]: attention output back to the local tokens, all heads."""
+        T, D = o_full.shape[0], self.cfg.head_dim
+        Tl = T // self.tp
+        _, unpack = self._uly_maps(Tl)
+        recv = torch.empty(T * self.Hl, D, dtype=o_full.dtype, device=o_full.device)
+        n = recv.shape[0] // self.tp
+        comm.all_to_all(recv, o_full.view(-1, D), [n] * self.tp, [n] * self.tp, self.tpg)
+        out = torch.empty(Tl, self.cfg.hidden, dtype=o_full.dtype, device=o_full.device)
+        K.scatter_rows(recv, unpack, out.view(-1, D))
+        return out
+
+    def _uly_tokens_to_o(self, do_local):
+        """inverse of _uly_o_to_tokens (gradient direction)."""
+        Tl, D = do_local.shape[0], self.cfg.head_dim
+        _, unpack = self._uly_maps(Tl)
+        send = torch.empty(unpack.numel(), D, dtype=do_local.dtype, device=do_local.device)
+        K.gather_rows(do_local.view(-1, D), unpack, send)
+        out = torch.empty(Tl * self.tp, self.ahl, dtype=do_local.dtype, device=do_local.device)
+        n = send.shape[0] // self.tp
+        comm.all_to_all(out.view(-1, D), send, [n] * self.tp, [n] * self.tp, self.tpg)
+        return out
+
     def _attn_views(self, qkv, B, S):
-        hl, D = self.hl, self.cfg.head_dim
+        hl, D = self.ahl, self.cfg.head_dim
         st = qkv.stride(0)
         base = qkv.storage_offset()
         mk = lambda j: qkv.as_strided((B, S, self.Hl, D), (S * st, st, D, 1), base + j * hl)
@@ -190,18 +268,24 @@ class DecoderLayer:
         n1f = self._gather_seq(n1)
         T = n1f.shape[0]
         qkv = _linear(n1f, w["qkv.weight"], bias=w["qkv.bias"] if gpt else None)
+        if self.uly:
+            qkv = self._uly_qkv_to_heads(qkv)
+            T = qkv.shape[0]
         q, k, v = self._attn_views(qkv, B, S)
         if not gpt:
             for j in (0, 1):
                 K.rope_(qkv.as_strided((T, self.Hl, cfg.head_dim),
                                        (qkv.stride(0), cfg.head_dim, 1),
-                                       qkv.storage_offset() + j * self.hl),
+                                       qkv.storage_offset() + j * self.ahl),
                         S, theta=cfg.rope_theta)
-        o = torch.empty(T, self.hl, device=x.device, dtype=x.dtype)
+        o = torch.empty(T, self.ahl, device=x.device, dtype=x.dtype)
         lse = torch.empty(B, self.Hl, S, device=x.device, dtype=torch.float32)
         K.attn_fwd(q, k, v, o.view(B, S, self.Hl, cfg.head_dim), lse, scale=self.scale,
                    causal=True)
-        fuse_bias = gpt and self.tp == 1
+        o_full = o
+        if self.uly:
+            o = self._uly_o_to_tokens(o_full)
+        fuse_bias = gpt and self.wtp == 1
         a = _linear(o, w["proj.weight"], bias=w["proj.bias"] if fuse_bias else None)
         a = self._reduce_out(a)
         if gpt and not fuse_bias:
@@ -222,8 +306,8 @@ class DecoderLayer:
             K.bias_add_(m, w["fc2.bias"])
         y = K.axpby(h1, m, 1.0, 1.0)
         if save:
-            saved = dict(x=x, st1=st1, n1f=n1f, qkv=qkv, o=o, lse=lse, h1=h1, st2=st2, n2f=n2f,
-                         act=act, B=B)
+            saved = dict(x=x, st1=st1, n1f=n1f, qkv=qkv, o=o, o_full=o_full, lse=lse, h1=h1,
+                         st2=st2, n2f=n2f, act=act, B=B)
             saved["pre"] = f1 if gpt else gu
             return y, saved
         return y, None
@@ -284,6 +368,8 @@ class DecoderLayer:
         do = _dgrad(daf, w["proj.weight"])
         _wgrad(daf, sv["o"], gw["proj.weight"])
         del daf
+        if self.uly:
+            do = self._uly_tokens_to_o(do)
         qkv = sv["qkv"]
         T = qkv.shape[0]
         dqkv = torch.empty_like(qkv)
@@ -292,7 +378,7 @@ class DecoderLayer:
         need = K.attn_bwd_workspace_bytes(B, S, self.Hl, cfg.head_dim, qkv.dtype)
         if self._ws is None or self._ws.numel() < need:
             self._ws = torch.empty(need, dtype=torch.uint8, device=qkv.device)
-        K.attn_bwd(q, k, v, sv["o"].view(B, S, self.Hl, cfg.head_dim),
+        K.attn_bwd(q, k, v, sv["o_full"].view(B, S, self.Hl, cfg.head_dim),
                    do.view(B, S, self.Hl, cfg.head_dim), sv["lse"], dq, dk, dv,
                    scale=self.scale, causal=True, workspace=self._ws)
         del do
@@ -300,8 +386,10 @@ class DecoderLayer:
             for j in (0, 1):
                 K.rope_(dqkv.as_strided((T, self.Hl, cfg.head_dim),
                                         (dqkv.stride(0), cfg.head_dim, 1),
-                                        dqkv.storage_offset() + j * self.hl),
+                                        dqkv.storage_offset() + j * self.ahl),
                         S, theta=cfg.rope_theta, inverse=True)
+        if self.uly:
+            dqkv = self._uly_heads_to_qkv(dqkv)
         if gpt:
             K.colsum(dqkv, sg["qkv.bias"])
         dn1f = _dgrad(dqkv, w["qkv.weight"])

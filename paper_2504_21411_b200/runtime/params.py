@@ -32,9 +32,11 @@ def _roundup(x: int, m: int) -> int:
 
 class ParamStore:
     def __init__(self, entries, *, dtype, grad_dtype, device, dp, zero: int,
-                 small_names=()):
+                 small_names=(), extra_allreduce=None):
         """entries: ordered list of (name, local_shape)."""
         self.dtype, self.grad_dtype, self.device = dtype, grad_dtype, device
+        # group whose members hold token-partial grads of replicated weights (Ulysses)
+        self.extra = extra_allreduce
         self.dp = dp                          # GroupHandle or None
         self.ndp = dp.size if dp is not None else 1
         self.rank_dp = dp.index if dp is not None else 0
@@ -131,11 +133,14 @@ class ParamStore:
             K.axpby(g, views[n], 1.0, 1.0)
         self.acc32.zero_()
         if self.zero >= 2:
+            comm.all_reduce(target, self.extra)
             part = comm.reduce_scatter(target, self.dp)
             K.axpby(part, self.g_shard, 1.0, 1.0)
 
     def sync(self) -> None:
         """End of the accumulation window: dp reduction of the gradients."""
+        if self.zero < 2:
+            comm.all_reduce(self.g_full, self.extra)
         if self.zero == 0:
             comm.all_reduce(self.g_full, self.dp)
             self._owned_grad = self.g_full

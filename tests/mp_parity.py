@@ -22,10 +22,10 @@ from paper_2504_21411_b200.planner.strategy import ParallelStrategy as PS  # noq
 from paper_2504_21411_b200.runtime.config import HybridConfig  # noqa: E402
 
 
-def hc(strats, *, pp=1, mb=2, m=2):
+def hc(strats, *, pp=1, mb=2, m=2, sp_mode="megatron"):
     return HybridConfig(pp=pp, microbatch=mb, n_microbatches=m,
                         stage_ranges=near_equal_split(len(strats), pp),
-                        layer_strategies=tuple(strats))
+                        layer_strategies=tuple(strats), sp_mode=sp_mode)
 
 
 F32, BF16 = torch.float32, torch.bfloat16
@@ -47,6 +47,14 @@ SCENARIOS = {
     "mixed2_bf16": (2, "tiny-llama", hc([PS(2, 1, 0, True, False), PS(1, 2, 2, False, True),
                                          PS(2, 1, 0, False, False), PS(1, 2, 0, False, False)]),
                     BF16, 2e-2),
+    "uly2": (2, "micro-llama", hc([PS(2, 1, 0, True, False)] * 2, sp_mode="ulysses"), F32, 1e-5),
+    "uly2_gpt_rc_mixed": (2, "tiny-gpt", hc([PS(2, 1, 0, True, True), PS(1, 2, 1, False, False),
+                                             PS(2, 1, 0, False, False), PS(2, 1, 0, True, False)],
+                                            sp_mode="ulysses"), F32, 1e-5),
+    "uly2_bf16": (2, "tiny-llama", hc([PS(2, 1, 0, True, False)] * 4, sp_mode="ulysses"),
+                  BF16, 2e-2),
+    "uly4_z3": (4, "micro-llama", hc([PS(4, 1, 0, True, True), PS(2, 2, 3, True, False)],
+                                     mb=2, sp_mode="ulysses"), F32, 1e-5),
     "tp2dp2": (4, "micro-llama", hc([PS(2, 2, 1, True, False)] * 2, mb=2), F32, 1e-5),
     "pp2_tp2": (4, "tiny-llama", hc([PS(2, 1, 0, False, False), PS(1, 2, 2, False, False),
                                      PS(2, 1, 0, True, True), PS(2, 1, 0, False, False)],
