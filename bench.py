@@ -52,6 +52,8 @@ def parse():
                     help="explicit per-layer strategies instead of the search, cycled over "
                          "layers, e.g. 'tp8,dp8z3,tp4dp2' (BASELINE config 4)")
     ap.add_argument("--microbatch", type=int, default=None, help="with --layer-pattern")
+    ap.add_argument("--sp-mode", choices=("megatron", "ulysses"), default="megatron",
+                    help="how sp=True layers run: Megatron-SP or DeepSpeed-Ulysses")
     return ap.parse_args()
 
 
@@ -277,6 +279,9 @@ def main():
                                            args.microbatch or max(n, 1))
     else:
         plan, hc, training = plan_for(cfg, n, gb, cluster)
+    if args.sp_mode != "megatron":
+        import dataclasses
+        hc = dataclasses.replace(hc, sp_mode=args.sp_mode)
     if args.plan_out and rank == 0:
         from paper_2504_21411_b200.planner.serialize import dumps_canonical
         with open(args.plan_out, "w") as fh:
@@ -350,7 +355,8 @@ def main():
         "data": "synthetic tokens (seeded randint), random-init weights",
         "config": {"workload": f"{cfg.name} training step (fwd+bwd+AdamW)", "model": cfg.name,
                    "global_batch": gb, "seq_len": cfg.seq_len,
-                   "parallelism": describe(hc),
+                   "parallelism": describe(hc) + ("" if hc.sp_mode == "megatron"
+                                                  else f" sp_mode={hc.sp_mode}"),
                    "l2": "working set (weights/activations) >> 126 MB L2; no flush"},
         "mfu": mfu, "mfu_basis": "2.25 PFLOP/s dense bf16 per GPU",
         "flops_per_token": flops_tok,
