@@ -204,10 +204,16 @@ __global__ void __launch_bounds__(384, 1)
       const int k0 = j * BKV + half * HC;
       const bool mask = (k0 + HC > p.S) || (p.causal && k0 + HC - 1 > q0);
       float mx = -INFINITY;
+      if (mask) {  // diagonal / tail block: keys >= lim are invisible to this row
+        const int lim = (p.causal ? min(p.S, qi + 1) : p.S) - k0;
 #pragma unroll
-      for (int i = 0; i < HC; ++i) {
-        if (mask && (k0 + i >= p.S || (p.causal && k0 + i > qi))) s[i] = -INFINITY;
-        mx = fmaxf(mx, s[i]);
+        for (int i = 0; i < HC; ++i) {
+          s[i] = i < lim ? s[i] : -INFINITY;
+          mx = fmaxf(mx, s[i]);
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < HC; ++i) mx = fmaxf(mx, s[i]);
       }
       // combine the two halves' row maxima (pair barrier: 64 threads of this quarter)
       xch[(j & 1) * 256 + half * 128 + r] = mx;
@@ -522,13 +528,22 @@ __global__ void __launch_bounds__(384, 1)
       const float* l2 = reinterpret_cast<const float*>(sm + L::LSE + st * 256) + half * 32;
       const float* dd = reinterpret_cast<const float*>(sm + L::DV + st * 256) + half * 32;
       const int qbase = q0 + half * 32;
-      const bool need_mask = p.causal && (key > qbase);
+      const float sl2 = p.scale_log2;
+      if (p.causal && key > qbase) {  // diagonal: queries < key are masked
+        const int first = key - qbase;  // first visible query index in this half
 #pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        float pv = exp2_mufu(fmaf(s[i], p.scale_log2, -l2[i]));
-        if (need_mask && key > qbase + i) pv = 0.f;
-        s[i] = pv;
-        dp[i] = pv * (dp[i] - dd[i]);
+        for (int i = 0; i < 32; ++i) {
+          const float pv = i >= first ? exp2_mufu(fmaf(s[i], sl2, -l2[i])) : 0.f;
+          s[i] = pv;
+          dp[i] = pv * (dp[i] - dd[i]);
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const float pv = exp2_mufu(fmaf(s[i], sl2, -l2[i]));
+          s[i] = pv;
+          dp[i] = pv * (dp[i] - dd[i]);
+        }
       }
       if (it > 0) mbar_wait(mm_done, (it - 1) & 1);
       store_half_row(sm + L::PT, r, half, s);
@@ -695,12 +710,20 @@ __global__ void __launch_bounds__(384, 1)
       tc_fence_before();
       mbar_arrive(&st_empty[st]);
       const int kbase = it * 64 + half * 32;
-      const bool need_mask = (kbase + 32 > p.S) || (p.causal && kbase + 31 > qi);
+      const float sl2 = p.scale_log2;
+      if ((kbase + 32 > p.S) || (p.causal && kbase + 31 > qi)) {
+        const int lim = (p.causal ? min(p.S, qi + 1) : p.S) - kbase;
 #pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        float pv = exp2_mufu(fmaf(s[i], p.scale_log2, -l2));
-        if (need_mask && (kbase + i >= p.S || (p.causal && kbase + i > qi))) pv = 0.f;
-        dp[i] = pv * (dp[i] - dd);
+        for (int i = 0; i < 32; ++i) {
+          const float pv = i < lim ? exp2_mufu(fmaf(s[i], sl2, -l2)) : 0.f;
+          dp[i] = pv * (dp[i] - dd);
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const float pv = exp2_mufu(fmaf(s[i], sl2, -l2));
+          dp[i] = pv * (dp[i] - dd);
+        }
       }
       if (it > 0) mbar_wait(dq_done, (it - 1) & 1);
       store_half_row(sm + L::DS, r, half, dp);
