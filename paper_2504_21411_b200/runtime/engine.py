@@ -121,7 +121,9 @@ class HybridParallelModel:
         else:
             x = x_in
         prev = None
-        for layer in self.layers:
+        for idx, layer in enumerate(self.layers):
+            if idx + 1 < len(self.layers):
+                self.layers[idx + 1].store.prefetch()
             lay = Layout.of(layer.s)
             if prev is not None and prev != lay:
                 x = self.resharder(x, prev, lay, T)
@@ -148,7 +150,14 @@ class HybridParallelModel:
     def _bwd(self, rec, dy):
         T = self.hc.microbatch * self.cfg.seq_len
         dx = rec.pop("head_dx") if self.last else dy
-        for item in reversed(rec["ctxs"]):
+        items = list(reversed(rec["ctxs"]))
+        layer_items = [it for it in items if it[0] == "layer"]
+        if layer_items:
+            layer_items[0][1].store.prefetch()
+        nxt_layer = {id(a[1]): b[1] for a, b in zip(layer_items, layer_items[1:])}
+        for item in items:
+            if item[0] == "layer" and id(item[1]) in nxt_layer:
+                nxt_layer[id(item[1])].store.prefetch()
             if item[0] == "reshard":
                 _, src, dst = item
                 dx = self.resharder(dx, dst, src, T)
@@ -216,6 +225,9 @@ class HybridParallelModel:
                         grads[nxt[1] - 1] = buf
                     self._p2p(p2p)
             else:
+                if k1 == m:  # last microbatch: layers launch their dp sync as they finish
+                    for _, store, _ in self.stores():
+                        store.last_window = True
                 if not self.last and k not in grads:
                     buf, op = recv_bwd(k)
                     self._p2p([op])

@@ -19,9 +19,15 @@ from __future__ import annotations
 import math
 
 import torch
+import torch.distributed as dist
 
 from .. import kernels as K
 from . import comm
+
+
+def _async(fn, *args, **kw):
+    """Launch a torch.distributed collective asynchronously (None for single-rank groups)."""
+    return fn(*args, async_op=True, **kw)
 
 ALIGN = 64
 
@@ -74,7 +80,13 @@ class ParamStore:
         self.acc32 = torch.zeros(max(soff, 1), dtype=torch.float32, **kw)
         self.master = self.m = self.v = None
         self._gathered = None
+        self._gather_work = None
         self._owned_grad = None
+        # overlap state: collectives in flight on NCCL streams, drained before use
+        self.pending: list = []       # (work, finalize callback, keep-alive refs)
+        self.last_window = False      # set by the engine for the last microbatch's backward
+        self._synced = False
+        self._param_ag = None
 
     # ------------------------------------------------------------------ values
     def views(self, flat: torch.Tensor) -> dict:
@@ -106,15 +118,31 @@ class ParamStore:
         self.v = torch.zeros_like(owned)
 
     def materialize(self) -> torch.Tensor:
-        """Full flat parameters (z3: all-gather into a transient buffer)."""
+        """Full flat parameters (z3: all-gather into a transient buffer, maybe prefetched)."""
+        if self._param_ag is not None:  # post-step param all-gather still in flight
+            self._param_ag[0].wait()
+            self._param_ag = None
         if self.zero < 3:
             return self.p_full
         if self._gathered is None:
-            self._gathered = comm.all_gather(self.p_shard, self.dp)
+            self.prefetch()
+        if self._gather_work is not None:
+            self._gather_work.wait()
+            self._gather_work = None
         return self._gathered
+
+    def prefetch(self) -> None:
+        """z3: start the parameter all-gather for the next use on the dp NCCL stream."""
+        if self.zero < 3 or self._gathered is not None:
+            return
+        out = torch.empty(self.total, dtype=self.dtype, device=self.device)
+        self._gather_work = _async(dist.all_gather_into_tensor, out, self.p_shard,
+                                   group=self.dp.group)
+        self._gathered = out
 
     def release(self) -> None:
         self._gathered = None
+        self._gather_work = None
 
     # ------------------------------------------------------------------ grads
     def grad_target(self) -> torch.Tensor:
@@ -123,7 +151,10 @@ class ParamStore:
         return self.g_full
 
     def finish_microbatch(self, target: torch.Tensor, tp_partial=(), tp_group=None) -> None:
-        """Fold the fp32 small-entry grads in, and (z>=2) reduce-scatter into the shard."""
+        """Fold the fp32 small-entry grads in; launch this layer's gradient collective
+        asynchronously so it overlaps the backward of the layers below:
+        z>=2 reduce-scatter into the shard accumulator every microbatch; z0/z1 the dp
+        all-reduce / reduce-scatter after the last microbatch (DDP-style)."""
         sg = self.small_grads()
         for n in tp_partial:
             if n in sg:
@@ -134,25 +165,52 @@ class ParamStore:
         self.acc32.zero_()
         if self.zero >= 2:
             comm.all_reduce(target, self.extra)
-            part = comm.reduce_scatter(target, self.dp)
-            K.axpby(part, self.g_shard, 1.0, 1.0)
+            part = torch.empty(self.shard, dtype=self.grad_dtype, device=self.device)
+            work = _async(dist.reduce_scatter_tensor, part, target, group=self.dp.group)
+            self.pending.append((work, lambda part=part: K.axpby(part, self.g_shard, 1.0, 1.0),
+                                 (target, part)))
+        elif self.last_window:
+            self._launch_sync()
 
-    def sync(self) -> None:
-        """End of the accumulation window: dp reduction of the gradients."""
+    def _launch_sync(self) -> None:
+        if self._synced:
+            return
+        self._synced = True
         if self.zero < 2:
             comm.all_reduce(self.g_full, self.extra)
         if self.zero == 0:
-            comm.all_reduce(self.g_full, self.dp)
             self._owned_grad = self.g_full
+            if self.ndp > 1:
+                self.pending.append((_async(dist.all_reduce, self.g_full, group=self.dp.group),
+                                     None, ()))
         elif self.zero == 1:
-            self._owned_grad = comm.reduce_scatter(self.g_full, self.dp)
+            out = torch.empty(self.shard, dtype=self.grad_dtype, device=self.device)
+            self._owned_grad = out
+            self.pending.append((_async(dist.reduce_scatter_tensor, out, self.g_full,
+                                        group=self.dp.group), None, (out,)))
         else:
             self._owned_grad = self.g_shard
+
+    def drain(self) -> None:
+        """Wait for this store's in-flight collectives and apply their epilogues."""
+        for work, fin, _keep in self.pending:
+            work.wait()
+            if fin is not None:
+                fin()
+        self.pending.clear()
+
+    def sync(self) -> None:
+        """End of the accumulation window: dp reduction of the gradients."""
+        self.drain()
+        self._launch_sync()
+        self.drain()
+        self.last_window = False
 
     def owned_grad(self) -> torch.Tensor:
         return self._owned_grad
 
     def zero_grads(self) -> None:
+        self._synced = False
         if self.g_full is not None:
             self.g_full.zero_()
         if self.g_shard is not None:
@@ -178,7 +236,9 @@ class ParamStore:
         K.adamw(self.master, self.m, self.v, g, out, lr=lr, beta1=beta1, beta2=beta2, eps=eps,
                 weight_decay=weight_decay, step=step, grad_scale=grad_scale)
         if self.zero in (1, 2):
-            comm.all_gather(out.clone(), self.dp, out=self.p_full)
+            src = out.clone()
+            self._param_ag = (_async(dist.all_gather_into_tensor, self.p_full, src,
+                                     group=self.dp.group), src)
 
     def memory_bytes(self) -> dict:
         def nb(t):
