@@ -24,7 +24,9 @@ int sm_count() {
 int32_t gemm_bf16_sm100(const void* A, const void* B, void* C, const void* bias, int64_t M,
                         int64_t N, int64_t K, int64_t lda, int64_t ldb, int64_t ldc,
                         int32_t trans_a, int32_t trans_b, float alpha, int32_t accumulate,
-                        int32_t c_dtype, int32_t bias_dtype, cudaStream_t stream);
+                        int32_t c_dtype, int32_t bias_dtype, cudaStream_t stream,
+                        void* const* peer_c = nullptr, int64_t rows_per_rank = 0,
+                        int32_t my_slot = 0);
 int32_t gemm_f32_simt(const float* A, const float* B, void* C, const float* bias, int64_t batch,
                       int64_t sa, int64_t sb, int64_t sc, int64_t M, int64_t N, int64_t K,
                       int64_t lda, int64_t ldb, int64_t ldc, int32_t ta, int32_t tb, float alpha,

@@ -38,6 +38,10 @@ struct Params {
   float alpha;
   int accumulate;
   int tiles_m, tiles_n, num_tiles, k_blocks;
+  // fused reduce-scatter epilogue over NVLink peer memory (tensor-parallel row GEMMs):
+  // row r goes to rank j = r / rows_per_rank, slot `my_slot`, of that rank's receive buffer
+  void* const* peer_c;
+  int rows_per_rank, my_slot;
 };
 
 __device__ __forceinline__ void tile_coords(const Params& p, int t, int& mt, int& nt) {
@@ -55,6 +59,13 @@ __device__ __forceinline__ void tile_coords(const Params& p, int t, int& mt, int
 __device__ __forceinline__ void epilogue_tile(const Params& p, uint32_t taddr, int row,
                                               int col_base, bool vec_ok) {
   const bool row_ok = row < p.M;
+  char* cbase = reinterpret_cast<char*>(p.C);
+  long long row_off = (long long)row * p.ldc;
+  if (p.peer_c != nullptr && row_ok) {  // store straight into the owning rank's buffer
+    const int j = row / p.rows_per_rank;
+    cbase = reinterpret_cast<char*>(p.peer_c[j]);
+    row_off = (long long)(p.my_slot * p.rows_per_rank + (row - j * p.rows_per_rank)) * p.ldc;
+  }
 #pragma unroll 1
   for (int cc = 0; cc < BN; cc += 32) {
     uint32_t r[32];
@@ -71,9 +82,9 @@ __device__ __forceinline__ void epilogue_tile(const Params& p, uint32_t taddr, i
                                   reinterpret_cast<const __nv_bfloat16*>(p.bias)[col0 + i])
                             : reinterpret_cast<const float*>(p.bias)[col0 + i];
     }
-    const long long off = (long long)row * p.ldc + col0;
+    const long long off = row_off + col0;
     if (p.c_bf16) {
-      __nv_bfloat16* c = reinterpret_cast<__nv_bfloat16*>(p.C) + off;
+      __nv_bfloat16* c = reinterpret_cast<__nv_bfloat16*>(cbase) + off;
       if (ncol == 32 && vec_ok) {
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
@@ -91,7 +102,7 @@ __device__ __forceinline__ void epilogue_tile(const Params& p, uint32_t taddr, i
         }
       }
     } else {
-      float* c = reinterpret_cast<float*>(p.C) + off;
+      float* c = reinterpret_cast<float*>(cbase) + off;
       if (ncol == 32 && (p.ldc % 4) == 0) {
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
@@ -438,7 +449,9 @@ static bool make_map(CUtensorMap* map, const void* base, uint64_t inner, uint64_
 int32_t gemm_bf16_sm100(const void* A, const void* B, void* C, const void* bias, int64_t M,
                         int64_t N, int64_t K, int64_t lda, int64_t ldb, int64_t ldc,
                         int32_t trans_a, int32_t trans_b, float alpha, int32_t accumulate,
-                        int32_t c_dtype, int32_t bias_dtype, cudaStream_t stream) {
+                        int32_t c_dtype, int32_t bias_dtype, cudaStream_t stream,
+                        void* const* peer_c = nullptr, int64_t rows_per_rank = 0,
+                        int32_t my_slot = 0) {
   using namespace tc;
   GALV_CHECK_ARG(M > 0 && N > 0 && K > 0, "empty problem");
   GALV_CHECK_ARG(M < (1ll << 31) && N < (1ll << 31) && K < (1ll << 31), "problem too large");
@@ -469,6 +482,9 @@ int32_t gemm_bf16_sm100(const void* A, const void* B, void* C, const void* bias,
   p.tiles_n = (int)((N + BN - 1) / BN);
   p.num_tiles = p.tiles_m * p.tiles_n;
   p.k_blocks = (int)((K + BK - 1) / BK);
+  p.peer_c = peer_c;
+  p.rows_per_rank = (int)rows_per_rank;
+  p.my_slot = my_slot;
   static bool attr_set = false;
   if (!attr_set) {
     GALV_CUDA_RET(cudaFuncSetAttribute(gemm_bf16_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -502,3 +518,14 @@ int32_t gemm_bf16_sm100(const void* A, const void* B, void* C, const void* bias,
 }
 
 }  // namespace galv
+
+extern "C" int32_t galv_gemm_rs(const void* A, const void* B, void* const* peer_c,
+                                int64_t rows_per_rank, int32_t my_slot, int64_t M, int64_t N,
+                                int64_t K, int64_t lda, int64_t ldb, int64_t ldc, int32_t trans_a,
+                                int32_t trans_b, void* stream) {
+  GALV_CHECK_ARG(A && B && peer_c && rows_per_rank > 0 && M % rows_per_rank == 0,
+                 "bad arguments");
+  return galv::gemm_bf16_sm100(A, B, nullptr, nullptr, M, N, K, lda, ldb, ldc, trans_a, trans_b,
+                               1.0f, 0, GALV_BF16, GALV_F32, galv::as_stream(stream), peer_c,
+                               rows_per_rank, my_slot);
+}

@@ -30,6 +30,10 @@ _SIGS = {
                    _I32, _I32, _I32, _P], _I32),
     "galv_gemm_batched": ([_P, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _I64,
                            _I64, _I32, _I32, _F, _I32, _I32, _I32, _P], _I32),
+    "galv_gemm_rs": ([_P, _P, _P, _I64, _I32, _I64, _I64, _I64, _I64, _I64, _I64, _I32, _I32,
+                      _P], _I32),
+    "galv_tp_signal_reduce": ([_P, _I32, _I32, C.c_uint32, _P, _P, _I64, _I32, _P], _I32),
+    "galv_tp_allgather": ([_P, _P, _P, _I32, _I32, C.c_uint32, _I64, _P], _I32),
     "galv_attn_fwd": ([_P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _F, _I32,
                        _I32, _P], _I32),
     "galv_attn_bwd_workspace": ([_I64, _I64, _I64, _I64, _I32], _I64),
@@ -416,3 +420,36 @@ def bias_add_(x, bias):
     T, F = x.shape
     _call("galv_bias_add", _ptr(x), _ptr(bias), T, F, dtype_code(x.dtype), _stream())
     return x
+
+
+# ---------------------------------------------------------------------------- TP over NVLink
+
+
+def gemm_rs(a, b, peer_ptrs, rows_per_rank, my_slot, *, trans_a=False, trans_b=False,
+            ldc=None):
+    """Row-parallel GEMM whose epilogue stores rows into the tp ranks' receive buffers."""
+    M, K = (a.shape[1], a.shape[0]) if trans_a else (a.shape[0], a.shape[1])
+    N = b.shape[0] if trans_b else b.shape[1]
+    if a.dtype != torch.bfloat16 or b.dtype != torch.bfloat16:
+        raise RuntimeError("gemm_rs is bf16-only")
+    timed = _stats is not None and _stats.time_gemm
+    if timed:
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record()
+    _call("galv_gemm_rs", _ptr(a), _ptr(b), _ptr(peer_ptrs), rows_per_rank, my_slot, M, N, K,
+          a.stride(0), b.stride(0), ldc if ldc is not None else N, int(trans_a), int(trans_b),
+          _stream())
+    if timed:
+        ev1.record()
+        _stats.gemm_events.append((2.0 * M * N * K, ev0, ev1, (M, N, K)))
+
+
+def tp_signal_reduce(flag_ptrs, me, t, epoch, recv, out):
+    _call("galv_tp_signal_reduce", _ptr(flag_ptrs), me, t, epoch & 0xFFFFFFFF, _ptr(recv),
+          _ptr(out), out.numel(), dtype_code(out.dtype), _stream())
+    return out
+
+
+def tp_allgather(src, dst_ptrs, flag_ptrs, me, t, epoch):
+    _call("galv_tp_allgather", _ptr(src), _ptr(dst_ptrs), _ptr(flag_ptrs), me, t,
+          epoch & 0xFFFFFFFF, src.numel() * src.element_size(), _stream())

@@ -143,6 +143,14 @@ class DecoderLayer:
             n for n in self.names if _is_small(n) and strategy.sp and
             n not in ("qkv.bias", "fc1.bias")]
         self._uly_idx = {}
+        # Megatron-SP row GEMMs: reduce-scatter fused into the GEMM over NVLink peer memory
+        self.peer = None
+        if (strategy.sp and self.tp > 1 and not self.uly and dtype == torch.bfloat16
+                and topo.distributed):
+            from . import nvlink
+            if nvlink.enabled():
+                T = topo.hc.microbatch // strategy.dp * cfg.seq_len
+                self.peer = nvlink.peer_buffers(self.tpg, T * max(cfg.hidden, 1) * 2, device)
         self.scale = 1.0 / math.sqrt(cfg.head_dim)
         self._ws = None
 
@@ -159,6 +167,13 @@ class DecoderLayer:
         if self.s.sp:
             return comm.reduce_scatter(t, self.tpg)
         return comm.all_reduce(t, self.tpg)
+
+    def _row_gemm(self, x, w, *, trans_b, bias=None):
+        """Row-parallel GEMM + tp reduction (fused NVLink reduce-scatter under Megatron-SP)."""
+        if self.peer is not None and bias is None:
+            return self.peer.gemm_rs(x, w, trans_b=trans_b)
+        y = K.gemm(x, w, trans_b=trans_b, bias=bias)
+        return self._reduce_out(y)
 
     def _norm_fwd(self, x, w, prefix, residual=None):
         res_out = torch.empty_like(x) if residual is not None else None
@@ -286,8 +301,8 @@ class DecoderLayer:
         if self.uly:
             o = self._uly_o_to_tokens(o_full)
         fuse_bias = gpt and self.wtp == 1
-        a = _linear(o, w["proj.weight"], bias=w["proj.bias"] if fuse_bias else None)
-        a = self._reduce_out(a)
+        a = self._row_gemm(o, w["proj.weight"], trans_b=True,
+                           bias=w["proj.bias"] if fuse_bias else None)
         if gpt and not fuse_bias:
             K.bias_add_(a, w["proj.bias"])
         # h1 = x + a ; n2 = norm(h1)
@@ -296,12 +311,12 @@ class DecoderLayer:
         if gpt:
             f1 = _linear(n2f, w["fc1.weight"])           # pre-activation (bias in gelu)
             act = K.bias_gelu_fwd(f1, w["fc1.bias"])
-            m = _linear(act, w["fc2.weight"], bias=w["fc2.bias"] if fuse_bias else None)
+            m = self._row_gemm(act, w["fc2.weight"], trans_b=True,
+                               bias=w["fc2.bias"] if fuse_bias else None)
         else:
             gu = _linear(n2f, w["gate_up.weight"])
             act = K.swiglu_fwd(gu)
-            m = _linear(act, w["down.weight"])
-        m = self._reduce_out(m)
+            m = self._row_gemm(act, w["down.weight"], trans_b=True)
         if gpt and not fuse_bias:
             K.bias_add_(m, w["fc2.bias"])
         y = K.axpby(h1, m, 1.0, 1.0)
@@ -348,19 +363,18 @@ class DecoderLayer:
             dpre = K.bias_gelu_bwd(sv["pre"], w["fc1.bias"], dact)
             del dact
             K.colsum(dpre, sg["fc1.bias"])
-            dn2f = _dgrad(dpre, w["fc1.weight"])
+            dn2 = self._row_gemm(dpre, w["fc1.weight"], trans_b=False)
             _wgrad(dpre, sv["n2f"], gw["fc1.weight"])
         else:
             dact = _dgrad(dmf, w["down.weight"])
             _wgrad(dmf, sv["act"], gw["down.weight"])
             dpre = K.swiglu_bwd(sv["pre"], dact)
             del dact
-            dn2f = _dgrad(dpre, w["gate_up.weight"])
+            dn2 = self._row_gemm(dpre, w["gate_up.weight"], trans_b=False)
             _wgrad(dpre, sv["n2f"], gw["gate_up.weight"])
         del dpre, dmf
-        dn2 = self._reduce_out(dn2f)
         dh1 = self._norm_bwd(sv["h1"], w, sv["st2"], dn2, "mlp_norm", sg, dres=dy)
-        del dn2, dn2f
+        del dn2
         # ---- attention
         daf = self._gather_seq(dh1)
         if gpt:
@@ -392,10 +406,9 @@ class DecoderLayer:
             dqkv = self._uly_heads_to_qkv(dqkv)
         if gpt:
             K.colsum(dqkv, sg["qkv.bias"])
-        dn1f = _dgrad(dqkv, w["qkv.weight"])
+        dn1 = self._row_gemm(dqkv, w["qkv.weight"], trans_b=False)
         _wgrad(dqkv, sv["n1f"], gw["qkv.weight"])
         del dqkv
-        dn1 = self._reduce_out(dn1f)
         dx = self._norm_bwd(sv["x"], w, sv["st1"], dn1, "attn_norm", sg, dres=dh1)
         self.store.release()
         self.store.finish_microbatch(gflat, self.tp_partial, self.tpg)

@@ -55,6 +55,9 @@ SCENARIOS = {
                   BF16, 2e-2),
     "uly4_z3": (4, "micro-llama", hc([PS(4, 1, 0, True, True), PS(2, 2, 3, True, False)],
                                      mb=2, sp_mode="ulysses"), F32, 1e-5),
+    "tp2_sp_bf16": (2, "tiny-llama", hc([PS(2, 1, 0, True, False)] * 4), BF16, 2e-2),
+    "tp2_sp_gpt_bf16": (2, "tiny-gpt", hc([PS(2, 1, 0, True, True)] * 4), BF16, 2e-2),
+    "tp4_sp_bf16": (4, "tiny-llama", hc([PS(4, 1, 0, True, False)] * 4, mb=4), BF16, 2e-2),
     "tp2dp2": (4, "micro-llama", hc([PS(2, 2, 1, True, False)] * 2, mb=2), F32, 1e-5),
     "pp2_tp2": (4, "tiny-llama", hc([PS(2, 1, 0, False, False), PS(1, 2, 2, False, False),
                                      PS(2, 1, 0, True, True), PS(2, 1, 0, False, False)],
