@@ -267,24 +267,74 @@ __global__ void __launch_bounds__(256, 1)
 // issues MMAs; TMA bytes of both CTAs complete on the leader's `full` barriers; MMA
 // completion is multicast to both CTAs' `empty` / `tfull` barriers; both CTAs' epilogues
 // release the accumulator by arriving remotely on the leader's `tempty` barrier.
-constexpr int STAGES2 = 6;
 constexpr int HALF_STAGE = 128 * BK * 2;  // 16 KB: 128 rows of A (or of B)
-constexpr int SMEM2_BYTES = STAGES2 * 2 * HALF_STAGE + 1024 + 256;
+template <bool PEER> struct Cfg2 {
+  // the peer (fused reduce-scatter) variant trades one pipeline stage for an epilogue
+  // staging area so NVLink stores go out as 256-byte row segments
+  static constexpr int STAGES = PEER ? 5 : 6;
+  static constexpr int STAGE_PITCH = 128 * 2 + 16;                 // bytes per staged row
+  static constexpr int STAGING = PEER ? 4 * 32 * STAGE_PITCH : 0;  // 4 warps x 32 rows
+  static constexpr int SMEM = STAGES * 2 * HALF_STAGE + STAGING + 1024 + 256;
+};
+
+// peer epilogue: a warp's 32 rows x 256 cols go TMEM -> bf16 -> smem staging -> coalesced
+// 256-byte row stores into the owning rank's receive buffer (two 128-column halves)
+__device__ __forceinline__ void epilogue_peer(const Params& p, uint32_t taddr, int row0,
+                                              int col_base, uint8_t* stage) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll 1
+  for (int half = 0; half < 2; ++half) {
+#pragma unroll 1
+    for (int cc = 0; cc < 4; ++cc) {
+      uint32_t r[32];
+      tmem_ld32(taddr + half * 128 + cc * 32, r);
+      uint32_t pk[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        __nv_bfloat162 v = __floats2bfloat162_rn(__uint_as_float(r[2 * i]) * p.alpha,
+                                                 __uint_as_float(r[2 * i + 1]) * p.alpha);
+        pk[i] = *reinterpret_cast<uint32_t*>(&v);
+      }
+      uint4* dst = reinterpret_cast<uint4*>(stage + lane * Cfg2<true>::STAGE_PITCH + cc * 64);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) dst[u] = make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+    }
+    __syncwarp();
+    const int col0 = col_base + half * 128;
+#pragma unroll 4
+    for (int i = 0; i < 16; ++i) {  // 32 rows x 16 chunks of 16 B
+      const int c = i * 32 + lane, rr = c >> 4, part = c & 15;
+      const int row = row0 + rr, col = col0 + part * 8;
+      if (row < p.M && col < p.N) {
+        const int j = row / p.rows_per_rank;
+        __nv_bfloat16* base = reinterpret_cast<__nv_bfloat16*>(p.peer_c[j]);
+        const long long off =
+            (long long)(p.my_slot * p.rows_per_rank + (row - j * p.rows_per_rank)) * p.ldc + col;
+        *reinterpret_cast<uint4*>(base + off) =
+            *reinterpret_cast<const uint4*>(stage + rr * Cfg2<true>::STAGE_PITCH + part * 16);
+      }
+    }
+    __syncwarp();
+  }
+}
 
 __device__ __forceinline__ void tile_coords2(const Params& p, int t, int& mt, int& nt) {
   // pair tiles are 256 x 256; p.tiles_m counts 256-row tiles here
   tile_coords(p, t, mt, nt);
 }
 
+template <bool PEER>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     gemm_bf16_tc2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                   const Params p) {
+  constexpr int STAGES2 = Cfg2<PEER>::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES2 * HALF_STAGE;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES2 * 2 * HALF_STAGE);
+  uint8_t* staging = smem + STAGES2 * 2 * HALF_STAGE;
+  uint64_t* full = reinterpret_cast<uint64_t*>(staging + Cfg2<PEER>::STAGING);
   uint64_t* empty = full + STAGES2;
   uint64_t* tfull = empty + STAGES2;
   uint64_t* tempty = tfull + 2;
@@ -390,8 +440,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       tile_coords2(p, t, mt, nt);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      epilogue_tile(p, tmem + acc * BN + ((uint32_t)(q * 32) << 16),
-                    mt * 256 + (int)cr * 128 + q * 32 + lane, nt * BN, vec_ok);
+      if constexpr (PEER)
+        epilogue_peer(p, tmem + acc * BN + ((uint32_t)(q * 32) << 16),
+                      mt * 256 + (int)cr * 128 + q * 32, nt * BN,
+                      staging + q * 32 * Cfg2<true>::STAGE_PITCH);
+      else
+        epilogue_tile(p, tmem + acc * BN + ((uint32_t)(q * 32) << 16),
+                      mt * 256 + (int)cr * 128 + q * 32 + lane, nt * BN, vec_ok);
       tc_fence_before();
       mbar_arrive_remote(&tempty[acc], 0);
       if (++acc == 2) {
@@ -502,12 +557,19 @@ int32_t gemm_bf16_sm100(const void* A, const void* B, void* C, const void* bias,
     p2.num_tiles = p2.tiles_m * p2.tiles_n;
     static bool attr2 = false;
     if (!attr2) {
-      GALV_CUDA_RET(cudaFuncSetAttribute(gemm_bf16_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         SMEM2_BYTES));
+      GALV_CUDA_RET(cudaFuncSetAttribute(gemm_bf16_tc2<false>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         Cfg2<false>::SMEM));
+      GALV_CUDA_RET(cudaFuncSetAttribute(gemm_bf16_tc2<true>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         Cfg2<true>::SMEM));
       attr2 = true;
     }
     const int pairs = min(p2.num_tiles, sm_count() / 2);
-    gemm_bf16_tc2<<<2 * pairs, 256, SMEM2_BYTES, stream>>>(ma2, mb2, p2);
+    if (peer_c != nullptr)
+      gemm_bf16_tc2<true><<<2 * pairs, 256, Cfg2<true>::SMEM, stream>>>(ma2, mb2, p2);
+    else
+      gemm_bf16_tc2<false><<<2 * pairs, 256, Cfg2<false>::SMEM, stream>>>(ma2, mb2, p2);
     GALV_LAUNCH_CHECK();
     return 0;
   }

@@ -25,6 +25,22 @@ from .. import kernels as K
 from . import comm
 
 
+# bounded window of stores with reduce-scatters in flight (each holds a full-size temporary
+# gradient until drained, so an unbounded window would cost one layer's grads per layer)
+_INFLIGHT: "collections.deque" = None
+MAX_INFLIGHT = 2
+
+
+def _track(store) -> None:
+    global _INFLIGHT
+    import collections
+    if _INFLIGHT is None:
+        _INFLIGHT = collections.deque()
+    _INFLIGHT.append(store)
+    while len(_INFLIGHT) > MAX_INFLIGHT:
+        _INFLIGHT.popleft().drain()
+
+
 def _async(fn, *args, **kw):
     """Launch a torch.distributed collective asynchronously (None for single-rank groups)."""
     return fn(*args, async_op=True, **kw)
@@ -169,6 +185,7 @@ class ParamStore:
             work = _async(dist.reduce_scatter_tensor, part, target, group=self.dp.group)
             self.pending.append((work, lambda part=part: K.axpby(part, self.g_shard, 1.0, 1.0),
                                  (target, part)))
+            _track(self)
         elif self.last_window:
             self._launch_sync()
 
