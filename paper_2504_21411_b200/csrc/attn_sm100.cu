@@ -366,6 +366,29 @@ struct SmemKV {
   static constexpr int BYTES = BAR + 256 + 1024;
 };
 
+constexpr int BWD_SPLIT = 4;                    // math warps per TMEM lane quarter
+constexpr int BWD_CP = 64 / BWD_SPLIT;          // columns per math warp (16)
+constexpr int BWD_THREADS = 128 + 128 * BWD_SPLIT;
+
+__device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+// 16 values of row r, column part `part` -> bf16 into a K-major SW128 [rows][64] tile
+__device__ __forceinline__ void store_part_row(uint8_t* tile, int r, int part, const float* v) {
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    uint4 w = make_uint4(pack2(v[u * 8 + 0], v[u * 8 + 1]), pack2(v[u * 8 + 2], v[u * 8 + 3]),
+                         pack2(v[u * 8 + 4], v[u * 8 + 5]), pack2(v[u * 8 + 6], v[u * 8 + 7]));
+    *reinterpret_cast<uint4*>(tile + r * 128 + (((part * 2 + u) ^ (r & 7)) * 16)) = w;
+  }
+}
+
 // rows of a half-row (32 values) -> bf16 into a K-major SW128 [rows][64] tile
 __device__ __forceinline__ void store_half_row(uint8_t* tile, int r, int half, const float* v) {
 #pragma unroll
@@ -392,8 +415,26 @@ __device__ __forceinline__ void store_row_out(__nv_bfloat16* dst, uint32_t taddr
   }
 }
 
+// 16 output columns of one row: TMEM -> bf16 -> global (warp-collective load)
+__device__ __forceinline__ void store_row_out16(__nv_bfloat16* dst, uint32_t taddr, float mul,
+                                                bool write) {
+  uint32_t ov[16];
+  tmem_ld16_nowait(taddr, ov);
+  tmem_wait_ld();
+  if (!write) return;
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    uint4 w;
+    w.x = pack2(__uint_as_float(ov[u * 8 + 0]) * mul, __uint_as_float(ov[u * 8 + 1]) * mul);
+    w.y = pack2(__uint_as_float(ov[u * 8 + 2]) * mul, __uint_as_float(ov[u * 8 + 3]) * mul);
+    w.z = pack2(__uint_as_float(ov[u * 8 + 4]) * mul, __uint_as_float(ov[u * 8 + 5]) * mul);
+    w.w = pack2(__uint_as_float(ov[u * 8 + 6]) * mul, __uint_as_float(ov[u * 8 + 7]) * mul);
+    *reinterpret_cast<uint4*>(dst + u * 8) = w;
+  }
+}
+
 template <int D>
-__global__ void __launch_bounds__(384, 1)
+__global__ void __launch_bounds__(BWD_THREADS, 1)
     bwd_dkdv_tc(const __grid_constant__ CUtensorMap mq, const __grid_constant__ CUtensorMap mk,
                 const __grid_constant__ CUtensorMap mv, const __grid_constant__ CUtensorMap mdo,
                 const BwdParams p) {
@@ -426,9 +467,9 @@ __global__ void __launch_bounds__(384, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&st_full[i], 1);
-      mbar_init(&st_empty[i], 256);
+      mbar_init(&st_empty[i], 128 * BWD_SPLIT);
     }
-    mbar_init(p_full, 256);
+    mbar_init(p_full, 128 * BWD_SPLIT);
     mbar_init(mm_done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     fence_async_smem();
@@ -512,42 +553,43 @@ __global__ void __launch_bounds__(384, 1)
       grads(n_it - 1);
     }
   } else if (warp >= 4) {
-    const int q = warp & 3, half = (warp - 4) >> 2;
+    const int q = warp & 3, part = (warp - 4) >> 2;
     const int r = q * 32 + lane, key = k0 + r;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     for (int it = 0; it < n_it; ++it) {
       const int st = it % NST, sb = it & 1, q0 = (i0 + it) * 64;
       mbar_wait(&st_full[sb], (it >> 1) & 1);
       tc_fence_after();
-      float s[32], dp[32];
-      tmem_ld32_nowait(tmem + sb * 128 + half * 32 + lane_off, reinterpret_cast<uint32_t*>(s));
-      tmem_ld32_nowait(tmem + sb * 128 + 64 + half * 32 + lane_off, reinterpret_cast<uint32_t*>(dp));
+      float s[BWD_CP], dp[BWD_CP];
+      tmem_ld16_nowait(tmem + sb * 128 + part * BWD_CP + lane_off, reinterpret_cast<uint32_t*>(s));
+      tmem_ld16_nowait(tmem + sb * 128 + 64 + part * BWD_CP + lane_off,
+                       reinterpret_cast<uint32_t*>(dp));
       tmem_wait_ld();
       tc_fence_before();
       mbar_arrive(&st_empty[sb]);
-      const float* l2 = reinterpret_cast<const float*>(sm + L::LSE + st * 256) + half * 32;
-      const float* dd = reinterpret_cast<const float*>(sm + L::DV + st * 256) + half * 32;
-      const int qbase = q0 + half * 32;
+      const float* l2 = reinterpret_cast<const float*>(sm + L::LSE + st * 256) + part * BWD_CP;
+      const float* dd = reinterpret_cast<const float*>(sm + L::DV + st * 256) + part * BWD_CP;
+      const int qbase = q0 + part * BWD_CP;
       const float sl2 = p.scale_log2;
       if (p.causal && key > qbase) {  // diagonal: queries < key are masked
-        const int first = key - qbase;  // first visible query index in this half
+        const int first = key - qbase;
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
+        for (int i = 0; i < BWD_CP; ++i) {
           const float pv = i >= first ? exp2_mufu(fmaf(s[i], sl2, -l2[i])) : 0.f;
           s[i] = pv;
           dp[i] = pv * (dp[i] - dd[i]);
         }
       } else {
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
+        for (int i = 0; i < BWD_CP; ++i) {
           const float pv = exp2_mufu(fmaf(s[i], sl2, -l2[i]));
           s[i] = pv;
           dp[i] = pv * (dp[i] - dd[i]);
         }
       }
       if (it > 0) mbar_wait(mm_done, (it - 1) & 1);
-      store_half_row(sm + L::PT, r, half, s);
-      store_half_row(sm + L::DST, r, half, dp);
+      store_part_row(sm + L::PT, r, part, s);
+      store_part_row(sm + L::DST, r, part, dp);
       fence_async_smem();
       tc_fence_before();
       mbar_arrive(p_full);
@@ -556,12 +598,18 @@ __global__ void __launch_bounds__(384, 1)
       mbar_wait(mm_done, (n_it - 1) & 1);
       tc_fence_after();
       const bool ok = key < p.S;
+      constexpr int OC = D / BWD_SPLIT;  // output columns per warp
       const long long off =
-          (long long)(tok0 + (ok ? key : 0)) * p.st + (long long)h * p.sh + half * (D / 2);
+          (long long)(tok0 + (ok ? key : 0)) * p.st + (long long)h * p.sh + part * OC;
+      if constexpr (OC >= 32) {
 #pragma unroll 1
-      for (int c = 0; c < D / 64; ++c) {
-        store_row_out(p.g1 + off + c * 32, t_dv + half * (D / 2) + c * 32 + lane_off, 1.f, ok);
-        store_row_out(p.g0 + off + c * 32, t_dk + half * (D / 2) + c * 32 + lane_off, p.scale, ok);
+        for (int c = 0; c < OC / 32; ++c) {
+          store_row_out(p.g1 + off + c * 32, t_dv + part * OC + c * 32 + lane_off, 1.f, ok);
+          store_row_out(p.g0 + off + c * 32, t_dk + part * OC + c * 32 + lane_off, p.scale, ok);
+        }
+      } else {
+        store_row_out16(p.g1 + off, t_dv + part * OC + lane_off, 1.f, ok);
+        store_row_out16(p.g0 + off, t_dk + part * OC + lane_off, p.scale, ok);
       }
     }
   }
@@ -584,7 +632,7 @@ struct SmemQ {
 };
 
 template <int D>
-__global__ void __launch_bounds__(384, 1)
+__global__ void __launch_bounds__(BWD_THREADS, 1)
     bwd_dq_tc(const __grid_constant__ CUtensorMap mq, const __grid_constant__ CUtensorMap mk,
               const __grid_constant__ CUtensorMap mv, const __grid_constant__ CUtensorMap mdo,
               const BwdParams p) {
@@ -617,9 +665,9 @@ __global__ void __launch_bounds__(384, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&st_full[i], 1);
-      mbar_init(&st_empty[i], 256);
+      mbar_init(&st_empty[i], 128 * BWD_SPLIT);
     }
-    mbar_init(ds_full, 256);
+    mbar_init(ds_full, 128 * BWD_SPLIT);
     mbar_init(dq_done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     fence_async_smem();
@@ -694,7 +742,7 @@ __global__ void __launch_bounds__(384, 1)
       grads(n_it - 1);
     }
   } else if (warp >= 4) {
-    const int q = warp & 3, half = (warp - 4) >> 2;
+    const int q = warp & 3, part = (warp - 4) >> 2;
     const int r = q * 32 + lane, qi = q0 + r;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     const float l2 = p.lse2[(long long)bh * p.S_pad + qi];
@@ -703,30 +751,31 @@ __global__ void __launch_bounds__(384, 1)
       const int st = it & 1;
       mbar_wait(&st_full[st], (it >> 1) & 1);
       tc_fence_after();
-      float s[32], dp[32];
-      tmem_ld32_nowait(tmem + st * 128 + half * 32 + lane_off, reinterpret_cast<uint32_t*>(s));
-      tmem_ld32_nowait(tmem + st * 128 + 64 + half * 32 + lane_off, reinterpret_cast<uint32_t*>(dp));
+      float s[BWD_CP], dp[BWD_CP];
+      tmem_ld16_nowait(tmem + st * 128 + part * BWD_CP + lane_off, reinterpret_cast<uint32_t*>(s));
+      tmem_ld16_nowait(tmem + st * 128 + 64 + part * BWD_CP + lane_off,
+                       reinterpret_cast<uint32_t*>(dp));
       tmem_wait_ld();
       tc_fence_before();
       mbar_arrive(&st_empty[st]);
-      const int kbase = it * 64 + half * 32;
+      const int kbase = it * 64 + part * BWD_CP;
       const float sl2 = p.scale_log2;
-      if ((kbase + 32 > p.S) || (p.causal && kbase + 31 > qi)) {
+      if ((kbase + BWD_CP > p.S) || (p.causal && kbase + BWD_CP - 1 > qi)) {
         const int lim = (p.causal ? min(p.S, qi + 1) : p.S) - kbase;
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
+        for (int i = 0; i < BWD_CP; ++i) {
           const float pv = i < lim ? exp2_mufu(fmaf(s[i], sl2, -l2)) : 0.f;
           dp[i] = pv * (dp[i] - dd);
         }
       } else {
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
+        for (int i = 0; i < BWD_CP; ++i) {
           const float pv = exp2_mufu(fmaf(s[i], sl2, -l2));
           dp[i] = pv * (dp[i] - dd);
         }
       }
       if (it > 0) mbar_wait(dq_done, (it - 1) & 1);
-      store_half_row(sm + L::DS, r, half, dp);
+      store_part_row(sm + L::DS, r, part, dp);
       fence_async_smem();
       tc_fence_before();
       mbar_arrive(ds_full);
@@ -734,11 +783,16 @@ __global__ void __launch_bounds__(384, 1)
     mbar_wait(dq_done, (n_it - 1) & 1);
     tc_fence_after();
     const bool ok = qi < p.S;
+    constexpr int OC = D / BWD_SPLIT;
     const long long off =
-        (long long)(tok0 + (ok ? qi : 0)) * p.st + (long long)h * p.sh + half * (D / 2);
+        (long long)(tok0 + (ok ? qi : 0)) * p.st + (long long)h * p.sh + part * OC;
+    if constexpr (OC >= 32) {
 #pragma unroll 1
-    for (int c = 0; c < D / 64; ++c)
-      store_row_out(p.g0 + off + c * 32, t_dq + half * (D / 2) + c * 32 + lane_off, p.scale, ok);
+      for (int c = 0; c < OC / 32; ++c)
+        store_row_out(p.g0 + off + c * 32, t_dq + part * OC + c * 32 + lane_off, p.scale, ok);
+    } else {
+      store_row_out16(p.g0 + off, t_dq + part * OC + lane_off, p.scale, ok);
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -878,11 +932,11 @@ int32_t attn_bwd_sm100(const void* q, const void* k, const void* v, const void* 
     }                                                                                            \
     p.g0 = (__nv_bfloat16*)dk;                                                                   \
     p.g1 = (__nv_bfloat16*)dv;                                                                   \
-    bwd_dkdv_tc<DD><<<g_kv, 384, SmemKV<DD>::BYTES, stream>>>(mq64, mk128, mv128, mdo64, p);     \
+    bwd_dkdv_tc<DD><<<g_kv, BWD_THREADS, SmemKV<DD>::BYTES, stream>>>(mq64, mk128, mv128, mdo64, p);     \
     GALV_LAUNCH_CHECK();                                                                         \
     p.g0 = (__nv_bfloat16*)dq;                                                                   \
     p.g1 = nullptr;                                                                              \
-    bwd_dq_tc<DD><<<g_q, 384, SmemQ<DD>::BYTES, stream>>>(mq128, mk64, mv64, mdo128, p);         \
+    bwd_dq_tc<DD><<<g_q, BWD_THREADS, SmemQ<DD>::BYTES, stream>>>(mq128, mk64, mv64, mdo128, p);         \
     GALV_LAUNCH_CHECK();                                                                         \
   } while (0)
   if (D == 128)
