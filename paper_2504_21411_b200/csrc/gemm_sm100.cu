@@ -269,18 +269,20 @@ __global__ void __launch_bounds__(256, 1)
 // release the accumulator by arriving remotely on the leader's `tempty` barrier.
 constexpr int HALF_STAGE = 128 * BK * 2;  // 16 KB: 128 rows of A (or of B)
 template <bool PEER> struct Cfg2 {
-  // the peer (fused reduce-scatter) variant trades one pipeline stage for an epilogue
-  // staging area so NVLink stores go out as 256-byte row segments
-  static constexpr int STAGES = PEER ? 5 : 6;
-  static constexpr int STAGE_PITCH = 128 * 2 + 16;                 // bytes per staged row
-  static constexpr int STAGING = PEER ? 4 * 32 * STAGE_PITCH : 0;  // 4 warps x 32 rows
+  // 5 pipeline stages + an epilogue staging area so every output store leaves the SM as a
+  // full row segment: plain = 32 rows x 64 fp32 columns per warp (128/256-byte segments,
+  // read-modify-write capable); PEER = 32 rows x 128 bf16 columns (256-byte NVLink stores)
+  static constexpr int STAGES = 5;
+  static constexpr int STAGE_PITCH = PEER ? 128 * 2 + 16 : 64 * 4 + 16;
+  static constexpr int STAGING = 4 * 32 * STAGE_PITCH;
   static constexpr int SMEM = STAGES * 2 * HALF_STAGE + STAGING + 1024 + 256;
 };
 
-// peer epilogue: a warp's 32 rows x 256 cols go TMEM -> bf16 -> smem staging -> coalesced
-// 256-byte row stores into the owning rank's receive buffer (two 128-column halves)
+// fused reduce-scatter epilogue: rows -> bf16 -> smem -> 256-byte stores into the owning
+// rank's receive buffer (two 128-column halves per 256-column tile)
 __device__ __forceinline__ void epilogue_peer(const Params& p, uint32_t taddr, int row0,
                                               int col_base, uint8_t* stage) {
+  constexpr int PITCH = Cfg2<true>::STAGE_PITCH;
   const int lane = threadIdx.x & 31;
 #pragma unroll 1
   for (int half = 0; half < 2; ++half) {
@@ -295,9 +297,10 @@ __device__ __forceinline__ void epilogue_peer(const Params& p, uint32_t taddr, i
                                                  __uint_as_float(r[2 * i + 1]) * p.alpha);
         pk[i] = *reinterpret_cast<uint32_t*>(&v);
       }
-      uint4* dst = reinterpret_cast<uint4*>(stage + lane * Cfg2<true>::STAGE_PITCH + cc * 64);
+      uint4* dst = reinterpret_cast<uint4*>(stage + lane * PITCH + cc * 64);
 #pragma unroll
-      for (int u = 0; u < 4; ++u) dst[u] = make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+      for (int u = 0; u < 4; ++u)
+        dst[u] = make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
     }
     __syncwarp();
     const int col0 = col_base + half * 128;
@@ -311,7 +314,92 @@ __device__ __forceinline__ void epilogue_peer(const Params& p, uint32_t taddr, i
         const long long off =
             (long long)(p.my_slot * p.rows_per_rank + (row - j * p.rows_per_rank)) * p.ldc + col;
         *reinterpret_cast<uint4*>(base + off) =
-            *reinterpret_cast<const uint4*>(stage + rr * Cfg2<true>::STAGE_PITCH + part * 16);
+            *reinterpret_cast<const uint4*>(stage + rr * PITCH + part * 16);
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// Staged epilogue: a warp's 32 rows x 256 columns go TMEM -> (alpha, bias) fp32 -> smem ->
+// coalesced row-segment stores (+ read-modify-write when accumulating).  With PEER the
+// destination row lives in rank row / rows_per_rank's receive buffer (fused NVLink RS).
+template <bool PEER>
+__device__ __forceinline__ void epilogue_staged(const Params& p, uint32_t taddr, int row0,
+                                                int col_base, uint8_t* stage) {
+  constexpr int PITCH = Cfg2<PEER>::STAGE_PITCH;
+  const int lane = threadIdx.x & 31;
+#pragma unroll 1
+  for (int q4 = 0; q4 < 4; ++q4) {
+#pragma unroll
+    for (int cc = 0; cc < 2; ++cc) {
+      uint32_t r[32];
+      tmem_ld32(taddr + q4 * 64 + cc * 32, r);
+      const int c0 = col_base + q4 * 64 + cc * 32;
+      float v[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]) * p.alpha;
+      if (p.bias != nullptr) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const int c = min(c0 + i, p.N - 1);
+          v[i] += p.bias_bf16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(p.bias)[c])
+                              : reinterpret_cast<const float*>(p.bias)[c];
+        }
+      }
+      float4* dst = reinterpret_cast<float4*>(stage + lane * PITCH + cc * 128);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) dst[u] = make_float4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);
+    }
+    __syncwarp();
+    const int colq = col_base + q4 * 64;
+    if (p.c_bf16) {
+#pragma unroll 2
+      for (int it = 0; it < 8; ++it) {  // 32 rows x 8 units of 8 bf16
+        const int u = it * 32 + lane, rr = u >> 3, part = u & 7;
+        const int row = row0 + rr, col = colq + part * 8;
+        if (row < p.M && col < p.N) {
+          __nv_bfloat16* base = reinterpret_cast<__nv_bfloat16*>(p.C);
+          long long off = (long long)row * p.ldc + col;
+          if (PEER) {
+            const int j = row / p.rows_per_rank;
+            base = reinterpret_cast<__nv_bfloat16*>(p.peer_c[j]);
+            off = (long long)(p.my_slot * p.rows_per_rank + (row - j * p.rows_per_rank)) * p.ldc +
+                  col;
+          }
+          const float4* src = reinterpret_cast<const float4*>(stage + rr * PITCH + part * 32);
+          float4 a = src[0], b = src[1];
+          float o[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+          if (p.accumulate) {
+            float old[8];
+            load16(base + off, old);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) o[e] += old[e];
+          }
+          store16(base + off, o);
+        }
+      }
+    } else {
+#pragma unroll 2
+      for (int it = 0; it < 16; ++it) {  // 32 rows x 16 units of 4 fp32
+        const int u = it * 32 + lane, rr = u >> 4, part = u & 15;
+        const int row = row0 + rr, col = colq + part * 4;
+        if (row < p.M && col < p.N) {
+          float* base = reinterpret_cast<float*>(p.C);
+          long long off = (long long)row * p.ldc + col;
+          if (PEER) {
+            const int j = row / p.rows_per_rank;
+            base = reinterpret_cast<float*>(p.peer_c[j]);
+            off = (long long)(p.my_slot * p.rows_per_rank + (row - j * p.rows_per_rank)) * p.ldc +
+                  col;
+          }
+          float4 o = *reinterpret_cast<const float4*>(stage + rr * PITCH + part * 16);
+          if (p.accumulate) {
+            const float4 old = *reinterpret_cast<const float4*>(base + off);
+            o.x += old.x; o.y += old.y; o.z += old.z; o.w += old.w;
+          }
+          *reinterpret_cast<float4*>(base + off) = o;
+        }
       }
     }
     __syncwarp();
@@ -319,8 +407,7 @@ __device__ __forceinline__ void epilogue_peer(const Params& p, uint32_t taddr, i
 }
 
 __device__ __forceinline__ void tile_coords2(const Params& p, int t, int& mt, int& nt) {
-  // pair tiles are 256 x 256; p.tiles_m counts 256-row tiles here
-  tile_coords(p, t, mt, nt);
+  tile_coords(p, t, mt, nt);  // pair tiles are 256 x 256; p.tiles_m counts 256-row tiles
 }
 
 template <bool PEER>
@@ -434,7 +521,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     const int q = warp & 3;
     int acc = 0;
     uint32_t acc_phase = 0;
-    const bool vec_ok = (p.ldc % 8) == 0;
     for (int t = pair; t < p.num_tiles; t += npairs) {
       int mt, nt;
       tile_coords2(p, t, mt, nt);
@@ -445,8 +531,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
                       mt * 256 + (int)cr * 128 + q * 32, nt * BN,
                       staging + q * 32 * Cfg2<true>::STAGE_PITCH);
       else
-        epilogue_tile(p, tmem + acc * BN + ((uint32_t)(q * 32) << 16),
-                      mt * 256 + (int)cr * 128 + q * 32 + lane, nt * BN, vec_ok);
+        epilogue_staged<false>(p, tmem + acc * BN + ((uint32_t)(q * 32) << 16),
+                               mt * 256 + (int)cr * 128 + q * 32, nt * BN,
+                               staging + q * 32 * Cfg2<false>::STAGE_PITCH);
       tc_fence_before();
       mbar_arrive_remote(&tempty[acc], 0);
       if (++acc == 2) {
@@ -546,7 +633,9 @@ int32_t gemm_bf16_sm100(const void* A, const void* B, void* C, const void* bias,
                                        SMEM_BYTES));
     attr_set = true;
   }
-  if (M > 128 && getenv("GALV_GEMM_1CTA") == nullptr) {
+  const bool c_aligned = (ldc % 8) == 0 &&
+                         ((reinterpret_cast<uintptr_t>(C) & 15) == 0 || peer_c != nullptr);
+  if (M > 128 && c_aligned && getenv("GALV_GEMM_1CTA") == nullptr) {
     // 2-CTA path: 256x256 pair tiles, per-CTA boxes of 128 rows
     CUtensorMap ma2, mb2;
     bool ok2 = a_mn ? make_map(&ma2, A, M, K, lda, 64, 64) : make_map(&ma2, A, K, M, lda, 64, 128);
