@@ -635,7 +635,7 @@ int32_t gemm_bf16_sm100(const void* A, const void* B, void* C, const void* bias,
   }
   const bool c_aligned = (ldc % 8) == 0 &&
                          ((reinterpret_cast<uintptr_t>(C) & 15) == 0 || peer_c != nullptr);
-  if (M > 128 && c_aligned && getenv("GALV_GEMM_1CTA") == nullptr) {
+  if (M > 128 && c_aligned) {
     // 2-CTA path: 256x256 pair tiles, per-CTA boxes of 128 rows
     CUtensorMap ma2, mb2;
     bool ok2 = a_mn ? make_map(&ma2, A, M, K, lda, 64, 64) : make_map(&ma2, A, K, M, lda, 64, 128);
