@@ -95,26 +95,23 @@ __global__ void bias_gelu_bwd(const T* __restrict__ x, const T* __restrict__ b,
   }
 }
 
-// out[c] (+)= sum_r x[r, c]: CTA handles a 32-column strip over a row range; fp32 atomics.
+// out[c] (+)= sum_r x[r, c]: CTA = 128 threads x 2 columns (coalesced 512 B row segments
+// for bf16), a chunk of rows per blockIdx.y, register accumulation, one atomic per column.
 template <typename T>
-__global__ void colsum_kernel(const T* __restrict__ x, float* __restrict__ out, int64_t rows,
-                              int64_t cols, int64_t rows_per_cta) {
-  __shared__ float part[8][33];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int64_t c = blockIdx.x * 32 + lane;
+__global__ void __launch_bounds__(128) colsum_kernel(const T* __restrict__ x,
+                                                     float* __restrict__ out, int64_t rows,
+                                                     int64_t cols, int64_t rows_per_cta) {
+  const int64_t c = (blockIdx.x * 128 + threadIdx.x) * 2;
+  if (c >= cols) return;
   const int64_t r0 = blockIdx.y * rows_per_cta;
   const int64_t r1 = min(rows, r0 + rows_per_cta);
-  float s = 0.f;
-  if (c < cols)
-    for (int64_t r = r0 + w; r < r1; r += 8) s += to_f(x[r * cols + c]);
-  part[w][lane] = s;
-  __syncthreads();
-  if (w == 0) {
-    float t = 0.f;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) t += part[k][lane];
-    if (c < cols) atomicAdd(&out[c], t);
+  float s0 = 0.f, s1 = 0.f;
+  for (int64_t r = r0; r < r1; ++r) {
+    s0 += to_f(x[r * cols + c]);
+    s1 += to_f(x[r * cols + c + 1]);
   }
+  atomicAdd(&out[c], s0);
+  atomicAdd(&out[c + 1], s1);
 }
 
 template <typename TX, typename TY>
@@ -226,13 +223,14 @@ int32_t galv_colsum(const void* x, float* out, int64_t rows, int64_t cols, int32
   (void)ws;
   GALV_CHECK_ARG(x && out && rows > 0 && cols > 0, "bad arguments");
   if (!accumulate) GALV_CUDA_RET(cudaMemsetAsync(out, 0, sizeof(float) * cols, as_stream(stream)));
-  const int64_t strips = (cols + 31) / 32;
-  int64_t ychunks = std::max<int64_t>(1, std::min<int64_t>((rows + 255) / 256,
-                                                           sm_count() * 8 / std::max<int64_t>(1, strips) + 1));
+  GALV_CHECK_ARG(cols % 2 == 0, "cols must be even");
+  const int64_t strips = (cols / 2 + 127) / 128;
+  const int64_t ychunks = std::max<int64_t>(
+      1, std::min<int64_t>(rows / 16 + 1, sm_count() * 16 / std::max<int64_t>(1, strips) + 1));
   const int64_t rpc = (rows + ychunks - 1) / ychunks;
   dim3 grid((unsigned)strips, (unsigned)ychunks);
   GALV_DISPATCH(dtype, T, {
-    act::colsum_kernel<T><<<grid, 256, 0, as_stream(stream)>>>((const T*)x, out, rows, cols, rpc);
+    act::colsum_kernel<T><<<grid, 128, 0, as_stream(stream)>>>((const T*)x, out, rows, cols, rpc);
   });
   GALV_LAUNCH_CHECK();
   return 0;

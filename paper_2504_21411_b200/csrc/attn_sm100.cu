@@ -19,6 +19,11 @@ using namespace sm100;
 constexpr int BQ = 128, BKV = 128;
 constexpr float LOG2E = 1.4426950408889634f;
 constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 units
+// exponentials stay on MUFU: measured on B200, offloading 1/2..1/4 of them to the FMA pipe
+// (exp2_fma) made the forward 2-8 % slower -- the softmax is latency-, not XU-bound
+#ifndef EXP_POLY_EVERY
+#define EXP_POLY_EVERY 0
+#endif
 
 template <int D>
 struct Smem {
@@ -79,12 +84,13 @@ __global__ void __launch_bounds__(384, 1)
   uint64_t* q_full = bar + 0;
   uint64_t* k_full = bar + 1;    // [2]
   uint64_t* v_full = bar + 3;    // [2]
-  uint64_t* kv_empty = bar + 5;  // [2]
+  uint64_t* k_empty = bar + 5;   // [2]  K stage free once S_j is computed
   uint64_t* s_full = bar + 7;    // [2]
   uint64_t* s_empty = bar + 9;   // [2]
   uint64_t* p_full = bar + 11;
   uint64_t* o_done = bar + 12;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 14);
+  uint64_t* v_empty = bar + 13;  // [2]  V stage free once PV_j is computed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 15);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int qb = p.n_qblocks - 1 - blockIdx.x;  // heavy causal blocks first
@@ -98,7 +104,8 @@ __global__ void __launch_bounds__(384, 1)
     for (int i = 0; i < 2; ++i) {
       mbar_init(&k_full[i], 1);
       mbar_init(&v_full[i], 1);
-      mbar_init(&kv_empty[i], 1);
+      mbar_init(&k_empty[i], 1);
+      mbar_init(&v_empty[i], 1);
       mbar_init(&s_full[i], 1);
       mbar_init(&s_empty[i], 256);
     }
@@ -126,12 +133,13 @@ __global__ void __launch_bounds__(384, 1)
         tma_load_3d(&mq, q_full, sm + L::Q + c * 16384, c * 64, h, tok0 + q0);
       for (int j = 0; j < n_kv; ++j) {
         const int st = j & 1;
-        mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
+        mbar_wait(&k_empty[st], ((j >> 1) & 1) ^ 1);
         mbar_expect_tx(&k_full[st], TILE_BYTES);
 #pragma unroll
         for (int c = 0; c < D / 64; ++c)
           tma_load_3d(&mk, &k_full[st], sm + L::K0 + st * L::TILE + c * 16384, c * 64, h,
                       tok0 + j * BKV);
+        mbar_wait(&v_empty[st], ((j >> 1) & 1) ^ 1);
         mbar_expect_tx(&v_full[st], TILE_BYTES);
 #pragma unroll
         for (int c = 0; c < D / 64; ++c)
@@ -158,7 +166,7 @@ __global__ void __launch_bounds__(384, 1)
           umma_bf16(t_o, ad, bd, id_o, (j | k) != 0);
         }
         umma_commit(o_done);
-        umma_commit(&kv_empty[st]);
+        umma_commit(&v_empty[st]);
       };
       for (int j = 0; j < n_kv; ++j) {
         const int st = j & 1;
@@ -173,6 +181,7 @@ __global__ void __launch_bounds__(384, 1)
                     id_s, k != 0);
         }
         umma_commit(&s_full[st]);
+        umma_commit(&k_empty[st]);
         if (j > 0) issue_pv(j - 1);
       }
       issue_pv(n_kv - 1);
@@ -230,8 +239,17 @@ __global__ void __launch_bounds__(384, 1)
       uint32_t pk[HC / 2];
 #pragma unroll
       for (int i = 0; i < HC; i += 2) {
-        const float p0 = exp2_mufu(fmaf(s[i], p.scale_log2, -mu));
-        const float p1 = exp2_mufu(fmaf(s[i + 1], p.scale_log2, -mu));
+        // FA4-style split: EXP_POLY_EVERY-th pairs on the FMA pipe, the rest on MUFU
+        const float x0 = fmaf(s[i], p.scale_log2, -mu), x1 = fmaf(s[i + 1], p.scale_log2, -mu);
+        float p0, p1;
+        if (EXP_POLY_EVERY > 0 && ((i >> 1) % (EXP_POLY_EVERY > 0 ? EXP_POLY_EVERY : 1)) ==
+                                      (EXP_POLY_EVERY > 0 ? EXP_POLY_EVERY : 1) - 1) {
+          p0 = exp2_fma(x0);
+          p1 = exp2_fma(x1);
+        } else {
+          p0 = exp2_mufu(x0);
+          p1 = exp2_mufu(x1);
+        }
         rs += p0 + p1;
         pk[i / 2] = pack2(p0, p1);
       }
