@@ -17,6 +17,12 @@ namespace fa {
 using namespace sm100;
 
 constexpr int BQ = 128, BKV = 128;
+// K/V multicast across CTA pairs (fwd_tc<D, true>) is correct but measured slower on B200
+// (663 vs 701 TF at S=4K, 933 vs 942 TF at S=32K, 203 vs 237 TF at D=64): the forward is not
+// L2-bandwidth bound, and pairing couples the two CTAs' pipelines.  Off by default.
+#ifndef ATTN_FWD_MC
+#define ATTN_FWD_MC 0
+#endif
 constexpr float LOG2E = 1.4426950408889634f;
 constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 units
 // exponentials stay on MUFU: measured on B200, offloading 1/2..1/4 of them to the FMA pipe
@@ -72,7 +78,10 @@ __device__ __forceinline__ uint32_t pack2(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
-template <int D>
+// MC: CTA pairs (cluster of 2 on adjacent query blocks of the same (b, h)) share every K/V
+// tile: the leader loads it once with a multicast TMA into both CTAs' rings (halving L2->SM
+// traffic per FLOP); both CTAs' MMA completions release the leader's k/v_empty barriers.
+template <int D, bool MC>
 __global__ void __launch_bounds__(384, 1)
     fwd_tc(const __grid_constant__ CUtensorMap mq, const __grid_constant__ CUtensorMap mk,
            const __grid_constant__ CUtensorMap mv, const FwdParams p) {
@@ -96,16 +105,21 @@ __global__ void __launch_bounds__(384, 1)
   const int qb = p.n_qblocks - 1 - blockIdx.x;  // heavy causal blocks first
   const int bh = blockIdx.y, b = bh / p.H, h = bh % p.H;
   const int q0 = qb * BQ;
-  const int n_kv = p.causal ? min(qb + 1, (p.S + BKV - 1) / BKV) : (p.S + BKV - 1) / BKV;
+  const uint32_t cr = MC ? cluster_ctarank() : 0;
+  // a cluster pair iterates the leader's (larger) KV range; the extra causal block is fully
+  // masked for the peer and contributes nothing
+  const int qb_lead = MC ? p.n_qblocks - 1 - (int)(blockIdx.x & ~1u) : qb;
+  const int n_kv = p.causal ? min(qb_lead + 1, (p.S + BKV - 1) / BKV) : (p.S + BKV - 1) / BKV;
   const int tok0 = b * p.S;
+  constexpr uint32_t TILE_BYTES = L::TILE;
 
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&k_full[i], 1);
       mbar_init(&v_full[i], 1);
-      mbar_init(&k_empty[i], 1);
-      mbar_init(&v_empty[i], 1);
+      mbar_init(&k_empty[i], MC ? 2 : 1);
+      mbar_init(&v_empty[i], MC ? 2 : 1);
       mbar_init(&s_full[i], 1);
       mbar_init(&s_empty[i], 256);
     }
@@ -113,38 +127,62 @@ __global__ void __launch_bounds__(384, 1)
     mbar_init(o_done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     fence_async_smem();
+    if (MC) {  // every CTA arms its own K/V barriers for the first use of each stage
+      for (int i = 0; i < 2 && i < n_kv; ++i) {
+        mbar_expect_tx(&k_full[i], TILE_BYTES);
+        mbar_expect_tx(&v_full[i], TILE_BYTES);
+      }
+    }
     prefetch_map(&mq);
     prefetch_map(&mk);
     prefetch_map(&mv);
   }
   if (warp == 2) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
-  __syncthreads();
+  if (MC)
+    cluster_sync();
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t t_s = tmem, t_o = tmem + 256;
 
   if (warp == 0) {
     if (lane == 0) {
-      constexpr uint32_t TILE_BYTES = L::TILE;
       mbar_expect_tx(q_full, TILE_BYTES);
 #pragma unroll
       for (int c = 0; c < D / 64; ++c)
         tma_load_3d(&mq, q_full, sm + L::Q + c * 16384, c * 64, h, tok0 + q0);
-      for (int j = 0; j < n_kv; ++j) {
-        const int st = j & 1;
-        mbar_wait(&k_empty[st], ((j >> 1) & 1) ^ 1);
-        mbar_expect_tx(&k_full[st], TILE_BYTES);
+      if (!MC || cr == 0) {
+        for (int j = 0; j < n_kv; ++j) {
+          const int st = j & 1;
+          mbar_wait(&k_empty[st], ((j >> 1) & 1) ^ 1);
+          if (!MC) mbar_expect_tx(&k_full[st], TILE_BYTES);
 #pragma unroll
-        for (int c = 0; c < D / 64; ++c)
-          tma_load_3d(&mk, &k_full[st], sm + L::K0 + st * L::TILE + c * 16384, c * 64, h,
-                      tok0 + j * BKV);
-        mbar_wait(&v_empty[st], ((j >> 1) & 1) ^ 1);
-        mbar_expect_tx(&v_full[st], TILE_BYTES);
+          for (int c = 0; c < D / 64; ++c) {
+            uint8_t* dst = sm + L::K0 + st * L::TILE + c * 16384;
+            if (MC)
+              tma_load_3d_mc(&mk, &k_full[st], dst, c * 64, h, tok0 + j * BKV, 0x3);
+            else
+              tma_load_3d(&mk, &k_full[st], dst, c * 64, h, tok0 + j * BKV);
+          }
+          mbar_wait(&v_empty[st], ((j >> 1) & 1) ^ 1);
+          if (!MC) mbar_expect_tx(&v_full[st], TILE_BYTES);
 #pragma unroll
-        for (int c = 0; c < D / 64; ++c)
-          tma_load_3d(&mv, &v_full[st], sm + L::V0 + st * L::TILE + c * 16384, c * 64, h,
-                      tok0 + j * BKV);
+          for (int c = 0; c < D / 64; ++c) {
+            uint8_t* dst = sm + L::V0 + st * L::TILE + c * 16384;
+            if (MC)
+              tma_load_3d_mc(&mv, &v_full[st], dst, c * 64, h, tok0 + j * BKV, 0x3);
+            else
+              tma_load_3d(&mv, &v_full[st], dst, c * 64, h, tok0 + j * BKV);
+          }
+        }
+        if (MC) {  // drain: the peer's final releases must land before this CTA exits
+          for (int j = n_kv; j < n_kv + 2; ++j) {
+            mbar_wait(&k_empty[j & 1], ((j >> 1) & 1) ^ 1);
+            mbar_wait(&v_empty[j & 1], ((j >> 1) & 1) ^ 1);
+          }
+        }
       }
     }
   } else if (warp == 1) {
@@ -166,7 +204,12 @@ __global__ void __launch_bounds__(384, 1)
           umma_bf16(t_o, ad, bd, id_o, (j | k) != 0);
         }
         umma_commit(o_done);
-        umma_commit(&v_empty[st]);
+        if (MC) {
+          umma_commit_mc(&v_empty[st], 0x1);  // release to the leader's producer
+          if (j + 2 < n_kv) mbar_expect_tx(&v_full[st], TILE_BYTES);  // re-arm own stage
+        } else {
+          umma_commit(&v_empty[st]);
+        }
       };
       for (int j = 0; j < n_kv; ++j) {
         const int st = j & 1;
@@ -181,7 +224,12 @@ __global__ void __launch_bounds__(384, 1)
                     id_s, k != 0);
         }
         umma_commit(&s_full[st]);
-        umma_commit(&k_empty[st]);
+        if (MC) {
+          umma_commit_mc(&k_empty[st], 0x1);
+          if (j + 2 < n_kv) mbar_expect_tx(&k_full[st], TILE_BYTES);
+        } else {
+          umma_commit(&k_empty[st]);
+        }
         if (j > 0) issue_pv(j - 1);
       }
       issue_pv(n_kv - 1);
@@ -307,7 +355,10 @@ __global__ void __launch_bounds__(384, 1)
           (m_used + log2f(l)) * 0.6931471805599453f;
   }
   tc_fence_before();
-  __syncthreads();
+  if (MC)
+    cluster_sync();
+  else
+    __syncthreads();
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
@@ -873,23 +924,32 @@ int32_t attn_fwd_sm100(const void* q, const void* k, const void* v, void* o, flo
   p.o_st = ost;
   p.sh = sh;
   const dim3 grid((unsigned)p.n_qblocks, (unsigned)(B * H));
-  if (D == 128) {
-    static bool set = false;
-    if (!set) {
-      GALV_CUDA_RET(cudaFuncSetAttribute(fwd_tc<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         Smem<128>::BYTES));
-      set = true;
-    }
-    fwd_tc<128><<<grid, 384, Smem<128>::BYTES, stream>>>(mq, mk, mv, p);
-  } else {
-    static bool set = false;
-    if (!set) {
-      GALV_CUDA_RET(cudaFuncSetAttribute(fwd_tc<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         Smem<64>::BYTES));
-      set = true;
-    }
-    fwd_tc<64><<<grid, 384, Smem<64>::BYTES, stream>>>(mq, mk, mv, p);
-  }
+  const bool mc = ATTN_FWD_MC && (p.n_qblocks % 2) == 0;  // cluster pairs share K/V loads
+  auto launch = [&](auto kernel, int smem) -> int32_t {
+    GALV_CUDA_RET(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(384);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = mc ? 2 : 1;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    GALV_CUDA_RET(cudaLaunchKernelEx(&cfg, kernel, mq, mk, mv, p));
+    return 0;
+  };
+  int32_t rc;
+  if (D == 128)
+    rc = mc ? launch(fwd_tc<128, true>, Smem<128>::BYTES)
+            : launch(fwd_tc<128, false>, Smem<128>::BYTES);
+  else
+    rc = mc ? launch(fwd_tc<64, true>, Smem<64>::BYTES)
+            : launch(fwd_tc<64, false>, Smem<64>::BYTES);
+  if (rc) return rc;
   GALV_LAUNCH_CHECK();
   return 0;
 }
