@@ -145,10 +145,9 @@ class DecoderLayer:
         self._uly_idx = {}
         # Megatron-SP row GEMMs: reduce-scatter fused into the GEMM over NVLink peer memory
         self.peer = None
-        if (strategy.sp and self.tp > 1 and not self.uly and dtype == torch.bfloat16
-                and topo.distributed):
+        if (self.tp > 1 and not self.uly and dtype == torch.bfloat16 and topo.distributed):
             from . import nvlink
-            if nvlink.enabled():
+            if nvlink.enabled() and (strategy.sp or nvlink.allreduce_enabled()):
                 T = topo.hc.microbatch // strategy.dp * cfg.seq_len
                 self.peer = nvlink.peer_buffers(self.tpg, T * max(cfg.hidden, 1) * 2, device)
         self.scale = 1.0 / math.sqrt(cfg.head_dim)
@@ -171,7 +170,9 @@ class DecoderLayer:
     def _row_gemm(self, x, w, *, trans_b, bias=None):
         """Row-parallel GEMM + tp reduction (fused NVLink reduce-scatter under Megatron-SP)."""
         if self.peer is not None and bias is None:
-            return self.peer.gemm_rs(x, w, trans_b=trans_b)
+            if self.s.sp:
+                return self.peer.gemm_rs(x, w, trans_b=trans_b)
+            return self.peer.gemm_ar(x, w, trans_b=trans_b)
         y = K.gemm(x, w, trans_b=trans_b, bias=bias)
         return self._reduce_out(y)
 

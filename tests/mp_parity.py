@@ -58,6 +58,10 @@ SCENARIOS = {
     "tp2_sp_bf16": (2, "tiny-llama", hc([PS(2, 1, 0, True, False)] * 4), BF16, 2e-2),
     "tp2_sp_gpt_bf16": (2, "tiny-gpt", hc([PS(2, 1, 0, True, True)] * 4), BF16, 2e-2),
     "tp4_sp_bf16": (4, "tiny-llama", hc([PS(4, 1, 0, True, False)] * 4, mb=4), BF16, 2e-2),
+    "tp2_bf16": (2, "tiny-llama", hc([PS(2, 1, 0, False, False)] * 4), BF16, 2e-2),
+    "tp2_gpt_bf16_rc": (2, "tiny-gpt", hc([PS(2, 1, 0, False, True)] * 4), BF16, 2e-2),
+    "tp4_bf16": (4, "tiny-gpt", hc([PS(4, 1, 0, False, False), PS(4, 1, 0, True, False)] * 2,
+                                   mb=4), BF16, 2e-2),
     "tp2dp2": (4, "micro-llama", hc([PS(2, 2, 1, True, False)] * 2, mb=2), F32, 1e-5),
     "pp2_tp2": (4, "tiny-llama", hc([PS(2, 1, 0, False, False), PS(1, 2, 2, False, False),
                                      PS(2, 1, 0, True, True), PS(2, 1, 0, False, False)],
@@ -69,6 +73,7 @@ SCENARIOS = {
 
 
 def main():
+    os.environ.setdefault("GALV_TP_NVLINK_AR", "1")  # exercise the NVLink all-reduce path too
     local = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
