@@ -343,6 +343,18 @@ def main():
     e2e = tokens_per_step / (e_ms / 1e3)
 
     peaks, peak_src = measured_peaks()
+    # DRAM traffic of the dominant kernel from the committed ncu --set full capture
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01", "ncu_full_summary_latest.json")) as fh:
+            cap = json.load(fh)["gemm_2cta_8192x22016x4096"][0]
+        rd = float(cap["dram__bytes_read.sum"].split()[0]) * 1e6
+        wr = float(cap["dram__bytes_write.sum"].split()[0]) * 1e6
+        traffic = {"bytes_per_launch": rd + wr, "shape": "8192x22016x4096 (gate|up fwd, mb2)",
+                   "algorithmic_bytes": 2 * (8192 * 4096 + 22016 * 4096 + 8192 * 22016),
+                   "source": "profiles/r01/gemm_2cta_gate_up_fwd.ncu-rep"}
+    except (OSError, KeyError, ValueError, IndexError):
+        pass
     flops_tok = cfg.train_flops_per_token()
     mfu = value * flops_tok / (n * PEAK_BF16_DENSE)
     peak_tf = peaks.get("bf16_tflops_sustained", 1424.5)
@@ -367,7 +379,8 @@ def main():
         "roofline": {"bound": "tensor", "kernel": "galv tcgen05 GEMM (all shapes of the step)",
                      "achieved": gemm["tflops"], "peak": peak_tf, "unit": "TFLOP/s",
                      "frac": gemm["tflops"] / peak_tf if peak_tf else None,
-                     "traffic": None, "peak_source": f"{peak_src} bf16_tflops_sustained",
+                     "traffic": traffic["bytes_per_launch"] if traffic else None,
+                     "traffic_detail": traffic, "peak_source": f"{peak_src} bf16_tflops_sustained",
                      "gemm_share_of_step": gemm["ms"] / (ms * args.steps),
                      "gemm_launches": gemm["launches"]},
         "gpu_launches": launches,

@@ -61,6 +61,7 @@ class HybridParallelModel:
         self.head = Head(cfg, hc.layer_strategies[-1], self.topo, **kw) if self.last else None
         self.resharder = Resharder(self.topo.stage_group, self.topo.local, self.device)
         self.step_count = 0
+        self._opt_stream = None
         self.trace: list = []
         self.record_trace = False
         self._init_params(seed, init, perturb, weights)
@@ -282,12 +283,23 @@ class HybridParallelModel:
             store.sync()
 
     def _optimizer_step(self):
+        """Fused AdamW per store on a side stream: the HBM-bound update of layer i overlaps
+        the next step's forward of layers < i (each store's next use waits on its event)."""
         self.step_count += 1
         o = self.optim
-        for _, store, _ in self.stores():
-            store.step(lr=o.lr, beta1=o.beta1, beta2=o.beta2, eps=o.eps,
-                       weight_decay=o.weight_decay, step=self.step_count)
-            store.zero_grads()
+        if self._opt_stream is None:
+            self._opt_stream = torch.cuda.Stream(device=self.device)
+        done = torch.cuda.Event()
+        done.record()
+        self._opt_stream.wait_event(done)
+        with torch.cuda.stream(self._opt_stream):
+            for _, store, _ in self.stores():
+                store.step(lr=o.lr, beta1=o.beta1, beta2=o.beta2, eps=o.eps,
+                           weight_decay=o.weight_decay, step=self.step_count)
+                store.zero_grads()
+                ev = torch.cuda.Event()
+                ev.record()
+                store.ready_event = ev
 
     def zero_grads(self):
         for _, store, _ in self.stores():

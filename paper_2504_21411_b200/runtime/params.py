@@ -103,6 +103,7 @@ class ParamStore:
         self.last_window = False      # set by the engine for the last microbatch's backward
         self._synced = False
         self._param_ag = None
+        self.ready_event = None       # optimizer update (side stream) done -> params usable
 
     # ------------------------------------------------------------------ values
     def views(self, flat: torch.Tensor) -> dict:
@@ -133,8 +134,14 @@ class ParamStore:
         self.m = torch.zeros_like(owned)
         self.v = torch.zeros_like(owned)
 
+    def _await_update(self) -> None:
+        if self.ready_event is not None:
+            torch.cuda.current_stream().wait_event(self.ready_event)
+            self.ready_event = None
+
     def materialize(self) -> torch.Tensor:
         """Full flat parameters (z3: all-gather into a transient buffer, maybe prefetched)."""
+        self._await_update()
         if self._param_ag is not None:  # post-step param all-gather still in flight
             self._param_ag[0].wait()
             self._param_ag = None
@@ -151,6 +158,7 @@ class ParamStore:
         """z3: start the parameter all-gather for the next use on the dp NCCL stream."""
         if self.zero < 3 or self._gathered is not None:
             return
+        self._await_update()
         out = torch.empty(self.total, dtype=self.dtype, device=self.device)
         self._gather_work = _async(dist.all_gather_into_tensor, out, self.p_shard,
                                    group=self.dp.group)
@@ -162,6 +170,7 @@ class ParamStore:
 
     # ------------------------------------------------------------------ grads
     def grad_target(self) -> torch.Tensor:
+        self._await_update()
         if self.zero >= 2:
             return torch.zeros(self.total, dtype=self.grad_dtype, device=self.device)
         return self.g_full

@@ -62,6 +62,11 @@ SCENARIOS = {
     "tp2_gpt_bf16_rc": (2, "tiny-gpt", hc([PS(2, 1, 0, False, True)] * 4), BF16, 2e-2),
     "tp4_bf16": (4, "tiny-gpt", hc([PS(4, 1, 0, False, False), PS(4, 1, 0, True, False)] * 2,
                                    mb=4), BF16, 2e-2),
+    # (scenarios with "_opt" run two optimizer steps first: ZeRO-sharded AdamW + param AG)
+    "dp2_z1_opt": (2, "micro-llama", hc([PS(1, 2, 1, False, False)] * 2), F32, 1e-3),
+    "dp2_z3_opt": (2, "micro-llama", hc([PS(1, 2, 3, False, False), PS(1, 2, 2, False, True)]),
+                   F32, 1e-3),
+    "tp2_sp_opt": (2, "micro-gpt", hc([PS(2, 1, 0, True, False)] * 2), F32, 1e-3),
     "tp2dp2": (4, "micro-llama", hc([PS(2, 2, 1, True, False)] * 2, mb=2), F32, 1e-5),
     "pp2_tp2": (4, "tiny-llama", hc([PS(2, 1, 0, False, False), PS(1, 2, 2, False, False),
                                      PS(2, 1, 0, True, True), PS(2, 1, 0, False, False)],
@@ -85,7 +90,8 @@ def main():
         if need != world:
             continue
         gb = 4 if model.startswith("tiny") else None
-        lerr, errs = run_parity(model, cfg_hc, dtype, grad_bytes=4, oracle_cache=cache)
+        lerr, errs = run_parity(model, cfg_hc, dtype, grad_bytes=4, oracle_cache=cache,
+                                opt_steps=2 if name.endswith("_opt") else 0)
         worst = max(errs.items(), key=lambda kv: kv[1]) if errs else ("-", 0.0)
         good = lerr <= tol and worst[1] <= tol
         ok &= good

@@ -58,3 +58,13 @@ def test_bf16_grad_buffers():
     hc = uniform_config(cfg, S1, microbatch=1, n_microbatches=2)
     lerr, errs = run_parity("micro-llama", hc, torch.bfloat16, grad_bytes=2)
     assert lerr <= 2e-2 and max(errs.values()) <= 2e-2
+
+
+@pytest.mark.parametrize("name,strategy", [("micro-llama", S1), ("micro-gpt", S1R)])
+def test_fp32_parity_after_adamw_steps(name, strategy):
+    """Two fused-AdamW steps (side-stream overlap) then loss/grads vs torch.optim.AdamW (fp64)."""
+    cfg = MODEL_PRESETS[name]
+    hc = uniform_config(cfg, strategy, microbatch=1, n_microbatches=2)
+    lerr, errs = run_parity(name, hc, torch.float32, opt_steps=2)
+    assert lerr <= 1e-4
+    assert max(errs.values()) <= 1e-3, max(errs.items(), key=lambda kv: kv[1])
