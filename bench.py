@@ -360,6 +360,7 @@ def main():
     peak_tf = peaks.get("bf16_tflops_sustained", 1424.5)
     clk = clocks.summary()
     mem = torch.cuda.max_memory_allocated() / 1e9
+    alloc_retries = torch.cuda.memory_stats().get("num_alloc_retries", 0)
     line = {
         "metric": metric, "value": value, "unit": "tokens/s", "n_gpus": n,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
@@ -387,7 +388,7 @@ def main():
         "e2e": {"value": e2e, "unit": "tokens/s",
                 "h2d_bytes_per_step": tokens_host.numel() * tokens_host.element_size(),
                 "d2h_bytes_per_step": 4},
-        "clocks": clk, "loss": loss_val, "peak_mem_gb": mem,
+        "clocks": clk, "loss": loss_val, "peak_mem_gb": mem, "alloc_retries": alloc_retries,
     }
     if args.trace_out:
         model.record_trace = True

@@ -36,11 +36,12 @@ __device__ __forceinline__ void signal_and_wait(void* const* flag_ptrs, int me, 
   __syncthreads();
 }
 
+// out[n] = sum_s recv[s][n]; launched after signal_wait_kernel on the same stream.  The
+// wait is a single spinning CTA so NCCL kernels on other streams (dp collectives launched by
+// the optimizer / ZeRO overlap) can always get SMs -- a full-grid spin could starve them.
 template <typename T>
-__global__ void __launch_bounds__(256) signal_reduce(void* const* flag_ptrs, int me, int t,
-                                                     uint32_t epoch, const T* __restrict__ recv,
-                                                     T* __restrict__ out, int64_t n) {
-  signal_and_wait(flag_ptrs, me, t, epoch);
+__global__ void __launch_bounds__(256) slot_reduce(int t, const T* __restrict__ recv,
+                                                   T* __restrict__ out, int64_t n) {
   constexpr int V = 16 / sizeof(T);
   const int64_t nv = n / V;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nv;
@@ -82,11 +83,12 @@ int32_t galv_tp_signal_reduce(void* const* flag_ptrs, int32_t me, int32_t t, uin
                               const void* recv, void* out, int64_t n, int32_t dtype,
                               void* stream) {
   GALV_CHECK_ARG(flag_ptrs && recv && out && t >= 1 && t <= 32 && n % 8 == 0, "bad arguments");
+  tpl::signal_wait_kernel<<<1, 32, 0, as_stream(stream)>>>(flag_ptrs, me, t, epoch);
+  GALV_LAUNCH_CHECK();
   const unsigned grid = (unsigned)std::max<int64_t>(
       1, std::min<int64_t>((n / 8 + 255) / 256, sm_count()));
   GALV_DISPATCH(dtype, T, {
-    tpl::signal_reduce<T><<<grid, 256, 0, as_stream(stream)>>>(flag_ptrs, me, t, epoch,
-                                                               (const T*)recv, (T*)out, n);
+    tpl::slot_reduce<T><<<grid, 256, 0, as_stream(stream)>>>(t, (const T*)recv, (T*)out, n);
   });
   GALV_LAUNCH_CHECK();
   return 0;

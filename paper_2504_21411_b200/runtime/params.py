@@ -262,9 +262,10 @@ class ParamStore:
         K.adamw(self.master, self.m, self.v, g, out, lr=lr, beta1=beta1, beta2=beta2, eps=eps,
                 weight_decay=weight_decay, step=step, grad_scale=grad_scale)
         if self.zero in (1, 2):
-            src = out.clone()
-            self._param_ag = (_async(dist.all_gather_into_tensor, self.p_full, src,
-                                     group=self.dp.group), src)
+            # in-place all-gather (input == output + rank*count): no temporary, so nothing is
+            # allocated on the optimizer stream's allocator pool
+            self._param_ag = (_async(dist.all_gather_into_tensor, self.p_full, out,
+                                     group=self.dp.group), None)
 
     def memory_bytes(self) -> dict:
         def nb(t):
