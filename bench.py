@@ -359,7 +359,8 @@ def main():
     mfu = value * flops_tok / (n * PEAK_BF16_DENSE)
     peak_tf = peaks.get("bf16_tflops_sustained", 1424.5)
     clk = clocks.summary()
-    mem = torch.cuda.max_memory_allocated() / 1e9
+    # caching-allocator peak + the symmetric (NVLink) pools, which live outside it
+    mem = (torch.cuda.max_memory_allocated() + sum(p.nbytes for p in model.dp_pools)) / 1e9
     alloc_retries = torch.cuda.memory_stats().get("num_alloc_retries", 0)
     line = {
         "metric": metric, "value": value, "unit": "tokens/s", "n_gpus": n,
@@ -389,6 +390,10 @@ def main():
                 "h2d_bytes_per_step": tokens_host.numel() * tokens_host.element_size(),
                 "d2h_bytes_per_step": 4},
         "clocks": clk, "loss": loss_val, "peak_mem_gb": mem, "alloc_retries": alloc_retries,
+        "dp_collectives": ({"impl": "nvlink", "pools": len(model.dp_pools),
+                            "multicast": all(bool(p.mc) for p in model.dp_pools)}
+                           if model.dp_pools else {"impl": "nccl" if n > 1 else "none"}),
+        "predicted_peak_mem_gb": max(plan.predicted_stage_peak_memory) / 1e9,
     }
     if args.trace_out:
         model.record_trace = True

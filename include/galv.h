@@ -163,6 +163,46 @@ int32_t galv_axpby(const void* x, void* y, int64_t n, float a, float b, int32_t 
                    int32_t y_dtype, void* stream);
 int32_t galv_sumsq(const void* x, int64_t n, float* out, int32_t dtype, void* stream);
 
+/* ---- NVLink / NVSwitch collectives over symmetric (peer-mapped) buffers ----------------
+ * Replace the NCCL collectives the cost model charges (collectives.py:49-69 ring passes;
+ * costmodel.py:110-118 TP all-reduce, :199-213 dp_sync).  Flag arrays hold one uint32 per
+ * source rank; epochs increase monotonically per (buffer, stream).  `*_ptrs` arguments are
+ * DEVICE arrays of per-rank base addresses (rank order of the group). */
+
+/* Row-parallel GEMM C = op(A) op(B) whose epilogue stores output rows r into
+ * peer_c[r / rows_per_rank] at row slot my_slot (Megatron-SP reduce-scatter fused into the
+ * GEMM; bf16 only). */
+int32_t galv_gemm_rs(const void* A, const void* B, void* const* peer_c, int64_t rows_per_rank,
+                     int32_t my_slot, int64_t M, int64_t N, int64_t K, int64_t lda, int64_t ldb,
+                     int64_t ldc, int32_t trans_a, int32_t trans_b, void* stream);
+/* Signal + wait (one CTA), then out[n] = sum_s recv[s*n + i] over the t slots. */
+int32_t galv_tp_signal_reduce(void* const* flag_ptrs, int32_t me, int32_t t, uint32_t epoch,
+                              const void* recv, void* out, int64_t n, int32_t dtype,
+                              void* stream);
+/* Store `bytes` of src into slot `me` of every rank's dst buffer, then signal + wait. */
+int32_t galv_tp_allgather(const void* src, void* const* dst_ptrs, void* const* flag_ptrs,
+                          int32_t me, int32_t t, uint32_t epoch, int64_t bytes, void* stream);
+/* Raise flag[me] = epoch in every rank's flag array (release, system scope). */
+int32_t galv_nvl_signal(void* const* flag_ptrs, int32_t me, int32_t t, uint32_t epoch,
+                        void* stream);
+/* One CTA spins until my_flags[0..t) >= epoch (acquire, system scope). */
+int32_t galv_nvl_wait(const uint32_t* my_flags, int32_t t, uint32_t epoch, void* stream);
+/* dp reduce over bf16 chunks [offset, offset+n): sum over ranks read from the multicast
+ * address mc_src (NVSwitch multimem.ld_reduce, fp32 accumulate) or, if mc_src is NULL, from
+ * peer_src[r] + offset; out = sum (+ out if accumulate); the result is also stored to every
+ * rank at mc_dst (multimem.st) or peer_dst[r] + offset when given (all-reduce).
+ * max_ctas > 0 caps the grid (leave SMs to the concurrent GEMMs). */
+int32_t galv_dp_reduce(const void* mc_src, void* const* peer_src, int32_t t, int64_t offset,
+                       void* out, int32_t accumulate, void* mc_dst, void* const* peer_dst,
+                       int64_t n, int32_t max_ctas, void* stream);
+/* AdamW (as galv_adamw) on this rank's fp32 shard of n params whose bf16 result is stored to
+ * every dp rank's full parameter buffer: multicast address mc_dst, or peer_dst[r] + offset
+ * (ZeRO-1/2 parameter all-gather fused into the optimizer; n, offset multiples of 8). */
+int32_t galv_adamw_bcast(float* master, float* m, float* v, const void* grad, void* mc_dst,
+                         void* const* peer_dst, int32_t t, int64_t offset, int64_t n, float lr,
+                         float beta1, float beta2, float eps, float weight_decay,
+                         float grad_scale, int64_t step, int32_t grad_dtype, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

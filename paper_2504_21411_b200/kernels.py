@@ -34,6 +34,11 @@ _SIGS = {
                       _P], _I32),
     "galv_tp_signal_reduce": ([_P, _I32, _I32, C.c_uint32, _P, _P, _I64, _I32, _P], _I32),
     "galv_tp_allgather": ([_P, _P, _P, _I32, _I32, C.c_uint32, _I64, _P], _I32),
+    "galv_nvl_signal": ([_P, _I32, _I32, C.c_uint32, _P], _I32),
+    "galv_nvl_wait": ([_P, _I32, C.c_uint32, _P], _I32),
+    "galv_dp_reduce": ([_P, _P, _I32, _I64, _P, _I32, _P, _P, _I64, _I32, _P], _I32),
+    "galv_adamw_bcast": ([_P, _P, _P, _P, _P, _P, _I32, _I64, _I64, _F, _F, _F, _F, _F, _F,
+                          _I64, _I32, _P], _I32),
     "galv_attn_fwd": ([_P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _F, _I32,
                        _I32, _P], _I32),
     "galv_attn_bwd_workspace": ([_I64, _I64, _I64, _I64, _I32], _I64),
@@ -94,7 +99,7 @@ def load_library(path: str | os.PathLike | None = None):
 
 
 # kernels launched per C-ABI call (for the bench's gpu_launches count)
-KERNELS_PER_CALL = {"galv_attn_bwd": 3}
+KERNELS_PER_CALL = {"galv_attn_bwd": 3, "galv_tp_signal_reduce": 2, "galv_tp_allgather": 2}
 
 
 class KernelStats:
@@ -442,6 +447,34 @@ def gemm_rs(a, b, peer_ptrs, rows_per_rank, my_slot, *, trans_a=False, trans_b=F
     if timed:
         ev1.record()
         _stats.gemm_events.append((2.0 * M * N * K, ev0, ev1, (M, N, K)))
+
+
+def nvl_signal(flag_ptrs, me, t, epoch):
+    """Raise this rank's flag (epoch) in every peer's flag array (one warp)."""
+    _call("galv_nvl_signal", _ptr(flag_ptrs), me, t, epoch & 0xFFFFFFFF, _stream())
+
+
+def nvl_wait(my_flags_addr: int, t, epoch):
+    """Single-CTA wait until every source rank's flag in this rank's array reached epoch."""
+    _call("galv_nvl_wait", my_flags_addr, t, epoch & 0xFFFFFFFF, _stream())
+
+
+def dp_reduce(*, n, t, mc_src=None, peer_src=None, offset=0, out=None, accumulate=False,
+              mc_dst=None, peer_dst=None, max_ctas=0):
+    """out (+)= sum over the dp ranks of their [offset, offset+n) bf16 slice (NVSwitch
+    multimem.ld_reduce at mc_src, else unicast loads via the peer_src pointer array); the
+    reduced slice is optionally stored to every rank (mc_dst / peer_dst): an all-reduce."""
+    _call("galv_dp_reduce", mc_src, _ptr(peer_src), t, offset, _ptr(out), int(accumulate),
+          mc_dst, _ptr(peer_dst), n, max_ctas, _stream())
+
+
+def adamw_bcast(master, m, v, grad, *, t, offset, mc_dst=None, peer_dst=None, lr, beta1,
+                beta2, eps, weight_decay, step, grad_scale=1.0):
+    """AdamW on this rank's shard; bf16 params stored to every dp rank (fused all-gather)."""
+    _call("galv_adamw_bcast", _ptr(master), _ptr(m), _ptr(v), _ptr(grad), mc_dst,
+          _ptr(peer_dst), t, offset, master.numel(), float(lr), float(beta1), float(beta2),
+          float(eps), float(weight_decay), float(grad_scale), int(step),
+          dtype_code(grad.dtype), _stream())
 
 
 def tp_signal_reduce(flag_ptrs, me, t, epoch, recv, out):

@@ -24,6 +24,7 @@ from . import comm
 from .config import HybridConfig, ModelConfig
 from .init import init_tensor, param_shapes
 from .layers import DecoderLayer, Embedding, Head, tp_slice
+from . import dp_nvlink
 from .reshard import Layout, Resharder
 from .topology import Topology
 
@@ -65,6 +66,8 @@ class HybridParallelModel:
         self.trace: list = []
         self.record_trace = False
         self._init_params(seed, init, perturb, weights)
+        # dp collectives of bf16 ZeRO-0/1/2 stores over NVLink/NVSwitch (symmetric pools)
+        self.dp_pools = dp_nvlink.attach([st for _, st, _ in self.stores()], self.device)
 
     # ------------------------------------------------------------------ init
     def stores(self):

@@ -104,6 +104,23 @@ class ParamStore:
         self._synced = False
         self._param_ag = None
         self.ready_event = None       # optimizer update (side stream) done -> params usable
+        self.nvl = None               # dp_nvlink.DpPool holding this store's flat buffers
+        self._slot = None             # z2 grad-target ring slot of the current microbatch
+        self._param_epoch = None      # channel-1 epoch of the peers' parameter broadcast
+
+    def attach_nvlink(self, pool) -> None:
+        """Move the full param / grad buffers into the dp group's symmetric pool
+        (dp_nvlink.attach); the collectives then run over NVLink/NVSwitch."""
+        reg = pool.regions[id(self)]
+        if "param" in reg:
+            v = pool.view(reg["param"], self.total)
+            v.copy_(self.p_full)
+            self.p_full = v
+        if "grad" in reg:
+            v = pool.view(reg["grad"], self.total)
+            v.copy_(self.g_full)
+            self.g_full = v
+        self.nvl = pool
 
     # ------------------------------------------------------------------ values
     def views(self, flat: torch.Tensor) -> dict:
@@ -142,6 +159,9 @@ class ParamStore:
     def materialize(self) -> torch.Tensor:
         """Full flat parameters (z3: all-gather into a transient buffer, maybe prefetched)."""
         self._await_update()
+        if self._param_epoch is not None:  # peers' fused AdamW + broadcast of their shards
+            self.nvl.wait_params(self._param_epoch)
+            self._param_epoch = None
         if self._param_ag is not None:  # post-step param all-gather still in flight
             self._param_ag[0].wait()
             self._param_ag = None
@@ -172,6 +192,9 @@ class ParamStore:
     def grad_target(self) -> torch.Tensor:
         self._await_update()
         if self.zero >= 2:
+            if self.nvl is not None:
+                self._slot, v = self.nvl.grad_slot(self.total)
+                return v
             return torch.zeros(self.total, dtype=self.grad_dtype, device=self.device)
         return self.g_full
 
@@ -190,6 +213,10 @@ class ParamStore:
         self.acc32.zero_()
         if self.zero >= 2:
             comm.all_reduce(target, self.extra)
+            if self.nvl is not None:
+                self.pending.append((self.nvl.reduce_scatter_slot(self, self._slot), None, ()))
+                self._slot = None
+                return
             part = torch.empty(self.shard, dtype=self.grad_dtype, device=self.device)
             work = _async(dist.reduce_scatter_tensor, part, target, group=self.dp.group)
             self.pending.append((work, lambda part=part: K.axpby(part, self.g_shard, 1.0, 1.0),
@@ -206,12 +233,17 @@ class ParamStore:
             comm.all_reduce(self.g_full, self.extra)
         if self.zero == 0:
             self._owned_grad = self.g_full
-            if self.ndp > 1:
+            if self.nvl is not None:
+                self.pending.append((self.nvl.all_reduce_grad(self), None, ()))
+            elif self.ndp > 1:
                 self.pending.append((_async(dist.all_reduce, self.g_full, group=self.dp.group),
                                      None, ()))
         elif self.zero == 1:
             out = torch.empty(self.shard, dtype=self.grad_dtype, device=self.device)
             self._owned_grad = out
+            if self.nvl is not None:
+                self.pending.append((self.nvl.reduce_scatter_grad(self, out), None, (out,)))
+                return
             self.pending.append((_async(dist.reduce_scatter_tensor, out, self.g_full,
                                         group=self.dp.group), None, (out,)))
         else:
@@ -259,6 +291,12 @@ class ParamStore:
             out = self.p_full
         else:
             out = self.p_full[self.lo:self.lo + self.shard]
+        if self.nvl is not None and self.zero in (1, 2):
+            # fused AdamW + parameter all-gather over NVSwitch (dp_nvlink.py)
+            self._param_epoch = self.nvl.adamw_bcast(
+                self, g, lr=lr, beta1=beta1, beta2=beta2, eps=eps, weight_decay=weight_decay,
+                step=step, grad_scale=grad_scale)
+            return
         K.adamw(self.master, self.m, self.v, g, out, lr=lr, beta1=beta1, beta2=beta2, eps=eps,
                 weight_decay=weight_decay, step=step, grad_scale=grad_scale)
         if self.zero in (1, 2):

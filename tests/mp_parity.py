@@ -29,6 +29,7 @@ def hc(strats, *, pp=1, mb=2, m=2, sp_mode="megatron"):
 
 
 F32, BF16 = torch.float32, torch.bfloat16
+BF16_OPT = 4e-2
 # name -> (world, model, hybrid config, dtype, tolerance)
 SCENARIOS = {
     "dp2_z0": (2, "micro-llama", hc([PS(1, 2, 0, False, False)] * 2), F32, 1e-5),
@@ -67,6 +68,33 @@ SCENARIOS = {
     "dp2_z3_opt": (2, "micro-llama", hc([PS(1, 2, 3, False, False), PS(1, 2, 2, False, True)]),
                    F32, 1e-3),
     "tp2_sp_opt": (2, "micro-gpt", hc([PS(2, 1, 0, True, False)] * 2), F32, 1e-3),
+    # bf16 params AND bf16 grads: the dp collectives run over NVLink/NVSwitch (dp_nvlink.py);
+    # "_peer" forces unicast peer loads/stores, "_nccl" the NCCL fallback (6th field: grad bytes).
+    # After 2 AdamW steps (lr 1e-3) bf16 parameter rounding (2^-9 relative) is as large as the
+    # update itself, so the gradients drift ~2.7e-2 from the fp64 oracle for NCCL and NVLink
+    # alike (measured: 2.75e-2 NCCL, 2.67e-2 multicast, 2.73e-2 peer): BF16_OPT = 4e-2.
+    "dp2_z0_bf16": (2, "tiny-llama", hc([PS(1, 2, 0, False, False)] * 4, mb=4), BF16, 2e-2, 2),
+    "dp2_z1_bf16": (2, "tiny-llama", hc([PS(1, 2, 1, False, False)] * 4, mb=4), BF16, 2e-2, 2),
+    "dp2_z2_bf16": (2, "tiny-llama", hc([PS(1, 2, 2, False, False)] * 4, mb=4), BF16, 2e-2, 2),
+    "dp2_z2_bf16_nccl": (2, "tiny-llama", hc([PS(1, 2, 2, False, False)] * 4, mb=4), BF16, 2e-2,
+                         2),
+    "dp2_z0_bf16_opt": (2, "tiny-llama", hc([PS(1, 2, 0, False, False)] * 4, mb=4), BF16, BF16_OPT,
+                        2),
+    "dp2_z1_bf16_opt": (2, "tiny-llama", hc([PS(1, 2, 1, False, False)] * 4, mb=4), BF16, BF16_OPT,
+                        2),
+    "dp2_z2_bf16_opt": (2, "tiny-llama", hc([PS(1, 2, 2, False, False)] * 4, mb=4), BF16, BF16_OPT,
+                        2),
+    "dp2_mixed_bf16_opt": (2, "tiny-llama", hc([PS(1, 2, 2, False, False),
+                                                PS(1, 2, 1, False, True),
+                                                PS(1, 2, 0, False, False),
+                                                PS(2, 1, 0, True, False)], mb=4), BF16, BF16_OPT, 2),
+    "dp2_z2_bf16_opt_nccl": (2, "tiny-llama", hc([PS(1, 2, 2, False, False)] * 4, mb=4), BF16, BF16_OPT, 2),
+    "dp2_z2_bf16_opt_peer": (2, "tiny-llama", hc([PS(1, 2, 2, False, False)] * 4, mb=4), BF16, BF16_OPT, 2),
+    "dp4_z2_bf16_opt": (4, "tiny-llama", hc([PS(1, 4, 2, False, False)] * 4, mb=4), BF16, BF16_OPT,
+                        2),
+    "tp2dp2_bf16_opt": (4, "tiny-llama", hc([PS(2, 2, 1, True, False), PS(2, 2, 2, True, False),
+                                             PS(1, 4, 0, False, False), PS(1, 4, 2, False, True)],
+                                            mb=4), BF16, BF16_OPT, 2),
     "tp2dp2": (4, "micro-llama", hc([PS(2, 2, 1, True, False)] * 2, mb=2), F32, 1e-5),
     "pp2_tp2": (4, "tiny-llama", hc([PS(2, 1, 0, False, False), PS(1, 2, 2, False, False),
                                      PS(2, 1, 0, True, True), PS(2, 1, 0, False, False)],
@@ -86,12 +114,23 @@ def main():
     ok = True
     cache = {}
     for name in sys.argv[1:]:
-        need, model, cfg_hc, dtype, tol = SCENARIOS[name]
+        need, model, cfg_hc, dtype, tol, *rest = SCENARIOS[name]
         if need != world:
             continue
-        gb = 4 if model.startswith("tiny") else None
-        lerr, errs = run_parity(model, cfg_hc, dtype, grad_bytes=4, oracle_cache=cache,
-                                opt_steps=2 if name.endswith("_opt") else 0)
+        env = {"GALV_DP_NVLINK_MC": "0"} if name.endswith("_peer") else \
+            {"GALV_DP_NVLINK": "0"} if name.endswith("_nccl") else {}
+        saved = {k: os.environ.get(k) for k in env}
+        os.environ.update(env)
+        try:
+            lerr, errs = run_parity(model, cfg_hc, dtype, grad_bytes=rest[0] if rest else 4,
+                                    oracle_cache=cache,
+                                    opt_steps=2 if "_opt" in name else 0)
+        finally:
+            for k, v in saved.items():
+                if v is None:
+                    os.environ.pop(k, None)
+                else:
+                    os.environ[k] = v
         worst = max(errs.items(), key=lambda kv: kv[1]) if errs else ("-", 0.0)
         good = lerr <= tol and worst[1] <= tol
         ok &= good

@@ -13,8 +13,12 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 TWO = ["dp2_z0", "dp2_z1", "dp2_z2", "dp2_z3_rc", "tp2", "tp2_sp", "tp2_gpt", "tp2_sp_gpt_rc",
        "pp2", "pp2_gpt", "mixed2", "mixed2_bf16", "uly2", "uly2_gpt_rc_mixed", "uly2_bf16",
        "tp2_sp_bf16", "tp2_sp_gpt_bf16", "tp2_bf16", "tp2_gpt_bf16_rc",
-       "dp2_z1_opt", "dp2_z3_opt", "tp2_sp_opt"]
-FOUR = ["tp2dp2", "pp2_tp2", "alt4", "uly4_z3", "tp4_sp_bf16", "tp4_bf16"]
+       "dp2_z1_opt", "dp2_z3_opt", "tp2_sp_opt",
+       "dp2_z0_bf16", "dp2_z1_bf16", "dp2_z2_bf16", "dp2_z2_bf16_nccl", "dp2_z0_bf16_opt",
+       "dp2_z1_bf16_opt", "dp2_z2_bf16_opt", "dp2_z2_bf16_opt_nccl", "dp2_z2_bf16_opt_peer",
+       "dp2_mixed_bf16_opt"]
+FOUR = ["tp2dp2", "pp2_tp2", "alt4", "uly4_z3", "tp4_sp_bf16", "tp4_bf16", "dp4_z2_bf16_opt",
+        "tp2dp2_bf16_opt"]
 
 
 def _run(n, scenarios, port):
