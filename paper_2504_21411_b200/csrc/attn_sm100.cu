@@ -87,8 +87,7 @@ __global__ void __launch_bounds__(384, 1)
            const __grid_constant__ CUtensorMap mv, const FwdParams p) {
   using L = Smem<D>;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                           ~uintptr_t(1023));
+  uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // keeps the shared window
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::BAR);
   uint64_t* q_full = bar + 0;
   uint64_t* k_full = bar + 1;    // [2]
@@ -509,17 +508,16 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
                 const BwdParams p) {
   using L = SmemKV<D>;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                           ~uintptr_t(1023));
+  uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // keeps the shared window
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::BAR);
   constexpr int NST = L::NST;
   uint64_t* kv_full = bar + 0;
   uint64_t* q_full = bar + 1;          // [NST]
   uint64_t* q_empty = q_full + NST;    // [NST]
   uint64_t* st_full = q_empty + NST;   // [2]
-  uint64_t* st_empty = st_full + 2;    // [2]
-  uint64_t* p_full = st_empty + 2;
-  uint64_t* mm_done = p_full + 1;
+  uint64_t* st_empty = st_full + 2;    // [2]  buffer free once dV/dK of its step are done
+  uint64_t* p_full = st_empty + 2;     // [2]  P^T / dS^T packed into the buffer (TMEM)
+  uint64_t* mm_done = p_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mm_done + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int kb = blockIdx.x;
@@ -536,9 +534,9 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&st_full[i], 1);
-      mbar_init(&st_empty[i], 128 * BWD_SPLIT);
+      mbar_init(&st_empty[i], 1);
+      mbar_init(&p_full[i], 128 * BWD_SPLIT);
     }
-    mbar_init(p_full, 128 * BWD_SPLIT);
     mbar_init(mm_done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     fence_async_smem();
@@ -578,23 +576,25 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       const uint32_t id_st = make_idesc(128, 64, 0, 0);
       const uint32_t id_g = make_idesc(128, D, 0, 1);
       const uint32_t a_k = smem_u32(sm + L::K), a_v = smem_u32(sm + L::V);
-      const uint32_t a_pt = smem_u32(sm + L::PT), a_ds = smem_u32(sm + L::DST);
       mbar_wait(kv_full, 0);
+      // dV += P^T dO, dK += dS^T Q with A read from TMEM (P^T / dS^T packed by the math
+      // warps into the first 8 of every 16 columns of the S^T / dP^T buffer)
       auto grads = [&](int it) {
-        const int st = it % NST;
-        mbar_wait(p_full, it & 1);
+        const int st = it % NST, sb = it & 1;
+        mbar_wait(&p_full[sb], (it >> 1) & 1);
         tc_fence_after();
         const uint32_t b_do = smem_u32(sm + L::O0 + st * L::QT);
         const uint32_t b_q = smem_u32(sm + L::Q0 + st * L::QT);
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-          umma_bf16(t_dv, sdesc(a_pt + k * 32, 16, 1024), sdesc(b_do + k * 2048, 8192, 1024), id_g,
-                    (it | k) != 0);
+          umma_bf16_ts(t_dv, tmem + sb * 128 + k * 16, sdesc(b_do + k * 2048, 8192, 1024), id_g,
+                       (it | k) != 0);
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-          umma_bf16(t_dk, sdesc(a_ds + k * 32, 16, 1024), sdesc(b_q + k * 2048, 8192, 1024), id_g,
-                    (it | k) != 0);
-        umma_commit(mm_done);
+          umma_bf16_ts(t_dk, tmem + sb * 128 + 64 + k * 16, sdesc(b_q + k * 2048, 8192, 1024),
+                       id_g, (it | k) != 0);
+        if (it == n_it - 1) umma_commit(mm_done);  // single phase: final dK/dV complete
+        umma_commit(&st_empty[sb]);
         umma_commit(&q_empty[st]);
       };
       for (int it = 0; it < n_it; ++it) {
@@ -634,8 +634,6 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       tmem_ld16_nowait(tmem + sb * 128 + 64 + part * BWD_CP + lane_off,
                        reinterpret_cast<uint32_t*>(dp));
       tmem_wait_ld();
-      tc_fence_before();
-      mbar_arrive(&st_empty[sb]);
       const float* l2 = reinterpret_cast<const float*>(sm + L::LSE + st * 256) + part * BWD_CP;
       const float* dd = reinterpret_cast<const float*>(sm + L::DV + st * 256) + part * BWD_CP;
       const int qbase = q0 + part * BWD_CP;
@@ -656,15 +654,19 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
           dp[i] = pv * (dp[i] - dd[i]);
         }
       }
-      if (it > 0) mbar_wait(mm_done, (it - 1) & 1);
-      store_part_row(sm + L::PT, r, part, s);
-      store_part_row(sm + L::DST, r, part, dp);
-      fence_async_smem();
+      uint32_t pk[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) pk[i] = pack2(s[2 * i], s[2 * i + 1]);
+      tmem_st8(tmem + sb * 128 + part * BWD_CP + lane_off, pk);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) pk[i] = pack2(dp[2 * i], dp[2 * i + 1]);
+      tmem_st8(tmem + sb * 128 + 64 + part * BWD_CP + lane_off, pk);
+      tmem_wait_st();
       tc_fence_before();
-      mbar_arrive(p_full);
+      mbar_arrive(&p_full[sb]);
     }
     if (n_it > 0) {
-      mbar_wait(mm_done, (n_it - 1) & 1);
+      mbar_wait(mm_done, 0);
       tc_fence_after();
       const bool ok = key < p.S;
       constexpr int OC = D / BWD_SPLIT;  // output columns per warp
@@ -707,17 +709,16 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
               const BwdParams p) {
   using L = SmemQ<D>;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                           ~uintptr_t(1023));
+  uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // keeps the shared window
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::BAR);
   constexpr int NST = L::NST;
   uint64_t* qo_full = bar + 0;
   uint64_t* kv_full = bar + 1;          // [NST]
   uint64_t* kv_empty = kv_full + NST;   // [NST]
   uint64_t* st_full = kv_empty + NST;   // [2]
-  uint64_t* st_empty = st_full + 2;     // [2]
-  uint64_t* ds_full = st_empty + 2;
-  uint64_t* dq_done = ds_full + 1;
+  uint64_t* st_empty = st_full + 2;     // [2]  buffer free once dQ of its step is done
+  uint64_t* ds_full = st_empty + 2;     // [2]  dS packed into the buffer (TMEM)
+  uint64_t* dq_done = ds_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dq_done + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_q = (p.S + 127) / 128;
@@ -734,9 +735,9 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&st_full[i], 1);
-      mbar_init(&st_empty[i], 128 * BWD_SPLIT);
+      mbar_init(&st_empty[i], 1);
+      mbar_init(&ds_full[i], 128 * BWD_SPLIT);
     }
-    mbar_init(ds_full, 128 * BWD_SPLIT);
     mbar_init(dq_done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     fence_async_smem();
@@ -772,18 +773,19 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       const uint32_t id_s = make_idesc(128, 64, 0, 0);
       const uint32_t id_g = make_idesc(128, D, 0, 1);
       const uint32_t a_q = smem_u32(sm + L::Q), a_o = smem_u32(sm + L::O);
-      const uint32_t a_ds = smem_u32(sm + L::DS);
       mbar_wait(qo_full, 0);
+      // dQ += dS K with dS read from TMEM (packed over the dP buffer by the math warps)
       auto grads = [&](int it) {
-        const int st = it % NST;
-        mbar_wait(ds_full, it & 1);
+        const int st = it % NST, sb = it & 1;
+        mbar_wait(&ds_full[sb], (it >> 1) & 1);
         tc_fence_after();
         const uint32_t b_k = smem_u32(sm + L::K0 + st * L::KT);
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-          umma_bf16(t_dq, sdesc(a_ds + k * 32, 16, 1024), sdesc(b_k + k * 2048, 8192, 1024), id_g,
-                    (it | k) != 0);
-        umma_commit(dq_done);
+          umma_bf16_ts(t_dq, tmem + sb * 128 + 64 + k * 16, sdesc(b_k + k * 2048, 8192, 1024),
+                       id_g, (it | k) != 0);
+        if (it == n_it - 1) umma_commit(dq_done);  // single phase: final dQ complete
+        umma_commit(&st_empty[sb]);
         umma_commit(&kv_empty[st]);
       };
       for (int it = 0; it < n_it; ++it) {
@@ -825,8 +827,6 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       tmem_ld16_nowait(tmem + st * 128 + 64 + part * BWD_CP + lane_off,
                        reinterpret_cast<uint32_t*>(dp));
       tmem_wait_ld();
-      tc_fence_before();
-      mbar_arrive(&st_empty[st]);
       const int kbase = it * 64 + part * BWD_CP;
       const float sl2 = p.scale_log2;
       if ((kbase + BWD_CP > p.S) || (p.causal && kbase + BWD_CP - 1 > qi)) {
@@ -843,13 +843,15 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
           dp[i] = pv * (dp[i] - dd);
         }
       }
-      if (it > 0) mbar_wait(dq_done, (it - 1) & 1);
-      store_part_row(sm + L::DS, r, part, dp);
-      fence_async_smem();
+      uint32_t pk[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) pk[i] = pack2(dp[2 * i], dp[2 * i + 1]);
+      tmem_st8(tmem + st * 128 + 64 + part * BWD_CP + lane_off, pk);
+      tmem_wait_st();
       tc_fence_before();
-      mbar_arrive(ds_full);
+      mbar_arrive(&ds_full[st]);
     }
-    mbar_wait(dq_done, (n_it - 1) & 1);
+    mbar_wait(dq_done, 0);
     tc_fence_after();
     const bool ok = qi < p.S;
     constexpr int OC = D / BWD_SPLIT;
