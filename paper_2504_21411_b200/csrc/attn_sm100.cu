@@ -185,23 +185,26 @@ __global__ void __launch_bounds__(384, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      const uint32_t id_s = make_idesc(BQ, BKV, 0, 0);  // Q (K-major) x K (K-major)
-      const uint32_t id_o = make_idesc(BQ, D, 0, 1);    // P (K-major) x V (MN-major)
-      const uint32_t a_q = smem_u32(sm + L::Q), a_p = smem_u32(sm + L::P);
-      mbar_wait(q_full, 0);
-      auto issue_pv = [&](int j) {
-        const int st = j & 1;
-        mbar_wait(p_full, j & 1);
-        mbar_wait(&v_full[st], (j >> 1) & 1);
-        tc_fence_after();
-        const uint32_t b_v = smem_u32(sm + L::V0 + st * L::TILE);
+    // MMA warp: all lanes run the loop (warp-uniform state, descriptors precomputed once and
+    // advanced by constant offsets); one elected lane issues each group of tcgen05.mma
+    const uint32_t id_s = make_idesc(BQ, BKV, 0, 0);  // Q (K-major) x K (K-major)
+    const uint32_t id_o = make_idesc(BQ, D, 0, 1);    // P (K-major) x V (MN-major)
+    const uint64_t d_q = sdesc(smem_u32(sm + L::Q), 16, 1024);
+    const uint64_t d_p = sdesc(smem_u32(sm + L::P), 16, 1024);
+    const uint64_t d_k = sdesc(smem_u32(sm + L::K0), 16, 1024);
+    const uint64_t d_v = sdesc(smem_u32(sm + L::V0), 16384, 1024);
+    mbar_wait(q_full, 0);
+    auto issue_pv = [&](int j) {
+      const int st = j & 1;
+      mbar_wait(p_full, j & 1);
+      mbar_wait(&v_full[st], (j >> 1) & 1);
+      tc_fence_after();
+      const uint64_t bv = d_v + (uint64_t)((st * L::TILE) >> 4);
+      if (elect_one()) {
 #pragma unroll
-        for (int k = 0; k < BKV / 16; ++k) {
-          const uint64_t ad = sdesc(a_p + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024);
-          const uint64_t bd = sdesc(b_v + k * 2048, 16384, 1024);
-          umma_bf16(t_o, ad, bd, id_o, (j | k) != 0);
-        }
+        for (int k = 0; k < BKV / 16; ++k)
+          umma_bf16(t_o, d_p + (uint64_t)((((k >> 2) * 16384) + (k & 3) * 32) >> 4),
+                    bv + (uint64_t)((k * 2048) >> 4), id_o, (j | k) != 0);
         umma_commit(o_done);
         if (MC) {
           umma_commit_mc(&v_empty[st], 0x1);  // release to the leader's producer
@@ -209,18 +212,20 @@ __global__ void __launch_bounds__(384, 1)
         } else {
           umma_commit(&v_empty[st]);
         }
-      };
-      for (int j = 0; j < n_kv; ++j) {
-        const int st = j & 1;
-        mbar_wait(&k_full[st], (j >> 1) & 1);
-        mbar_wait(&s_empty[st], ((j >> 1) & 1) ^ 1);
-        tc_fence_after();
-        const uint32_t b_k = smem_u32(sm + L::K0 + st * L::TILE);
+      }
+      __syncwarp();
+    };
+    for (int j = 0; j < n_kv; ++j) {
+      const int st = j & 1;
+      mbar_wait(&k_full[st], (j >> 1) & 1);
+      mbar_wait(&s_empty[st], ((j >> 1) & 1) ^ 1);
+      tc_fence_after();
+      const uint64_t bk = d_k + (uint64_t)((st * L::TILE) >> 4);
+      if (elect_one()) {
 #pragma unroll
         for (int k = 0; k < D / 16; ++k) {
-          const uint32_t off = (k >> 2) * 16384 + (k & 3) * 32;
-          umma_bf16(t_s + st * BKV, sdesc(a_q + off, 16, 1024), sdesc(b_k + off, 16, 1024),
-                    id_s, k != 0);
+          const uint64_t off = (uint64_t)(((k >> 2) * 16384 + (k & 3) * 32) >> 4);
+          umma_bf16(t_s + st * BKV, d_q + off, bk + off, id_s, k != 0);
         }
         umma_commit(&s_full[st]);
         if (MC) {
@@ -229,10 +234,11 @@ __global__ void __launch_bounds__(384, 1)
         } else {
           umma_commit(&k_empty[st]);
         }
-        if (j > 0) issue_pv(j - 1);
       }
-      issue_pv(n_kv - 1);
+      __syncwarp();
+      if (j > 0) issue_pv(j - 1);
     }
+    issue_pv(n_kv - 1);
   } else if (warp >= 4) {
     // softmax: warps 4..11; quarter q = warp % 4 owns TMEM lanes (rows) [32q, 32q+32),
     // half = (warp - 4) / 4 owns key columns [64*half, 64*half + 64) of every S block and
@@ -572,10 +578,15 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && n_it > 0) {
+    if (n_it > 0) {  // whole warp; elected lane issues (see fwd_tc)
       const uint32_t id_st = make_idesc(128, 64, 0, 0);
       const uint32_t id_g = make_idesc(128, D, 0, 1);
-      const uint32_t a_k = smem_u32(sm + L::K), a_v = smem_u32(sm + L::V);
+      const uint64_t d_k = sdesc(smem_u32(sm + L::K), 16, 1024);
+      const uint64_t d_v = sdesc(smem_u32(sm + L::V), 16, 1024);
+      const uint64_t d_q = sdesc(smem_u32(sm + L::Q0), 16, 1024);
+      const uint64_t d_o = sdesc(smem_u32(sm + L::O0), 16, 1024);
+      const uint64_t m_q = sdesc(smem_u32(sm + L::Q0), 8192, 1024);   // MN-major views
+      const uint64_t m_o = sdesc(smem_u32(sm + L::O0), 8192, 1024);
       mbar_wait(kv_full, 0);
       // dV += P^T dO, dK += dS^T Q with A read from TMEM (P^T / dS^T packed by the math
       // warps into the first 8 of every 16 columns of the S^T / dP^T buffer)
@@ -583,40 +594,44 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         const int st = it % NST, sb = it & 1;
         mbar_wait(&p_full[sb], (it >> 1) & 1);
         tc_fence_after();
-        const uint32_t b_do = smem_u32(sm + L::O0 + st * L::QT);
-        const uint32_t b_q = smem_u32(sm + L::Q0 + st * L::QT);
+        const uint64_t so = (uint64_t)((st * L::QT) >> 4);
+        if (elect_one()) {
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
-          umma_bf16_ts(t_dv, tmem + sb * 128 + k * 16, sdesc(b_do + k * 2048, 8192, 1024), id_g,
-                       (it | k) != 0);
+          for (int k = 0; k < 4; ++k)
+            umma_bf16_ts(t_dv, tmem + sb * 128 + k * 16, m_o + so + (uint64_t)((k * 2048) >> 4),
+                         id_g, (it | k) != 0);
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
-          umma_bf16_ts(t_dk, tmem + sb * 128 + 64 + k * 16, sdesc(b_q + k * 2048, 8192, 1024),
-                       id_g, (it | k) != 0);
-        if (it == n_it - 1) umma_commit(mm_done);  // single phase: final dK/dV complete
-        umma_commit(&st_empty[sb]);
-        umma_commit(&q_empty[st]);
+          for (int k = 0; k < 4; ++k)
+            umma_bf16_ts(t_dk, tmem + sb * 128 + 64 + k * 16,
+                         m_q + so + (uint64_t)((k * 2048) >> 4), id_g, (it | k) != 0);
+          if (it == n_it - 1) umma_commit(mm_done);  // single phase: final dK/dV complete
+          umma_commit(&st_empty[sb]);
+          umma_commit(&q_empty[st]);
+        }
+        __syncwarp();
       };
       for (int it = 0; it < n_it; ++it) {
         const int st = it % NST, sb = it & 1;
         mbar_wait(&q_full[st], (it / NST) & 1);
         mbar_wait(&st_empty[sb], ((it >> 1) & 1) ^ 1);
         tc_fence_after();
-        const uint32_t b_q = smem_u32(sm + L::Q0 + st * L::QT);
-        const uint32_t b_do = smem_u32(sm + L::O0 + st * L::QT);
+        const uint64_t so = (uint64_t)((st * L::QT) >> 4);
+        if (elect_one()) {
 #pragma unroll
-        for (int k = 0; k < D / 16; ++k) {
-          const uint32_t oa = (k >> 2) * 16384 + (k & 3) * 32, ob = (k >> 2) * 8192 + (k & 3) * 32;
-          umma_bf16(tmem + sb * 128, sdesc(a_k + oa, 16, 1024), sdesc(b_q + ob, 16, 1024), id_st,
-                    k != 0);
-        }
+          for (int k = 0; k < D / 16; ++k) {
+            const uint64_t oa = (uint64_t)(((k >> 2) * 16384 + (k & 3) * 32) >> 4);
+            const uint64_t ob = (uint64_t)(((k >> 2) * 8192 + (k & 3) * 32) >> 4);
+            umma_bf16(tmem + sb * 128, d_k + oa, d_q + so + ob, id_st, k != 0);
+          }
 #pragma unroll
-        for (int k = 0; k < D / 16; ++k) {
-          const uint32_t oa = (k >> 2) * 16384 + (k & 3) * 32, ob = (k >> 2) * 8192 + (k & 3) * 32;
-          umma_bf16(tmem + sb * 128 + 64, sdesc(a_v + oa, 16, 1024), sdesc(b_do + ob, 16, 1024),
-                    id_st, k != 0);
+          for (int k = 0; k < D / 16; ++k) {
+            const uint64_t oa = (uint64_t)(((k >> 2) * 16384 + (k & 3) * 32) >> 4);
+            const uint64_t ob = (uint64_t)(((k >> 2) * 8192 + (k & 3) * 32) >> 4);
+            umma_bf16(tmem + sb * 128 + 64, d_v + oa, d_o + so + ob, id_st, k != 0);
+          }
+          umma_commit(&st_full[sb]);
         }
-        umma_commit(&st_full[sb]);
+        __syncwarp();
         if (it > 0) grads(it - 1);
       }
       grads(n_it - 1);
@@ -692,13 +707,17 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
   }
 }
 
+// dq kernel: CTA = 128 queries, 128-key steps.  TMEM: S double-buffered (cols 0-255), dP
+// single (256-383; released as soon as the math warps have loaded it), dQ (384-).  dS is
+// packed (bf16) over the first half of its own S columns and read from TMEM as the A
+// operand of dQ += dS K, so S(it+1)/dP(it+1) overlap the softmax of step it and only the
+// dQ MMA of step it-1 separates them.
 template <int D>
 struct SmemQ {
-  static constexpr int NST = 4;  // K/V pipeline depth
-  static constexpr int QT = D * 128 * 2, KT = D * 64 * 2;
+  static constexpr int NST = D == 128 ? 2 : 3;  // K/V pipeline depth (128-key stages)
+  static constexpr int QT = D * 128 * 2, KT = D * 128 * 2;
   static constexpr int Q = 0, O = QT, K0 = 2 * QT, V0 = K0 + NST * KT;
-  static constexpr int DS = V0 + NST * KT;
-  static constexpr int BAR = DS + 128 * 64 * 2;
+  static constexpr int BAR = V0 + NST * KT;
   static constexpr int BYTES = BAR + 256 + 1024;
 };
 
@@ -715,18 +734,19 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
   uint64_t* qo_full = bar + 0;
   uint64_t* kv_full = bar + 1;          // [NST]
   uint64_t* kv_empty = kv_full + NST;   // [NST]
-  uint64_t* st_full = kv_empty + NST;   // [2]
-  uint64_t* st_empty = st_full + 2;     // [2]  buffer free once dQ of its step is done
-  uint64_t* ds_full = st_empty + 2;     // [2]  dS packed into the buffer (TMEM)
-  uint64_t* dq_done = ds_full + 2;
+  uint64_t* st_full = kv_empty + NST;   // [2]  S (buffer sb) and dP computed
+  uint64_t* s_free = st_full + 2;       // [2]  dQ MMA of the buffer's step done
+  uint64_t* ds_full = s_free + 2;       // [2]  dS packed into the S buffer
+  uint64_t* dp_free = ds_full + 2;      // dP loaded by every math thread
+  uint64_t* dq_done = dp_free + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dq_done + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_q = (p.S + 127) / 128;
-  const int qb = n_q - 1 - blockIdx.x;
+  const int qb = n_q - 1 - blockIdx.x;  // heavy causal blocks first
   const int bh = blockIdx.y, b = bh / p.H, h = bh % p.H;
   const int q0 = qb * 128, tok0 = b * p.S;
-  const int n_kb = (p.S + 63) / 64;
-  const int n_it = p.causal ? min(n_kb, (q0 + 128) / 64) : n_kb;
+  const int n_kb = (p.S + 127) / 128;
+  const int n_it = p.causal ? min(n_kb, qb + 1) : n_kb;
   if (threadIdx.x == 0) {
     mbar_init(qo_full, 1);
     for (int i = 0; i < NST; ++i) {
@@ -735,9 +755,10 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&st_full[i], 1);
-      mbar_init(&st_empty[i], 1);
+      mbar_init(&s_free[i], 1);
       mbar_init(&ds_full[i], 128 * BWD_SPLIT);
     }
+    mbar_init(dp_free, 128 * BWD_SPLIT);
     mbar_init(dq_done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     fence_async_smem();
@@ -747,7 +768,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t t_dq = tmem + 256;
+  const uint32_t t_dp = tmem + 256, t_dq = tmem + 384;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -763,93 +784,110 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         mbar_expect_tx(&kv_full[st], 2 * L::KT);
 #pragma unroll
         for (int c = 0; c < D / 64; ++c) {
-          tma_load_3d(&mk, &kv_full[st], sm + L::K0 + st * L::KT + c * 8192, c * 64, h, tok0 + it * 64);
-          tma_load_3d(&mv, &kv_full[st], sm + L::V0 + st * L::KT + c * 8192, c * 64, h, tok0 + it * 64);
+          tma_load_3d(&mk, &kv_full[st], sm + L::K0 + st * L::KT + c * 16384, c * 64, h,
+                      tok0 + it * 128);
+          tma_load_3d(&mv, &kv_full[st], sm + L::V0 + st * L::KT + c * 16384, c * 64, h,
+                      tok0 + it * 128);
         }
       }
     }
-  } else if (warp == 1) {
-    if (lane == 0) {
-      const uint32_t id_s = make_idesc(128, 64, 0, 0);
-      const uint32_t id_g = make_idesc(128, D, 0, 1);
-      const uint32_t a_q = smem_u32(sm + L::Q), a_o = smem_u32(sm + L::O);
-      mbar_wait(qo_full, 0);
-      // dQ += dS K with dS read from TMEM (packed over the dP buffer by the math warps)
-      auto grads = [&](int it) {
-        const int st = it % NST, sb = it & 1;
-        mbar_wait(&ds_full[sb], (it >> 1) & 1);
-        tc_fence_after();
-        const uint32_t b_k = smem_u32(sm + L::K0 + st * L::KT);
+  } else if (warp == 1) {  // whole warp; elected lane issues (see fwd_tc)
+    const uint32_t id_s = make_idesc(128, 128, 0, 0);
+    const uint32_t id_g = make_idesc(128, D, 0, 1);
+    const uint64_t d_q = sdesc(smem_u32(sm + L::Q), 16, 1024);
+    const uint64_t d_o = sdesc(smem_u32(sm + L::O), 16, 1024);
+    const uint64_t d_k = sdesc(smem_u32(sm + L::K0), 16, 1024);
+    const uint64_t d_v = sdesc(smem_u32(sm + L::V0), 16, 1024);
+    const uint64_t m_k = sdesc(smem_u32(sm + L::K0), 16384, 1024);  // K as MN-major B
+    mbar_wait(qo_full, 0);
+    // dQ += dS K: A = dS from TMEM (keys 16k.. packed at col 32*(k/2) + 8*(k%2) of the S
+    // buffer), B = the K tile as an MN-major operand (same smem bytes as the S GEMM's B)
+    auto grads = [&](int it) {
+      const int st = it % NST, sb = it & 1;
+      mbar_wait(&ds_full[sb], (it >> 1) & 1);
+      tc_fence_after();
+      const uint64_t so = (uint64_t)((st * L::KT) >> 4);
+      if (elect_one()) {
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
-          umma_bf16_ts(t_dq, tmem + sb * 128 + 64 + k * 16, sdesc(b_k + k * 2048, 8192, 1024),
-                       id_g, (it | k) != 0);
+        for (int k = 0; k < 8; ++k)
+          umma_bf16_ts(t_dq, tmem + sb * 128 + (k >> 1) * 32 + (k & 1) * 8,
+                       m_k + so + (uint64_t)((k * 2048) >> 4), id_g, (it | k) != 0);
         if (it == n_it - 1) umma_commit(dq_done);  // single phase: final dQ complete
-        umma_commit(&st_empty[sb]);
+        umma_commit(&s_free[sb]);
         umma_commit(&kv_empty[st]);
-      };
-      for (int it = 0; it < n_it; ++it) {
-        const int st = it % NST, sb = it & 1;
-        mbar_wait(&kv_full[st], (it / NST) & 1);
-        mbar_wait(&st_empty[sb], ((it >> 1) & 1) ^ 1);
-        tc_fence_after();
-        const uint32_t b_k = smem_u32(sm + L::K0 + st * L::KT);
-        const uint32_t b_v = smem_u32(sm + L::V0 + st * L::KT);
+      }
+      __syncwarp();
+    };
+    for (int it = 0; it < n_it; ++it) {
+      const int st = it % NST, sb = it & 1;
+      mbar_wait(&kv_full[st], (it / NST) & 1);
+      mbar_wait(&s_free[sb], ((it >> 1) & 1) ^ 1);
+      tc_fence_after();
+      const uint64_t so = (uint64_t)((st * L::KT) >> 4);
+      if (elect_one()) {
 #pragma unroll
         for (int k = 0; k < D / 16; ++k) {
-          const uint32_t oa = (k >> 2) * 16384 + (k & 3) * 32, ob = (k >> 2) * 8192 + (k & 3) * 32;
-          umma_bf16(tmem + sb * 128, sdesc(a_q + oa, 16, 1024), sdesc(b_k + ob, 16, 1024), id_s,
-                    k != 0);
+          const uint64_t o = (uint64_t)(((k >> 2) * 16384 + (k & 3) * 32) >> 4);
+          umma_bf16(tmem + sb * 128, d_q + o, d_k + so + o, id_s, k != 0);
         }
+      }
+      __syncwarp();
+      if (it > 0) {
+        mbar_wait(dp_free, (it - 1) & 1);
+        tc_fence_after();
+      }
+      if (elect_one()) {
 #pragma unroll
         for (int k = 0; k < D / 16; ++k) {
-          const uint32_t oa = (k >> 2) * 16384 + (k & 3) * 32, ob = (k >> 2) * 8192 + (k & 3) * 32;
-          umma_bf16(tmem + sb * 128 + 64, sdesc(a_o + oa, 16, 1024), sdesc(b_v + ob, 16, 1024),
-                    id_s, k != 0);
+          const uint64_t o = (uint64_t)(((k >> 2) * 16384 + (k & 3) * 32) >> 4);
+          umma_bf16(t_dp, d_o + o, d_v + so + o, id_s, k != 0);
         }
         umma_commit(&st_full[sb]);
-        if (it > 0) grads(it - 1);
       }
-      grads(n_it - 1);
+      __syncwarp();
+      if (it > 0) grads(it - 1);
     }
+    grads(n_it - 1);
   } else if (warp >= 4) {
-    const int q = warp & 3, part = (warp - 4) >> 2;
+    const int q = warp & 3, part = (warp - 4) >> 2;  // part: keys [32 part, 32 part + 32)
     const int r = q * 32 + lane, qi = q0 + r;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     const float l2 = p.lse2[(long long)bh * p.S_pad + qi];
     const float dd = p.dvec[(long long)bh * p.S_pad + qi];
+    const float sl2 = p.scale_log2;
     for (int it = 0; it < n_it; ++it) {
-      const int st = it & 1;
-      mbar_wait(&st_full[st], (it >> 1) & 1);
+      const int sb = it & 1;
+      mbar_wait(&st_full[sb], (it >> 1) & 1);
       tc_fence_after();
-      float s[BWD_CP], dp[BWD_CP];
-      tmem_ld16_nowait(tmem + st * 128 + part * BWD_CP + lane_off, reinterpret_cast<uint32_t*>(s));
-      tmem_ld16_nowait(tmem + st * 128 + 64 + part * BWD_CP + lane_off,
-                       reinterpret_cast<uint32_t*>(dp));
+      float s[32], dp[32];
+      tmem_ld32_nowait(tmem + sb * 128 + part * 32 + lane_off, reinterpret_cast<uint32_t*>(s));
+      tmem_ld32_nowait(t_dp + part * 32 + lane_off, reinterpret_cast<uint32_t*>(dp));
       tmem_wait_ld();
-      const int kbase = it * 64 + part * BWD_CP;
-      const float sl2 = p.scale_log2;
-      if ((kbase + BWD_CP > p.S) || (p.causal && kbase + BWD_CP - 1 > qi)) {
+      tc_fence_before();
+      mbar_arrive(dp_free);
+      const int kbase = it * 128 + part * 32;
+      if ((kbase + 32 > p.S) || (p.causal && kbase + 31 > qi)) {
         const int lim = (p.causal ? min(p.S, qi + 1) : p.S) - kbase;
 #pragma unroll
-        for (int i = 0; i < BWD_CP; ++i) {
+        for (int i = 0; i < 32; ++i) {
           const float pv = i < lim ? exp2_mufu(fmaf(s[i], sl2, -l2)) : 0.f;
           dp[i] = pv * (dp[i] - dd);
         }
       } else {
 #pragma unroll
-        for (int i = 0; i < BWD_CP; ++i) {
+        for (int i = 0; i < 32; ++i) {
           const float pv = exp2_mufu(fmaf(s[i], sl2, -l2));
           dp[i] = pv * (dp[i] - dd);
         }
       }
-      uint32_t pk[8];
+      uint32_t pk[16];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) pk[i] = pack2(dp[2 * i], dp[2 * i + 1]);
-      tmem_st8(tmem + st * 128 + 64 + part * BWD_CP + lane_off, pk);
+      for (int i = 0; i < 16; ++i) pk[i] = pack2(dp[2 * i], dp[2 * i + 1]);
+      tmem_st8(tmem + sb * 128 + part * 32 + lane_off, pk);
+      tmem_st8(tmem + sb * 128 + part * 32 + 8 + lane_off, pk + 8);
       tmem_wait_st();
       tc_fence_before();
-      mbar_arrive(&ds_full[st]);
+      mbar_arrive(&ds_full[sb]);
     }
     mbar_wait(dq_done, 0);
     tc_fence_after();
@@ -975,15 +1013,13 @@ int32_t attn_bwd_sm100(const void* q, const void* k, const void* v, const void* 
       (int)H, (int)D, ost, sh);
   GALV_LAUNCH_CHECK();
   const int64_t tokens = B * S;
-  CUtensorMap mq64, mdo64, mk128, mv128, mq128, mdo128, mk64, mv64;
+  CUtensorMap mq64, mdo64, mk128, mv128, mq128, mdo128;
   bool ok = qkv_map(&mq64, q, tokens, H, D, st, sh, 64) &&
             qkv_map(&mdo64, dout, tokens, H, D, ost, sh, 64) &&
             qkv_map(&mk128, k, tokens, H, D, st, sh, 128) &&
             qkv_map(&mv128, v, tokens, H, D, st, sh, 128) &&
             qkv_map(&mq128, q, tokens, H, D, st, sh, 128) &&
-            qkv_map(&mdo128, dout, tokens, H, D, ost, sh, 128) &&
-            qkv_map(&mk64, k, tokens, H, D, st, sh, 64) &&
-            qkv_map(&mv64, v, tokens, H, D, st, sh, 64);
+            qkv_map(&mdo128, dout, tokens, H, D, ost, sh, 128);
   GALV_CHECK_ARG(ok, "tensor map encode failed (alignment?)");
   BwdParams p;
   p.S = (int)S;
@@ -1016,7 +1052,7 @@ int32_t attn_bwd_sm100(const void* q, const void* k, const void* v, const void* 
     GALV_LAUNCH_CHECK();                                                                         \
     p.g0 = (__nv_bfloat16*)dq;                                                                   \
     p.g1 = nullptr;                                                                              \
-    bwd_dq_tc<DD><<<g_q, BWD_THREADS, SmemQ<DD>::BYTES, stream>>>(mq128, mk64, mv64, mdo128, p);         \
+    bwd_dq_tc<DD><<<g_q, BWD_THREADS, SmemQ<DD>::BYTES, stream>>>(mq128, mk128, mv128, mdo128, p);       \
     GALV_LAUNCH_CHECK();                                                                         \
   } while (0)
   if (D == 128)

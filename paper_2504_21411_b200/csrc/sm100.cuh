@@ -65,6 +65,16 @@ __device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t a, uint64_t 
       " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
       "l"(a), "l"(b), "r"(idesc), "r"(accum));
 }
+// one lane of a fully active warp returns true (the MMA-issuing warps run their loops with
+// all 32 lanes so loop state stays warp-uniform, and only the elected lane issues tcgen05)
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n .reg .b32 rx;\n .reg .pred px;\n elect.sync rx|px, 0xffffffff;\n"
+      " @px mov.s32 %0, 1;\n}\n"
+      : "+r"(pred));
+  return pred != 0;
+}
 // A operand from TMEM (rows = lanes, K packed 2 x bf16 per 32-bit column), B from smem
 __device__ __forceinline__ void umma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t b,
                                              uint32_t idesc, uint32_t accum) {
