@@ -17,6 +17,17 @@ namespace fa {
 using namespace sm100;
 
 constexpr int BQ = 128, BKV = 128;
+#ifdef GALV_ATTN_TRACE  // scratch builds only: clock64 timeline of CTA (0, 0)
+__device__ unsigned long long g_trace[8192];
+#define TRACE(slot)                                                        \
+  do {                                                                     \
+    if (blockIdx.x == 0 && blockIdx.y == 0) g_trace[(slot)] = clock64();   \
+  } while (0)
+#else
+#define TRACE(slot) \
+  do {              \
+  } while (0)
+#endif
 // K/V multicast across CTA pairs (fwd_tc<D, true>) is correct but measured slower on B200
 // (663 vs 701 TF at S=4K, 933 vs 942 TF at S=32K, 203 vs 237 TF at D=64): the forward is not
 // L2-bandwidth bound, and pairing couples the two CTAs' pipelines.  Off by default.
@@ -714,10 +725,12 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
 // dQ MMA of step it-1 separates them.
 template <int D>
 struct SmemQ {
-  static constexpr int NST = D == 128 ? 2 : 3;  // K/V pipeline depth (128-key stages)
+  // K is used by S(it) and dQ(it) (released late), V only by dP(it): separate rings, K one
+  // stage deeper so its TMA load for step it+2 starts a full step before S(it+2) needs it
+  static constexpr int NK = 3, NV = 2;
   static constexpr int QT = D * 128 * 2, KT = D * 128 * 2;
-  static constexpr int Q = 0, O = QT, K0 = 2 * QT, V0 = K0 + NST * KT;
-  static constexpr int BAR = V0 + NST * KT;
+  static constexpr int Q = 0, O = QT, K0 = 2 * QT, V0 = K0 + NK * KT;
+  static constexpr int BAR = V0 + NV * KT;
   static constexpr int BYTES = BAR + 256 + 1024;
 };
 
@@ -730,11 +743,12 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // keeps the shared window
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::BAR);
-  constexpr int NST = L::NST;
   uint64_t* qo_full = bar + 0;
-  uint64_t* kv_full = bar + 1;          // [NST]
-  uint64_t* kv_empty = kv_full + NST;   // [NST]
-  uint64_t* st_full = kv_empty + NST;   // [2]  S (buffer sb) and dP computed
+  uint64_t* k_full = bar + 1;           // [NK]
+  uint64_t* k_empty = k_full + L::NK;   // [NK]
+  uint64_t* v_full = k_empty + L::NK;   // [NV]
+  uint64_t* v_empty = v_full + L::NV;   // [NV]
+  uint64_t* st_full = v_empty + L::NV;  // [2]  S (buffer sb) and dP computed
   uint64_t* s_free = st_full + 2;       // [2]  dQ MMA of the buffer's step done
   uint64_t* ds_full = s_free + 2;       // [2]  dS packed into the S buffer
   uint64_t* dp_free = ds_full + 2;      // dP loaded by every math thread
@@ -749,9 +763,13 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
   const int n_it = p.causal ? min(n_kb, qb + 1) : n_kb;
   if (threadIdx.x == 0) {
     mbar_init(qo_full, 1);
-    for (int i = 0; i < NST; ++i) {
-      mbar_init(&kv_full[i], 1);
-      mbar_init(&kv_empty[i], 1);
+    for (int i = 0; i < L::NK; ++i) {
+      mbar_init(&k_full[i], 1);
+      mbar_init(&k_empty[i], 1);
+    }
+    for (int i = 0; i < L::NV; ++i) {
+      mbar_init(&v_full[i], 1);
+      mbar_init(&v_empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&st_full[i], 1);
@@ -778,17 +796,26 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         tma_load_3d(&mq, qo_full, sm + L::Q + c * 16384, c * 64, h, tok0 + q0);
         tma_load_3d(&mdo, qo_full, sm + L::O + c * 16384, c * 64, h, tok0 + q0);
       }
-      for (int it = 0; it < n_it; ++it) {
-        const int st = it % NST;
-        mbar_wait(&kv_empty[st], ((it / NST) & 1) ^ 1);
-        mbar_expect_tx(&kv_full[st], 2 * L::KT);
+      for (int it = 0; it < n_it; ++it) {  // K ring
+        const int st = it % L::NK;
+        mbar_wait(&k_empty[st], ((it / L::NK) & 1) ^ 1);
+        mbar_expect_tx(&k_full[st], L::KT);
 #pragma unroll
-        for (int c = 0; c < D / 64; ++c) {
-          tma_load_3d(&mk, &kv_full[st], sm + L::K0 + st * L::KT + c * 16384, c * 64, h,
+        for (int c = 0; c < D / 64; ++c)
+          tma_load_3d(&mk, &k_full[st], sm + L::K0 + st * L::KT + c * 16384, c * 64, h,
                       tok0 + it * 128);
-          tma_load_3d(&mv, &kv_full[st], sm + L::V0 + st * L::KT + c * 16384, c * 64, h,
+      }
+    }
+  } else if (warp == 3) {
+    if (lane == 0) {
+      for (int it = 0; it < n_it; ++it) {  // V ring
+        const int st = it % L::NV;
+        mbar_wait(&v_empty[st], ((it / L::NV) & 1) ^ 1);
+        mbar_expect_tx(&v_full[st], L::KT);
+#pragma unroll
+        for (int c = 0; c < D / 64; ++c)
+          tma_load_3d(&mv, &v_full[st], sm + L::V0 + st * L::KT + c * 16384, c * 64, h,
                       tok0 + it * 128);
-        }
       }
     }
   } else if (warp == 1) {  // whole warp; elected lane issues (see fwd_tc)
@@ -803,9 +830,10 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     // dQ += dS K: A = dS from TMEM (keys 16k.. packed at col 32*(k/2) + 8*(k%2) of the S
     // buffer), B = the K tile as an MN-major operand (same smem bytes as the S GEMM's B)
     auto grads = [&](int it) {
-      const int st = it % NST, sb = it & 1;
+      const int st = it % L::NK, sb = it & 1;
       mbar_wait(&ds_full[sb], (it >> 1) & 1);
       tc_fence_after();
+      if (lane == 0) TRACE(it * 8 + 3);
       const uint64_t so = (uint64_t)((st * L::KT) >> 4);
       if (elect_one()) {
 #pragma unroll
@@ -814,35 +842,38 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
                        m_k + so + (uint64_t)((k * 2048) >> 4), id_g, (it | k) != 0);
         if (it == n_it - 1) umma_commit(dq_done);  // single phase: final dQ complete
         umma_commit(&s_free[sb]);
-        umma_commit(&kv_empty[st]);
+        umma_commit(&k_empty[st]);
       }
       __syncwarp();
     };
     for (int it = 0; it < n_it; ++it) {
-      const int st = it % NST, sb = it & 1;
-      mbar_wait(&kv_full[st], (it / NST) & 1);
+      const int sk = it % L::NK, sv = it % L::NV, sb = it & 1;
+      if (lane == 0) TRACE(it * 8 + 0);
+      mbar_wait(&k_full[sk], (it / L::NK) & 1);
       mbar_wait(&s_free[sb], ((it >> 1) & 1) ^ 1);
       tc_fence_after();
-      const uint64_t so = (uint64_t)((st * L::KT) >> 4);
+      if (lane == 0) TRACE(it * 8 + 1);
+      const uint64_t ok = (uint64_t)((sk * L::KT) >> 4), ov = (uint64_t)((sv * L::KT) >> 4);
       if (elect_one()) {
 #pragma unroll
         for (int k = 0; k < D / 16; ++k) {
           const uint64_t o = (uint64_t)(((k >> 2) * 16384 + (k & 3) * 32) >> 4);
-          umma_bf16(tmem + sb * 128, d_q + o, d_k + so + o, id_s, k != 0);
+          umma_bf16(tmem + sb * 128, d_q + o, d_k + ok + o, id_s, k != 0);
         }
       }
       __syncwarp();
-      if (it > 0) {
-        mbar_wait(dp_free, (it - 1) & 1);
-        tc_fence_after();
-      }
+      mbar_wait(&v_full[sv], (it / L::NV) & 1);
+      if (it > 0) mbar_wait(dp_free, (it - 1) & 1);
+      tc_fence_after();
+      if (lane == 0) TRACE(it * 8 + 2);
       if (elect_one()) {
 #pragma unroll
         for (int k = 0; k < D / 16; ++k) {
           const uint64_t o = (uint64_t)(((k >> 2) * 16384 + (k & 3) * 32) >> 4);
-          umma_bf16(t_dp, d_o + o, d_v + so + o, id_s, k != 0);
+          umma_bf16(t_dp, d_o + o, d_v + ov + o, id_s, k != 0);
         }
         umma_commit(&st_full[sb]);
+        umma_commit(&v_empty[sv]);
       }
       __syncwarp();
       if (it > 0) grads(it - 1);
@@ -859,12 +890,14 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       const int sb = it & 1;
       mbar_wait(&st_full[sb], (it >> 1) & 1);
       tc_fence_after();
+      if (warp == 4 && lane == 0) TRACE(it * 8 + 4);
       float s[32], dp[32];
       tmem_ld32_nowait(tmem + sb * 128 + part * 32 + lane_off, reinterpret_cast<uint32_t*>(s));
       tmem_ld32_nowait(t_dp + part * 32 + lane_off, reinterpret_cast<uint32_t*>(dp));
       tmem_wait_ld();
       tc_fence_before();
       mbar_arrive(dp_free);
+      if (warp == 4 && lane == 0) TRACE(it * 8 + 5);
       const int kbase = it * 128 + part * 32;
       if ((kbase + 32 > p.S) || (p.causal && kbase + 31 > qi)) {
         const int lim = (p.causal ? min(p.S, qi + 1) : p.S) - kbase;
@@ -883,11 +916,13 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       uint32_t pk[16];
 #pragma unroll
       for (int i = 0; i < 16; ++i) pk[i] = pack2(dp[2 * i], dp[2 * i + 1]);
+      if (warp == 4 && lane == 0) TRACE(it * 8 + 6);
       tmem_st8(tmem + sb * 128 + part * 32 + lane_off, pk);
       tmem_st8(tmem + sb * 128 + part * 32 + 8 + lane_off, pk + 8);
       tmem_wait_st();
       tc_fence_before();
       mbar_arrive(&ds_full[sb]);
+      if (warp == 4 && lane == 0) TRACE(it * 8 + 7);
     }
     mbar_wait(dq_done, 0);
     tc_fence_after();
@@ -994,6 +1029,12 @@ int32_t attn_fwd_sm100(const void* q, const void* k, const void* v, void* o, flo
   return 0;
 }
 
+
+#ifdef GALV_ATTN_TRACE
+extern "C" int32_t galv_attn_trace_read(void* host) {
+  return (int32_t)cudaMemcpyFromSymbol(host, fa::g_trace, sizeof(fa::g_trace));
+}
+#endif
 
 int64_t attn_bwd_ws_sm100(int64_t B, int64_t S, int64_t H) {
   const int64_t S_pad = (S + 127) / 128 * 128;
