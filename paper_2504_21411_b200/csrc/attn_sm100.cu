@@ -605,6 +605,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         const int st = it % NST, sb = it & 1;
         mbar_wait(&p_full[sb], (it >> 1) & 1);
         tc_fence_after();
+        if (lane == 0) TRACE(4096 + it * 8 + 3);
         const uint64_t so = (uint64_t)((st * L::QT) >> 4);
         if (elect_one()) {
 #pragma unroll
@@ -623,9 +624,12 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       };
       for (int it = 0; it < n_it; ++it) {
         const int st = it % NST, sb = it & 1;
+        if (lane == 0) TRACE(4096 + it * 8 + 0);
         mbar_wait(&q_full[st], (it / NST) & 1);
+        if (lane == 0) TRACE(4096 + it * 8 + 2);
         mbar_wait(&st_empty[sb], ((it >> 1) & 1) ^ 1);
         tc_fence_after();
+        if (lane == 0) TRACE(4096 + it * 8 + 1);
         const uint64_t so = (uint64_t)((st * L::QT) >> 4);
         if (elect_one()) {
 #pragma unroll
@@ -655,11 +659,13 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       const int st = it % NST, sb = it & 1, q0 = (i0 + it) * 64;
       mbar_wait(&st_full[sb], (it >> 1) & 1);
       tc_fence_after();
+      if (warp == 4 && lane == 0) TRACE(4096 + it * 8 + 4);
       float s[BWD_CP], dp[BWD_CP];
       tmem_ld16_nowait(tmem + sb * 128 + part * BWD_CP + lane_off, reinterpret_cast<uint32_t*>(s));
       tmem_ld16_nowait(tmem + sb * 128 + 64 + part * BWD_CP + lane_off,
                        reinterpret_cast<uint32_t*>(dp));
       tmem_wait_ld();
+      if (warp == 4 && lane == 0) TRACE(4096 + it * 8 + 5);
       const float* l2 = reinterpret_cast<const float*>(sm + L::LSE + st * 256) + part * BWD_CP;
       const float* dd = reinterpret_cast<const float*>(sm + L::DV + st * 256) + part * BWD_CP;
       const int qbase = q0 + part * BWD_CP;
@@ -683,6 +689,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       uint32_t pk[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) pk[i] = pack2(s[2 * i], s[2 * i + 1]);
+      if (warp == 4 && lane == 0) TRACE(4096 + it * 8 + 6);
       tmem_st8(tmem + sb * 128 + part * BWD_CP + lane_off, pk);
 #pragma unroll
       for (int i = 0; i < 8; ++i) pk[i] = pack2(dp[2 * i], dp[2 * i + 1]);
@@ -690,6 +697,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       tmem_wait_st();
       tc_fence_before();
       mbar_arrive(&p_full[sb]);
+      if (warp == 4 && lane == 0) TRACE(4096 + it * 8 + 7);
     }
     if (n_it > 0) {
       mbar_wait(mm_done, 0);

@@ -32,3 +32,15 @@ print("softmax: wait->ld", (t[:,5]-t[:,4])[2:].mean(), " ld->comp", (t[:,6]-t[:,
 print("dQ issue - ds_arr", (t[:,3]-t[:,7])[2:].mean())
 print("S issue - dQ(it-2) issue", (t[2:,1]-t[:-2,3])[2:].mean())
 print("st_full seen - dP issue", (t[:,4]-t[:,2])[2:].mean())
+print("==== dkdv CTA (0,0): 64 x 64-query steps")
+t = buf[4096:4096 + 64*8].reshape(64, 8).astype(np.int64)
+t = t - t[0, 0]
+names = ["mma:loop", "mma:S", "mma:qful", "mma:grad", "sm:st_full", "sm:ld", "sm:comp", "sm:p_arr"]
+print("it " + " ".join(f"{n:>10}" for n in names))
+for i in list(range(0, 12)) + list(range(58, 64)):
+    print(f"{i:2d} " + " ".join(f"{x:10d}" for x in t[i]))
+print("S issue interval mean", np.diff(t[:, 1])[4:-4].mean())
+print("loop->qfull", (t[:,2]-t[:,0])[4:-4].mean(), "qfull->S", (t[:,1]-t[:,2])[4:-4].mean())
+print("softmax: wait->ld", (t[:,5]-t[:,4])[4:-4].mean(), " ld->comp", (t[:,6]-t[:,5])[4:-4].mean(), " comp->arr", (t[:,7]-t[:,6])[4:-4].mean())
+print("grad issue - p_arr", (t[:,3]-t[:,7])[4:-4].mean())
+print("st_full seen - S issue", (t[:,4]-t[:,1])[4:-4].mean())
