@@ -203,6 +203,23 @@ int32_t galv_adamw_bcast(float* master, float* m, float* v, const void* grad, vo
                          float beta1, float beta2, float eps, float weight_decay,
                          float grad_scale, int64_t step, int32_t grad_dtype, void* stream);
 
+/* ---- NCCL communicators (opaque ncclComm_t as void*), collectives.py:49-89 ring passes --
+ * libnccl.so.2 is dlopen'ed on first use (no link-time dependency).  dtype 0 = f32, 1 = bf16;
+ * counts in elements; the ncclResult_t is returned on failure. */
+int32_t galv_comm_unique_id(void* out /* 128 bytes */);
+int32_t galv_comm_init(const void* unique_id, int32_t nranks, int32_t rank, void** comm);
+int32_t galv_comm_split(void* comm, int32_t color, int32_t key, void** out);
+int32_t galv_comm_destroy(void* comm);
+int32_t galv_all_reduce(void* comm, const void* send, void* recv, int64_t count, int32_t dtype,
+                        void* stream);
+int32_t galv_reduce_scatter(void* comm, const void* send, void* recv, int64_t recv_count,
+                            int32_t dtype, void* stream);
+int32_t galv_all_gather(void* comm, const void* send, void* recv, int64_t send_count,
+                        int32_t dtype, void* stream);
+/* one grouped send + recv of raw bytes (pipeline-stage boundary exchange) */
+int32_t galv_sendrecv(void* comm, const void* send, int64_t send_bytes, int32_t peer_send,
+                      void* recv, int64_t recv_bytes, int32_t peer_recv, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -63,7 +63,7 @@ def build(clean: bool = False, verbose: bool = False) -> Path:
     objs = [OBJ / (s.stem + ".o") for s in sources]
     if jobs or not LIB.exists() or any(o.stat().st_mtime > LIB.stat().st_mtime for o in objs):
         cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", str(LIB),
-               *map(str, objs), "-lcudart"]
+               *map(str, objs), "-lcudart", "-ldl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")

@@ -34,6 +34,14 @@ _SIGS = {
                       _P], _I32),
     "galv_tp_signal_reduce": ([_P, _I32, _I32, C.c_uint32, _P, _P, _I64, _I32, _P], _I32),
     "galv_tp_allgather": ([_P, _P, _P, _I32, _I32, C.c_uint32, _I64, _P], _I32),
+    "galv_comm_unique_id": ([_P], _I32),
+    "galv_comm_init": ([_P, _I32, _I32, C.POINTER(C.c_void_p)], _I32),
+    "galv_comm_split": ([_P, _I32, _I32, C.POINTER(C.c_void_p)], _I32),
+    "galv_comm_destroy": ([_P], _I32),
+    "galv_all_reduce": ([_P, _P, _P, _I64, _I32, _P], _I32),
+    "galv_reduce_scatter": ([_P, _P, _P, _I64, _I32, _P], _I32),
+    "galv_all_gather": ([_P, _P, _P, _I64, _I32, _P], _I32),
+    "galv_sendrecv": ([_P, _P, _I64, _I32, _P, _I64, _I32, _P], _I32),
     "galv_nvl_signal": ([_P, _I32, _I32, C.c_uint32, _P], _I32),
     "galv_nvl_wait": ([_P, _I32, C.c_uint32, _P], _I32),
     "galv_dp_reduce": ([_P, _P, _I32, _I64, _P, _I32, _P, _P, _I64, _I32, _P], _I32),
@@ -447,6 +455,56 @@ def gemm_rs(a, b, peer_ptrs, rows_per_rank, my_slot, *, trans_a=False, trans_b=F
     if timed:
         ev1.record()
         _stats.gemm_events.append((2.0 * M * N * K, ev0, ev1, (M, N, K)))
+
+
+# ---------------------------------------------------------------- NCCL through the C ABI
+def comm_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _call("galv_comm_unique_id", C.cast(buf, C.c_void_p))
+    return buf.raw
+
+
+def comm_init(unique_id: bytes, nranks: int, rank: int) -> int:
+    """Opaque NCCL communicator handle (call on every rank with the same id)."""
+    buf = C.create_string_buffer(unique_id, 128)
+    out = C.c_void_p()
+    _call("galv_comm_init", C.cast(buf, C.c_void_p), nranks, rank, C.byref(out))
+    return out.value
+
+
+def comm_split(comm: int, color: int, key: int) -> int:
+    out = C.c_void_p()
+    _call("galv_comm_split", comm, color, key, C.byref(out))
+    return out.value
+
+
+def comm_destroy(comm: int) -> None:
+    _call("galv_comm_destroy", comm)
+
+
+def comm_all_reduce(comm: int, send, recv=None):
+    recv = send if recv is None else recv
+    _call("galv_all_reduce", comm, _ptr(send), _ptr(recv), send.numel(),
+          dtype_code(send.dtype), _stream())
+    return recv
+
+
+def comm_reduce_scatter(comm: int, send, recv):
+    _call("galv_reduce_scatter", comm, _ptr(send), _ptr(recv), recv.numel(),
+          dtype_code(send.dtype), _stream())
+    return recv
+
+
+def comm_all_gather(comm: int, send, recv):
+    _call("galv_all_gather", comm, _ptr(send), _ptr(recv), send.numel(),
+          dtype_code(send.dtype), _stream())
+    return recv
+
+
+def comm_sendrecv(comm: int, send, peer_send: int, recv, peer_recv: int):
+    nb = lambda t: 0 if t is None else t.numel() * t.element_size()
+    _call("galv_sendrecv", comm, _ptr(send), nb(send), peer_send, _ptr(recv), nb(recv),
+          peer_recv, _stream())
 
 
 def nvl_signal(flag_ptrs, me, t, epoch):

@@ -39,3 +39,16 @@ def test_two_gpu_strategies():
 
 def test_four_gpu_strategies():
     _run(4, FOUR, 29512)
+
+
+def test_two_gpu_c_abi_nccl():
+    """galv_comm_* / galv_all_reduce / reduce_scatter / all_gather / sendrecv / split."""
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", "29513",
+           os.path.join(HERE, "mp_comm.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300)
+    print(r.stdout[-3000:])
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "FAIL" not in r.stdout and r.stdout.count("PASS") == 2
