@@ -72,38 +72,69 @@ __global__ void wait_kernel(const uint32_t* my_flags, int t, uint32_t epoch) {
   __syncthreads();
 }
 
-// out[i] (+)= sum over ranks of src[i], i over this rank's chunk (8 bf16 per step).
+// out[i] (+)= sum over ranks of src[i], i over this rank's chunk (8 bf16 per vector).
 // mc_src: multicast address of the chunk, or null -> unicast loads from peer_src[r] + off.
 // bcast: also store the reduced chunk to every rank (multicast or peer_dst[r] + off).
+// U vectors per thread are loaded before any is consumed, so a small grid keeps enough
+// NVLink round trips in flight (the kernel runs next to the backward GEMMs and should
+// occupy as few SMs as possible).
+constexpr int RU = 4;
+
+__device__ __forceinline__ void reduce_store(uint4 raw_sum, float* extra, int64_t i, uint4* out,
+                                             int accumulate, uint4* mc_dst,
+                                             void* const* peer_dst, int t, int64_t off16) {
+  float acc[8];
+  bf16x8_to_f(raw_sum, acc);
+  if (extra) {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[e] = extra[e];
+  }
+  if (accumulate) {
+    float v[8];
+    bf16x8_to_f(out[i], v);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[e] += v[e];
+  }
+  const uint4 res = f_to_bf16x8(acc);
+  if (out) out[i] = res;
+  if (mc_dst) {
+    mc_st16(mc_dst + i, res);
+  } else if (peer_dst) {
+    for (int r = 0; r < t; ++r) reinterpret_cast<uint4*>(peer_dst[r])[off16 + i] = res;
+  }
+}
+
 __global__ void __launch_bounds__(512) reduce_chunk(const uint4* mc_src, void* const* peer_src,
                                                     int t, int64_t off16, uint4* out,
                                                     int accumulate, uint4* mc_dst,
                                                     void* const* peer_dst, int64_t n8) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n8;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    float acc[8], v[8];
-    if (mc_src) {
-      bf16x8_to_f(mc_ld_reduce_bf16x8(mc_src + i), acc);
-    } else {
-      bf16x8_to_f(reinterpret_cast<const uint4*>(peer_src[0])[off16 + i], acc);
-      for (int r = 1; r < t; ++r) {
-        bf16x8_to_f(reinterpret_cast<const uint4*>(peer_src[r])[off16 + i], v);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t base = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (mc_src) {
+    // RU independent multimem loads in flight per thread
+    for (; base + (RU - 1) * stride < n8; base += stride * RU) {
+      uint4 raw[RU];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) acc[e] += v[e];
-      }
+      for (int u = 0; u < RU; ++u) raw[u] = mc_ld_reduce_bf16x8(mc_src + base + u * stride);
+#pragma unroll
+      for (int u = 0; u < RU; ++u)
+        reduce_store(raw[u], nullptr, base + u * stride, out, accumulate, mc_dst, peer_dst, t,
+                     off16);
     }
-    if (accumulate) {
-      bf16x8_to_f(out[i], v);
+    for (; base < n8; base += stride)
+      reduce_store(mc_ld_reduce_bf16x8(mc_src + base), nullptr, base, out, accumulate, mc_dst,
+                   peer_dst, t, off16);
+    return;
+  }
+  for (; base < n8; base += stride) {  // unicast: sum the peers' copies over NVLink
+    float acc[8], v[8];
+    bf16x8_to_f(reinterpret_cast<const uint4*>(peer_src[0])[off16 + base], acc);
+    for (int r = 1; r < t; ++r) {
+      bf16x8_to_f(reinterpret_cast<const uint4*>(peer_src[r])[off16 + base], v);
 #pragma unroll
       for (int e = 0; e < 8; ++e) acc[e] += v[e];
     }
-    const uint4 res = f_to_bf16x8(acc);
-    if (out) out[i] = res;
-    if (mc_dst) {
-      mc_st16(mc_dst + i, res);
-    } else if (peer_dst) {
-      for (int r = 0; r < t; ++r) reinterpret_cast<uint4*>(peer_dst[r])[off16 + i] = res;
-    }
+    reduce_store(make_uint4(0, 0, 0, 0), acc, base, out, accumulate, mc_dst, peer_dst, t, off16);
   }
 }
 

@@ -34,7 +34,7 @@ from .. import kernels as K
 
 _FLAGS = 512                  # [ch0 flags: 64 x u32][ch1 flags: 64 x u32][pad]
 RING = 3                      # ZeRO-2 grad-target slots in flight (written / reducing / free)
-MAX_CTAS = int(os.environ.get("GALV_DP_NVLINK_CTAS", "32"))
+MAX_CTAS = int(os.environ.get("GALV_DP_NVLINK_CTAS", "16"))
 
 
 def enabled() -> bool:
