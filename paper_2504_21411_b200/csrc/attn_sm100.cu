@@ -48,9 +48,8 @@ struct Smem {
   static constexpr int Q = 0;
   static constexpr int K0 = Q + TILE;
   static constexpr int V0 = K0 + 2 * TILE;
-  static constexpr int P = V0 + 2 * TILE;
-  static constexpr int BAR = P + BQ * BKV * 2;   // 32 KB of P
-  static constexpr int BYTES = BAR + 128 + 3 * 1024 + 1024;  // barriers, xch, slack
+  static constexpr int BAR = V0 + 2 * TILE;      // P lives in TMEM (over its S buffer)
+  static constexpr int BYTES = BAR + 160 + 3 * 1024 + 1024;  // barriers, xch, slack
 };
 
 struct FwdParams {
@@ -104,12 +103,12 @@ __global__ void __launch_bounds__(384, 1)
   uint64_t* k_full = bar + 1;    // [2]
   uint64_t* v_full = bar + 3;    // [2]
   uint64_t* k_empty = bar + 5;   // [2]  K stage free once S_j is computed
-  uint64_t* s_full = bar + 7;    // [2]
-  uint64_t* s_empty = bar + 9;   // [2]
-  uint64_t* p_full = bar + 11;
-  uint64_t* o_done = bar + 12;
-  uint64_t* v_empty = bar + 13;  // [2]  V stage free once PV_j is computed
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 15);
+  uint64_t* s_full = bar + 7;    // [3]
+  uint64_t* s_empty = bar + 10;  // [3]  S buffer free once PV of its block is done
+  uint64_t* p_full = bar + 13;   // [3]  P (bf16) packed over its S buffer
+  uint64_t* o_done = bar + 16;
+  uint64_t* v_empty = bar + 17;  // [2]  V stage free once PV_j is computed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 19);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int qb = p.n_qblocks - 1 - blockIdx.x;  // heavy causal blocks first
@@ -130,10 +129,12 @@ __global__ void __launch_bounds__(384, 1)
       mbar_init(&v_full[i], 1);
       mbar_init(&k_empty[i], MC ? 2 : 1);
       mbar_init(&v_empty[i], MC ? 2 : 1);
-      mbar_init(&s_full[i], 1);
-      mbar_init(&s_empty[i], 256);
     }
-    mbar_init(p_full, 256);
+    for (int i = 0; i < 3; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&s_empty[i], 1);
+      mbar_init(&p_full[i], 256);
+    }
     mbar_init(o_done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     fence_async_smem();
@@ -155,7 +156,9 @@ __global__ void __launch_bounds__(384, 1)
     __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t t_s = tmem, t_o = tmem + 256;
+  // TMEM: S triple-buffered (cols 0-383; P(j) bf16 is packed over the first half of each
+  // softmax half's S columns and read by PV as the A operand), O at cols 384-511
+  const uint32_t t_s = tmem, t_o = tmem + 384;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -201,22 +204,24 @@ __global__ void __launch_bounds__(384, 1)
     const uint32_t id_s = make_idesc(BQ, BKV, 0, 0);  // Q (K-major) x K (K-major)
     const uint32_t id_o = make_idesc(BQ, D, 0, 1);    // P (K-major) x V (MN-major)
     const uint64_t d_q = sdesc(smem_u32(sm + L::Q), 16, 1024);
-    const uint64_t d_p = sdesc(smem_u32(sm + L::P), 16, 1024);
     const uint64_t d_k = sdesc(smem_u32(sm + L::K0), 16, 1024);
     const uint64_t d_v = sdesc(smem_u32(sm + L::V0), 16384, 1024);
     mbar_wait(q_full, 0);
+    // O += P V: A = P from TMEM (keys 16k.. packed at col 64*(k/4) + 8*(k%4) of the block's S
+    // buffer), B = the V tile as an MN-major operand
     auto issue_pv = [&](int j) {
-      const int st = j & 1;
-      mbar_wait(p_full, j & 1);
+      const int st = j & 1, sb = j % 3;
+      mbar_wait(&p_full[sb], (j / 3) & 1);
       mbar_wait(&v_full[st], (j >> 1) & 1);
       tc_fence_after();
       const uint64_t bv = d_v + (uint64_t)((st * L::TILE) >> 4);
       if (elect_one()) {
 #pragma unroll
         for (int k = 0; k < BKV / 16; ++k)
-          umma_bf16(t_o, d_p + (uint64_t)((((k >> 2) * 16384) + (k & 3) * 32) >> 4),
-                    bv + (uint64_t)((k * 2048) >> 4), id_o, (j | k) != 0);
+          umma_bf16_ts(t_o, t_s + sb * BKV + (k >> 2) * 64 + (k & 3) * 8,
+                       bv + (uint64_t)((k * 2048) >> 4), id_o, (j | k) != 0);
         umma_commit(o_done);
+        umma_commit(&s_empty[sb]);
         if (MC) {
           umma_commit_mc(&v_empty[st], 0x1);  // release to the leader's producer
           if (j + 2 < n_kv) mbar_expect_tx(&v_full[st], TILE_BYTES);  // re-arm own stage
@@ -227,18 +232,18 @@ __global__ void __launch_bounds__(384, 1)
       __syncwarp();
     };
     for (int j = 0; j < n_kv; ++j) {
-      const int st = j & 1;
+      const int st = j & 1, sb = j % 3;
       mbar_wait(&k_full[st], (j >> 1) & 1);
-      mbar_wait(&s_empty[st], ((j >> 1) & 1) ^ 1);
+      mbar_wait(&s_empty[sb], ((j / 3) & 1) ^ 1);
       tc_fence_after();
       const uint64_t bk = d_k + (uint64_t)((st * L::TILE) >> 4);
       if (elect_one()) {
 #pragma unroll
         for (int k = 0; k < D / 16; ++k) {
           const uint64_t off = (uint64_t)(((k >> 2) * 16384 + (k & 3) * 32) >> 4);
-          umma_bf16(t_s + st * BKV, d_q + off, bk + off, id_s, k != 0);
+          umma_bf16(t_s + sb * BKV, d_q + off, bk + off, id_s, k != 0);
         }
-        umma_commit(&s_full[st]);
+        umma_commit(&s_full[sb]);
         if (MC) {
           umma_commit_mc(&k_empty[st], 0x1);
           if (j + 2 < n_kv) mbar_expect_tx(&k_full[st], TILE_BYTES);
@@ -260,20 +265,17 @@ __global__ void __launch_bounds__(384, 1)
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     float* xch = reinterpret_cast<float*>(bar + 16);  // [2][128] partial maxima / sums
     float m_used = -INFINITY, l = 0.f;
-    uint8_t* prow = sm + L::P + half * 16384 + r * 128;
     constexpr int HC = BKV / 2;  // columns per half
     for (int j = 0; j < n_kv; ++j) {
-      const int st = j & 1;
-      mbar_wait(&s_full[st], (j >> 1) & 1);
+      const int sb = j % 3;
+      mbar_wait(&s_full[sb], (j / 3) & 1);
       tc_fence_after();
       float s[HC];
 #pragma unroll
       for (int c = 0; c < HC / 32; ++c)
-        tmem_ld32_nowait(t_s + st * BKV + half * HC + c * 32 + lane_off,
+        tmem_ld32_nowait(t_s + sb * BKV + half * HC + c * 32 + lane_off,
                          reinterpret_cast<uint32_t*>(s) + c * 32);
       tmem_wait_ld();
-      tc_fence_before();
-      mbar_arrive(&s_empty[st]);
       const int k0 = j * BKV + half * HC;
       const bool mask = (k0 + HC > p.S) || (p.causal && k0 + HC - 1 > q0);
       float mx = -INFINITY;
@@ -318,9 +320,11 @@ __global__ void __launch_bounds__(384, 1)
         pk[i / 2] = pack2(p0, p1);
       }
       l = l * alpha + rs;
-      if (j > 0) mbar_wait(o_done, (j - 1) & 1);
-      tc_fence_after();
+      // lazy rescale: O must hold PV(j-1) first.  When S(j) completed, PV(j-2) had too and
+      // PV(j) needs this P, so o_done has completed j-1 or j phases: the parity wait is exact
       if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
+        mbar_wait(o_done, (j - 1) & 1);
+        tc_fence_after();
 #pragma unroll 1
         for (int c = 0; c < D / 64; ++c) {
           uint32_t ov[32];
@@ -331,16 +335,10 @@ __global__ void __launch_bounds__(384, 1)
           tmem_st32(ta, ov);
         }
       }
-      // P half-row -> smem chunk `half` (keys 64*half..), K-major SW128
-#pragma unroll
-      for (int u = 0; u < HC / 8; ++u) {
-        const int unit = u ^ (r & 7);
-        uint4 v4 = make_uint4(pk[u * 4], pk[u * 4 + 1], pk[u * 4 + 2], pk[u * 4 + 3]);
-        *reinterpret_cast<uint4*>(prow + unit * 16) = v4;
-      }
-      fence_async_smem();
+      // P half-row (bf16 pairs) -> TMEM over this half's first 32 S columns
+      tmem_st32(t_s + sb * BKV + half * HC + lane_off, pk);  // includes wait::st
       tc_fence_before();
-      mbar_arrive(p_full);
+      mbar_arrive(&p_full[sb]);
     }
     // full row sum = both halves
     xch[512 + half * 128 + r] = l;
