@@ -206,14 +206,15 @@ __global__ void __launch_bounds__(384, 1)
     const uint64_t d_q = sdesc(smem_u32(sm + L::Q), 16, 1024);
     const uint64_t d_k = sdesc(smem_u32(sm + L::K0), 16, 1024);
     const uint64_t d_v = sdesc(smem_u32(sm + L::V0), 16384, 1024);
-    mbar_wait(q_full, 0);
+    mbar_wait_fast(q_full, 0);
     // O += P V: A = P from TMEM (keys 16k.. packed at col 64*(k/4) + 8*(k%4) of the block's S
     // buffer), B = the V tile as an MN-major operand
     auto issue_pv = [&](int j) {
       const int st = j & 1, sb = j % 3;
-      mbar_wait(&p_full[sb], (j / 3) & 1);
-      mbar_wait(&v_full[st], (j >> 1) & 1);
+      mbar_wait_fast(&p_full[sb], (j / 3) & 1);
+      mbar_wait_fast(&v_full[st], (j >> 1) & 1);
       tc_fence_after();
+      if (lane == 0) TRACE(6144 + j * 8 + 1);
       const uint64_t bv = d_v + (uint64_t)((st * L::TILE) >> 4);
       if (elect_one()) {
 #pragma unroll
@@ -233,9 +234,12 @@ __global__ void __launch_bounds__(384, 1)
     };
     for (int j = 0; j < n_kv; ++j) {
       const int st = j & 1, sb = j % 3;
-      mbar_wait(&k_full[st], (j >> 1) & 1);
-      mbar_wait(&s_empty[sb], ((j / 3) & 1) ^ 1);
+      if (lane == 0) TRACE(6144 + j * 8 + 6);
+      mbar_wait_fast(&k_full[st], (j >> 1) & 1);
+      if (lane == 0) TRACE(6144 + j * 8 + 7);
+      mbar_wait_fast(&s_empty[sb], ((j / 3) & 1) ^ 1);
       tc_fence_after();
+      if (lane == 0) TRACE(6144 + j * 8 + 0);
       const uint64_t bk = d_k + (uint64_t)((st * L::TILE) >> 4);
       if (elect_one()) {
 #pragma unroll
@@ -270,12 +274,14 @@ __global__ void __launch_bounds__(384, 1)
       const int sb = j % 3;
       mbar_wait(&s_full[sb], (j / 3) & 1);
       tc_fence_after();
+      if (warp == 4 && lane == 0) TRACE(6144 + j * 8 + 2);
       float s[HC];
 #pragma unroll
       for (int c = 0; c < HC / 32; ++c)
         tmem_ld32_nowait(t_s + sb * BKV + half * HC + c * 32 + lane_off,
                          reinterpret_cast<uint32_t*>(s) + c * 32);
       tmem_wait_ld();
+      if (warp == 4 && lane == 0) TRACE(6144 + j * 8 + 3);
       const int k0 = j * BKV + half * HC;
       const bool mask = (k0 + HC > p.S) || (p.causal && k0 + HC - 1 > q0);
       float mx = -INFINITY;
@@ -320,6 +326,7 @@ __global__ void __launch_bounds__(384, 1)
         pk[i / 2] = pack2(p0, p1);
       }
       l = l * alpha + rs;
+      if (warp == 4 && lane == 0) TRACE(6144 + j * 8 + 4);
       // lazy rescale: O must hold PV(j-1) first.  When S(j) completed, PV(j-2) had too and
       // PV(j) needs this P, so o_done has completed j-1 or j phases: the parity wait is exact
       if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
@@ -339,6 +346,7 @@ __global__ void __launch_bounds__(384, 1)
       tmem_st32(t_s + sb * BKV + half * HC + lane_off, pk);  // includes wait::st
       tc_fence_before();
       mbar_arrive(&p_full[sb]);
+      if (warp == 4 && lane == 0) TRACE(6144 + j * 8 + 5);
     }
     // full row sum = both halves
     xch[512 + half * 128 + r] = l;
@@ -596,12 +604,12 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       const uint64_t d_o = sdesc(smem_u32(sm + L::O0), 16, 1024);
       const uint64_t m_q = sdesc(smem_u32(sm + L::Q0), 8192, 1024);   // MN-major views
       const uint64_t m_o = sdesc(smem_u32(sm + L::O0), 8192, 1024);
-      mbar_wait(kv_full, 0);
+      mbar_wait_fast(kv_full, 0);
       // dV += P^T dO, dK += dS^T Q with A read from TMEM (P^T / dS^T packed by the math
       // warps into the first 8 of every 16 columns of the S^T / dP^T buffer)
       auto grads = [&](int it) {
         const int st = it % NST, sb = it & 1;
-        mbar_wait(&p_full[sb], (it >> 1) & 1);
+        mbar_wait_fast(&p_full[sb], (it >> 1) & 1);
         tc_fence_after();
         if (lane == 0) TRACE(4096 + it * 8 + 3);
         const uint64_t so = (uint64_t)((st * L::QT) >> 4);
@@ -623,9 +631,9 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       for (int it = 0; it < n_it; ++it) {
         const int st = it % NST, sb = it & 1;
         if (lane == 0) TRACE(4096 + it * 8 + 0);
-        mbar_wait(&q_full[st], (it / NST) & 1);
+        mbar_wait_fast(&q_full[st], (it / NST) & 1);
         if (lane == 0) TRACE(4096 + it * 8 + 2);
-        mbar_wait(&st_empty[sb], ((it >> 1) & 1) ^ 1);
+        mbar_wait_fast(&st_empty[sb], ((it >> 1) & 1) ^ 1);
         tc_fence_after();
         if (lane == 0) TRACE(4096 + it * 8 + 1);
         const uint64_t so = (uint64_t)((st * L::QT) >> 4);
@@ -832,12 +840,12 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     const uint64_t d_k = sdesc(smem_u32(sm + L::K0), 16, 1024);
     const uint64_t d_v = sdesc(smem_u32(sm + L::V0), 16, 1024);
     const uint64_t m_k = sdesc(smem_u32(sm + L::K0), 16384, 1024);  // K as MN-major B
-    mbar_wait(qo_full, 0);
+    mbar_wait_fast(qo_full, 0);
     // dQ += dS K: A = dS from TMEM (keys 16k.. packed at col 32*(k/2) + 8*(k%2) of the S
     // buffer), B = the K tile as an MN-major operand (same smem bytes as the S GEMM's B)
     auto grads = [&](int it) {
       const int st = it % L::NK, sb = it & 1;
-      mbar_wait(&ds_full[sb], (it >> 1) & 1);
+      mbar_wait_fast(&ds_full[sb], (it >> 1) & 1);
       tc_fence_after();
       if (lane == 0) TRACE(it * 8 + 3);
       const uint64_t so = (uint64_t)((st * L::KT) >> 4);
@@ -855,8 +863,8 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     for (int it = 0; it < n_it; ++it) {
       const int sk = it % L::NK, sv = it % L::NV, sb = it & 1;
       if (lane == 0) TRACE(it * 8 + 0);
-      mbar_wait(&k_full[sk], (it / L::NK) & 1);
-      mbar_wait(&s_free[sb], ((it >> 1) & 1) ^ 1);
+      mbar_wait_fast(&k_full[sk], (it / L::NK) & 1);
+      mbar_wait_fast(&s_free[sb], ((it >> 1) & 1) ^ 1);
       tc_fence_after();
       if (lane == 0) TRACE(it * 8 + 1);
       const uint64_t ok = (uint64_t)((sk * L::KT) >> 4), ov = (uint64_t)((sv * L::KT) >> 4);
@@ -868,8 +876,8 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         }
       }
       __syncwarp();
-      mbar_wait(&v_full[sv], (it / L::NV) & 1);
-      if (it > 0) mbar_wait(dp_free, (it - 1) & 1);
+      mbar_wait_fast(&v_full[sv], (it / L::NV) & 1);
+      if (it > 0) mbar_wait_fast(dp_free, (it - 1) & 1);
       tc_fence_after();
       if (lane == 0) TRACE(it * 8 + 2);
       if (elect_one()) {

@@ -117,6 +117,97 @@ __global__ void __launch_bounds__(WARPS * 32) bwd_dx_kernel(
   }
 }
 
+// Single-pass variant for rows of up to 128 * NV vectors: one 128-thread CTA per row keeps
+// its x / dy vectors in registers between the reduction and the output pass, so x and dy
+// are read from HBM once (the warp-per-row kernel above re-reads them).
+template <typename T, bool LAYER, int NV>
+__global__ void __launch_bounds__(128) bwd_dx_row(
+    const T* __restrict__ x, const T* __restrict__ gamma, const float* __restrict__ mean,
+    const float* __restrict__ rstd, const T* __restrict__ dy, const T* __restrict__ dres,
+    T* __restrict__ dx, int cols) {
+  constexpr int V = 16 / sizeof(T);
+  __shared__ float red[2][4];
+  const int64_t row = blockIdx.x;
+  const T* xr = x + row * cols;
+  const T* dyr = dy + row * cols;
+  const float mu = LAYER ? mean[row] : 0.f, rs = rstd[row];
+  uint4 xv[NV], dv[NV];
+  float a1 = 0.f, a2 = 0.f;
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    const int c = (j * 128 + threadIdx.x) * V;
+    if (c < cols) {
+      xv[j] = *reinterpret_cast<const uint4*>(xr + c);
+      dv[j] = *reinterpret_cast<const uint4*>(dyr + c);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    const int c = (j * 128 + threadIdx.x) * V;
+    if (c < cols) {
+      float v[V], d[V], g[V];
+      load16(reinterpret_cast<const T*>(&xv[j]), v);
+      load16(reinterpret_cast<const T*>(&dv[j]), d);
+      load16(gamma + c, g);
+#pragma unroll
+      for (int i = 0; i < V; ++i) {
+        const float gd = g[i] * d[i];
+        a1 += gd * (v[i] - mu) * rs;
+        a2 += gd;
+      }
+    }
+  }
+  a1 = warp_sum(a1);
+  a2 = warp_sum(a2);
+  if ((threadIdx.x & 31) == 0) {
+    red[0][threadIdx.x >> 5] = a1;
+    red[1][threadIdx.x >> 5] = a2;
+  }
+  __syncthreads();
+  a1 = (red[0][0] + red[0][1] + red[0][2] + red[0][3]) / cols;
+  a2 = (red[1][0] + red[1][1] + red[1][2] + red[1][3]) / cols;
+  T* dxr = dx + row * cols;
+  const T* drr = dres ? dres + row * cols : nullptr;
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    const int c = (j * 128 + threadIdx.x) * V;
+    if (c < cols) {
+      float v[V], d[V], g[V], r[V];
+      load16(reinterpret_cast<const T*>(&xv[j]), v);
+      load16(reinterpret_cast<const T*>(&dv[j]), d);
+      load16(gamma + c, g);
+      if (drr) load16(drr + c, r);
+#pragma unroll
+      for (int i = 0; i < V; ++i) {
+        const float xh = (v[i] - mu) * rs;
+        float o = rs * (g[i] * d[i] - xh * a1 - (LAYER ? a2 : 0.f));
+        if (drr) o += r[i];
+        v[i] = o;
+      }
+      store16(dxr + c, v);
+    }
+  }
+}
+
+template <typename T, bool LAYER>
+bool launch_dx_row(const void* x, const void* gamma, const float* mean, const float* rstd,
+                   const void* dy, const void* dres, void* dx, int64_t rows, int64_t cols,
+                   void* stream) {
+  const int64_t nv = (cols / (16 / (int64_t)sizeof(T)) + 127) / 128;
+  auto go = [&](auto kernel) {
+    kernel<<<(unsigned)rows, 128, 0, as_stream(stream)>>>(
+        (const T*)x, (const T*)gamma, mean, rstd, (const T*)dy, (const T*)dres, (T*)dx,
+        (int)cols);
+  };
+  if (rows > 2147483647LL) return false;
+  if (nv <= 1) go(bwd_dx_row<T, LAYER, 1>);
+  else if (nv <= 2) go(bwd_dx_row<T, LAYER, 2>);
+  else if (nv <= 4) go(bwd_dx_row<T, LAYER, 4>);
+  else if (nv <= 8) go(bwd_dx_row<T, LAYER, 8>);
+  else return false;
+  return true;
+}
+
 // dgamma[c] += sum_r dy[r,c] * xhat[r,c] (and dbeta[c] += sum_r dy[r,c]): column strips of
 // 2*blockDim columns (bf16x2 / float2 loads, coalesced), row chunks across blockIdx.y.
 template <typename T, bool LAYER>
@@ -195,9 +286,10 @@ static int32_t norm_bwd(const void* x, const void* gamma, const float* mean, con
                                                                 (int64_t)sm_count() * 8 / strips + 1));
   const int64_t rpc = (rows + chunks - 1) / chunks;
   GALV_DISPATCH(dtype, T, {
-    norm::bwd_dx_kernel<T, LAYER><<<grid, norm::WARPS * 32, 0, as_stream(stream)>>>(
-        (const T*)x, (const T*)gamma, mean, rstd, (const T*)dy, (const T*)dres, (T*)dx, rows,
-        (int)cols);
+    if (!norm::launch_dx_row<T, LAYER>(x, gamma, mean, rstd, dy, dres, dx, rows, cols, stream))
+      norm::bwd_dx_kernel<T, LAYER><<<grid, norm::WARPS * 32, 0, as_stream(stream)>>>(
+          (const T*)x, (const T*)gamma, mean, rstd, (const T*)dy, (const T*)dres, (T*)dx, rows,
+          (int)cols);
     norm::bwd_dgamma_kernel<T, LAYER><<<dim3((unsigned)strips, (unsigned)chunks), 128, 0,
                                         as_stream(stream)>>>(
         (const T*)x, mean, rstd, (const T*)dy, dgamma, dbeta, rows, (int)cols, rpc);

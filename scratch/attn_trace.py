@@ -44,3 +44,18 @@ print("loop->qfull", (t[:,2]-t[:,0])[4:-4].mean(), "qfull->S", (t[:,1]-t[:,2])[4
 print("softmax: wait->ld", (t[:,5]-t[:,4])[4:-4].mean(), " ld->comp", (t[:,6]-t[:,5])[4:-4].mean(), " comp->arr", (t[:,7]-t[:,6])[4:-4].mean())
 print("grad issue - p_arr", (t[:,3]-t[:,7])[4:-4].mean())
 print("st_full seen - S issue", (t[:,4]-t[:,1])[4:-4].mean())
+print("==== fwd CTA (0,0) (heaviest q block): 32 KV blocks")
+K.attn_fwd(q,k,v,o,lse,scale=1/math.sqrt(D),causal=True)
+torch.cuda.synchronize()
+assert lib.galv_attn_trace_read(buf.ctypes.data) == 0
+t = buf[6144:6144 + 32*8].reshape(32, 8).astype(np.int64)
+t = t - t[0, 6]
+names = ["mma:S", "mma:PV", "sm:s_full", "sm:ld", "sm:exp", "sm:p_arr", "mma:top", "mma:kful"]
+print("j  " + " ".join(f"{n:>10}" for n in names))
+for i in range(32):
+    print(f"{i:2d} " + " ".join(f"{x:10d}" for x in t[i]))
+m = slice(3, 29)
+print("block interval (S issue)", np.diff(t[:, 0])[m].mean())
+print("s_full seen - S issue", (t[:,2]-t[:,0])[m].mean(), " ld", (t[:,3]-t[:,2])[m].mean(), " exp", (t[:,4]-t[:,3])[m].mean(), " exp->arr", (t[:,5]-t[:,4])[m].mean())
+print("PV issue - p_arr", (t[:,1]-t[:,5])[m].mean())
+print("top->kfull", (t[:,7]-t[:,6])[m].mean(), " kfull->S(s_empty)", (t[:,0]-t[:,7])[m].mean())
