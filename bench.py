@@ -143,12 +143,23 @@ def cluster_profile(n: int, path: str):
     return c, "builtin placeholder (device_flops 1.2e15, busbw 7e11, reserve 0.1)"
 
 
+def model_profile(cfg):
+    """Planner ModelProfile: the profiler's activation-calibrated one when committed
+    (profiles/b200_model_<name>.json, `profiler --model-out`), else the analytic one."""
+    from paper_2504_21411_b200.planner.profiles import load_model_profile
+    from paper_2504_21411_b200.runtime.config import profile_for
+    path = os.path.join(ROOT, "profiles", f"b200_model_{cfg.name}.json")
+    if os.path.exists(path):
+        return load_model_profile(path)
+    return profile_for(cfg)
+
+
 def plan_for(cfg, n: int, global_batch: int, cluster):
     from paper_2504_21411_b200.planner.profiles import TrainingConfig
     from paper_2504_21411_b200.planner.search import SearchConfig, optimize
     from paper_2504_21411_b200.runtime.config import get_hybrid_parallel_configs, profile_for
     training = TrainingConfig(global_batch=global_batch)
-    plan = optimize(profile_for(cfg), cluster, training, SearchConfig())
+    plan = optimize(model_profile(cfg), cluster, training, SearchConfig())
     return plan, get_hybrid_parallel_configs(plan, cfg), training
 
 
@@ -175,7 +186,7 @@ def explicit_plan(cfg, n, global_batch, cluster, pattern, microbatch):
     strats = parse_pattern(pattern, n)
     layers = [strats[i % len(strats)] for i in range(cfg.n_layers)]
     training = TrainingConfig(global_batch=global_batch)
-    plan = make_plan(profile_for(cfg), cluster, training, 1, microbatch, layers)
+    plan = make_plan(model_profile(cfg), cluster, training, 1, microbatch, layers)
     return plan, get_hybrid_parallel_configs(plan, cfg), training
 
 
@@ -378,6 +389,10 @@ def main():
         "measured_iteration_time_s": ms / 1e3,
         "prediction_error": (ms / 1e3 - plan.predicted_iteration_time) / plan.predicted_iteration_time,
         "cluster_profile": cluster_src,
+        "model_profile": ("profiles/b200_model_%s.json (activation-calibrated)" % cfg.name
+                          if os.path.exists(os.path.join(ROOT, "profiles",
+                                                         "b200_model_%s.json" % cfg.name))
+                          else "analytic (runtime.config.profile_for)"),
         "roofline": {"bound": "tensor", "kernel": "galv tcgen05 GEMM (all shapes of the step)",
                      "achieved": gemm["tflops"], "peak": peak_tf, "unit": "TFLOP/s",
                      "frac": gemm["tflops"] / peak_tf if peak_tf else None,
@@ -403,7 +418,7 @@ def main():
         measured = model.measured_trace()
         from paper_2504_21411_b200.planner.pipesim import simulate, trace_to_jsonl, SimResult
         from paper_2504_21411_b200.runtime.config import profile_for
-        sim = simulate(plan, profile_for(cfg), cluster, training)
+        sim = simulate(plan, model_profile(cfg), cluster, training)
         def per_kind(events):
             acc = {}
             for e in events:

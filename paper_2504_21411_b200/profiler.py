@@ -93,6 +93,63 @@ def measure_layer_flops(cfg, microbatch: int, *, iters: int = 3, sustain_s: floa
             "device_flops": 3.0 * fwd_flops / t}
 
 
+def measure_activation_bytes(cfg, microbatch: int) -> dict:
+    """Bytes per token one decoder layer keeps alive between its forward and backward
+    (tp=1): the allocator delta across ``layer.forward`` with saved state, and with
+    recompute (only the boundary tensor survives).  Feeds the cost model's activation
+    coefficients (costmodel.py:162-175) instead of the analytic count."""
+    from .runtime.config import HybridConfig
+    from .runtime.init import layer_param_shapes
+    from .runtime.layers import DecoderLayer
+    from .runtime.topology import Topology
+    one = cfg.with_(n_layers=1)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    T = microbatch * cfg.seq_len
+    out = {}
+    for rc in (False, True):
+        s = ParallelStrategy(1, 1, 0, False, rc)
+        hc = HybridConfig(pp=1, microbatch=microbatch, n_microbatches=1,
+                          stage_ranges=((0, 1),), layer_strategies=(s,))
+        layer = DecoderLayer(one, 0, s, Topology(hc, rank=0, world=1), dtype=torch.bfloat16,
+                             grad_dtype=torch.bfloat16, device=dev)
+        layer.store.load({n: 0.02 * torch.ones(shp, device=dev)
+                          for n, shp in layer_param_shapes(one).items()})
+        x = torch.randn(T, cfg.hidden, device=dev, dtype=torch.bfloat16)
+        y, ctx = layer.forward(x, microbatch)  # warm the allocator / tables
+        layer.backward(torch.zeros_like(y), ctx)
+        del y, ctx
+        torch.cuda.synchronize()
+        m0 = torch.cuda.memory_allocated()
+        y, ctx = layer.forward(x, microbatch)
+        torch.cuda.synchronize()
+        out["recompute" if rc else "saved"] = (torch.cuda.memory_allocated() - m0) / T
+        del y, ctx, layer
+        torch.cuda.synchronize()
+    return {"bytes_per_token_saved": out["saved"],
+            "bytes_per_token_recompute": out["recompute"], "microbatch": microbatch}
+
+
+def calibrated_model_profile(cfg, act: dict) -> P.ModelProfile:
+    """The analytic profile with its activation coefficients scaled to the measured bytes:
+    shardable/replicated keep their analytic split; boundary = the recompute residue."""
+    from .runtime.config import profile_for
+    base = profile_for(cfg)
+    lp = base.layers[0]
+    analytic = lp.act_shardable_bytes_per_token + lp.act_replicated_bytes_per_token
+    f = act["bytes_per_token_saved"] / analytic
+    layer = P.LayerProfile(
+        param_count=lp.param_count, flops_per_token=lp.flops_per_token,
+        flops_per_token_sq=lp.flops_per_token_sq,
+        act_shardable_bytes_per_token=lp.act_shardable_bytes_per_token * f,
+        act_replicated_bytes_per_token=lp.act_replicated_bytes_per_token * f,
+        boundary_bytes_per_token=max(act["bytes_per_token_recompute"],
+                                     lp.boundary_bytes_per_token))
+    prof = P.ModelProfile(n_layers=base.n_layers, hidden_size=base.hidden_size,
+                          seq_len=base.seq_len, layers=(layer,) * base.n_layers)
+    prof.validate()
+    return prof
+
+
 def measure_collectives(sizes=(2 ** 20, 2 ** 24, 2 ** 28)) -> dict:
     """busbw (bytes/s) and alpha per contiguous group size; rank 0 returns the table."""
     world = dist.get_world_size()
@@ -144,6 +201,10 @@ def main(argv=None) -> int:
     ap.add_argument("--devices", type=int, default=8, help="n_devices written to the profile")
     ap.add_argument("--reserve", type=float, default=0.1)
     ap.add_argument("--table-from", default=None, help="reuse the bandwidth table of a profile")
+    ap.add_argument("--model-out", default=None,
+                    help="also write the activation-calibrated ModelProfile of --model here")
+    ap.add_argument("--skip-flops", action="store_true",
+                    help="with --table-from + --model-out: only measure activations")
     args = ap.parse_args(argv)
     from .runtime.config import MODEL_PRESETS
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -158,6 +219,15 @@ def main(argv=None) -> int:
         table = {e.group_size: {"bus_bandwidth": e.bus_bandwidth, "latency": e.latency}
                  for e in c.bandwidth_table if e.span == "intra_node"}
     rank = dist.get_rank() if world > 1 else 0
+    if rank == 0 and args.model_out:
+        cfg = MODEL_PRESETS[args.model]
+        act = measure_activation_bytes(cfg, args.microbatch)
+        P.save_profiles(args.model_out, model=calibrated_model_profile(cfg, act))
+        with open(os.path.splitext(args.model_out)[0] + ".meta.json", "w") as fh:
+            json.dump({"model": args.model, "activation": act}, fh, indent=1)
+        print(json.dumps({"activation": act}))
+        if args.skip_flops:
+            return 0
     if rank == 0:
         lay = measure_layer_flops(MODEL_PRESETS[args.model], args.microbatch)
         if not table:  # single GPU: NVLink table from the pool's published measurements
