@@ -9,6 +9,7 @@
 // Operands may be K-major or MN-major independently (idesc bits 15/16), which covers
 // forward (X W^T), dgrad (dY W) and wgrad (dY^T X) without transposes.
 #include <cuda.h>
+#include <cstdio>
 #include <cstdlib>
 #include <mutex>
 
@@ -25,7 +26,7 @@ constexpr int B_STAGE = BN * BK * 2;          // 32 KB
 constexpr int STAGE_BYTES = A_STAGE + B_STAGE;
 constexpr int TMEM_COLS = 512;
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
-constexpr int GROUP_M = 16;
+constexpr int GROUP_M = 8;  // raster group (256-row pair tiles); sustained sweep: 8 >= 16 > 4 > 32
 
 struct Params {
   int M, N, K;
@@ -42,16 +43,28 @@ struct Params {
   // row r goes to rank j = r / rows_per_rank, slot `my_slot`, of that rank's receive buffer
   void* const* peer_c;
   int rows_per_rank, my_slot;
+  // tile raster: groups of `group` tiles along M (gdim 0) or N (gdim 1); L2 cache hints
+  int group, gdim, hint;
 };
 
 __device__ __forceinline__ void tile_coords(const Params& p, int t, int& mt, int& nt) {
-  const int per_group = GROUP_M * p.tiles_n;
-  const int group = t / per_group;
-  const int first_m = group * GROUP_M;
-  const int gm = min(p.tiles_m - first_m, GROUP_M);
-  const int r = t - group * per_group;
-  mt = first_m + r % gm;
-  nt = r / gm;
+  if (p.gdim == 0) {
+    const int per_group = p.group * p.tiles_n;
+    const int group = t / per_group;
+    const int first_m = group * p.group;
+    const int gm = min(p.tiles_m - first_m, p.group);
+    const int r = t - group * per_group;
+    mt = first_m + r % gm;
+    nt = r / gm;
+  } else {
+    const int per_group = p.group * p.tiles_m;
+    const int group = t / per_group;
+    const int first_n = group * p.group;
+    const int gn = min(p.tiles_n - first_n, p.group);
+    const int r = t - group * per_group;
+    nt = first_n + r % gn;
+    mt = r / gn;
+  }
 }
 
 // Epilogue of one 128-lane accumulator slice: this thread owns output row `row` and
@@ -328,6 +341,7 @@ __device__ __forceinline__ void epilogue_staged(const Params& p, uint32_t taddr,
                                                 int col_base, uint8_t* stage) {
   constexpr int PITCH = Cfg2<PEER>::STAGE_PITCH;
   const int lane = threadIdx.x & 31;
+  const uint64_t st_pol = l2_evict_first();
 #pragma unroll 1
   for (int q4 = 0; q4 < 4; ++q4) {
 #pragma unroll
@@ -375,7 +389,15 @@ __device__ __forceinline__ void epilogue_staged(const Params& p, uint32_t taddr,
 #pragma unroll
             for (int e = 0; e < 8; ++e) o[e] += old[e];
           }
-          store16(base + off, o);
+          if (p.hint & 2) {
+            uint4 raw;
+            __nv_bfloat16* e8 = reinterpret_cast<__nv_bfloat16*>(&raw);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) e8[e] = __float2bfloat16_rn(o[e]);
+            st_global_hint(base + off, raw, st_pol);
+          } else {
+            store16(base + off, o);
+          }
         }
       }
     } else {
@@ -449,40 +471,66 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
-    if (lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int t = pair; t < p.num_tiles; t += npairs) {
-        int mt, nt;
-        tile_coords2(p, t, mt, nt);
-        const int m0 = mt * 256 + (int)cr * 128, n0 = nt * 256 + (int)cr * 128;
-        for (int kb = 0; kb < p.k_blocks; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
+    // TMA producer: the whole warp runs the loop (warp-uniform state), one elected lane
+    // issues each stage's loads
+    int stage = 0;
+    uint32_t phase = 0;
+    const uint64_t pol = l2_evict_last();
+    for (int t = pair; t < p.num_tiles; t += npairs) {
+      int mt, nt;
+      tile_coords2(p, t, mt, nt);
+      const int m0 = mt * 256 + (int)cr * 128, n0 = nt * 256 + (int)cr * 128;
+      for (int kb = 0; kb < p.k_blocks; ++kb) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        if (elect_one()) {
           if (cr == 0) mbar_expect_tx(&full[stage], 4 * HALF_STAGE);
           uint8_t* a_dst = sA + stage * HALF_STAGE;
           uint8_t* b_dst = sB + stage * HALF_STAGE;
-          if (!p.a_mn) {
-            tma_load_2d_2sm(&tmA, &full[stage], a_dst, kb * BK, m0);
+          if (p.hint & 1) {
+            if (!p.a_mn) {
+              tma_load_2d_2sm_hint(&tmA, &full[stage], a_dst, kb * BK, m0, pol);
+            } else {
+              tma_load_2d_2sm_hint(&tmA, &full[stage], a_dst, m0, kb * BK, pol);
+              tma_load_2d_2sm_hint(&tmA, &full[stage], a_dst + 8192, m0 + 64, kb * BK, pol);
+            }
+            if (!p.b_mn) {
+              tma_load_2d_2sm_hint(&tmB, &full[stage], b_dst, kb * BK, n0, pol);
+            } else {
+              tma_load_2d_2sm_hint(&tmB, &full[stage], b_dst, n0, kb * BK, pol);
+              tma_load_2d_2sm_hint(&tmB, &full[stage], b_dst + 8192, n0 + 64, kb * BK, pol);
+            }
           } else {
-            tma_load_2d_2sm(&tmA, &full[stage], a_dst, m0, kb * BK);
-            tma_load_2d_2sm(&tmA, &full[stage], a_dst + 8192, m0 + 64, kb * BK);
+            if (!p.a_mn) {
+              tma_load_2d_2sm(&tmA, &full[stage], a_dst, kb * BK, m0);
+            } else {
+              tma_load_2d_2sm(&tmA, &full[stage], a_dst, m0, kb * BK);
+              tma_load_2d_2sm(&tmA, &full[stage], a_dst + 8192, m0 + 64, kb * BK);
+            }
+            if (!p.b_mn) {
+              tma_load_2d_2sm(&tmB, &full[stage], b_dst, kb * BK, n0);
+            } else {
+              tma_load_2d_2sm(&tmB, &full[stage], b_dst, n0, kb * BK);
+              tma_load_2d_2sm(&tmB, &full[stage], b_dst + 8192, n0 + 64, kb * BK);
+            }
           }
-          if (!p.b_mn) {
-            tma_load_2d_2sm(&tmB, &full[stage], b_dst, kb * BK, n0);
-          } else {
-            tma_load_2d_2sm(&tmB, &full[stage], b_dst, n0, kb * BK);
-            tma_load_2d_2sm(&tmB, &full[stage], b_dst + 8192, n0 + 64, kb * BK);
-          }
-          if (++stage == STAGES2) {
-            stage = 0;
-            phase ^= 1;
-          }
+        }
+        __syncwarp();
+        if (++stage == STAGES2) {
+          stage = 0;
+          phase ^= 1;
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && cr == 0) {
+    // MMA issuer (leader CTA): descriptors precomputed once and advanced by constant
+    // offsets; one elected lane issues a stage's four UMMAs back to back
+    if (cr == 0) {
       const uint32_t idesc = make_idesc(256, 256, p.a_mn, p.b_mn);
+      const uint64_t a0 = p.a_mn ? sdesc(smem_u32(sA), 8192, 1024) : sdesc(smem_u32(sA), 16, 1024);
+      const uint64_t b0 = p.b_mn ? sdesc(smem_u32(sB), 8192, 1024) : sdesc(smem_u32(sB), 16, 1024);
+      const uint64_t a_k = p.a_mn ? (2048 >> 4) : (32 >> 4);
+      const uint64_t b_k = p.b_mn ? (2048 >> 4) : (32 >> 4);
+      constexpr uint64_t STG = HALF_STAGE >> 4;
       int stage = 0, acc = 0;
       uint32_t phase = 0, acc_phase = 0;
       for (int t = pair; t < p.num_tiles; t += npairs) {
@@ -492,23 +540,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
         for (int kb = 0; kb < p.k_blocks; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          const uint32_t a_base = smem_u32(sA + stage * HALF_STAGE);
-          const uint32_t b_base = smem_u32(sB + stage * HALF_STAGE);
+          const uint64_t ad = a0 + (uint64_t)stage * STG, bd = b0 + (uint64_t)stage * STG;
+          if (elect_one()) {
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
-            const uint64_t ad = p.a_mn ? sdesc(a_base + k * 2048, 8192, 1024)
-                                       : sdesc(a_base + k * 32, 16, 1024);
-            const uint64_t bd = p.b_mn ? sdesc(b_base + k * 2048, 8192, 1024)
-                                       : sdesc(b_base + k * 32, 16, 1024);
-            umma_bf16_2sm(d, ad, bd, idesc, (kb | k) != 0);
+            for (int k = 0; k < BK / 16; ++k)
+              umma_bf16_2sm(d, ad + k * a_k, bd + k * b_k, idesc, (kb | k) != 0);
+            umma_commit_2sm(&empty[stage], 0x3);
           }
-          umma_commit_2sm(&empty[stage], 0x3);
+          __syncwarp();
           if (++stage == STAGES2) {
             stage = 0;
             phase ^= 1;
           }
         }
-        umma_commit_2sm(&tfull[acc], 0x3);
+        if (elect_one()) umma_commit_2sm(&tfull[acc], 0x3);
+        __syncwarp();
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
@@ -522,7 +568,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     for (int t = pair; t < p.num_tiles; t += npairs) {
       int mt, nt;
       tile_coords2(p, t, mt, nt);
-      mbar_wait(&tfull[acc], acc_phase);
+      if (p.hint & 8) mbar_wait(&tfull[acc], acc_phase);
+      else mbar_wait_sleep(&tfull[acc], acc_phase, 512);
       tc_fence_after();
       if constexpr (PEER)
         epilogue_peer(p, tmem + acc * BN + ((uint32_t)(q * 32) << 16),
@@ -625,6 +672,17 @@ int32_t gemm_bf16_sm100(const void* A, const void* B, void* C, const void* bias,
   p.peer_c = peer_c;
   p.rows_per_rank = (int)rows_per_rank;
   p.my_slot = my_slot;
+  {
+    static int v_group = -1, v_gdim = 0, v_hint = 0;
+    if (v_group < 0) {  // GALV_GEMM_RASTER="group,gdim,hint" (tuning sweeps only)
+      v_group = GROUP_M;
+      if (const char* e = getenv("GALV_GEMM_RASTER")) sscanf(e, "%d,%d,%d", &v_group, &v_gdim, &v_hint);
+      if (v_group < 1) v_group = 1;
+    }
+    p.group = v_group;
+    p.gdim = v_gdim;
+    p.hint = v_hint;
+  }
   static bool attr_set = false;
   if (!attr_set) {
     GALV_CUDA_RET(cudaFuncSetAttribute(gemm_bf16_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
