@@ -267,7 +267,8 @@ __global__ void __launch_bounds__(384, 1)
     const int r = q * 32 + lane;
     const int qi = q0 + r;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-    float* xch = reinterpret_cast<float*>(bar + 16);  // [2][128] partial maxima / sums
+    // [2][256] partial maxima + [256] partial sums, after the 20 barrier words (160 bytes)
+    float* xch = reinterpret_cast<float*>(bar + 20);
     float m_used = -INFINITY, l = 0.f;
     constexpr int HC = BKV / 2;  // columns per half
     for (int j = 0; j < n_kv; ++j) {

@@ -15,7 +15,7 @@ from pathlib import Path
 
 import torch
 
-LIB_PATH = Path(__file__).resolve().parent / "libgalv_b200.so"
+LIB_PATH = Path(os.environ["GALV_LIB"]) if os.environ.get("GALV_LIB") else Path(__file__).resolve().parent / "libgalv_b200.so"
 F32, BF16 = 0, 1
 _DT = {torch.float32: F32, torch.bfloat16: BF16}
 

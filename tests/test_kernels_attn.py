@@ -53,3 +53,33 @@ def test_attention(dt, D, S, causal):
     K.attn_bwd(q, k, v, o, do.to(dt).contiguous(), lse, dq, dk, dv, scale=scale, causal=causal)
     for got, want in ((dq, qr.grad), (dk, kr.grad), (dv, vr.grad)):
         assert rel(got, want) < (1e-5 if dt == torch.float32 else 2e-2)
+
+
+def test_attention_fwd_repeatable_rescale_heavy():
+    """Regression: the softmax row-max exchange buffer once overlapped the O-done / V-empty
+    mbarriers, which corrupted barrier state and intermittently faulted the forward.
+    Sharply peaked, row-varying scores force lazy O rescales on most key blocks; the output
+    must match the fp32 reference on every row (incl. rows 0-7 of each tile) and be
+    bitwise repeatable across launches."""
+    from paper_2504_21411_b200 import kernels as K
+    torch.manual_seed(1)
+    B, S, H, D = 1, 1024, 4, 128
+    qkv = torch.randn(B, S, 3, H, D, device="cuda")
+    qkv[:, :, :2] *= torch.linspace(0.5, 6.0, S, device="cuda").view(1, S, 1, 1, 1)
+    qkv = qkv.bfloat16()
+    q, k, v = qkv[:, :, 0], qkv[:, :, 1], qkv[:, :, 2]
+    lse = torch.empty(B, H, S, device="cuda")
+    scale = 1 / math.sqrt(D)
+    o_ref, lse_ref = ref_attn(q.float(), k.float(), v.float(), True)
+    first = None
+    for _ in range(40):
+        o = torch.empty(B, S, H, D, device="cuda", dtype=torch.bfloat16)
+        K.attn_fwd(q, k, v, o, lse, scale=scale, causal=True)
+        if first is None:
+            first = o.clone()
+            err_rows = ((o.float() - o_ref).norm(dim=-1) / (o_ref.norm(dim=-1) + 1e-6))
+            assert err_rows.max().item() < 5e-2
+            assert rel(lse, lse_ref) < 1e-3
+        else:
+            assert torch.equal(o, first)
+    torch.cuda.synchronize()
