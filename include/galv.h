@@ -115,6 +115,26 @@ int32_t galv_swiglu_fwd(const void* gu, void* h, int64_t T, int64_t F, int32_t d
                         void* stream);
 int32_t galv_swiglu_bwd(const void* gu, const void* dh, void* dgu, int64_t T, int64_t F,
                         int32_t dtype, void* stream);
+/* bf16 SwiGLU backward with dh rows ld_dh elements apart (dh may alias dgu's up half). */
+int32_t galv_swiglu_bwd_strided(const void* gu, const void* dh, int64_t ld_dh, void* dgu,
+                                int64_t T, int64_t F, void* stream);
+/*
+ * Llama MLP GEMMs with the SwiGLU fused into the tcgen05 epilogue (bf16):
+ *   fwd: gu[M,2F] = X[M,K] W_gu[2F,K]^T (rows gate then up), h[M,F] = silu(gate) * up;
+ *        each CTA pair accumulates 128 gate + the matching 128 up columns, so the
+ *        activation is computed from TMEM and h is written by the same epilogue.
+ *   bwd: dgu[M,2F] = swiglu_bwd(gu, dh) with dh = dY[M,K] W_down[K,F] (nn.Linear layout
+ *        of the down projection) kept in TMEM -- dh never reaches HBM.
+ * Same values as galv_gemm + galv_swiglu_fwd/bwd (gate/up/dh rounded to bf16 first);
+ * shapes the 2-CTA path cannot take run exactly that unfused sequence.
+ * Realizes fwd_compute/bwd_compute of the MLP (costmodel.py:104-106).
+ */
+int32_t galv_gemm_swiglu_fwd(const void* X, const void* Wgu, void* gu, void* h, int64_t M,
+                             int64_t F, int64_t K, int64_t ldx, int64_t ldw, int64_t ld_gu,
+                             int64_t ld_h, void* stream);
+int32_t galv_gemm_swiglu_bwd(const void* dY, const void* Wdown, const void* gu, void* dgu,
+                             int64_t M, int64_t F, int64_t K, int64_t ldy, int64_t ldw,
+                             int64_t ld_gu, int64_t ld_dgu, void* stream);
 /* GeLU(tanh) with bias: y = gelu(x + b); backward dx = dy * gelu'(x + b). */
 int32_t galv_bias_gelu_fwd(const void* x, const void* bias, void* y, int64_t T, int64_t F,
                            int32_t dtype, void* stream);

@@ -26,8 +26,8 @@ __global__ void swiglu_fwd(const T* __restrict__ gu, T* __restrict__ h, int64_t 
 }
 
 template <typename T>
-__global__ void swiglu_bwd(const T* __restrict__ gu, const T* __restrict__ dh,
-                           T* __restrict__ dgu, int64_t T_, int64_t F) {
+__global__ void swiglu_bwd(const T* gu, const T* dh, T* dgu, int64_t T_, int64_t F,
+                           int64_t ld_dh) {  // dh may alias dgu's up half (read before write)
   constexpr int V = 16 / sizeof(T);
   const int64_t nvec = T_ * F / V;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nvec;
@@ -36,7 +36,7 @@ __global__ void swiglu_bwd(const T* __restrict__ gu, const T* __restrict__ dh,
     float g[V], u[V], d[V], dg[V], du[V];
     load16(gu + t * 2 * F + f, g);
     load16(gu + t * 2 * F + F + f, u);
-    load16(dh + e, d);
+    load16(dh + t * ld_dh + f, d);
 #pragma unroll
     for (int k = 0; k < V; ++k) {
       const float s = 1.f / (1.f + expf(-g[k]));
@@ -188,8 +188,21 @@ int32_t galv_swiglu_bwd(const void* gu, const void* dh, void* dgu, int64_t T_, i
   GALV_DISPATCH(dtype, T, {
     const int64_t nvec = T_ * F / (16 / sizeof(T));
     act::swiglu_bwd<T><<<act::grid_for(nvec, 256), 256, 0, as_stream(stream)>>>(
-        (const T*)gu, (const T*)dh, (T*)dgu, T_, F);
+        (const T*)gu, (const T*)dh, (T*)dgu, T_, F, F);
   });
+  GALV_LAUNCH_CHECK();
+  return 0;
+}
+
+// bf16 SwiGLU backward with dh rows `ld_dh` apart (the fused-GEMM fallback stages dh in the
+// up half of dgu)
+int32_t galv_swiglu_bwd_strided(const void* gu, const void* dh, int64_t ld_dh, void* dgu,
+                                int64_t T_, int64_t F, void* stream) {
+  GALV_CHECK_ARG(gu && dh && dgu && T_ > 0 && F % 8 == 0 && ld_dh % 8 == 0, "bad arguments");
+  using T = __nv_bfloat16;
+  const int64_t nvec = T_ * F / 8;
+  act::swiglu_bwd<T><<<act::grid_for(nvec, 256), 256, 0, as_stream(stream)>>>(
+      (const T*)gu, (const T*)dh, (T*)dgu, T_, F, ld_dh);
   GALV_LAUNCH_CHECK();
   return 0;
 }

@@ -26,7 +26,10 @@ int32_t gemm_bf16_sm100(const void* A, const void* B, void* C, const void* bias,
                         int32_t trans_a, int32_t trans_b, float alpha, int32_t accumulate,
                         int32_t c_dtype, int32_t bias_dtype, cudaStream_t stream,
                         void* const* peer_c = nullptr, int64_t rows_per_rank = 0,
-                        int32_t my_slot = 0);
+                        int32_t my_slot = 0, int32_t epi = 0, const void* aux = nullptr,
+                        int64_t aux_ld = 0, int64_t ff = 0);
+bool swiglu_fusable(const void* A, const void* B, const void* C, const void* aux, int64_t M,
+                    int64_t ldc, int64_t aux_ld, int64_t ff, int32_t trans_b, int32_t epi);
 int32_t gemm_f32_simt(const float* A, const float* B, void* C, const float* bias, int64_t batch,
                       int64_t sa, int64_t sb, int64_t sc, int64_t M, int64_t N, int64_t K,
                       int64_t lda, int64_t ldb, int64_t ldc, int32_t ta, int32_t tb, float alpha,
@@ -89,6 +92,42 @@ int32_t galv_gemm_batched(const void* A, const void* B, void* C, int64_t batch, 
     if (rc) return rc;
   }
   return 0;
+}
+
+// gate|up = X W_gu^T (W_gu [2F, K], rows gate then up) and h = silu(gate) * up, with the
+// SwiGLU in the GEMM epilogue (each CTA pair computes 128 gate and the matching 128 up
+// columns); other shapes run the GEMM and then the standalone SwiGLU kernel.
+int32_t galv_gemm_swiglu_fwd(const void* X, const void* Wgu, void* gu, void* h, int64_t M,
+                             int64_t F, int64_t K, int64_t ldx, int64_t ldw, int64_t ld_gu,
+                             int64_t ld_h, void* stream) {
+  GALV_CHECK_ARG(X && Wgu && gu && h && M > 0 && F > 0 && K > 0 && F % 8 == 0, "bad arguments");
+  GALV_CHECK_ARG(ld_gu == 2 * F && ld_h == F, "gate|up and h must be dense [M,2F] / [M,F]");
+  if (galv::swiglu_fusable(X, Wgu, gu, h, M, ld_gu, ld_h, F, 1, 2))
+    return galv::gemm_bf16_sm100(X, Wgu, gu, nullptr, M, 2 * F, K, ldx, ldw, ld_gu, 0, 1, 1.0f, 0,
+                                 GALV_BF16, GALV_F32, galv::as_stream(stream), nullptr, 0, 0, 2, h,
+                                 ld_h, F);
+  int32_t rc = galv::gemm_bf16_sm100(X, Wgu, gu, nullptr, M, 2 * F, K, ldx, ldw, ld_gu, 0, 1, 1.0f,
+                                     0, GALV_BF16, GALV_F32, galv::as_stream(stream));
+  return rc ? rc : galv_swiglu_fwd(gu, h, M, F, GALV_BF16, stream);
+}
+
+// d(gate|up) [M, 2F] from dh = dY W_down (W_down [K=hidden, F], the nn.Linear layout of the
+// down projection) and the saved gate|up, with the SwiGLU backward in the dgrad epilogue
+// (dh never reaches HBM); the unfused fallback stages dh in the up half of dgu.
+int32_t galv_gemm_swiglu_bwd(const void* dY, const void* Wdown, const void* gu, void* dgu,
+                             int64_t M, int64_t F, int64_t K, int64_t ldy, int64_t ldw,
+                             int64_t ld_gu, int64_t ld_dgu, void* stream) {
+  GALV_CHECK_ARG(dY && Wdown && gu && dgu && M > 0 && F > 0 && K > 0 && F % 8 == 0,
+                 "bad arguments");
+  GALV_CHECK_ARG(ld_gu == 2 * F && ld_dgu == 2 * F, "gate|up tensors must be dense [M,2F]");
+  if (galv::swiglu_fusable(dY, Wdown, dgu, gu, M, ld_dgu, ld_gu, F, 0, 1))
+    return galv::gemm_bf16_sm100(dY, Wdown, dgu, nullptr, M, F, K, ldy, ldw, ld_dgu, 0, 0, 1.0f, 0,
+                                 GALV_BF16, GALV_F32, galv::as_stream(stream), nullptr, 0, 0, 1, gu,
+                                 ld_gu, F);
+  char* up_half = static_cast<char*>(dgu) + 2 * F;  // dh staged where du will land
+  int32_t rc = galv::gemm_bf16_sm100(dY, Wdown, up_half, nullptr, M, F, K, ldy, ldw, ld_dgu, 0, 0,
+                                     1.0f, 0, GALV_BF16, GALV_F32, galv::as_stream(stream));
+  return rc ? rc : galv_swiglu_bwd_strided(gu, up_half, ld_dgu, dgu, M, F, stream);
 }
 
 }  // extern "C"

@@ -45,6 +45,12 @@ struct Params {
   int rows_per_rank, my_slot;
   // tile raster: groups of `group` tiles along M (gdim 0) or N (gdim 1); L2 cache hints
   int group, gdim, hint;
+  // fused SwiGLU epilogues (Llama MLP): 1 = backward (C = d(gate|up) from dh = acc, aux =
+  // saved gate|up), 2 = forward (pair tile = 128 gate + 128 up columns; C = gate|up,
+  // aux = h = silu(gate) * up); ff = F (gate/up split), aux_ld its leading dim
+  int epi, ff;
+  const void* aux;
+  long long aux_ld;
 };
 
 __device__ __forceinline__ void tile_coords(const Params& p, int t, int& mt, int& nt) {
@@ -427,6 +433,77 @@ __device__ __forceinline__ void epilogue_staged(const Params& p, uint32_t taddr,
   }
 }
 
+__device__ __forceinline__ float bf16_round(float x) {
+  return __bfloat162float(__float2bfloat16_rn(x));
+}
+
+// epi 1: this thread owns output row `row`, columns [col_base, col_base + 256) of dh
+// (fp32 in TMEM); d(gate|up) computed exactly as act::swiglu_bwd does from the bf16 dh
+__device__ __forceinline__ void epilogue_swiglu_bwd(const Params& p, uint32_t taddr, int row,
+                                                    int col_base) {
+  const bool row_ok = row < p.M;
+  const __nv_bfloat16* gu = reinterpret_cast<const __nv_bfloat16*>(p.aux) + (long long)row * p.aux_ld;
+  __nv_bfloat16* dgu = reinterpret_cast<__nv_bfloat16*>(p.C) + (long long)row * p.ldc;
+#pragma unroll 1
+  for (int cc = 0; cc < BN; cc += 32) {
+    uint32_t r[32];
+    tmem_ld32(taddr + cc, r);
+    const int col0 = col_base + cc;
+    if (!row_ok || col0 >= p.N) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int col = col0 + j * 8;
+      if (col >= p.N) break;
+      float g[8], u[8], dg[8], du[8];
+      load16(gu + col, g);
+      load16(gu + p.ff + col, u);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const float d = bf16_round(__uint_as_float(r[j * 8 + e]) * p.alpha);
+        const float sg = 1.f / (1.f + expf(-g[e]));
+        du[e] = d * g[e] * sg;
+        dg[e] = d * u[e] * sg * (1.f + g[e] * (1.f - sg));
+      }
+      store16(dgu + col, dg);
+      store16(dgu + p.ff + col, du);
+    }
+  }
+}
+
+// epi 2: accumulator columns [0,128) are gate columns [col_base, +128), [128,256) the
+// matching up columns; gate/up rounded to bf16 (what the unfused path stores) and
+// h = silu(g) * u from the rounded values, exactly as act::swiglu_fwd
+__device__ __forceinline__ void epilogue_swiglu_fwd(const Params& p, uint32_t taddr, int row,
+                                                    int col_base) {
+  const bool row_ok = row < p.M;
+  __nv_bfloat16* gu = reinterpret_cast<__nv_bfloat16*>(p.C) + (long long)row * p.ldc;
+  __nv_bfloat16* h = reinterpret_cast<__nv_bfloat16*>(const_cast<void*>(p.aux)) +
+                     (long long)row * p.aux_ld;
+#pragma unroll 1
+  for (int cc = 0; cc < 128; cc += 32) {
+    uint32_t rg[32], ru[32];
+    tmem_ld32(taddr + cc, rg);
+    tmem_ld32(taddr + 128 + cc, ru);
+    const int col0 = col_base + cc;
+    if (!row_ok || col0 >= p.ff) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int col = col0 + j * 8;
+      if (col >= p.ff) break;
+      float g[8], u[8], o[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        g[e] = bf16_round(__uint_as_float(rg[j * 8 + e]) * p.alpha);
+        u[e] = bf16_round(__uint_as_float(ru[j * 8 + e]) * p.alpha);
+        o[e] = g[e] / (1.f + expf(-g[e])) * u[e];
+      }
+      store16(gu + col, g);
+      store16(gu + p.ff + col, u);
+      store16(h + col, o);
+    }
+  }
+}
+
 __device__ __forceinline__ void tile_coords2(const Params& p, int t, int& mt, int& nt) {
   tile_coords(p, t, mt, nt);  // pair tiles are 256 x 256; p.tiles_m counts 256-row tiles
 }
@@ -479,7 +556,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     for (int t = pair; t < p.num_tiles; t += npairs) {
       int mt, nt;
       tile_coords2(p, t, mt, nt);
-      const int m0 = mt * 256 + (int)cr * 128, n0 = nt * 256 + (int)cr * 128;
+      const int m0 = mt * 256 + (int)cr * 128;
+      const int n0 = p.epi == 2 ? (cr == 0 ? nt * 128 : p.ff + nt * 128) : nt * 256 + (int)cr * 128;
       for (int kb = 0; kb < p.k_blocks; ++kb) {
         mbar_wait(&empty[stage], phase ^ 1);
         if (elect_one()) {
@@ -575,6 +653,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
         epilogue_peer(p, tmem + acc * BN + ((uint32_t)(q * 32) << 16),
                       mt * 256 + (int)cr * 128 + q * 32, nt * BN,
                       staging + q * 32 * Cfg2<true>::STAGE_PITCH);
+      else if (p.epi == 1)
+        epilogue_swiglu_bwd(p, tmem + acc * BN + ((uint32_t)(q * 32) << 16),
+                            mt * 256 + (int)cr * 128 + q * 32 + lane, nt * BN);
+      else if (p.epi == 2)
+        epilogue_swiglu_fwd(p, tmem + acc * BN + ((uint32_t)(q * 32) << 16),
+                            mt * 256 + (int)cr * 128 + q * 32 + lane, nt * 128);
       else
         epilogue_staged<false>(p, tmem + acc * BN + ((uint32_t)(q * 32) << 16),
                                mt * 256 + (int)cr * 128 + q * 32, nt * BN,
@@ -633,12 +717,21 @@ static bool make_map(CUtensorMap* map, const void* base, uint64_t inner, uint64_
 
 }  // namespace tc
 
+// the fused SwiGLU epilogues need the 2-CTA path (M > 128, 16-byte aligned rows) and
+// 8-element aligned gate/up/h rows; epi 2 also needs the nn.Linear (K-major) weight
+bool swiglu_fusable(const void* A, const void* B, const void* C, const void* aux, int64_t M,
+                    int64_t ldc, int64_t aux_ld, int64_t ff, int32_t trans_b, int32_t epi) {
+  auto al = [](const void* x) { return (reinterpret_cast<uintptr_t>(x) & 15) == 0; };
+  return M > 128 && al(A) && al(B) && al(C) && al(aux) && ldc % 8 == 0 && aux_ld % 8 == 0 &&
+         ff % 8 == 0 && ff > 0 && (epi != 2 || trans_b);
+}
+
 int32_t gemm_bf16_sm100(const void* A, const void* B, void* C, const void* bias, int64_t M,
                         int64_t N, int64_t K, int64_t lda, int64_t ldb, int64_t ldc,
                         int32_t trans_a, int32_t trans_b, float alpha, int32_t accumulate,
                         int32_t c_dtype, int32_t bias_dtype, cudaStream_t stream,
-                        void* const* peer_c = nullptr, int64_t rows_per_rank = 0,
-                        int32_t my_slot = 0) {
+                        void* const* peer_c, int64_t rows_per_rank, int32_t my_slot,
+                        int32_t epi, const void* aux, int64_t aux_ld, int64_t ff) {
   using namespace tc;
   GALV_CHECK_ARG(M > 0 && N > 0 && K > 0, "empty problem");
   GALV_CHECK_ARG(M < (1ll << 31) && N < (1ll << 31) && K < (1ll << 31), "problem too large");
@@ -672,6 +765,10 @@ int32_t gemm_bf16_sm100(const void* A, const void* B, void* C, const void* bias,
   p.peer_c = peer_c;
   p.rows_per_rank = (int)rows_per_rank;
   p.my_slot = my_slot;
+  p.epi = epi;
+  p.aux = aux;
+  p.aux_ld = aux_ld;
+  p.ff = (int)ff;
   {
     static int v_group = -1, v_gdim = 0, v_hint = 0;
     if (v_group < 0) {  // GALV_GEMM_RASTER="group,gdim,hint" (tuning sweeps only)
@@ -691,6 +788,11 @@ int32_t gemm_bf16_sm100(const void* A, const void* B, void* C, const void* bias,
   }
   const bool c_aligned = (ldc % 8) == 0 &&
                          ((reinterpret_cast<uintptr_t>(C) & 15) == 0 || peer_c != nullptr);
+  if (epi != 0) {  // fused SwiGLU epilogues exist on the 2-CTA path only (callers check)
+    GALV_CHECK_ARG(swiglu_fusable(A, B, C, aux, M, ldc, aux_ld, ff, trans_b, epi) &&
+                       peer_c == nullptr && bias == nullptr && !accumulate && c_dtype == GALV_BF16,
+                   "fused SwiGLU epilogue: unsupported operands");
+  }
   if (M > 128 && c_aligned) {
     // 2-CTA path: 256x256 pair tiles, per-CTA boxes of 128 rows
     CUtensorMap ma2, mb2;
@@ -699,6 +801,7 @@ int32_t gemm_bf16_sm100(const void* A, const void* B, void* C, const void* bias,
     GALV_CHECK_ARG(ok2, "cuTensorMapEncodeTiled failed");
     Params p2 = p;
     p2.tiles_m = (int)((M + 255) / 256);
+    if (epi == 2) p2.tiles_n = (int)((ff + 127) / 128);  // pair tile = 128 gate + 128 up cols
     p2.num_tiles = p2.tiles_m * p2.tiles_n;
     static bool attr2 = false;
     if (!attr2) {
@@ -734,5 +837,5 @@ extern "C" int32_t galv_gemm_rs(const void* A, const void* B, void* const* peer_
                  "bad arguments");
   return galv::gemm_bf16_sm100(A, B, nullptr, nullptr, M, N, K, lda, ldb, ldc, trans_a, trans_b,
                                1.0f, 0, GALV_BF16, GALV_F32, galv::as_stream(stream), peer_c,
-                               rows_per_rank, my_slot);
+                               rows_per_rank, my_slot, 0, nullptr, 0, 0);
 }

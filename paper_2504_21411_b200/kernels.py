@@ -62,6 +62,11 @@ _SIGS = {
     "galv_rope_table": ([_P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _I32, _I32, _P], _I32),
     "galv_swiglu_fwd": ([_P, _P, _I64, _I64, _I32, _P], _I32),
     "galv_swiglu_bwd": ([_P, _P, _P, _I64, _I64, _I32, _P], _I32),
+    "galv_swiglu_bwd_strided": ([_P, _P, _I64, _P, _I64, _I64, _P], _I32),
+    "galv_gemm_swiglu_fwd": ([_P, _P, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _P],
+                             _I32),
+    "galv_gemm_swiglu_bwd": ([_P, _P, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _P],
+                             _I32),
     "galv_bias_gelu_fwd": ([_P, _P, _P, _I64, _I64, _I32, _P], _I32),
     "galv_bias_gelu_bwd": ([_P, _P, _P, _P, _I64, _I64, _I32, _P], _I32),
     "galv_bias_add": ([_P, _P, _I64, _I64, _I32, _P], _I32),
@@ -211,6 +216,54 @@ def gemm(a, b, out=None, *, trans_a=False, trans_b=False, alpha=1.0, accumulate=
         ev1.record()
         _stats.gemm_events.append((2.0 * M * N * K, ev0, ev1, (M, N, K)))
     return out
+
+
+def _timed_call(flops, shape, name, *args):
+    timed = _stats is not None and _stats.time_gemm
+    if timed:
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record()
+    _call(name, *args)
+    if timed:
+        ev1.record()
+        _stats.gemm_events.append((flops, ev0, ev1, shape))
+
+
+def _bf16_rows(*ts):
+    for t in ts:
+        if t.dtype != torch.bfloat16 or t.dim() != 2 or t.stride(1) != 1:
+            raise RuntimeError("fused SwiGLU GEMMs take bf16 2-D row-major tensors")
+
+
+def gemm_swiglu_fwd(x, w_gu, gu=None, h=None):
+    """gu = x @ w_gu^T ([T, 2F], gate then up) and h = silu(gate) * up ([T, F]), the
+    activation fused into the GEMM epilogue (galv_gemm_swiglu_fwd)."""
+    _bf16_rows(x, w_gu)
+    T, Kd = x.shape
+    F = w_gu.shape[0] // 2
+    if w_gu.shape != (2 * F, Kd):
+        raise RuntimeError("gate_up weight must be [2F, K]")
+    gu = torch.empty(T, 2 * F, device=x.device, dtype=x.dtype) if gu is None else gu
+    h = torch.empty(T, F, device=x.device, dtype=x.dtype) if h is None else h
+    _timed_call(2.0 * T * 2 * F * Kd, (T, 2 * F, Kd), "galv_gemm_swiglu_fwd", _ptr(x),
+                _ptr(w_gu), _ptr(gu), _ptr(h), T, F, Kd, x.stride(0), w_gu.stride(0),
+                gu.stride(0), h.stride(0), _stream())
+    return gu, h
+
+
+def gemm_swiglu_bwd(dy, w_down, gu, dgu=None):
+    """d(gate|up) = swiglu_bwd(gu, dy @ w_down) with w_down [K, F] (the down projection's
+    nn.Linear weight); the SwiGLU backward runs in the dgrad epilogue."""
+    _bf16_rows(dy, w_down, gu)
+    T, Kd = dy.shape
+    F = w_down.shape[1]
+    if w_down.shape[0] != Kd or gu.shape != (T, 2 * F):
+        raise RuntimeError("gemm_swiglu_bwd shape mismatch")
+    dgu = torch.empty_like(gu) if dgu is None else dgu
+    _timed_call(2.0 * T * F * Kd, (T, F, Kd), "galv_gemm_swiglu_bwd", _ptr(dy), _ptr(w_down),
+                _ptr(gu), _ptr(dgu), T, F, Kd, dy.stride(0), w_down.stride(0), gu.stride(0),
+                dgu.stride(0), _stream())
+    return dgu
 
 
 def gemm_batched(a, b, out, *, trans_a=False, trans_b=False, alpha=1.0, accumulate=False):

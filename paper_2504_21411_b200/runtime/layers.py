@@ -315,8 +315,11 @@ class DecoderLayer:
             m = self._row_gemm(act, w["fc2.weight"], trans_b=True,
                                bias=w["fc2.bias"] if fuse_bias else None)
         else:
-            gu = _linear(n2f, w["gate_up.weight"])
-            act = K.swiglu_fwd(gu)
+            if n2f.dtype == torch.bfloat16:  # SwiGLU fused into the gate|up GEMM epilogue
+                gu, act = K.gemm_swiglu_fwd(n2f, w["gate_up.weight"])
+            else:
+                gu = _linear(n2f, w["gate_up.weight"])
+                act = K.swiglu_fwd(gu)
             m = self._row_gemm(act, w["down.weight"], trans_b=True)
         if gpt and not fuse_bias:
             K.bias_add_(m, w["fc2.bias"])
@@ -367,10 +370,13 @@ class DecoderLayer:
             dn2 = self._row_gemm(dpre, w["fc1.weight"], trans_b=False)
             _wgrad(dpre, sv["n2f"], gw["fc1.weight"])
         else:
-            dact = _dgrad(dmf, w["down.weight"])
+            if dmf.dtype == torch.bfloat16:  # SwiGLU bwd fused into the down dgrad epilogue
+                dpre = K.gemm_swiglu_bwd(dmf, w["down.weight"], sv["pre"])
+            else:
+                dact = _dgrad(dmf, w["down.weight"])
+                dpre = K.swiglu_bwd(sv["pre"], dact)
+                del dact
             _wgrad(dmf, sv["act"], gw["down.weight"])
-            dpre = K.swiglu_bwd(sv["pre"], dact)
-            del dact
             dn2 = self._row_gemm(dpre, w["gate_up.weight"], trans_b=False)
             _wgrad(dpre, sv["n2f"], gw["gate_up.weight"])
         del dpre, dmf
