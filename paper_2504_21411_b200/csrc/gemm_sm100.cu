@@ -433,74 +433,131 @@ __device__ __forceinline__ void epilogue_staged(const Params& p, uint32_t taddr,
   }
 }
 
-__device__ __forceinline__ float bf16_round(float x) {
-  return __bfloat162float(__float2bfloat16_rn(x));
+__device__ __forceinline__ uint32_t pack2(float a, float b) {  // bf16x2, round to nearest
+  __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+__device__ __forceinline__ float2 bf2_to_f2(uint32_t w) {
+  return make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xFFFF0000u));
+}
+// sigmoid on MUFU (ex2 + rcp): the fused epilogues must keep pace with the MMA mainloop;
+// saturates cleanly (x -> -inf gives 0) without the IEEE-division slow path
+__device__ __forceinline__ float fast_sigmoid(float x) {
+  return __fdividef(1.f, 1.f + __expf(-x));
 }
 
-// epi 1: this thread owns output row `row`, columns [col_base, col_base + 256) of dh
-// (fp32 in TMEM); d(gate|up) computed exactly as act::swiglu_bwd does from the bf16 dh
-__device__ __forceinline__ void epilogue_swiglu_bwd(const Params& p, uint32_t taddr, int row,
-                                                    int col_base) {
-  const bool row_ok = row < p.M;
-  const __nv_bfloat16* gu = reinterpret_cast<const __nv_bfloat16*>(p.aux) + (long long)row * p.aux_ld;
-  __nv_bfloat16* dgu = reinterpret_cast<__nv_bfloat16*>(p.C) + (long long)row * p.ldc;
+// Fused SwiGLU epilogues.  A warp owns 32 rows; global traffic goes through the warp's
+// smem staging rows (PITCH bytes each) so every load/store is a coalesced row segment.
+constexpr int SW_PITCH = Cfg2<false>::STAGE_PITCH;  // 272 >= 2 x 128-byte halves + pad
+
+// epi 1 (backward): 64-column chunks of dh (fp32 in TMEM, rounded to bf16 as the unfused
+// dgrad would store it); gate/up row segments are loaded coalesced into smem, each lane
+// turns its row into d(gate)/d(up) in place, then the chunk is stored coalesced.
+__device__ __forceinline__ void epilogue_swiglu_bwd(const Params& p, uint32_t taddr, int row0,
+                                                    int col_base, uint8_t* stage) {
+  const int lane = threadIdx.x & 31;
+  const __nv_bfloat16* gu = reinterpret_cast<const __nv_bfloat16*>(p.aux);
+  __nv_bfloat16* dgu = reinterpret_cast<__nv_bfloat16*>(p.C);
 #pragma unroll 1
-  for (int cc = 0; cc < BN; cc += 32) {
-    uint32_t r[32];
-    tmem_ld32(taddr + cc, r);
-    const int col0 = col_base + cc;
-    if (!row_ok || col0 >= p.N) continue;
+  for (int q4 = 0; q4 < 4; ++q4) {
+    const int colq = col_base + q4 * 64;
+    // coalesced loads: 32 rows x (gate 8 units | up 8 units) of 16 bytes
+    uint4 ld[16];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int col = col0 + j * 8;
-      if (col >= p.N) break;
-      float g[8], u[8], dg[8], du[8];
-      load16(gu + col, g);
-      load16(gu + p.ff + col, u);
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const float d = bf16_round(__uint_as_float(r[j * 8 + e]) * p.alpha);
-        const float sg = 1.f / (1.f + expf(-g[e]));
-        du[e] = d * g[e] * sg;
-        dg[e] = d * u[e] * sg * (1.f + g[e] * (1.f - sg));
-      }
-      store16(dgu + col, dg);
-      store16(dgu + p.ff + col, du);
+    for (int it = 0; it < 16; ++it) {
+      const int u = it * 32 + lane, rr = u >> 4, part = u & 15;
+      const int row = row0 + rr, col = colq + (part & 7) * 8;
+      ld[it] = make_uint4(0, 0, 0, 0);
+      if (row < p.M && col < p.N)
+        ld[it] = *reinterpret_cast<const uint4*>(gu + (long long)row * p.aux_ld +
+                                                 (part >> 3) * p.ff + col);
     }
+    uint32_t r[64];
+    tmem_ld32(taddr + q4 * 64, r);
+    tmem_ld32(taddr + q4 * 64 + 32, r + 32);
+#pragma unroll
+    for (int it = 0; it < 16; ++it) {
+      const int u = it * 32 + lane, rr = u >> 4, part = u & 15;
+      *reinterpret_cast<uint4*>(stage + rr * SW_PITCH + part * 16) = ld[it];
+    }
+    __syncwarp();
+    // this lane's row: gate at bytes [0,128), up at [128,256)
+    __nv_bfloat16* srow = reinterpret_cast<__nv_bfloat16*>(stage + lane * SW_PITCH);
+#pragma unroll
+    for (int c = 0; c < 64; c += 8) {
+      uint4 graw = *reinterpret_cast<const uint4*>(srow + c);
+      uint4 uraw = *reinterpret_cast<const uint4*>(srow + 64 + c);
+      const uint32_t* gw = reinterpret_cast<const uint32_t*>(&graw);
+      const uint32_t* uw = reinterpret_cast<const uint32_t*>(&uraw);
+      uint32_t dgw[4], duw[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 g = bf2_to_f2(gw[e]), u = bf2_to_f2(uw[e]);
+        const float2 d = bf2_to_f2(pack2(__uint_as_float(r[c + 2 * e]), __uint_as_float(r[c + 2 * e + 1])));
+        const float s0 = fast_sigmoid(g.x), s1 = fast_sigmoid(g.y);
+        duw[e] = pack2(d.x * g.x * s0, d.y * g.y * s1);
+        dgw[e] = pack2(d.x * u.x * s0 * (1.f + g.x * (1.f - s0)),
+                       d.y * u.y * s1 * (1.f + g.y * (1.f - s1)));
+      }
+      *reinterpret_cast<uint4*>(srow + c) = make_uint4(dgw[0], dgw[1], dgw[2], dgw[3]);
+      *reinterpret_cast<uint4*>(srow + 64 + c) = make_uint4(duw[0], duw[1], duw[2], duw[3]);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int it = 0; it < 16; ++it) {
+      const int u = it * 32 + lane, rr = u >> 4, part = u & 15;
+      const int row = row0 + rr, col = colq + (part & 7) * 8;
+      if (row < p.M && col < p.N)
+        *reinterpret_cast<uint4*>(dgu + (long long)row * p.ldc + (part >> 3) * p.ff + col) =
+            *reinterpret_cast<const uint4*>(stage + rr * SW_PITCH + part * 16);
+    }
+    __syncwarp();
   }
 }
 
-// epi 2: accumulator columns [0,128) are gate columns [col_base, +128), [128,256) the
-// matching up columns; gate/up rounded to bf16 (what the unfused path stores) and
-// h = silu(g) * u from the rounded values, exactly as act::swiglu_fwd
-__device__ __forceinline__ void epilogue_swiglu_fwd(const Params& p, uint32_t taddr, int row,
-                                                    int col_base) {
-  const bool row_ok = row < p.M;
-  __nv_bfloat16* gu = reinterpret_cast<__nv_bfloat16*>(p.C) + (long long)row * p.ldc;
-  __nv_bfloat16* h = reinterpret_cast<__nv_bfloat16*>(const_cast<void*>(p.aux)) +
-                     (long long)row * p.aux_ld;
+// epi 2 (forward): accumulator columns [0,128) are gate columns [col_base, +128), [128,256)
+// the matching up columns.  gate/up are rounded to bf16 (what the unfused GEMM stores) and
+// h = silu(g) * u from the rounded values, as act::swiglu_fwd; per 32-column chunk the lane
+// writes its row's gate | up | h (3 x 64 bytes) to smem, then the warp stores coalesced.
+__device__ __forceinline__ void epilogue_swiglu_fwd(const Params& p, uint32_t taddr, int row0,
+                                                    int col_base, uint8_t* stage) {
+  const int lane = threadIdx.x & 31;
+  __nv_bfloat16* gu = reinterpret_cast<__nv_bfloat16*>(p.C);
+  __nv_bfloat16* hout = reinterpret_cast<__nv_bfloat16*>(const_cast<void*>(p.aux));
+  __nv_bfloat16* srow = reinterpret_cast<__nv_bfloat16*>(stage + lane * SW_PITCH);
 #pragma unroll 1
   for (int cc = 0; cc < 128; cc += 32) {
     uint32_t rg[32], ru[32];
     tmem_ld32(taddr + cc, rg);
     tmem_ld32(taddr + 128 + cc, ru);
-    const int col0 = col_base + cc;
-    if (!row_ok || col0 >= p.ff) continue;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int col = col0 + j * 8;
-      if (col >= p.ff) break;
-      float g[8], u[8], o[8];
+    for (int c = 0; c < 32; c += 8) {
+      uint32_t gw[4], uw[4], hw[4];
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        g[e] = bf16_round(__uint_as_float(rg[j * 8 + e]) * p.alpha);
-        u[e] = bf16_round(__uint_as_float(ru[j * 8 + e]) * p.alpha);
-        o[e] = g[e] / (1.f + expf(-g[e])) * u[e];
+      for (int e = 0; e < 4; ++e) {
+        gw[e] = pack2(__uint_as_float(rg[c + 2 * e]), __uint_as_float(rg[c + 2 * e + 1]));
+        uw[e] = pack2(__uint_as_float(ru[c + 2 * e]), __uint_as_float(ru[c + 2 * e + 1]));
+        const float2 g = bf2_to_f2(gw[e]), u = bf2_to_f2(uw[e]);
+        hw[e] = pack2(g.x * fast_sigmoid(g.x) * u.x, g.y * fast_sigmoid(g.y) * u.y);
       }
-      store16(gu + col, g);
-      store16(gu + p.ff + col, u);
-      store16(h + col, o);
+      *reinterpret_cast<uint4*>(srow + c) = make_uint4(gw[0], gw[1], gw[2], gw[3]);
+      *reinterpret_cast<uint4*>(srow + 32 + c) = make_uint4(uw[0], uw[1], uw[2], uw[3]);
+      *reinterpret_cast<uint4*>(srow + 64 + c) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
     }
+    __syncwarp();
+    const int colq = col_base + cc;
+#pragma unroll
+    for (int it = 0; it < 12; ++it) {  // 32 rows x (gate 4 | up 4 | h 4) units of 16 bytes
+      const int u = it * 32 + lane, rr = u / 12, part = u % 12, arr = part >> 2;
+      const int row = row0 + rr, col = colq + (part & 3) * 8;
+      if (row < p.M && col < p.ff) {
+        __nv_bfloat16* dst = arr == 2 ? hout + (long long)row * p.aux_ld + col
+                                      : gu + (long long)row * p.ldc + arr * p.ff + col;
+        *reinterpret_cast<uint4*>(dst) =
+            *reinterpret_cast<const uint4*>(stage + rr * SW_PITCH + part * 16);
+      }
+    }
+    __syncwarp();
   }
 }
 
@@ -655,10 +712,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
                       staging + q * 32 * Cfg2<true>::STAGE_PITCH);
       else if (p.epi == 1)
         epilogue_swiglu_bwd(p, tmem + acc * BN + ((uint32_t)(q * 32) << 16),
-                            mt * 256 + (int)cr * 128 + q * 32 + lane, nt * BN);
+                            mt * 256 + (int)cr * 128 + q * 32, nt * BN,
+                            staging + q * 32 * Cfg2<false>::STAGE_PITCH);
       else if (p.epi == 2)
         epilogue_swiglu_fwd(p, tmem + acc * BN + ((uint32_t)(q * 32) << 16),
-                            mt * 256 + (int)cr * 128 + q * 32 + lane, nt * 128);
+                            mt * 256 + (int)cr * 128 + q * 32, nt * 128,
+                            staging + q * 32 * Cfg2<false>::STAGE_PITCH);
       else
         epilogue_staged<false>(p, tmem + acc * BN + ((uint32_t)(q * 32) << 16),
                                mt * 256 + (int)cr * 128 + q * 32, nt * BN,
