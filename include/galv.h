@@ -140,6 +140,21 @@ int32_t galv_bias_gelu_fwd(const void* x, const void* bias, void* y, int64_t T, 
                            int32_t dtype, void* stream);
 int32_t galv_bias_gelu_bwd(const void* x, const void* bias, const void* dy, void* dx,
                            int64_t T, int64_t F, int32_t dtype, void* stream);
+/*
+ * GPT MLP GEMMs with the bias-GeLU(tanh) fused into the tcgen05 epilogue (bf16):
+ *   fwd: pre[M,F] = X[M,K] W1[F,K]^T, act[M,F] = gelu(pre + bias)   (fc1)
+ *   bwd: dpre[M,F] = (dY[M,K] W2[K,F]) * gelu'(pre + bias)          (fc2 dgrad)
+ * GeLU/tanh on MUFU (tanh.approx); same roundings as galv_gemm + galv_bias_gelu_*
+ * otherwise.  bias may be null; bias_dtype GALV_BF16 or GALV_F32.
+ */
+int32_t galv_gemm_bias_gelu_fwd(const void* X, const void* W1, const void* bias, void* pre,
+                                void* act, int64_t M, int64_t F, int64_t K, int64_t ldx,
+                                int64_t ldw, int64_t ld_pre, int64_t ld_act, int32_t bias_dtype,
+                                void* stream);
+int32_t galv_gemm_bias_gelu_bwd(const void* dY, const void* W2, const void* pre,
+                                const void* bias, void* dpre, int64_t M, int64_t F, int64_t K,
+                                int64_t ldy, int64_t ldw, int64_t ld_pre, int64_t ld_dpre,
+                                int32_t bias_dtype, void* stream);
 /* x[T, F] += bias[F] (row broadcast) */
 int32_t galv_bias_add(void* x, const void* bias, int64_t T, int64_t F, int32_t dtype, void* stream);
 /* column sums: out[c] (+)= sum_r x[r, c] (fp32 out, for bias gradients) */

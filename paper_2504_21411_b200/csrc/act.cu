@@ -114,6 +114,42 @@ __global__ void __launch_bounds__(128) colsum_kernel(const T* __restrict__ x,
   atomicAdd(&out[c + 1], s1);
 }
 
+// vectorized column sums: CTA = 8 column-threads (16-byte vectors) x 32 row lanes over a
+// 16-byte-aligned matrix; row lanes are reduced through smem, so each column gets one
+// atomic per CTA (few CTAs per column strip -> no L2 atomic contention)
+template <typename T>
+__global__ void __launch_bounds__(256) colsum_vec(const T* __restrict__ x, float* __restrict__ out,
+                                                  int64_t rows, int64_t cols,
+                                                  int64_t rows_per_cta) {
+  constexpr int V = 16 / sizeof(T);
+  __shared__ float red[32][8 * V + 1];
+  const int tx = threadIdx.x & 7, ty = threadIdx.x >> 3;
+  const int64_t c = ((int64_t)blockIdx.x * 8 + tx) * V;
+  const int64_t r0 = blockIdx.y * rows_per_cta, r1 = min(rows, r0 + rows_per_cta);
+  float s[V];
+#pragma unroll
+  for (int e = 0; e < V; ++e) s[e] = 0.f;
+  if (c < cols) {
+#pragma unroll 4
+    for (int64_t r = r0 + ty; r < r1; r += 32) {
+      float v[V];
+      load16(x + r * cols + c, v);
+#pragma unroll
+      for (int e = 0; e < V; ++e) s[e] += v[e];
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < V; ++e) red[ty][tx * V + e] = s[e];
+  __syncthreads();
+  if (threadIdx.x < 8 * V) {
+    const int64_t col = (int64_t)blockIdx.x * 8 * V + threadIdx.x;
+    float t = 0.f;
+#pragma unroll 8
+    for (int k = 0; k < 32; ++k) t += red[k][threadIdx.x];
+    if (col < cols) atomicAdd(&out[col], t);
+  }
+}
+
 template <typename TX, typename TY>
 __global__ void axpby_kernel(const TX* __restrict__ x, TY* __restrict__ y, int64_t n, float a,
                              float b) {
@@ -237,6 +273,20 @@ int32_t galv_colsum(const void* x, float* out, int64_t rows, int64_t cols, int32
   GALV_CHECK_ARG(x && out && rows > 0 && cols > 0, "bad arguments");
   if (!accumulate) GALV_CUDA_RET(cudaMemsetAsync(out, 0, sizeof(float) * cols, as_stream(stream)));
   GALV_CHECK_ARG(cols % 2 == 0, "cols must be even");
+  const int esz = dtype == GALV_BF16 ? 2 : 4;
+  if ((cols * esz) % 16 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0) {
+    const int64_t per = 8 * (16 / esz);  // columns per CTA
+    const int64_t strips_v = (cols + per - 1) / per;
+    const int64_t ych = std::max<int64_t>(
+        1, std::min<int64_t>((rows + 31) / 32, (int64_t)sm_count() * 4 / strips_v));
+    const int64_t rpc_v = (rows + ych - 1) / ych;
+    dim3 g((unsigned)strips_v, (unsigned)ych);
+    GALV_DISPATCH(dtype, T, {
+      act::colsum_vec<T><<<g, 256, 0, as_stream(stream)>>>((const T*)x, out, rows, cols, rpc_v);
+    });
+    GALV_LAUNCH_CHECK();
+    return 0;
+  }
   const int64_t strips = (cols / 2 + 127) / 128;
   const int64_t ychunks = std::max<int64_t>(
       1, std::min<int64_t>(rows / 16 + 1, sm_count() * 16 / std::max<int64_t>(1, strips) + 1));

@@ -130,4 +130,45 @@ int32_t galv_gemm_swiglu_bwd(const void* dY, const void* Wdown, const void* gu, 
   return rc ? rc : galv_swiglu_bwd_strided(gu, up_half, ld_dgu, dgu, M, F, stream);
 }
 
+// GPT fc1: pre = X W1^T (W1 [F, K]) and act = gelu_tanh(pre + bias), the activation in the
+// GEMM epilogue; unfused fallback = GEMM + galv_bias_gelu_fwd.
+int32_t galv_gemm_bias_gelu_fwd(const void* X, const void* W1, const void* bias, void* pre,
+                                void* act, int64_t M, int64_t F, int64_t K, int64_t ldx,
+                                int64_t ldw, int64_t ld_pre, int64_t ld_act, int32_t bias_dtype,
+                                void* stream) {
+  GALV_CHECK_ARG(X && W1 && pre && act && M > 0 && F > 0 && K > 0 && F % 8 == 0,
+                 "bad arguments");
+  GALV_CHECK_ARG(bias_dtype == GALV_BF16 || bias_dtype == GALV_F32, "bad bias dtype");
+  if (galv::swiglu_fusable(X, W1, pre, act, M, ld_pre, ld_act, F, 1, 3))
+    return galv::gemm_bf16_sm100(X, W1, pre, bias, M, F, K, ldx, ldw, ld_pre, 0, 1, 1.0f, 0,
+                                 GALV_BF16, bias_dtype, galv::as_stream(stream), nullptr, 0, 0, 3,
+                                 act, ld_act, F);
+  GALV_CHECK_ARG(ld_pre == F && ld_act == F && (bias == nullptr || bias_dtype == GALV_BF16),
+                 "unfused fallback needs dense pre/act and a bf16 bias");
+  int32_t rc = galv::gemm_bf16_sm100(X, W1, pre, nullptr, M, F, K, ldx, ldw, ld_pre, 0, 1, 1.0f,
+                                     0, GALV_BF16, GALV_F32, galv::as_stream(stream));
+  return rc ? rc : galv_bias_gelu_fwd(pre, bias, act, M, F, GALV_BF16, stream);
+}
+
+// GPT fc2 dgrad: dpre = (dY W2) * gelu_tanh'(pre + bias) with W2 [K=hidden, F] (nn.Linear
+// layout of fc2); d(act) stays in TMEM.  The fallback stages d(act) in dpre and transforms
+// it in place (each element is read before it is overwritten).
+int32_t galv_gemm_bias_gelu_bwd(const void* dY, const void* W2, const void* pre,
+                                const void* bias, void* dpre, int64_t M, int64_t F, int64_t K,
+                                int64_t ldy, int64_t ldw, int64_t ld_pre, int64_t ld_dpre,
+                                int32_t bias_dtype, void* stream) {
+  GALV_CHECK_ARG(dY && W2 && pre && dpre && M > 0 && F > 0 && K > 0 && F % 8 == 0,
+                 "bad arguments");
+  GALV_CHECK_ARG(bias_dtype == GALV_BF16 || bias_dtype == GALV_F32, "bad bias dtype");
+  if (galv::swiglu_fusable(dY, W2, dpre, pre, M, ld_dpre, ld_pre, F, 0, 4))
+    return galv::gemm_bf16_sm100(dY, W2, dpre, bias, M, F, K, ldy, ldw, ld_dpre, 0, 0, 1.0f, 0,
+                                 GALV_BF16, bias_dtype, galv::as_stream(stream), nullptr, 0, 0, 4,
+                                 pre, ld_pre, F);
+  GALV_CHECK_ARG(ld_pre == F && ld_dpre == F && (bias == nullptr || bias_dtype == GALV_BF16),
+                 "unfused fallback needs dense pre/dpre and a bf16 bias");
+  int32_t rc = galv::gemm_bf16_sm100(dY, W2, dpre, nullptr, M, F, K, ldy, ldw, ld_dpre, 0, 0,
+                                     1.0f, 0, GALV_BF16, GALV_F32, galv::as_stream(stream));
+  return rc ? rc : galv_bias_gelu_bwd(pre, bias, dpre, dpre, M, F, GALV_BF16, stream);
+}
+
 }  // extern "C"

@@ -561,6 +561,130 @@ __device__ __forceinline__ void epilogue_swiglu_fwd(const Params& p, uint32_t ta
   }
 }
 
+// tanh-GeLU on MUFU (tanh.approx), as used by the GPT MLP epilogues
+__device__ __forceinline__ float fast_tanh(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float gelu_fast(float x) {
+  const float k0 = 0.7978845608028654f, k1 = 0.044715f;
+  return 0.5f * x * (1.f + fast_tanh(k0 * (x + k1 * x * x * x)));
+}
+__device__ __forceinline__ float gelu_grad_fast(float x) {
+  const float k0 = 0.7978845608028654f, k1 = 0.044715f;
+  const float th = fast_tanh(k0 * (x + k1 * x * x * x));
+  return 0.5f * (1.f + th) + 0.5f * x * (1.f - th * th) * k0 * (1.f + 3.f * k1 * x * x);
+}
+__device__ __forceinline__ float2 bias_pair(const Params& p, int col) {  // bias[col], [col+1]
+  if (p.bias_bf16) return bf2_to_f2(*reinterpret_cast<const uint32_t*>(
+                       reinterpret_cast<const __nv_bfloat16*>(p.bias) + col));
+  return *reinterpret_cast<const float2*>(reinterpret_cast<const float*>(p.bias) + col);
+}
+
+// epi 3 (GPT fc1 forward): C = pre = acc (bf16, what the unfused GEMM stores), aux = act =
+// gelu(pre + bias); per 32-column chunk the lane stages its row's pre | act (2 x 64 B)
+__device__ __forceinline__ void epilogue_bias_gelu_fwd(const Params& p, uint32_t taddr, int row0,
+                                                       int col_base, uint8_t* stage) {
+  const int lane = threadIdx.x & 31;
+  __nv_bfloat16* pre = reinterpret_cast<__nv_bfloat16*>(p.C);
+  __nv_bfloat16* act = reinterpret_cast<__nv_bfloat16*>(const_cast<void*>(p.aux));
+  __nv_bfloat16* srow = reinterpret_cast<__nv_bfloat16*>(stage + lane * SW_PITCH);
+#pragma unroll 1
+  for (int cc = 0; cc < BN; cc += 32) {
+    const int colq = col_base + cc;
+    if (colq >= p.N) break;
+    uint32_t r[32];
+    tmem_ld32(taddr + cc, r);
+#pragma unroll
+    for (int c = 0; c < 32; c += 8) {
+      uint32_t pw[4], aw[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        pw[e] = pack2(__uint_as_float(r[c + 2 * e]), __uint_as_float(r[c + 2 * e + 1]));
+        const float2 x = bf2_to_f2(pw[e]);
+        const int col = min(colq + c + 2 * e, p.N - 2);
+        const float2 b = p.bias ? bias_pair(p, col) : make_float2(0.f, 0.f);
+        aw[e] = pack2(gelu_fast(x.x + b.x), gelu_fast(x.y + b.y));
+      }
+      *reinterpret_cast<uint4*>(srow + c) = make_uint4(pw[0], pw[1], pw[2], pw[3]);
+      *reinterpret_cast<uint4*>(srow + 32 + c) = make_uint4(aw[0], aw[1], aw[2], aw[3]);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int it = 0; it < 8; ++it) {  // 32 rows x (pre 4 | act 4) units of 16 bytes
+      const int u = it * 32 + lane, rr = u >> 3, part = u & 7;
+      const int row = row0 + rr, col = colq + (part & 3) * 8;
+      if (row < p.M && col < p.N) {
+        __nv_bfloat16* dst = (part >> 2) ? act + (long long)row * p.aux_ld + col
+                                         : pre + (long long)row * p.ldc + col;
+        *reinterpret_cast<uint4*>(dst) =
+            *reinterpret_cast<const uint4*>(stage + rr * SW_PITCH + part * 16);
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// epi 4 (GPT fc2 dgrad): acc = d(act) (rounded to bf16 as the unfused dgrad stores it),
+// aux = saved pre; C = d(pre) = d(act) * gelu'(pre + bias).  64-column chunks: pre loaded
+// coalesced into smem, transformed in place per row, stored coalesced.
+__device__ __forceinline__ void epilogue_bias_gelu_bwd(const Params& p, uint32_t taddr, int row0,
+                                                       int col_base, uint8_t* stage) {
+  const int lane = threadIdx.x & 31;
+  const __nv_bfloat16* pre = reinterpret_cast<const __nv_bfloat16*>(p.aux);
+  __nv_bfloat16* dpre = reinterpret_cast<__nv_bfloat16*>(p.C);
+  __nv_bfloat16* srow = reinterpret_cast<__nv_bfloat16*>(stage + lane * SW_PITCH);
+#pragma unroll 1
+  for (int q4 = 0; q4 < 4; ++q4) {
+    const int colq = col_base + q4 * 64;
+    if (colq >= p.N) break;
+    uint4 ld[8];
+#pragma unroll
+    for (int it = 0; it < 8; ++it) {  // 32 rows x 8 units of 16 bytes
+      const int u = it * 32 + lane, rr = u >> 3, part = u & 7;
+      const int row = row0 + rr, col = colq + part * 8;
+      ld[it] = make_uint4(0, 0, 0, 0);
+      if (row < p.M && col < p.N)
+        ld[it] = *reinterpret_cast<const uint4*>(pre + (long long)row * p.aux_ld + col);
+    }
+    uint32_t r[64];
+    tmem_ld32(taddr + q4 * 64, r);
+    tmem_ld32(taddr + q4 * 64 + 32, r + 32);
+#pragma unroll
+    for (int it = 0; it < 8; ++it) {
+      const int u = it * 32 + lane, rr = u >> 3, part = u & 7;
+      *reinterpret_cast<uint4*>(stage + rr * SW_PITCH + part * 16) = ld[it];
+    }
+    __syncwarp();
+#pragma unroll
+    for (int c = 0; c < 64; c += 8) {
+      uint4 xr = *reinterpret_cast<const uint4*>(srow + c);
+      const uint32_t* xw = reinterpret_cast<const uint32_t*>(&xr);
+      uint32_t ow[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 x = bf2_to_f2(xw[e]);
+        const float2 d = bf2_to_f2(pack2(__uint_as_float(r[c + 2 * e]), __uint_as_float(r[c + 2 * e + 1])));
+        const int col = min(colq + c + 2 * e, p.N - 2);
+        const float2 b = p.bias ? bias_pair(p, col) : make_float2(0.f, 0.f);
+        ow[e] = pack2(d.x * gelu_grad_fast(x.x + b.x), d.y * gelu_grad_fast(x.y + b.y));
+      }
+      *reinterpret_cast<uint4*>(srow + c) = make_uint4(ow[0], ow[1], ow[2], ow[3]);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int it = 0; it < 8; ++it) {
+      const int u = it * 32 + lane, rr = u >> 3, part = u & 7;
+      const int row = row0 + rr, col = colq + part * 8;
+      if (row < p.M && col < p.N)
+        *reinterpret_cast<uint4*>(dpre + (long long)row * p.ldc + col) =
+            *reinterpret_cast<const uint4*>(stage + rr * SW_PITCH + part * 16);
+    }
+    __syncwarp();
+  }
+}
+
 __device__ __forceinline__ void tile_coords2(const Params& p, int t, int& mt, int& nt) {
   tile_coords(p, t, mt, nt);  // pair tiles are 256 x 256; p.tiles_m counts 256-row tiles
 }
@@ -718,6 +842,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
         epilogue_swiglu_fwd(p, tmem + acc * BN + ((uint32_t)(q * 32) << 16),
                             mt * 256 + (int)cr * 128 + q * 32, nt * 128,
                             staging + q * 32 * Cfg2<false>::STAGE_PITCH);
+      else if (p.epi == 3)
+        epilogue_bias_gelu_fwd(p, tmem + acc * BN + ((uint32_t)(q * 32) << 16),
+                               mt * 256 + (int)cr * 128 + q * 32, nt * BN,
+                               staging + q * 32 * Cfg2<false>::STAGE_PITCH);
+      else if (p.epi == 4)
+        epilogue_bias_gelu_bwd(p, tmem + acc * BN + ((uint32_t)(q * 32) << 16),
+                               mt * 256 + (int)cr * 128 + q * 32, nt * BN,
+                               staging + q * 32 * Cfg2<false>::STAGE_PITCH);
       else
         epilogue_staged<false>(p, tmem + acc * BN + ((uint32_t)(q * 32) << 16),
                                mt * 256 + (int)cr * 128 + q * 32, nt * BN,
@@ -849,8 +981,9 @@ int32_t gemm_bf16_sm100(const void* A, const void* B, void* C, const void* bias,
                          ((reinterpret_cast<uintptr_t>(C) & 15) == 0 || peer_c != nullptr);
   if (epi != 0) {  // fused SwiGLU epilogues exist on the 2-CTA path only (callers check)
     GALV_CHECK_ARG(swiglu_fusable(A, B, C, aux, M, ldc, aux_ld, ff, trans_b, epi) &&
-                       peer_c == nullptr && bias == nullptr && !accumulate && c_dtype == GALV_BF16,
-                   "fused SwiGLU epilogue: unsupported operands");
+                       peer_c == nullptr && (bias == nullptr || epi >= 3) && !accumulate &&
+                       c_dtype == GALV_BF16 && alpha == 1.0f,
+                   "fused activation epilogue: unsupported operands");
   }
   if (M > 128 && c_aligned) {
     // 2-CTA path: 256x256 pair tiles, per-CTA boxes of 128 rows

@@ -67,6 +67,10 @@ _SIGS = {
                              _I32),
     "galv_gemm_swiglu_bwd": ([_P, _P, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _P],
                              _I32),
+    "galv_gemm_bias_gelu_fwd": ([_P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I64,
+                                 _I32, _P], _I32),
+    "galv_gemm_bias_gelu_bwd": ([_P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I64,
+                                 _I32, _P], _I32),
     "galv_bias_gelu_fwd": ([_P, _P, _P, _I64, _I64, _I32, _P], _I32),
     "galv_bias_gelu_bwd": ([_P, _P, _P, _P, _I64, _I64, _I32, _P], _I32),
     "galv_bias_add": ([_P, _P, _I64, _I64, _I32, _P], _I32),
@@ -264,6 +268,37 @@ def gemm_swiglu_bwd(dy, w_down, gu, dgu=None):
                 _ptr(gu), _ptr(dgu), T, F, Kd, dy.stride(0), w_down.stride(0), gu.stride(0),
                 dgu.stride(0), _stream())
     return dgu
+
+
+def gemm_bias_gelu_fwd(x, w1, bias, pre=None, act=None):
+    """pre = x @ w1^T and act = gelu_tanh(pre + bias), GeLU in the GEMM epilogue."""
+    _bf16_rows(x, w1)
+    T, Kd = x.shape
+    F = w1.shape[0]
+    if w1.shape[1] != Kd:
+        raise RuntimeError("fc1 weight must be [F, K]")
+    pre = torch.empty(T, F, device=x.device, dtype=x.dtype) if pre is None else pre
+    act = torch.empty(T, F, device=x.device, dtype=x.dtype) if act is None else act
+    _timed_call(2.0 * T * F * Kd, (T, F, Kd), "galv_gemm_bias_gelu_fwd", _ptr(x), _ptr(w1),
+                _ptr(bias), _ptr(pre), _ptr(act), T, F, Kd, x.stride(0), w1.stride(0),
+                pre.stride(0), act.stride(0), dtype_code(bias.dtype) if bias is not None else BF16,
+                _stream())
+    return pre, act
+
+
+def gemm_bias_gelu_bwd(dy, w2, pre, bias, dpre=None):
+    """dpre = (dy @ w2) * gelu_tanh'(pre + bias), w2 [K, F] (fc2's nn.Linear weight)."""
+    _bf16_rows(dy, w2, pre)
+    T, Kd = dy.shape
+    F = w2.shape[1]
+    if w2.shape[0] != Kd or pre.shape != (T, F):
+        raise RuntimeError("gemm_bias_gelu_bwd shape mismatch")
+    dpre = torch.empty_like(pre) if dpre is None else dpre
+    _timed_call(2.0 * T * F * Kd, (T, F, Kd), "galv_gemm_bias_gelu_bwd", _ptr(dy), _ptr(w2),
+                _ptr(pre), _ptr(bias), _ptr(dpre), T, F, Kd, dy.stride(0), w2.stride(0),
+                pre.stride(0), dpre.stride(0),
+                dtype_code(bias.dtype) if bias is not None else BF16, _stream())
+    return dpre
 
 
 def gemm_batched(a, b, out, *, trans_a=False, trans_b=False, alpha=1.0, accumulate=False):

@@ -86,6 +86,21 @@ def tp_unslice(cfg, name: str, parts: list) -> torch.Tensor:
 # ---------------------------------------------------------------------------- helpers
 
 
+# Fused activation epilogues pay off once the GEMM mainloop (K = hidden) is long enough to
+# hide them (scratch/gelu_bench.py, scratch/swiglu_bench.py on B200): forward from K >= 2048,
+# the backward (which also streams the saved pre-activation) from K >= 4096.
+FUSE_ACT_FWD_MIN_K = 2048
+FUSE_ACT_BWD_MIN_K = 4096
+
+
+def _fuse_fwd(x):
+    return x.dtype == torch.bfloat16 and x.shape[1] >= FUSE_ACT_FWD_MIN_K
+
+
+def _fuse_bwd(dy):
+    return dy.dtype == torch.bfloat16 and dy.shape[1] >= FUSE_ACT_BWD_MIN_K
+
+
 def _linear(x, w, out=None, bias=None):
     """x [T, K] @ w[N, K]^T (+bias) -> [T, N]."""
     return K.gemm(x, w, out, trans_b=True, bias=bias)
@@ -310,12 +325,15 @@ class DecoderLayer:
         n2, st2, h1 = self._norm_fwd(a, w, "mlp_norm", residual=x)
         n2f = self._gather_seq(n2)
         if gpt:
-            f1 = _linear(n2f, w["fc1.weight"])           # pre-activation (bias in gelu)
-            act = K.bias_gelu_fwd(f1, w["fc1.bias"])
+            if _fuse_fwd(n2f):  # bias-GeLU fused into the fc1 GEMM epilogue
+                f1, act = K.gemm_bias_gelu_fwd(n2f, w["fc1.weight"], w["fc1.bias"])
+            else:
+                f1 = _linear(n2f, w["fc1.weight"])       # pre-activation (bias in gelu)
+                act = K.bias_gelu_fwd(f1, w["fc1.bias"])
             m = self._row_gemm(act, w["fc2.weight"], trans_b=True,
                                bias=w["fc2.bias"] if fuse_bias else None)
         else:
-            if n2f.dtype == torch.bfloat16:  # SwiGLU fused into the gate|up GEMM epilogue
+            if _fuse_fwd(n2f):  # SwiGLU fused into the gate|up GEMM epilogue
                 gu, act = K.gemm_swiglu_fwd(n2f, w["gate_up.weight"])
             else:
                 gu = _linear(n2f, w["gate_up.weight"])
@@ -362,15 +380,18 @@ class DecoderLayer:
         dmf = self._gather_seq(dy)
         if gpt:
             K.colsum(dy, sg["fc2.bias"])
-            dact = _dgrad(dmf, w["fc2.weight"])
+            if _fuse_bwd(dmf):  # GeLU bwd fused into the fc2 dgrad epilogue
+                dpre = K.gemm_bias_gelu_bwd(dmf, w["fc2.weight"], sv["pre"], w["fc1.bias"])
+            else:
+                dact = _dgrad(dmf, w["fc2.weight"])
+                dpre = K.bias_gelu_bwd(sv["pre"], w["fc1.bias"], dact)
+                del dact
             _wgrad(dmf, sv["act"], gw["fc2.weight"])
-            dpre = K.bias_gelu_bwd(sv["pre"], w["fc1.bias"], dact)
-            del dact
             K.colsum(dpre, sg["fc1.bias"])
             dn2 = self._row_gemm(dpre, w["fc1.weight"], trans_b=False)
             _wgrad(dpre, sv["n2f"], gw["fc1.weight"])
         else:
-            if dmf.dtype == torch.bfloat16:  # SwiGLU bwd fused into the down dgrad epilogue
+            if _fuse_bwd(dmf):  # SwiGLU bwd fused into the down dgrad epilogue
                 dpre = K.gemm_swiglu_bwd(dmf, w["down.weight"], sv["pre"])
             else:
                 dact = _dgrad(dmf, w["down.weight"])

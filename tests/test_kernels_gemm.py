@@ -87,3 +87,35 @@ def test_gemm_swiglu_fused(M, F, Kd):
     g32, u32 = (x.float() @ w_gu.float().t()).split(F, dim=1)
     h32 = torch.nn.functional.silu(g32) * u32
     assert ((h.float() - h32).norm() / h32.norm()).item() < 1e-2
+
+
+@pytest.mark.parametrize("M,F,Kd", [(512, 4096, 1024), (300, 200, 136), (100, 256, 64)])
+@pytest.mark.parametrize("bias_dt", [torch.bfloat16, torch.float32, None])
+def test_gemm_bias_gelu_fused(M, F, Kd, bias_dt):
+    """bias-GeLU fused into the fc1 GEMM epilogue and the fc2 dgrad epilogue vs the unfused
+    GEMM + bias_gelu kernels and an fp32 torch reference (M <= 128: C-ABI fallback)."""
+    from paper_2504_21411_b200 import kernels as K
+    if bias_dt == torch.float32 and M <= 128:
+        pytest.skip("the unfused fallback takes a bf16 bias")
+    torch.manual_seed(0)
+    x = torch.randn(M, Kd, device="cuda").bfloat16()
+    w1 = (torch.randn(F, Kd, device="cuda") / Kd ** 0.5).bfloat16()
+    w2 = (torch.randn(Kd, F, device="cuda") / F ** 0.5).bfloat16()
+    b = None if bias_dt is None else (0.5 * torch.randn(F, device="cuda")).to(bias_dt)
+    dy = torch.randn(M, Kd, device="cuda").bfloat16()
+    pre, act = K.gemm_bias_gelu_fwd(x, w1, b)
+    pre_ref = K.gemm(x, w1, trans_b=True)
+    b16 = None if b is None else b.bfloat16()
+    act_ref = K.bias_gelu_fwd(pre_ref, b16) if b is not None else K.bias_gelu_fwd(pre_ref, None)
+    dpre = K.gemm_bias_gelu_bwd(dy, w2, pre_ref, b)
+    dact_ref = K.gemm(dy, w2)
+    dpre_ref = K.bias_gelu_bwd(pre_ref, b16, dact_ref)
+    torch.cuda.synchronize()
+    assert torch.equal(pre, pre_ref)
+    for got, want in ((act, act_ref), (dpre, dpre_ref)):
+        d = (got.float() - want.float()).abs()
+        assert d.max().item() <= 2e-2 * want.float().abs().max().item() + 1e-6
+        assert (d.norm() / want.float().norm()).item() < 6e-3
+    bb = 0 if b is None else b.float()
+    a32 = torch.nn.functional.gelu(x.float() @ w1.float().t() + bb, approximate="tanh")
+    assert ((act.float() - a32).norm() / a32.norm()).item() < 1e-2

@@ -180,3 +180,17 @@ def test_gather_scatter_rows():
     back = torch.zeros_like(src)
     K.scatter_rows(dst, idx, back)
     assert torch.equal(back[idx], src[idx])
+
+
+@pytest.mark.parametrize("dt", DT)
+@pytest.mark.parametrize("rows,cols", [(16384, 1024), (300, 4096), (7, 72), (1000, 130)])
+def test_colsum_shapes(dt, rows, cols):
+    """Column sums (bias gradients): vectorized path (16-byte rows) and the scalar fallback
+    (cols*esize not a multiple of 16), accumulate semantics."""
+    from paper_2504_21411_b200 import kernels as K
+    torch.manual_seed(5)
+    x = torch.randn(rows, cols, device="cuda").to(dt)
+    cs = torch.full((cols,), 0.5, device="cuda")
+    K.colsum(x, cs, accumulate=True)
+    want = x.double().sum(0) + 0.5
+    assert ((cs.double() - want).norm() / want.norm()).item() < 1e-5

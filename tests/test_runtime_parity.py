@@ -44,6 +44,21 @@ def test_bf16_parity(name):
     assert worst[1] <= 2e-2, worst
 
 
+@pytest.mark.parametrize("name", ["micro-llama", "micro-gpt"])
+def test_bf16_parity_fused_activation_epilogues(name, monkeypatch):
+    """Same bf16 parity with the SwiGLU / bias-GeLU GEMM-epilogue fusions forced on (the
+    runtime enables them only for hidden >= 2048 / 4096, larger than these presets)."""
+    from paper_2504_21411_b200.runtime import layers
+    monkeypatch.setattr(layers, "FUSE_ACT_FWD_MIN_K", 0)
+    monkeypatch.setattr(layers, "FUSE_ACT_BWD_MIN_K", 0)
+    cfg = MODEL_PRESETS[name]
+    hc = uniform_config(cfg, S1, microbatch=2, n_microbatches=2)
+    lerr, errs = run_parity(name, hc, torch.bfloat16, grad_bytes=4)
+    assert lerr <= 2e-2
+    worst = max(errs.items(), key=lambda kv: kv[1])
+    assert worst[1] <= 2e-2, worst
+
+
 def test_llama_fp32_parity():
     cfg = MODEL_PRESETS["micro-llama"]
     hc = uniform_config(cfg, S1R, microbatch=1, n_microbatches=2)
