@@ -9,7 +9,9 @@ cases = [("llama2-7b", 8, None, None), ("gpt2-medium", 16, None, None),
          ("llama2-13b", 1, None, None)]
 for name, spg, pattern, mb in cases:
     cfg = MODEL_PRESETS[name]
-    prof = 'profiles/b200_cluster_gpt2m.json' if name.startswith('gpt2') else 'profiles/b200_cluster.json'
+    prof = ('profiles/b200_cluster_gpt2m.json' if name.startswith('gpt2') else
+            'profiles/b200_cluster_llama13b.json' if name == 'llama2-13b' else
+            'profiles/b200_cluster.json')
     c, _ = bench.cluster_profile(8, prof)
     gb = spg * 8
     if pattern:
