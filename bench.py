@@ -52,6 +52,8 @@ def parse():
                     help="explicit per-layer strategies instead of the search, cycled over "
                          "layers, e.g. 'tp8,dp8z3,tp4dp2' (BASELINE config 4)")
     ap.add_argument("--microbatch", type=int, default=None, help="with --layer-pattern")
+    ap.add_argument("--pp", type=int, default=1,
+                    help="with --layer-pattern: pipeline stages (strategies cover n/pp GPUs)")
     ap.add_argument("--sp-mode", choices=("megatron", "ulysses"), default="megatron",
                     help="how sp=True layers run: Megatron-SP or DeepSpeed-Ulysses")
     return ap.parse_args()
@@ -179,14 +181,14 @@ def parse_pattern(text: str, n: int):
     return out
 
 
-def explicit_plan(cfg, n, global_batch, cluster, pattern, microbatch):
+def explicit_plan(cfg, n, global_batch, cluster, pattern, microbatch, pp=1):
     from paper_2504_21411_b200.planner.profiles import TrainingConfig
     from paper_2504_21411_b200.planner.search import make_plan
     from paper_2504_21411_b200.runtime.config import get_hybrid_parallel_configs, profile_for
-    strats = parse_pattern(pattern, n)
+    strats = parse_pattern(pattern, n // pp)
     layers = [strats[i % len(strats)] for i in range(cfg.n_layers)]
     training = TrainingConfig(global_batch=global_batch)
-    plan = make_plan(model_profile(cfg), cluster, training, 1, microbatch, layers)
+    plan = make_plan(model_profile(cfg), cluster, training, pp, microbatch, layers)
     return plan, get_hybrid_parallel_configs(plan, cfg), training
 
 
@@ -287,7 +289,7 @@ def main():
     cluster, cluster_src = cluster_profile(n, args.cluster_profile)
     if args.layer_pattern:
         plan, hc, training = explicit_plan(cfg, n, gb, cluster, args.layer_pattern,
-                                           args.microbatch or max(n, 1))
+                                           args.microbatch or max(n // args.pp, 1), args.pp)
     else:
         plan, hc, training = plan_for(cfg, n, gb, cluster)
     if args.sp_mode != "megatron":
