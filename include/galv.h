@@ -51,6 +51,20 @@ int32_t galv_gemm(const void* A, const void* B, void* C, const void* bias,
                   int32_t ab_dtype, int32_t c_dtype, int32_t bias_dtype, void* stream);
 
 /*
+ * Split-K variant of galv_gemm for bf16 operands (same op semantics): the K loop is cut into
+ * `splits` ranges computed as separate 2-CTA work units, fp32 partial tiles land in `ws`
+ * (>= splits*M*N*4 bytes, caller-owned), and one reduction pass applies alpha/bias/accumulate.
+ * galv_gemm_splits(M, N, K) returns the split count the cost heuristic picks (1 = none);
+ * it is > 1 only for GEMMs whose tiles cannot fill the chip (narrow-layer wgrad).
+ */
+int32_t galv_gemm_splits(int64_t M, int64_t N, int64_t K);
+int32_t galv_gemm_splitk(const void* A, const void* B, void* C, const void* bias, int64_t M,
+                         int64_t N, int64_t K, int64_t lda, int64_t ldb, int64_t ldc,
+                         int32_t trans_a, int32_t trans_b, float alpha, int32_t accumulate,
+                         int32_t c_dtype, int32_t bias_dtype, int32_t splits, void* ws,
+                         int64_t ws_bytes, void* stream);
+
+/*
  * Batched strided GEMM (same op semantics), `batch` problems at element offsets
  * stride_a/b/c.  Used by the small-head attention path and tests.
  */

@@ -27,7 +27,9 @@ int32_t gemm_bf16_sm100(const void* A, const void* B, void* C, const void* bias,
                         int32_t c_dtype, int32_t bias_dtype, cudaStream_t stream,
                         void* const* peer_c = nullptr, int64_t rows_per_rank = 0,
                         int32_t my_slot = 0, int32_t epi = 0, const void* aux = nullptr,
-                        int64_t aux_ld = 0, int64_t ff = 0);
+                        int64_t aux_ld = 0, int64_t ff = 0, int32_t splits = 1,
+                        float* ws = nullptr);
+int32_t gemm_pick_splits(int64_t M, int64_t N, int64_t K);
 bool swiglu_fusable(const void* A, const void* B, const void* C, const void* aux, int64_t M,
                     int64_t ldc, int64_t aux_ld, int64_t ff, int32_t trans_b, int32_t epi);
 int32_t gemm_f32_simt(const float* A, const float* B, void* C, const float* bias, int64_t batch,
@@ -70,6 +72,25 @@ int32_t galv_gemm(const void* A, const void* B, void* C, const void* bias, int64
   return galv::gemm_f32_simt((const float*)A, (const float*)B, C, (const float*)bias, 1, 0, 0, 0,
                              M, N, K, lda, ldb, ldc, trans_a, trans_b, alpha, accumulate, c_dtype,
                              galv::as_stream(stream));
+}
+
+int32_t galv_gemm_splits(int64_t M, int64_t N, int64_t K) {
+  return M > 0 && N > 0 && K > 0 ? galv::gemm_pick_splits(M, N, K) : 1;
+}
+
+int32_t galv_gemm_splitk(const void* A, const void* B, void* C, const void* bias, int64_t M,
+                         int64_t N, int64_t K, int64_t lda, int64_t ldb, int64_t ldc,
+                         int32_t trans_a, int32_t trans_b, float alpha, int32_t accumulate,
+                         int32_t c_dtype, int32_t bias_dtype, int32_t splits, void* ws,
+                         int64_t ws_bytes, void* stream) {
+  GALV_CHECK_ARG(A && B && C && splits >= 1, "bad arguments");
+  GALV_CHECK_ARG(c_dtype == GALV_F32 || c_dtype == GALV_BF16, "bad c_dtype");
+  GALV_CHECK_ARG(splits == 1 || (ws != nullptr && ws_bytes >= (int64_t)splits * M * N * 4 &&
+                                 (reinterpret_cast<uintptr_t>(ws) & 15) == 0),
+                 "split-K workspace must hold splits*M*N fp32 (16-byte aligned)");
+  return galv::gemm_bf16_sm100(A, B, C, bias, M, N, K, lda, ldb, ldc, trans_a, trans_b, alpha,
+                               accumulate, c_dtype, bias_dtype, galv::as_stream(stream), nullptr,
+                               0, 0, 0, nullptr, 0, 0, splits, static_cast<float*>(ws));
 }
 
 int32_t galv_gemm_batched(const void* A, const void* B, void* C, int64_t batch, int64_t sa,

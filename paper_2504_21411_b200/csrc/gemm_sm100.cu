@@ -10,6 +10,7 @@
 // forward (X W^T), dgrad (dY W) and wgrad (dY^T X) without transposes.
 #include <cuda.h>
 #include <cstdio>
+#include <algorithm>
 #include <cstdlib>
 #include <mutex>
 
@@ -51,6 +52,10 @@ struct Params {
   int epi, ff;
   const void* aux;
   long long aux_ld;
+  // split-K (2-CTA path): work unit u = tile (u % num_tiles) x K-split (u / num_tiles), each
+  // split covering kb_per k-blocks; partial fp32 tiles go to ws[split][M][N]
+  int splits, kb_per, num_units;
+  float* ws;
 };
 
 __device__ __forceinline__ void tile_coords(const Params& p, int t, int& mt, int& nt) {
@@ -734,12 +739,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     int stage = 0;
     uint32_t phase = 0;
     const uint64_t pol = l2_evict_last();
-    for (int t = pair; t < p.num_tiles; t += npairs) {
+    for (int u = pair; u < p.num_units; u += npairs) {
       int mt, nt;
-      tile_coords2(p, t, mt, nt);
+      tile_coords2(p, u % p.num_tiles, mt, nt);
+      const int kb0 = (u / p.num_tiles) * p.kb_per, kb1 = min(p.k_blocks, kb0 + p.kb_per);
       const int m0 = mt * 256 + (int)cr * 128;
       const int n0 = p.epi == 2 ? (cr == 0 ? nt * 128 : p.ff + nt * 128) : nt * 256 + (int)cr * 128;
-      for (int kb = 0; kb < p.k_blocks; ++kb) {
+      for (int kb = kb0; kb < kb1; ++kb) {
         mbar_wait(&empty[stage], phase ^ 1);
         if (elect_one()) {
           if (cr == 0) mbar_expect_tx(&full[stage], 4 * HALF_STAGE);
@@ -792,18 +798,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       constexpr uint64_t STG = HALF_STAGE >> 4;
       int stage = 0, acc = 0;
       uint32_t phase = 0, acc_phase = 0;
-      for (int t = pair; t < p.num_tiles; t += npairs) {
+      for (int u = pair; u < p.num_units; u += npairs) {
+        const int kb0 = (u / p.num_tiles) * p.kb_per, kb1 = min(p.k_blocks, kb0 + p.kb_per);
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d = tmem + acc * BN;
-        for (int kb = 0; kb < p.k_blocks; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint64_t ad = a0 + (uint64_t)stage * STG, bd = b0 + (uint64_t)stage * STG;
           if (elect_one()) {
 #pragma unroll
             for (int k = 0; k < BK / 16; ++k)
-              umma_bf16_2sm(d, ad + k * a_k, bd + k * b_k, idesc, (kb | k) != 0);
+              umma_bf16_2sm(d, ad + k * a_k, bd + k * b_k, idesc, (kb > kb0) || (k > 0));
             umma_commit_2sm(&empty[stage], 0x3);
           }
           __syncwarp();
@@ -824,9 +831,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     const int q = warp & 3;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = pair; t < p.num_tiles; t += npairs) {
+    for (int u = pair; u < p.num_units; u += npairs) {
       int mt, nt;
-      tile_coords2(p, t, mt, nt);
+      tile_coords2(p, u % p.num_tiles, mt, nt);
       if (p.hint & 8) mbar_wait(&tfull[acc], acc_phase);
       else mbar_wait_sleep(&tfull[acc], acc_phase, 512);
       tc_fence_after();
@@ -850,7 +857,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
         epilogue_bias_gelu_bwd(p, tmem + acc * BN + ((uint32_t)(q * 32) << 16),
                                mt * 256 + (int)cr * 128 + q * 32, nt * BN,
                                staging + q * 32 * Cfg2<false>::STAGE_PITCH);
-      else
+      else if (p.splits > 1) {  // fp32 partial tile of this K-split -> workspace
+        Params w = p;
+        w.C = p.ws + (long long)(u / p.num_tiles) * p.M * p.N;
+        w.ldc = p.N;
+        w.c_bf16 = 0;
+        w.accumulate = 0;
+        w.bias = nullptr;
+        w.alpha = 1.f;
+        epilogue_staged<false>(w, tmem + acc * BN + ((uint32_t)(q * 32) << 16),
+                               mt * 256 + (int)cr * 128 + q * 32, nt * BN,
+                               staging + q * 32 * Cfg2<false>::STAGE_PITCH);
+      } else
         epilogue_staged<false>(p, tmem + acc * BN + ((uint32_t)(q * 32) << 16),
                                mt * 256 + (int)cr * 128 + q * 32, nt * BN,
                                staging + q * 32 * Cfg2<false>::STAGE_PITCH);
@@ -867,6 +885,41 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc_2sm(tmem, TMEM_COLS);
+  }
+}
+
+// split-K reduction: C[m, n] (+)= alpha * sum_s ws[s][m][n] (+ bias[n]), 4 columns/thread
+__global__ void splitk_reduce(const float* __restrict__ ws, int splits, int M, int N, void* C,
+                              long long ldc, int c_bf16, float alpha, const void* bias,
+                              int bias_bf16, int accumulate) {
+  const long long n4 = N / 4, total = (long long)M * n4;
+  const long long MN = (long long)M * N;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int row = (int)(i / n4), col = (int)(i - (long long)row * n4) * 4;
+    const long long src = (long long)row * N + col;
+    float4 a = *reinterpret_cast<const float4*>(ws + src);
+    for (int s = 1; s < splits; ++s) {
+      const float4 b = *reinterpret_cast<const float4*>(ws + s * MN + src);
+      a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+    }
+    float v[4] = {a.x * alpha, a.y * alpha, a.z * alpha, a.w * alpha};
+    if (bias) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        v[e] += bias_bf16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(bias)[col + e])
+                          : reinterpret_cast<const float*>(bias)[col + e];
+    }
+    const long long dst = (long long)row * ldc + col;
+    if (c_bf16) {
+      __nv_bfloat16* c = reinterpret_cast<__nv_bfloat16*>(C) + dst;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) c[e] = __float2bfloat16_rn(v[e] + (accumulate ? __bfloat162float(c[e]) : 0.f));
+    } else {
+      float* c = reinterpret_cast<float*>(C) + dst;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) c[e] = v[e] + (accumulate ? c[e] : 0.f);
+    }
   }
 }
 
@@ -908,6 +961,32 @@ static bool make_map(CUtensorMap* map, const void* base, uint64_t inner, uint64_
 
 }  // namespace tc
 
+// K-split count for the 2-CTA path: minimise waves x k-blocks per unit (one k-block of a
+// 256x256 pair tile ~ 0.35 us) plus the fp32 partial round trip through HBM and one extra
+// launch; small-output / long-K GEMMs (wgrad of narrow layers) fill 74 pairs this way
+int32_t gemm_pick_splits(int64_t M, int64_t N, int64_t K) {
+  if (M <= 128 || N % 4 != 0) return 1;
+  const int64_t pairs = sm_count() / 2;
+  const int64_t tiles = ((M + 255) / 256) * ((N + 255) / 256), kb = (K + tc::BK - 1) / tc::BK;
+  auto cost = [&](int64_t s) {
+    const int64_t kbs = (kb + s - 1) / s, units = tiles * ((kb + kbs - 1) / kbs);
+    double t = (double)((units + pairs - 1) / pairs) * kbs * 0.35e-6;
+    if (s > 1) t += (double)M * N * 4.0 * (s + 1) / 6.0e12 + 4e-6;
+    return t;
+  };
+  int32_t best = 1;
+  double best_t = cost(1);
+  for (int64_t s = 2; s <= 16; ++s) {
+    if (kb / s < 8) break;
+    const double t = cost(s);
+    if (t < 0.9 * best_t) {
+      best = (int32_t)s;
+      best_t = t;
+    }
+  }
+  return best;
+}
+
 // the fused SwiGLU epilogues need the 2-CTA path (M > 128, 16-byte aligned rows) and
 // 8-element aligned gate/up/h rows; epi 2 also needs the nn.Linear (K-major) weight
 bool swiglu_fusable(const void* A, const void* B, const void* C, const void* aux, int64_t M,
@@ -922,7 +1001,8 @@ int32_t gemm_bf16_sm100(const void* A, const void* B, void* C, const void* bias,
                         int32_t trans_a, int32_t trans_b, float alpha, int32_t accumulate,
                         int32_t c_dtype, int32_t bias_dtype, cudaStream_t stream,
                         void* const* peer_c, int64_t rows_per_rank, int32_t my_slot,
-                        int32_t epi, const void* aux, int64_t aux_ld, int64_t ff) {
+                        int32_t epi, const void* aux, int64_t aux_ld, int64_t ff,
+                        int32_t splits, float* ws) {
   using namespace tc;
   GALV_CHECK_ARG(M > 0 && N > 0 && K > 0, "empty problem");
   GALV_CHECK_ARG(M < (1ll << 31) && N < (1ll << 31) && K < (1ll << 31), "problem too large");
@@ -952,10 +1032,14 @@ int32_t gemm_bf16_sm100(const void* A, const void* B, void* C, const void* bias,
   p.tiles_m = (int)((M + BM - 1) / BM);
   p.tiles_n = (int)((N + BN - 1) / BN);
   p.num_tiles = p.tiles_m * p.tiles_n;
+  p.num_units = p.num_tiles;
   p.k_blocks = (int)((K + BK - 1) / BK);
   p.peer_c = peer_c;
   p.rows_per_rank = (int)rows_per_rank;
   p.my_slot = my_slot;
+  p.splits = 1;
+  p.kb_per = (int)((K + BK - 1) / BK);
+  p.ws = nullptr;
   p.epi = epi;
   p.aux = aux;
   p.aux_ld = aux_ld;
@@ -995,6 +1079,11 @@ int32_t gemm_bf16_sm100(const void* A, const void* B, void* C, const void* bias,
     p2.tiles_m = (int)((M + 255) / 256);
     if (epi == 2) p2.tiles_n = (int)((ff + 127) / 128);  // pair tile = 128 gate + 128 up cols
     p2.num_tiles = p2.tiles_m * p2.tiles_n;
+    const bool split = splits > 1 && ws != nullptr && epi == 0 && peer_c == nullptr && N % 4 == 0;
+    p2.kb_per = split ? (p.k_blocks + splits - 1) / splits : p.k_blocks;
+    p2.splits = split ? (p.k_blocks + p2.kb_per - 1) / p2.kb_per : 1;
+    p2.num_units = p2.num_tiles * p2.splits;
+    p2.ws = split ? ws : nullptr;
     static bool attr2 = false;
     if (!attr2) {
       GALV_CUDA_RET(cudaFuncSetAttribute(gemm_bf16_tc2<false>,
@@ -1005,12 +1094,20 @@ int32_t gemm_bf16_sm100(const void* A, const void* B, void* C, const void* bias,
                                          Cfg2<true>::SMEM));
       attr2 = true;
     }
-    const int pairs = min(p2.num_tiles, sm_count() / 2);
+    const int pairs = min(p2.num_units, sm_count() / 2);
     if (peer_c != nullptr)
       gemm_bf16_tc2<true><<<2 * pairs, 256, Cfg2<true>::SMEM, stream>>>(ma2, mb2, p2);
     else
       gemm_bf16_tc2<false><<<2 * pairs, 256, Cfg2<false>::SMEM, stream>>>(ma2, mb2, p2);
     GALV_LAUNCH_CHECK();
+    if (p2.splits > 1) {
+      const long long work = M * (N / 4);
+      const int blocks = (int)std::min<long long>((work + 255) / 256, (long long)sm_count() * 8);
+      splitk_reduce<<<blocks, 256, 0, stream>>>(ws, p2.splits, (int)M, (int)N, C, ldc,
+                                                c_dtype == GALV_BF16, alpha, bias,
+                                                bias_dtype == GALV_BF16, accumulate);
+      GALV_LAUNCH_CHECK();
+    }
     return 0;
   }
   const int grid = min(p.num_tiles, sm_count());
@@ -1029,5 +1126,5 @@ extern "C" int32_t galv_gemm_rs(const void* A, const void* B, void* const* peer_
                  "bad arguments");
   return galv::gemm_bf16_sm100(A, B, nullptr, nullptr, M, N, K, lda, ldb, ldc, trans_a, trans_b,
                                1.0f, 0, GALV_BF16, GALV_F32, galv::as_stream(stream), peer_c,
-                               rows_per_rank, my_slot, 0, nullptr, 0, 0);
+                               rows_per_rank, my_slot, 0, nullptr, 0, 0, 1, nullptr);
 }

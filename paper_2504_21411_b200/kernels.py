@@ -28,6 +28,9 @@ _SIGS = {
     "galv_device_info": ([_P, _P, _P], _I32),
     "galv_gemm": ([_P, _P, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I32, _I32, _F, _I32,
                    _I32, _I32, _I32, _P], _I32),
+    "galv_gemm_splits": ([_I64, _I64, _I64], _I32),
+    "galv_gemm_splitk": ([_P, _P, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I32, _I32, _F,
+                          _I32, _I32, _I32, _I32, _P, _I64, _P], _I32),
     "galv_gemm_batched": ([_P, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _I64,
                            _I64, _I32, _I32, _F, _I32, _I32, _I32, _P], _I32),
     "galv_gemm_rs": ([_P, _P, _P, _I64, _I32, _I64, _I64, _I64, _I64, _I64, _I64, _I32, _I32,
@@ -186,6 +189,16 @@ def dtype_code(dt) -> int:
 # ---------------------------------------------------------------------------- GEMM
 
 
+_SPLITS: dict = {}
+
+
+def _gemm_splits(M, N, K) -> int:
+    key = (M, N, K)
+    if key not in _SPLITS:
+        _SPLITS[key] = int(load_library().galv_gemm_splits(M, N, K))
+    return _SPLITS[key]
+
+
 def gemm(a, b, out=None, *, trans_a=False, trans_b=False, alpha=1.0, accumulate=False,
          bias=None, out_dtype=None):
     """out[M,N] (+)= alpha * op(a) @ op(b) (+ bias).
@@ -212,10 +225,19 @@ def gemm(a, b, out=None, *, trans_a=False, trans_b=False, alpha=1.0, accumulate=
     if timed:
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev0.record()
-    _call("galv_gemm", _ptr(a), _ptr(b), _ptr(out), _ptr(bias), M, N, K, a.stride(0),
-          b.stride(0), out.stride(0), int(trans_a), int(trans_b), float(alpha),
-          int(accumulate), dtype_code(a.dtype), dtype_code(out.dtype),
-          dtype_code(bias.dtype) if bias is not None else F32, _stream())
+    splits = _gemm_splits(M, N, K) if a.dtype == torch.bfloat16 else 1
+    if splits > 1:  # narrow output, long K: K-split units + one fp32 reduction pass
+        ws = torch.empty(splits * M * N, device=a.device, dtype=torch.float32)
+        _call("galv_gemm_splitk", _ptr(a), _ptr(b), _ptr(out), _ptr(bias), M, N, K,
+              a.stride(0), b.stride(0), out.stride(0), int(trans_a), int(trans_b),
+              float(alpha), int(accumulate), dtype_code(out.dtype),
+              dtype_code(bias.dtype) if bias is not None else F32, splits, _ptr(ws),
+              ws.numel() * 4, _stream())
+    else:
+        _call("galv_gemm", _ptr(a), _ptr(b), _ptr(out), _ptr(bias), M, N, K, a.stride(0),
+              b.stride(0), out.stride(0), int(trans_a), int(trans_b), float(alpha),
+              int(accumulate), dtype_code(a.dtype), dtype_code(out.dtype),
+              dtype_code(bias.dtype) if bias is not None else F32, _stream())
     if timed:
         ev1.record()
         _stats.gemm_events.append((2.0 * M * N * K, ev0, ev1, (M, N, K)))

@@ -12,6 +12,7 @@ The measured per-op timeline can be exported in the simulator's JSONL trace sche
 
 from __future__ import annotations
 
+import os
 import time
 from dataclasses import dataclass
 
@@ -290,6 +291,12 @@ class HybridParallelModel:
         the next step's forward of layers < i (each store's next use waits on its event)."""
         self.step_count += 1
         o = self.optim
+        if os.environ.get("GALV_OPT_SIDE_STREAM", "1") == "0":  # A/B: serial optimizer
+            for _, store, _ in self.stores():
+                store.step(lr=o.lr, beta1=o.beta1, beta2=o.beta2, eps=o.eps,
+                           weight_decay=o.weight_decay, step=self.step_count)
+                store.zero_grads()
+            return
         if self._opt_stream is None:
             self._opt_stream = torch.cuda.Stream(device=self.device)
         done = torch.cuda.Event()
