@@ -30,7 +30,7 @@ int32_t gemm_bf16_sm100(const void* A, const void* B, void* C, const void* bias,
                         int64_t aux_ld = 0, int64_t ff = 0, int32_t splits = 1,
                         float* ws = nullptr);
 int32_t gemm_pick_splits(int64_t M, int64_t N, int64_t K);
-bool swiglu_fusable(const void* A, const void* B, const void* C, const void* aux, int64_t M,
+bool epilogue_fusable(const void* A, const void* B, const void* C, const void* aux, int64_t M,
                     int64_t ldc, int64_t aux_ld, int64_t ff, int32_t trans_b, int32_t epi);
 int32_t gemm_f32_simt(const float* A, const float* B, void* C, const float* bias, int64_t batch,
                       int64_t sa, int64_t sb, int64_t sc, int64_t M, int64_t N, int64_t K,
@@ -123,7 +123,7 @@ int32_t galv_gemm_swiglu_fwd(const void* X, const void* Wgu, void* gu, void* h, 
                              int64_t ld_h, void* stream) {
   GALV_CHECK_ARG(X && Wgu && gu && h && M > 0 && F > 0 && K > 0 && F % 8 == 0, "bad arguments");
   GALV_CHECK_ARG(ld_gu == 2 * F && ld_h == F, "gate|up and h must be dense [M,2F] / [M,F]");
-  if (galv::swiglu_fusable(X, Wgu, gu, h, M, ld_gu, ld_h, F, 1, 2))
+  if (galv::epilogue_fusable(X, Wgu, gu, h, M, ld_gu, ld_h, F, 1, 2))
     return galv::gemm_bf16_sm100(X, Wgu, gu, nullptr, M, 2 * F, K, ldx, ldw, ld_gu, 0, 1, 1.0f, 0,
                                  GALV_BF16, GALV_F32, galv::as_stream(stream), nullptr, 0, 0, 2, h,
                                  ld_h, F);
@@ -141,7 +141,7 @@ int32_t galv_gemm_swiglu_bwd(const void* dY, const void* Wdown, const void* gu, 
   GALV_CHECK_ARG(dY && Wdown && gu && dgu && M > 0 && F > 0 && K > 0 && F % 8 == 0,
                  "bad arguments");
   GALV_CHECK_ARG(ld_gu == 2 * F && ld_dgu == 2 * F, "gate|up tensors must be dense [M,2F]");
-  if (galv::swiglu_fusable(dY, Wdown, dgu, gu, M, ld_dgu, ld_gu, F, 0, 1))
+  if (galv::epilogue_fusable(dY, Wdown, dgu, gu, M, ld_dgu, ld_gu, F, 0, 1))
     return galv::gemm_bf16_sm100(dY, Wdown, dgu, nullptr, M, F, K, ldy, ldw, ld_dgu, 0, 0, 1.0f, 0,
                                  GALV_BF16, GALV_F32, galv::as_stream(stream), nullptr, 0, 0, 1, gu,
                                  ld_gu, F);
@@ -160,7 +160,7 @@ int32_t galv_gemm_bias_gelu_fwd(const void* X, const void* W1, const void* bias,
   GALV_CHECK_ARG(X && W1 && pre && act && M > 0 && F > 0 && K > 0 && F % 8 == 0,
                  "bad arguments");
   GALV_CHECK_ARG(bias_dtype == GALV_BF16 || bias_dtype == GALV_F32, "bad bias dtype");
-  if (galv::swiglu_fusable(X, W1, pre, act, M, ld_pre, ld_act, F, 1, 3))
+  if (galv::epilogue_fusable(X, W1, pre, act, M, ld_pre, ld_act, F, 1, 3))
     return galv::gemm_bf16_sm100(X, W1, pre, bias, M, F, K, ldx, ldw, ld_pre, 0, 1, 1.0f, 0,
                                  GALV_BF16, bias_dtype, galv::as_stream(stream), nullptr, 0, 0, 3,
                                  act, ld_act, F);
@@ -181,7 +181,7 @@ int32_t galv_gemm_bias_gelu_bwd(const void* dY, const void* W2, const void* pre,
   GALV_CHECK_ARG(dY && W2 && pre && dpre && M > 0 && F > 0 && K > 0 && F % 8 == 0,
                  "bad arguments");
   GALV_CHECK_ARG(bias_dtype == GALV_BF16 || bias_dtype == GALV_F32, "bad bias dtype");
-  if (galv::swiglu_fusable(dY, W2, dpre, pre, M, ld_dpre, ld_pre, F, 0, 4))
+  if (galv::epilogue_fusable(dY, W2, dpre, pre, M, ld_dpre, ld_pre, F, 0, 4))
     return galv::gemm_bf16_sm100(dY, W2, dpre, bias, M, F, K, ldy, ldw, ld_dpre, 0, 0, 1.0f, 0,
                                  GALV_BF16, bias_dtype, galv::as_stream(stream), nullptr, 0, 0, 4,
                                  pre, ld_pre, F);

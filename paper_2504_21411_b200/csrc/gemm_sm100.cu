@@ -987,9 +987,9 @@ int32_t gemm_pick_splits(int64_t M, int64_t N, int64_t K) {
   return best;
 }
 
-// the fused SwiGLU epilogues need the 2-CTA path (M > 128, 16-byte aligned rows) and
+// the fused activation epilogues (SwiGLU / bias-GeLU) need the 2-CTA path (M > 128, 16-byte aligned rows) and
 // 8-element aligned gate/up/h rows; epi 2 also needs the nn.Linear (K-major) weight
-bool swiglu_fusable(const void* A, const void* B, const void* C, const void* aux, int64_t M,
+bool epilogue_fusable(const void* A, const void* B, const void* C, const void* aux, int64_t M,
                     int64_t ldc, int64_t aux_ld, int64_t ff, int32_t trans_b, int32_t epi) {
   auto al = [](const void* x) { return (reinterpret_cast<uintptr_t>(x) & 15) == 0; };
   return M > 128 && al(A) && al(B) && al(C) && al(aux) && ldc % 8 == 0 && aux_ld % 8 == 0 &&
@@ -1064,7 +1064,7 @@ int32_t gemm_bf16_sm100(const void* A, const void* B, void* C, const void* bias,
   const bool c_aligned = (ldc % 8) == 0 &&
                          ((reinterpret_cast<uintptr_t>(C) & 15) == 0 || peer_c != nullptr);
   if (epi != 0) {  // fused SwiGLU epilogues exist on the 2-CTA path only (callers check)
-    GALV_CHECK_ARG(swiglu_fusable(A, B, C, aux, M, ldc, aux_ld, ff, trans_b, epi) &&
+    GALV_CHECK_ARG(epilogue_fusable(A, B, C, aux, M, ldc, aux_ld, ff, trans_b, epi) &&
                        peer_c == nullptr && (bias == nullptr || epi >= 3) && !accumulate &&
                        c_dtype == GALV_BF16 && alpha == 1.0f,
                    "fused activation epilogue: unsupported operands");
