@@ -359,13 +359,15 @@ def main():
     # DRAM traffic of the dominant kernel from the committed ncu --set full capture
     traffic = None
     try:
-        with open(os.path.join(ROOT, "profiles", "r01", "ncu_full_summary_latest.json")) as fh:
-            cap = json.load(fh)["gemm_2cta_8192x22016x4096"][0]
+        with open(os.path.join(ROOT, "profiles", "r01", "ncu_full_summary_final.json")) as fh:
+            cap = json.load(fh)[0]  # gate|up GEMM + fused SwiGLU, the step's largest launch
         rd = float(cap["dram__bytes_read.sum"].split()[0]) * 1e6
         wr = float(cap["dram__bytes_write.sum"].split()[0]) * 1e6
-        traffic = {"bytes_per_launch": rd + wr, "shape": "8192x22016x4096 (gate|up fwd, mb2)",
-                   "algorithmic_bytes": 2 * (8192 * 4096 + 22016 * 4096 + 8192 * 22016),
-                   "source": "profiles/r01/gemm_2cta_gate_up_fwd.ncu-rep"}
+        traffic = {"bytes_per_launch": rd + wr,
+                   "shape": "8192x22016x4096 gate|up fwd + SwiGLU epilogue (mb2)",
+                   "algorithmic_bytes": 2 * (8192 * 4096 + 22016 * 4096 + 8192 * 22016
+                                             + 8192 * 11008),
+                   "source": "profiles/r01/final_kernels.ncu-rep (launch 0)"}
     except (OSError, KeyError, ValueError, IndexError):
         pass
     flops_tok = cfg.train_flops_per_token()

@@ -690,6 +690,43 @@ __device__ __forceinline__ void epilogue_bias_gelu_bwd(const Params& p, uint32_t
   }
 }
 
+// plain bf16 epilogue (alpha only: no bias, no accumulate): TMEM -> bf16 pairs -> smem
+// (128 columns = 256 bytes per row) -> 16-byte coalesced row-segment stores.  Half the
+// staging bytes and no conversions in the store loop compared with the fp32 staging.
+__device__ __forceinline__ void epilogue_bf16(const Params& p, uint32_t taddr, int row0,
+                                              int col_base, uint8_t* stage) {
+  const int lane = threadIdx.x & 31;
+  __nv_bfloat16* C = reinterpret_cast<__nv_bfloat16*>(p.C);
+  uint8_t* srow = stage + lane * SW_PITCH;
+#pragma unroll 1
+  for (int h = 0; h < 2; ++h) {
+#pragma unroll
+    for (int cc = 0; cc < 4; ++cc) {
+      uint32_t r[32];
+      tmem_ld32(taddr + h * 128 + cc * 32, r);
+      uint32_t w[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        w[i] = pack2(__uint_as_float(r[2 * i]) * p.alpha, __uint_as_float(r[2 * i + 1]) * p.alpha);
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        *reinterpret_cast<uint4*>(srow + cc * 64 + u * 16) =
+            make_uint4(w[4 * u], w[4 * u + 1], w[4 * u + 2], w[4 * u + 3]);
+    }
+    __syncwarp();
+    const int colq = col_base + h * 128;
+#pragma unroll 4
+    for (int it = 0; it < 16; ++it) {  // 32 rows x 16 units of 16 bytes
+      const int u = it * 32 + lane, rr = u >> 4, part = u & 15;
+      const int row = row0 + rr, col = colq + part * 8;
+      if (row < p.M && col < p.N)
+        *reinterpret_cast<uint4*>(C + (long long)row * p.ldc + col) =
+            *reinterpret_cast<const uint4*>(stage + rr * SW_PITCH + part * 16);
+    }
+    __syncwarp();
+  }
+}
+
 __device__ __forceinline__ void tile_coords2(const Params& p, int t, int& mt, int& nt) {
   tile_coords(p, t, mt, nt);  // pair tiles are 256 x 256; p.tiles_m counts 256-row tiles
 }
@@ -868,7 +905,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
         epilogue_staged<false>(w, tmem + acc * BN + ((uint32_t)(q * 32) << 16),
                                mt * 256 + (int)cr * 128 + q * 32, nt * BN,
                                staging + q * 32 * Cfg2<false>::STAGE_PITCH);
-      } else
+      } else if (p.c_bf16 && p.bias == nullptr && !p.accumulate && !(p.hint & 32))
+        epilogue_bf16(p, tmem + acc * BN + ((uint32_t)(q * 32) << 16),
+                      mt * 256 + (int)cr * 128 + q * 32, nt * BN,
+                      staging + q * 32 * Cfg2<false>::STAGE_PITCH);
+      else
         epilogue_staged<false>(p, tmem + acc * BN + ((uint32_t)(q * 32) << 16),
                                mt * 256 + (int)cr * 128 + q * 32, nt * BN,
                                staging + q * 32 * Cfg2<false>::STAGE_PITCH);
