@@ -147,13 +147,15 @@ def cluster_profile(n: int, path: str):
 
 def model_profile(cfg):
     """Planner ModelProfile: the profiler's activation-calibrated one when committed
-    (profiles/b200_model_<name>.json, `profiler --model-out`), else the analytic one."""
+    (profiles/b200_model_<name>.json, `profiler --model-out`), else the analytic one;
+    both carry the embedding/head folded into the first/last layer
+    (profiler.fold_embedding_head)."""
     from paper_2504_21411_b200.planner.profiles import load_model_profile
-    from paper_2504_21411_b200.runtime.config import profile_for
+    from paper_2504_21411_b200.profiler import planned_profile
     path = os.path.join(ROOT, "profiles", f"b200_model_{cfg.name}.json")
     if os.path.exists(path):
         return load_model_profile(path)
-    return profile_for(cfg)
+    return planned_profile(cfg)
 
 
 def plan_for(cfg, n: int, global_batch: int, cluster):
@@ -396,7 +398,7 @@ def main():
         "model_profile": ("profiles/b200_model_%s.json (activation-calibrated)" % cfg.name
                           if os.path.exists(os.path.join(ROOT, "profiles",
                                                          "b200_model_%s.json" % cfg.name))
-                          else "analytic (runtime.config.profile_for)"),
+                          else "analytic (profiler.planned_profile: profile_for + embedding/head fold)"),
         "roofline": {"bound": "tensor", "kernel": "galv tcgen05 GEMM (all shapes of the step)",
                      "achieved": gemm["tflops"], "peak": peak_tf, "unit": "TFLOP/s",
                      "frac": gemm["tflops"] / peak_tf if peak_tf else None,

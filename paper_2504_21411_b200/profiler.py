@@ -129,6 +129,44 @@ def measure_activation_bytes(cfg, microbatch: int) -> dict:
             "bytes_per_token_recompute": out["recompute"], "microbatch": microbatch}
 
 
+def fold_embedding_head(prof: P.ModelProfile, cfg) -> P.ModelProfile:
+    """Charge the embedding and the LM head to the planned layers that share their
+    strategy (the runtime builds them on layer 0's / layer L-1's tp and dp groups,
+    runtime/engine.py): layer 0 gains the embedding tables' parameters, layer L-1 the
+    head's parameters and its 2*h*V forward FLOPs per token (backward = 2x fwd by
+    costmodel.py:106, i.e. the dgrad + wgrad GEMMs).  The reference has no
+    embedding/head layers, so without this the cost model under-predicts
+    by the head's share of the step (13% on GPT-2-medium, 9% on GPT-1.3B) and the
+    memory prediction misses 16 B/param of vocab tables.  Approximation: the tables
+    are dp-replicated (z0) in the runtime but inherit the layer's zero stage here."""
+    L, h, V = cfg.n_layers, cfg.hidden, cfg.vocab
+    emb = V * h + (cfg.seq_len * h if cfg.arch == "gpt" else 0)
+    head = V * h + h * (2 if cfg.arch == "gpt" else 1)
+    layers = list(prof.layers)
+
+    def bump(lp, params, fpt):
+        return P.LayerProfile(
+            param_count=lp.param_count + params, flops_per_token=lp.flops_per_token + fpt,
+            flops_per_token_sq=lp.flops_per_token_sq,
+            act_shardable_bytes_per_token=lp.act_shardable_bytes_per_token,
+            act_replicated_bytes_per_token=lp.act_replicated_bytes_per_token,
+            boundary_bytes_per_token=lp.boundary_bytes_per_token)
+
+    layers[0] = bump(layers[0], emb, 0)
+    layers[L - 1] = bump(layers[L - 1], head, 2 * h * V)
+    out = P.ModelProfile(n_layers=prof.n_layers, hidden_size=prof.hidden_size,
+                         seq_len=prof.seq_len, layers=tuple(layers))
+    out.validate()
+    return out
+
+
+def planned_profile(cfg) -> P.ModelProfile:
+    """Analytic decoder-layer profile with the embedding/head folded in (fallback when
+    no activation-calibrated profile was measured for ``cfg``)."""
+    from .runtime.config import profile_for
+    return fold_embedding_head(profile_for(cfg), cfg)
+
+
 def calibrated_model_profile(cfg, act: dict) -> P.ModelProfile:
     """The analytic profile with its activation coefficients scaled to the measured bytes:
     shardable/replicated keep their analytic split; boundary = the recompute residue."""
@@ -147,7 +185,7 @@ def calibrated_model_profile(cfg, act: dict) -> P.ModelProfile:
     prof = P.ModelProfile(n_layers=base.n_layers, hidden_size=base.hidden_size,
                           seq_len=base.seq_len, layers=(layer,) * base.n_layers)
     prof.validate()
-    return prof
+    return fold_embedding_head(prof, cfg)
 
 
 def measure_collectives(sizes=(2 ** 20, 2 ** 24, 2 ** 28)) -> dict:

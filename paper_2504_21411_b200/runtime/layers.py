@@ -304,11 +304,11 @@ class DecoderLayer:
             T = qkv.shape[0]
         q, k, v = self._attn_views(qkv, B, S)
         if not gpt:
-            for j in (0, 1):
-                K.rope_(qkv.as_strided((T, self.Hl, cfg.head_dim),
-                                       (qkv.stride(0), cfg.head_dim, 1),
-                                       qkv.storage_offset() + j * self.ahl),
-                        S, theta=cfg.rope_theta)
+            # q and k heads are adjacent in the qkv row ([q | k | v], ahl = Hl*D each):
+            # one launch rotates all 2*Hl of them
+            K.rope_(qkv.as_strided((T, 2 * self.Hl, cfg.head_dim),
+                                   (qkv.stride(0), cfg.head_dim, 1), qkv.storage_offset()),
+                    S, theta=cfg.rope_theta)
         o = torch.empty(T, self.ahl, device=x.device, dtype=x.dtype)
         lse = torch.empty(B, self.Hl, S, device=x.device, dtype=torch.float32)
         K.attn_fwd(q, k, v, o.view(B, S, self.Hl, cfg.head_dim), lse, scale=self.scale,
@@ -425,11 +425,9 @@ class DecoderLayer:
                    scale=self.scale, causal=True, workspace=self._ws)
         del do
         if not gpt:
-            for j in (0, 1):
-                K.rope_(dqkv.as_strided((T, self.Hl, cfg.head_dim),
-                                        (dqkv.stride(0), cfg.head_dim, 1),
-                                        dqkv.storage_offset() + j * self.ahl),
-                        S, theta=cfg.rope_theta, inverse=True)
+            K.rope_(dqkv.as_strided((T, 2 * self.Hl, cfg.head_dim),
+                                    (dqkv.stride(0), cfg.head_dim, 1), dqkv.storage_offset()),
+                    S, theta=cfg.rope_theta, inverse=True)
         if self.uly:
             dqkv = self._uly_heads_to_qkv(dqkv)
         if gpt:

@@ -149,3 +149,31 @@ def test_1f1b_order_is_complete_and_causal(pp, m):
                 assert k in seen_f
                 live -= 1
             assert live <= min(m, pp - stage)
+
+
+@pytest.mark.parametrize("name", ["tiny-gpt", "gpt2-medium", "gpt-1.3b", "llama2-7b", "llama2-13b"])
+def test_embedding_head_fold_accounts_for_the_whole_model(name):
+    """profiler.fold_embedding_head: the planned layers' parameters sum to the model's,
+    and the cost model's training FLOPs per token (3x fwd, costmodel.py:104-106) equal
+    the model's 6*L*P + 12*L*h*s + 6*h*V."""
+    from paper_2504_21411_b200.profiler import planned_profile
+    from paper_2504_21411_b200.runtime.config import MODEL_PRESETS, profile_for
+    cfg = MODEL_PRESETS[name]
+    prof = planned_profile(cfg)
+    assert sum(lp.param_count for lp in prof.layers) == cfg.total_params()
+    fwd = sum(lp.flops_per_token + lp.flops_per_token_sq * cfg.seq_len for lp in prof.layers)
+    assert 3.0 * fwd == pytest.approx(cfg.train_flops_per_token(), rel=1e-12)
+    base = profile_for(cfg)
+    assert prof.layers[1:-1] == base.layers[1:-1]
+
+
+@pytest.mark.parametrize("name", ["gpt2-medium", "llama2-7b", "llama2-13b"])
+def test_committed_model_profiles_carry_the_fold(name):
+    import json
+    from paper_2504_21411_b200.planner.profiles import load_model_profile
+    from paper_2504_21411_b200.profiler import calibrated_model_profile
+    from paper_2504_21411_b200.runtime.config import MODEL_PRESETS
+    meta = json.loads((ROOT / "profiles" / f"b200_model_{name}.meta.json").read_text())
+    prof = load_model_profile(str(ROOT / "profiles" / f"b200_model_{name}.json"))
+    assert prof == calibrated_model_profile(MODEL_PRESETS[name], meta["activation"])
+    assert sum(lp.param_count for lp in prof.layers) == MODEL_PRESETS[name].total_params()
