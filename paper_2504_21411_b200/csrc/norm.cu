@@ -10,6 +10,15 @@ namespace norm {
 
 constexpr int WARPS = 8;
 
+// GALV_NORM_UNFUSED=1 selects the two-kernel backward (dx pass, then dgamma pass) for A/B.
+static bool fused_disabled() {
+  static const bool off = [] {
+    const char* e = getenv("GALV_NORM_UNFUSED");
+    return e && e[0] == '1';
+  }();
+  return off;
+}
+
 template <typename T, bool LAYER, bool RESID>
 __global__ void __launch_bounds__(WARPS * 32) fwd_kernel(
     const T* __restrict__ x, const T* __restrict__ res, T* __restrict__ res_out,
@@ -189,6 +198,172 @@ __global__ void __launch_bounds__(128) bwd_dx_row(
   }
 }
 
+// Fused dx + dgamma(/dbeta): persistent 128-thread CTAs stride over rows; every thread owns
+// the same NV column vectors in every row, so its dgamma partials stay in registers across
+// rows and x / dy are read from HBM exactly once per backward (the dx-then-dgamma pair
+// above reads them twice).  The partials live in shared memory (each column is owned by
+// exactly one thread of the CTA, so plain read-modify-write, no atomics) to leave the
+// registers to the in-flight x / dy vectors, and are flushed once per CTA with 16-byte
+// atomics.
+// Per row: 2 reads (x, dy) [+ dres] + 1 write of rows*cols*sizeof(T).
+template <typename T, bool LAYER, int NV>
+__global__ void __launch_bounds__(128) bwd_fused_rows(
+    const T* __restrict__ x, const T* __restrict__ gamma, const float* __restrict__ mean,
+    const float* __restrict__ rstd, const T* __restrict__ dy, const T* __restrict__ dres,
+    T* __restrict__ dx, float* __restrict__ dgamma, float* __restrict__ dbeta, int64_t rows,
+    int cols) {
+  constexpr int V = 16 / sizeof(T);
+  __shared__ float red[2][2][4];
+  extern __shared__ float4 sacc4[];  // [cols] dgamma partials (+ [cols] dbeta)
+  float* gacc = reinterpret_cast<float*>(sacc4);
+  float* bacc = gacc + cols;
+  uint4 gv[NV];  // gamma kept packed (T) in registers for the whole kernel
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    const int c = (j * 128 + threadIdx.x) * V;
+    if (c < cols) {
+      gv[j] = *reinterpret_cast<const uint4*>(gamma + c);
+#pragma unroll
+      for (int i = 0; i < V; ++i) {
+        gacc[c + i] = 0.f;
+        if (LAYER) bacc[c + i] = 0.f;
+      }
+    }
+  }
+  int parity = 0;
+  for (int64_t row = blockIdx.x; row < rows; row += gridDim.x, parity ^= 1) {
+    const T* xr = x + row * cols;
+    const T* dyr = dy + row * cols;
+    const float mu = LAYER ? mean[row] : 0.f, rs = rstd[row];
+    uint4 xv[NV], dv[NV];
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      const int c = (j * 128 + threadIdx.x) * V;
+      if (c < cols) {
+        xv[j] = __ldcs(reinterpret_cast<const uint4*>(xr + c));
+        dv[j] = __ldcs(reinterpret_cast<const uint4*>(dyr + c));
+      }
+    }
+    float a1 = 0.f, a2 = 0.f;
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      const int c = (j * 128 + threadIdx.x) * V;
+      if (c < cols) {
+        float v[V], d[V], g[V];
+        load16(reinterpret_cast<const T*>(&xv[j]), v);
+        load16(reinterpret_cast<const T*>(&dv[j]), d);
+        load16(reinterpret_cast<const T*>(&gv[j]), g);
+        float ga[V], ba[V];
+#pragma unroll
+        for (int i = 0; i < V; i += 4) {
+          *reinterpret_cast<float4*>(ga + i) = *reinterpret_cast<const float4*>(gacc + c + i);
+          if (LAYER)
+            *reinterpret_cast<float4*>(ba + i) = *reinterpret_cast<const float4*>(bacc + c + i);
+        }
+#pragma unroll
+        for (int i = 0; i < V; ++i) {
+          const float xh = (v[i] - mu) * rs;
+          const float gd = g[i] * d[i];
+          a1 += gd * xh;
+          a2 += gd;
+          ga[i] += d[i] * xh;
+          if (LAYER) ba[i] += d[i];
+        }
+#pragma unroll
+        for (int i = 0; i < V; i += 4) {
+          *reinterpret_cast<float4*>(gacc + c + i) = *reinterpret_cast<const float4*>(ga + i);
+          if (LAYER)
+            *reinterpret_cast<float4*>(bacc + c + i) = *reinterpret_cast<const float4*>(ba + i);
+        }
+      }
+    }
+    a1 = warp_sum(a1);
+    a2 = warp_sum(a2);
+    // double-buffered by row parity: one barrier per row suffices
+    if ((threadIdx.x & 31) == 0) {
+      red[parity][0][threadIdx.x >> 5] = a1;
+      red[parity][1][threadIdx.x >> 5] = a2;
+    }
+    __syncthreads();
+    a1 = (red[parity][0][0] + red[parity][0][1] + red[parity][0][2] + red[parity][0][3]) / cols;
+    a2 = (red[parity][1][0] + red[parity][1][1] + red[parity][1][2] + red[parity][1][3]) / cols;
+    T* dxr = dx + row * cols;
+    const T* drr = dres ? dres + row * cols : nullptr;
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      const int c = (j * 128 + threadIdx.x) * V;
+      if (c < cols) {
+        float v[V], d[V], g[V], r[V];
+        load16(reinterpret_cast<const T*>(&xv[j]), v);
+        load16(reinterpret_cast<const T*>(&dv[j]), d);
+        load16(reinterpret_cast<const T*>(&gv[j]), g);
+        if (drr) load16(drr + c, r);
+#pragma unroll
+        for (int i = 0; i < V; ++i) {
+          const float xh = (v[i] - mu) * rs;
+          float o = rs * (g[i] * d[i] - xh * a1 - (LAYER ? a2 : 0.f));
+          if (drr) o += r[i];
+          v[i] = o;
+        }
+        store16(dxr + c, v);
+      }
+    }
+  }
+  const bool vec = ((reinterpret_cast<uintptr_t>(dgamma) |
+                     (LAYER ? reinterpret_cast<uintptr_t>(dbeta) : 0)) & 15) == 0;
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    const int c = (j * 128 + threadIdx.x) * V;
+    if (c >= cols) continue;
+#pragma unroll
+    for (int i = 0; i < V; i += 4) {
+      if (vec) {
+        atomicAdd(reinterpret_cast<float4*>(dgamma + c + i),
+                  *reinterpret_cast<const float4*>(gacc + c + i));
+        if (LAYER)
+          atomicAdd(reinterpret_cast<float4*>(dbeta + c + i),
+                    *reinterpret_cast<const float4*>(bacc + c + i));
+      } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          atomicAdd(dgamma + c + i + k, gacc[c + i + k]);
+          if (LAYER) atomicAdd(dbeta + c + i + k, bacc[c + i + k]);
+        }
+      }
+    }
+  }
+}
+
+template <typename T, bool LAYER>
+bool launch_fused(const void* x, const void* gamma, const float* mean, const float* rstd,
+                  const void* dy, const void* dres, void* dx, float* dgamma, float* dbeta,
+                  int64_t rows, int64_t cols, void* stream) {
+  if (fused_disabled()) return false;
+  const int64_t nv = (cols / (16 / (int64_t)sizeof(T)) + 127) / 128;
+  auto go = [&](auto kernel) {
+    const size_t smem = (size_t)cols * sizeof(float) * (LAYER ? 2 : 1);
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 128, smem);
+    const int64_t grid = std::min<int64_t>(rows, (int64_t)sm_count() * std::max(per_sm, 1));
+    kernel<<<(unsigned)grid, 128, smem, as_stream(stream)>>>(
+        (const T*)x, (const T*)gamma, mean, rstd, (const T*)dy, (const T*)dres, (T*)dx, dgamma,
+        dbeta, rows, (int)cols);
+  };
+  if (nv <= 1) go(bwd_fused_rows<T, LAYER, 1>);
+  else if (nv <= 2) go(bwd_fused_rows<T, LAYER, 2>);
+  else if (nv <= 4) go(bwd_fused_rows<T, LAYER, 4>);
+  else if constexpr (!LAYER) {  // LayerNorm keeps 2 accumulators per column: NV <= 4
+    if (nv <= 5) go(bwd_fused_rows<T, LAYER, 5>);
+    else if (nv <= 8) go(bwd_fused_rows<T, LAYER, 8>);
+    else return false;
+  } else {
+    return false;
+  }
+  return true;
+}
+
 template <typename T, bool LAYER>
 bool launch_dx_row(const void* x, const void* gamma, const float* mean, const float* rstd,
                    const void* dy, const void* dres, void* dx, int64_t rows, int64_t cols,
@@ -286,6 +461,9 @@ static int32_t norm_bwd(const void* x, const void* gamma, const float* mean, con
                                                                 (int64_t)sm_count() * 8 / strips + 1));
   const int64_t rpc = (rows + chunks - 1) / chunks;
   GALV_DISPATCH(dtype, T, {
+    if (norm::launch_fused<T, LAYER>(x, gamma, mean, rstd, dy, dres, dx, dgamma, dbeta, rows,
+                                     cols, stream))
+      break;
     if (!norm::launch_dx_row<T, LAYER>(x, gamma, mean, rstd, dy, dres, dx, rows, cols, stream))
       norm::bwd_dx_kernel<T, LAYER><<<grid, norm::WARPS * 32, 0, as_stream(stream)>>>(
           (const T*)x, (const T*)gamma, mean, rstd, (const T*)dy, (const T*)dres, (T*)dx, rows,

@@ -72,6 +72,47 @@ def test_layernorm(dt):
     assert rel(db, br.grad) < tol(dt) * 2
 
 
+@pytest.mark.parametrize("layer", [False, True])
+@pytest.mark.parametrize("rows,cols,off", [(3, 4096, 0), (2000, 4096, 1), (1500, 5120, 0),
+                                           (700, 2048, 3), (5000, 1024, 0), (64, 8192, 2)])
+def test_norm_bwd_fused_shapes(layer, rows, cols, off):
+    """Fused dx+dgamma backward (persistent rows, smem partials, one atomic flush per CTA)
+    across the model widths, rows not a multiple of the grid, and dgamma/dbeta views at
+    offsets that are not 16-byte aligned (scalar-atomic flush)."""
+    from paper_2504_21411_b200 import kernels as K
+    if layer and cols > 4096:
+        pytest.skip("LayerNorm widths > 4096 use the two-kernel path")
+    torch.manual_seed(rows + cols)
+    dt = torch.bfloat16
+    x = (torch.randn(rows, cols, device="cuda") * 1.5 + 0.2).to(dt)
+    g = (1 + 0.1 * torch.randn(cols, device="cuda")).to(dt)
+    b = (0.1 * torch.randn(cols, device="cuda")).to(dt)
+    dy = torch.randn(rows, cols, device="cuda").to(dt)
+    dres = torch.randn(rows, cols, device="cuda").to(dt)
+    xr = x.float().clone().requires_grad_(True)
+    gr = g.float().clone().requires_grad_(True)
+    br = b.float().clone().requires_grad_(True)
+    if layer:
+        y, mean, rstd = K.layernorm_fwd(x, g, b, 1e-5)
+        ref = torch.nn.functional.layer_norm(xr, (cols,), gr, br, 1e-5)
+    else:
+        y, rstd = K.rmsnorm_fwd(x, g, 1e-5)
+        ref = xr * torch.rsqrt(xr.pow(2).mean(-1, keepdim=True) + 1e-5) * gr
+    ref.backward(dy.float())
+    buf = torch.zeros(2 * cols + 8, device="cuda")
+    seed = torch.randn(cols, device="cuda")
+    dg = buf[off:off + cols]
+    dg.copy_(seed)  # accumulates into existing contents
+    db = buf[off + cols + 4:off + 2 * cols + 4]
+    if layer:
+        dx = K.layernorm_bwd(x, g, mean, rstd, dy, dg, db, dres=dres)
+        assert rel(db, br.grad) < 1e-4
+    else:
+        dx = K.rmsnorm_bwd(x, g, rstd, dy, dg, dres=dres)
+    assert rel(dx, xr.grad + dres.float()) < 2e-2
+    assert rel(dg - seed, gr.grad) < 1e-4
+
+
 def rope_ref(x, S, theta=10000.0):
     T, H, D = x.shape
     pos = (torch.arange(T, device=x.device) % S).float()
