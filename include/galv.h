@@ -154,6 +154,13 @@ int32_t galv_bias_gelu_fwd(const void* x, const void* bias, void* y, int64_t T, 
                            int32_t dtype, void* stream);
 int32_t galv_bias_gelu_bwd(const void* x, const void* bias, const void* dy, void* dx,
                            int64_t T, int64_t F, int32_t dtype, void* stream);
+/* bias-GeLU backward with the bias gradient fused: dx as galv_bias_gelu_bwd and
+ * dbias_acc[f] += sum_t dx[t, f] (fp32; equals galv_colsum(dx, accumulate=1)).
+ * x, dy, dx 16-byte aligned, F * element size a multiple of 16 B (bias: any alignment).
+ * Realizes K8 inside the bwd_compute term (costmodel.py:106). */
+int32_t galv_bias_gelu_bwd_colsum(const void* x, const void* bias, const void* dy, void* dx,
+                                  float* dbias_acc, int64_t T, int64_t F, int32_t dtype,
+                                  void* stream);
 /*
  * GPT MLP GEMMs with the bias-GeLU(tanh) fused into the tcgen05 epilogue (bf16):
  *   fwd: pre[M,F] = X[M,K] W1[F,K]^T, act[M,F] = gelu(pre + bias)   (fc1)

@@ -150,6 +150,52 @@ __global__ void __launch_bounds__(256) colsum_vec(const T* __restrict__ x, float
   }
 }
 
+// bias-GeLU backward with the bias gradient fused: dx = dy * gelu'(x + b) and
+// dbias[f] += sum_t dx[t, f] (of the stored, T-rounded dx, as galv_colsum would see it).
+// colsum_vec's geometry: CTA = 8 column-threads (16-byte vectors) x 32 row lanes, row lanes
+// reduced through smem, one atomic per column per CTA.  Saves the colsum re-read of dx.
+template <typename T>
+__global__ void __launch_bounds__(256) bias_gelu_bwd_colsum(
+    const T* __restrict__ x, const T* __restrict__ b, const T* __restrict__ dy,
+    T* __restrict__ dx, float* __restrict__ dbias, int64_t rows, int64_t cols,
+    int64_t rows_per_cta) {
+  constexpr int V = 16 / sizeof(T);
+  __shared__ float red[32][8 * V + 1];
+  const int tx = threadIdx.x & 7, ty = threadIdx.x >> 3;
+  const int64_t c = ((int64_t)blockIdx.x * 8 + tx) * V;
+  const int64_t r0 = blockIdx.y * rows_per_cta, r1 = min(rows, r0 + rows_per_cta);
+  float s[V], bb[V];
+#pragma unroll
+  for (int e = 0; e < V; ++e) s[e] = bb[e] = 0.f;
+  if (c < cols) {
+    if (b) {  // bias may be an unaligned view into a flat parameter buffer: scalar loads
+#pragma unroll
+      for (int e = 0; e < V; ++e) bb[e] = to_f(b[c + e]);
+    }
+#pragma unroll 2
+    for (int64_t r = r0 + ty; r < r1; r += 32) {
+      float v[V], d[V];
+      load16(x + r * cols + c, v);
+      load16(dy + r * cols + c, d);
+#pragma unroll
+      for (int e = 0; e < V; ++e) v[e] = d[e] * gelu_tanh_grad(v[e] + bb[e]);
+      store16(dx + r * cols + c, v);
+#pragma unroll
+      for (int e = 0; e < V; ++e) s[e] += to_f(from_f<T>(v[e]));  // sum what was stored
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < V; ++e) red[ty][tx * V + e] = s[e];
+  __syncthreads();
+  if (threadIdx.x < 8 * V) {
+    const int64_t col = (int64_t)blockIdx.x * 8 * V + threadIdx.x;
+    float t = 0.f;
+#pragma unroll 8
+    for (int k = 0; k < 32; ++k) t += red[k][threadIdx.x];
+    if (col < cols) atomicAdd(&dbias[col], t);
+  }
+}
+
 template <typename TX, typename TY>
 __global__ void axpby_kernel(const TX* __restrict__ x, TY* __restrict__ y, int64_t n, float a,
                              float b) {
@@ -246,6 +292,8 @@ int32_t galv_swiglu_bwd_strided(const void* gu, const void* dh, int64_t ld_dh, v
 int32_t galv_bias_gelu_fwd(const void* x, const void* bias, void* y, int64_t T_, int64_t F,
                            int32_t dtype, void* stream) {
   GALV_CHECK_ARG(x && y && T_ > 0 && F % 8 == 0, "bad arguments");
+  GALV_CHECK_ARG(((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(bias)) & 15) == 0,
+                 "x and bias must be 16-byte aligned (16-byte vector loads)");
   GALV_DISPATCH(dtype, T, {
     const int64_t nvec = T_ * F / (16 / sizeof(T));
     act::bias_gelu_fwd<T><<<act::grid_for(nvec, 256), 256, 0, as_stream(stream)>>>(
@@ -258,10 +306,36 @@ int32_t galv_bias_gelu_fwd(const void* x, const void* bias, void* y, int64_t T_,
 int32_t galv_bias_gelu_bwd(const void* x, const void* bias, const void* dy, void* dx, int64_t T_,
                            int64_t F, int32_t dtype, void* stream) {
   GALV_CHECK_ARG(x && dy && dx && T_ > 0 && F % 8 == 0, "bad arguments");
+  GALV_CHECK_ARG(((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(bias)) & 15) == 0,
+                 "x and bias must be 16-byte aligned (16-byte vector loads)");
   GALV_DISPATCH(dtype, T, {
     const int64_t nvec = T_ * F / (16 / sizeof(T));
     act::bias_gelu_bwd<T><<<act::grid_for(nvec, 256), 256, 0, as_stream(stream)>>>(
         (const T*)x, (const T*)bias, (const T*)dy, (T*)dx, T_, F);
+  });
+  GALV_LAUNCH_CHECK();
+  return 0;
+}
+
+int32_t galv_bias_gelu_bwd_colsum(const void* x, const void* bias, const void* dy, void* dx,
+                                  float* dbias_acc, int64_t T_, int64_t F, int32_t dtype,
+                                  void* stream) {
+  GALV_CHECK_ARG(x && dy && dx && dbias_acc && T_ > 0 && F > 0, "bad arguments");
+  const int esz = dtype == GALV_BF16 ? 2 : 4;
+  GALV_CHECK_ARG((F * esz) % 16 == 0, "F * element size must be a multiple of 16 bytes");
+  GALV_CHECK_ARG(((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(dy) |
+                   reinterpret_cast<uintptr_t>(dx)) & 15) == 0,
+                 "x, dy, dx must be 16-byte aligned");
+  const int64_t per = 8 * (16 / esz);  // columns per CTA
+  const int64_t strips = (F + per - 1) / per;
+  const int64_t ych = std::max<int64_t>(
+      1, std::min<int64_t>((T_ + 31) / 32, (int64_t)sm_count() * 8 / strips));
+  const int64_t rpc = (T_ + ych - 1) / ych;
+  GALV_DISPATCH(dtype, T, {
+    act::bias_gelu_bwd_colsum<T><<<dim3((unsigned)strips, (unsigned)ych), 256, 0,
+                                   as_stream(stream)>>>((const T*)x, (const T*)bias,
+                                                        (const T*)dy, (T*)dx, dbias_acc, T_, F,
+                                                        rpc);
   });
   GALV_LAUNCH_CHECK();
   return 0;
@@ -355,6 +429,8 @@ __global__ void bias_add_kernel(T* __restrict__ x, const T* __restrict__ b, int6
 extern "C" int32_t galv_bias_add(void* x, const void* bias, int64_t T_, int64_t F, int32_t dtype,
                                  void* stream) {
   GALV_CHECK_ARG(x && bias && T_ > 0 && F % 8 == 0, "bad arguments");
+  GALV_CHECK_ARG(((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(bias)) & 15) == 0,
+                 "x and bias must be 16-byte aligned (16-byte vector loads)");
   GALV_DISPATCH(dtype, T, {
     const int64_t nvec = T_ * F / (16 / sizeof(T));
     act::bias_add_kernel<T><<<act::grid_for(nvec, 256), 256, 0, as_stream(stream)>>>(

@@ -198,7 +198,7 @@ __global__ void __launch_bounds__(128) bwd_dx_row(
   }
 }
 
-// Fused dx + dgamma(/dbeta): persistent 128-thread CTAs stride over rows; every thread owns
+// Fused dx + dgamma(/dbeta): persistent NT-thread CTAs stride over rows; every thread owns
 // the same NV column vectors in every row, so its dgamma partials stay in registers across
 // rows and x / dy are read from HBM exactly once per backward (the dx-then-dgamma pair
 // above reads them twice).  The partials live in shared memory (each column is owned by
@@ -206,21 +206,22 @@ __global__ void __launch_bounds__(128) bwd_dx_row(
 // registers to the in-flight x / dy vectors, and are flushed once per CTA with 16-byte
 // atomics.
 // Per row: 2 reads (x, dy) [+ dres] + 1 write of rows*cols*sizeof(T).
-template <typename T, bool LAYER, int NV>
-__global__ void __launch_bounds__(128) bwd_fused_rows(
+template <typename T, bool LAYER, int NV, int NT>
+__global__ void __launch_bounds__(NT) bwd_fused_rows(
     const T* __restrict__ x, const T* __restrict__ gamma, const float* __restrict__ mean,
     const float* __restrict__ rstd, const T* __restrict__ dy, const T* __restrict__ dres,
     T* __restrict__ dx, float* __restrict__ dgamma, float* __restrict__ dbeta, int64_t rows,
     int cols) {
   constexpr int V = 16 / sizeof(T);
-  __shared__ float red[2][2][4];
+  constexpr int NW = NT / 32;
+  __shared__ float red[2][2][NW];
   extern __shared__ float4 sacc4[];  // [cols] dgamma partials (+ [cols] dbeta)
   float* gacc = reinterpret_cast<float*>(sacc4);
   float* bacc = gacc + cols;
   uint4 gv[NV];  // gamma kept packed (T) in registers for the whole kernel
 #pragma unroll
   for (int j = 0; j < NV; ++j) {
-    const int c = (j * 128 + threadIdx.x) * V;
+    const int c = (j * NT + threadIdx.x) * V;
     if (c < cols) {
       gv[j] = *reinterpret_cast<const uint4*>(gamma + c);
 #pragma unroll
@@ -238,7 +239,7 @@ __global__ void __launch_bounds__(128) bwd_fused_rows(
     uint4 xv[NV], dv[NV];
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
-      const int c = (j * 128 + threadIdx.x) * V;
+      const int c = (j * NT + threadIdx.x) * V;
       if (c < cols) {
         xv[j] = __ldcs(reinterpret_cast<const uint4*>(xr + c));
         dv[j] = __ldcs(reinterpret_cast<const uint4*>(dyr + c));
@@ -247,7 +248,7 @@ __global__ void __launch_bounds__(128) bwd_fused_rows(
     float a1 = 0.f, a2 = 0.f;
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
-      const int c = (j * 128 + threadIdx.x) * V;
+      const int c = (j * NT + threadIdx.x) * V;
       if (c < cols) {
         float v[V], d[V], g[V];
         load16(reinterpret_cast<const T*>(&xv[j]), v);
@@ -285,13 +286,20 @@ __global__ void __launch_bounds__(128) bwd_fused_rows(
       red[parity][1][threadIdx.x >> 5] = a2;
     }
     __syncthreads();
-    a1 = (red[parity][0][0] + red[parity][0][1] + red[parity][0][2] + red[parity][0][3]) / cols;
-    a2 = (red[parity][1][0] + red[parity][1][1] + red[parity][1][2] + red[parity][1][3]) / cols;
+    a1 = 0.f;
+    a2 = 0.f;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+      a1 += red[parity][0][w];
+      a2 += red[parity][1][w];
+    }
+    a1 /= cols;
+    a2 /= cols;
     T* dxr = dx + row * cols;
     const T* drr = dres ? dres + row * cols : nullptr;
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
-      const int c = (j * 128 + threadIdx.x) * V;
+      const int c = (j * NT + threadIdx.x) * V;
       if (c < cols) {
         float v[V], d[V], g[V], r[V];
         load16(reinterpret_cast<const T*>(&xv[j]), v);
@@ -313,7 +321,7 @@ __global__ void __launch_bounds__(128) bwd_fused_rows(
                      (LAYER ? reinterpret_cast<uintptr_t>(dbeta) : 0)) & 15) == 0;
 #pragma unroll
   for (int j = 0; j < NV; ++j) {
-    const int c = (j * 128 + threadIdx.x) * V;
+    const int c = (j * NT + threadIdx.x) * V;
     if (c >= cols) continue;
 #pragma unroll
     for (int i = 0; i < V; i += 4) {
@@ -334,29 +342,57 @@ __global__ void __launch_bounds__(128) bwd_fused_rows(
   }
 }
 
+// GALV_NORM_NT=128|256 forces the CTA width (A/B).  Default (B200 A/B, scratch/norm_ab.py,
+// profiles/r01/kernels_ab/norm_bwd_ab.jsonl): 256 threads, and the fused kernel only for rows of
+// >= 256 vectors (bf16 width >= 2048): 8192x4096 RMS 89.9 -> 65.3 us, 8192x5120 145.9 ->
+// 84.8 us, 16384x2048 LN 89.7 -> 84.6 us; at width 1024 the two-kernel pair is faster
+// (48.2 vs 53.3 us: one short row per CTA iteration leaves too little in flight).
+static int forced_nt() {
+  static const int nt = [] {
+    const char* e = getenv("GALV_NORM_NT");
+    return e ? atoi(e) : 0;
+  }();
+  return nt;
+}
+
 template <typename T, bool LAYER>
 bool launch_fused(const void* x, const void* gamma, const float* mean, const float* rstd,
                   const void* dy, const void* dres, void* dx, float* dgamma, float* dbeta,
                   int64_t rows, int64_t cols, void* stream) {
   if (fused_disabled()) return false;
-  const int64_t nv = (cols / (16 / (int64_t)sizeof(T)) + 127) / 128;
-  auto go = [&](auto kernel) {
+  const int64_t vecs = cols / (16 / (int64_t)sizeof(T));
+  if (!forced_nt() && vecs < 256) return false;
+  const int nt = forced_nt() ? forced_nt() : 256;
+  const int64_t nv = (vecs + nt - 1) / nt;
+  auto go = [&](auto kernel, int threads) {
     const size_t smem = (size_t)cols * sizeof(float) * (LAYER ? 2 : 1);
     if (smem > 48 * 1024)
       cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 128, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem);
     const int64_t grid = std::min<int64_t>(rows, (int64_t)sm_count() * std::max(per_sm, 1));
-    kernel<<<(unsigned)grid, 128, smem, as_stream(stream)>>>(
+    kernel<<<(unsigned)grid, threads, smem, as_stream(stream)>>>(
         (const T*)x, (const T*)gamma, mean, rstd, (const T*)dy, (const T*)dres, (T*)dx, dgamma,
         dbeta, rows, (int)cols);
   };
-  if (nv <= 1) go(bwd_fused_rows<T, LAYER, 1>);
-  else if (nv <= 2) go(bwd_fused_rows<T, LAYER, 2>);
-  else if (nv <= 4) go(bwd_fused_rows<T, LAYER, 4>);
+  if (nt == 256) {
+    if (nv <= 1) go(bwd_fused_rows<T, LAYER, 1, 256>, 256);
+    else if (nv <= 2) go(bwd_fused_rows<T, LAYER, 2, 256>, 256);
+    else if constexpr (!LAYER) {
+      if (nv <= 3) go(bwd_fused_rows<T, LAYER, 3, 256>, 256);
+      else if (nv <= 4) go(bwd_fused_rows<T, LAYER, 4, 256>, 256);
+      else return false;
+    } else {
+      return false;
+    }
+    return true;
+  }
+  if (nv <= 1) go(bwd_fused_rows<T, LAYER, 1, 128>, 128);
+  else if (nv <= 2) go(bwd_fused_rows<T, LAYER, 2, 128>, 128);
+  else if (nv <= 4) go(bwd_fused_rows<T, LAYER, 4, 128>, 128);
   else if constexpr (!LAYER) {  // LayerNorm keeps 2 accumulators per column: NV <= 4
-    if (nv <= 5) go(bwd_fused_rows<T, LAYER, 5>);
-    else if (nv <= 8) go(bwd_fused_rows<T, LAYER, 8>);
+    if (nv <= 5) go(bwd_fused_rows<T, LAYER, 5, 128>, 128);
+    else if (nv <= 8) go(bwd_fused_rows<T, LAYER, 8, 128>, 128);
     else return false;
   } else {
     return false;

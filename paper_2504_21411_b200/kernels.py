@@ -76,6 +76,7 @@ _SIGS = {
                                  _I32, _P], _I32),
     "galv_bias_gelu_fwd": ([_P, _P, _P, _I64, _I64, _I32, _P], _I32),
     "galv_bias_gelu_bwd": ([_P, _P, _P, _P, _I64, _I64, _I32, _P], _I32),
+    "galv_bias_gelu_bwd_colsum": ([_P, _P, _P, _P, _P, _I64, _I64, _I32, _P], _I32),
     "galv_bias_add": ([_P, _P, _I64, _I64, _I32, _P], _I32),
     "galv_colsum": ([_P, _P, _I64, _I64, _I32, _I32, _P, _P], _I32),
     "galv_embed_fwd": ([_P, _P, _P, _I64, _I64, _I64, _I64, _I32, _P], _I32),
@@ -471,6 +472,15 @@ def bias_gelu_bwd(x, bias, dy, dx=None):
     dx = torch.empty_like(x) if dx is None else dx
     _call("galv_bias_gelu_bwd", _ptr(x), _ptr(bias), _ptr(dy), _ptr(dx), T, F,
           dtype_code(x.dtype), _stream())
+    return dx
+
+
+def bias_gelu_bwd_colsum(x, bias, dy, dbias_acc, dx=None):
+    """dx = dy * gelu'(x + bias) and dbias_acc += dx.sum(0) in one pass."""
+    T, F = x.shape
+    dx = torch.empty_like(x) if dx is None else dx
+    _call("galv_bias_gelu_bwd_colsum", _ptr(x), _ptr(bias), _ptr(dy), _ptr(dx),
+          _ptr(dbias_acc), T, F, dtype_code(x.dtype), _stream())
     return dx
 
 

@@ -384,10 +384,12 @@ class DecoderLayer:
                 dpre = K.gemm_bias_gelu_bwd(dmf, w["fc2.weight"], sv["pre"], w["fc1.bias"])
             else:
                 dact = _dgrad(dmf, w["fc2.weight"])
-                dpre = K.bias_gelu_bwd(sv["pre"], w["fc1.bias"], dact)
+                # bias grad summed in the same pass over dpre
+                dpre = K.bias_gelu_bwd_colsum(sv["pre"], w["fc1.bias"], dact, sg["fc1.bias"])
                 del dact
             _wgrad(dmf, sv["act"], gw["fc2.weight"])
-            K.colsum(dpre, sg["fc1.bias"])
+            if _fuse_bwd(dmf):
+                K.colsum(dpre, sg["fc1.bias"])
             dn2 = self._row_gemm(dpre, w["fc1.weight"], trans_b=False)
             _wgrad(dpre, sv["n2f"], gw["fc1.weight"])
         else:

@@ -235,3 +235,31 @@ def test_colsum_shapes(dt, rows, cols):
     K.colsum(x, cs, accumulate=True)
     want = x.double().sum(0) + 0.5
     assert ((cs.double() - want).norm() / want.norm()).item() < 1e-5
+
+
+@pytest.mark.parametrize("dt", DT)
+@pytest.mark.parametrize("rows,cols", [(1000, 4096), (37, 1024), (4096, 8192), (5, 64)])
+def test_bias_gelu_bwd_colsum(dt, rows, cols):
+    """Fused bias-GeLU backward + bias gradient == galv_bias_gelu_bwd then galv_colsum
+    (bitwise for dx; the column sums agree to fp32 reduction order), with the bias an
+    unaligned view into a flat buffer as the runtime's parameter store hands it out."""
+    from paper_2504_21411_b200 import kernels as K
+    torch.manual_seed(rows)
+    x = torch.randn(rows, cols, device="cuda").to(dt)
+    dy = torch.randn(rows, cols, device="cuda").to(dt)
+    flat = torch.randn(cols + 3, device="cuda").to(dt)
+    b = flat[3:]
+    with pytest.raises(RuntimeError, match="aligned"):  # the vector kernel refuses it
+        K.bias_gelu_bwd(x, b, dy)
+    ref_dx = K.bias_gelu_bwd(x, b.clone(), dy)
+    ref_db = torch.full((cols,), 0.25, device="cuda")
+    K.colsum(ref_dx, ref_db, accumulate=True)
+    db = torch.full((cols,), 0.25, device="cuda")
+    dx = K.bias_gelu_bwd_colsum(x, b, dy, db)
+    assert torch.equal(dx, ref_dx)
+    assert ((db.double() - ref_db.double()).norm() / ref_db.double().norm()).item() < 1e-5
+    # and against a torch fp32 reference of the op
+    xf = (x.float() + b.float()).requires_grad_(True)
+    torch.nn.functional.gelu(xf, approximate="tanh").backward(dy.float())
+    assert rel(dx, xf.grad) < tol(dt)
+    assert rel(db - 0.25, xf.grad.sum(0)) < tol(dt)
