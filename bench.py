@@ -262,7 +262,7 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return 0
-        steps, warm = max(1, min(args.steps, 3)), min(args.warmup, 1)
+        steps, warm = max(1, min(args.steps, 3)), min(args.warmup, 3)  # ~5 s per CPU step
         tok_s, t1, cores, sample = cpu_reference(cfg, steps, warm)
         line = {"metric": metric, "value": tok_s, "unit": "tokens/s", "n_gpus": args.gpus,
                 "steps": steps, "warmup": warm, "ms_per_step": t1 * 1e3,
