@@ -154,6 +154,16 @@ int32_t galv_bias_gelu_fwd(const void* x, const void* bias, void* y, int64_t T, 
                            int32_t dtype, void* stream);
 int32_t galv_bias_gelu_bwd(const void* x, const void* bias, const void* dy, void* dx,
                            int64_t T, int64_t F, int32_t dtype, void* stream);
+/* Llama QKV projection with RoPE in the tcgen05 epilogue (bf16):
+ *   qkv[M,N] = X[M,K] Wqkv[N,K]^T, then rotate-half RoPE on columns [0, n_rot) as heads
+ *   of 128 (q | k), position = row % S, cos/sin from table [2][S][64] fp32 -- the same
+ *   arithmetic as galv_gemm followed by galv_rope_table on the stored bf16 values.
+ * n_rot, N multiples of 128.  Falls back to exactly that pair when the fused path does not
+ * apply (M <= 128, unaligned operands, S % 8 != 0, GALV_ROPE_UNFUSED=1).
+ * Realizes K1 + K6 inside fwd_compute (costmodel.py:104-105). */
+int32_t galv_gemm_rope_qkv(const void* X, const void* Wqkv, void* qkv, const float* table,
+                           int64_t M, int64_t N, int64_t K, int64_t ldx, int64_t ldw,
+                           int64_t ldc, int64_t n_rot, int64_t S, void* stream);
 /* bias-GeLU backward with the bias gradient fused: dx as galv_bias_gelu_bwd and
  * dbias_acc[f] += sum_t dx[t, f] (fp32; equals galv_colsum(dx, accumulate=1)).
  * x, dy, dx 16-byte aligned, F * element size a multiple of 16 B (bias: any alignment).

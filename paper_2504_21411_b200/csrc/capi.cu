@@ -115,6 +115,37 @@ int32_t galv_gemm_batched(const void* A, const void* B, void* C, int64_t batch, 
   return 0;
 }
 
+// GALV_ROPE_UNFUSED=1 runs the QKV GEMM and the standalone RoPE kernel (A/B).
+static bool rope_unfused() {
+  static const bool off = [] {
+    const char* e = getenv("GALV_ROPE_UNFUSED");
+    return e && e[0] == '1';
+  }();
+  return off;
+}
+
+// qkv = X Wqkv^T (Wqkv [N, K], nn.Linear layout; rows q heads | k heads | v heads of 128)
+// with RoPE (rotate-half, table [2][S][64] fp32 as kernels.rope_table builds it) applied to
+// the first n_rot columns in the GEMM epilogue; otherwise the GEMM then galv_rope_table.
+int32_t galv_gemm_rope_qkv(const void* X, const void* Wqkv, void* qkv, const float* table,
+                           int64_t M, int64_t N, int64_t K, int64_t ldx, int64_t ldw,
+                           int64_t ldc, int64_t n_rot, int64_t S, void* stream) {
+  GALV_CHECK_ARG(X && Wqkv && qkv && table && M > 0 && N > 0 && K > 0 && S > 0,
+                 "bad arguments");
+  GALV_CHECK_ARG(n_rot % 128 == 0 && n_rot <= N && N % 128 == 0,
+                 "q|k|v must be whole heads of 128 columns");
+  if (!rope_unfused() && S % 8 == 0 &&
+      (reinterpret_cast<uintptr_t>(table) & 15) == 0 &&
+      galv::epilogue_fusable(X, Wqkv, qkv, table, M, ldc, S, n_rot > 0 ? n_rot : 8, 1, 5))
+    return galv::gemm_bf16_sm100(X, Wqkv, qkv, nullptr, M, N, K, ldx, ldw, ldc, 0, 1, 1.0f, 0,
+                                 GALV_BF16, GALV_F32, galv::as_stream(stream), nullptr, 0, 0, 5,
+                                 table, S, n_rot);
+  int32_t rc = galv::gemm_bf16_sm100(X, Wqkv, qkv, nullptr, M, N, K, ldx, ldw, ldc, 0, 1, 1.0f,
+                                     0, GALV_BF16, GALV_F32, galv::as_stream(stream));
+  if (rc || n_rot == 0) return rc;
+  return galv_rope_table(qkv, table, M, S, n_rot / 128, 128, ldc, 128, 0, 0, GALV_BF16, stream);
+}
+
 // gate|up = X W_gu^T (W_gu [2F, K], rows gate then up) and h = silu(gate) * up, with the
 // SwiGLU in the GEMM epilogue (each CTA pair computes 128 gate and the matching 128 up
 // columns); other shapes run the GEMM and then the standalone SwiGLU kernel.

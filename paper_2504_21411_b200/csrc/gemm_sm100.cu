@@ -631,6 +631,72 @@ __device__ __forceinline__ void epilogue_bias_gelu_fwd(const Params& p, uint32_t
   }
 }
 
+// epi 5 (Llama QKV forward): C = qkv = acc rounded to bf16 (what the plain GEMM stores),
+// then RoPE rotate-half on columns < ff (the q | k heads, head_dim 128) in fp32 with the
+// cos/sin table aux = [2][S][64] (S = aux_ld, position = row % S), exactly the arithmetic of
+// galv_rope_table on the stored values; v columns pass through.  Per head (128 columns of
+// the 256-column tile) and 32-column quarter: the lane's row pairs columns j and j + 64.
+__device__ __forceinline__ void epilogue_rope_qkv(const Params& p, uint32_t taddr, int row0,
+                                                  int col_base, uint8_t* stage) {
+  const int lane = threadIdx.x & 31;
+  __nv_bfloat16* C = reinterpret_cast<__nv_bfloat16*>(p.C);
+  const float* cs = reinterpret_cast<const float*>(p.aux);
+  const float* sn = cs + p.aux_ld * 64;
+  const int my_row = row0 + lane;
+  const long long pos = (my_row < p.M ? my_row : 0) % p.aux_ld;
+  __nv_bfloat16* srow = reinterpret_cast<__nv_bfloat16*>(stage + lane * SW_PITCH);
+#pragma unroll 1
+  for (int hb = 0; hb < BN; hb += 128) {
+    const int colh = col_base + hb;
+    if (colh >= p.N) break;
+    const bool rot = colh < p.ff;
+#pragma unroll 1
+    for (int cc = 0; cc < 64; cc += 32) {
+      uint32_t ra[32], rb[32];
+      tmem_ld32(taddr + hb + cc, ra);
+      tmem_ld32(taddr + hb + 64 + cc, rb);
+#pragma unroll
+      for (int c = 0; c < 32; c += 8) {
+        uint32_t lo[4], hi[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          lo[e] = pack2(__uint_as_float(ra[c + 2 * e]), __uint_as_float(ra[c + 2 * e + 1]));
+          hi[e] = pack2(__uint_as_float(rb[c + 2 * e]), __uint_as_float(rb[c + 2 * e + 1]));
+        }
+        if (rot) {
+          const int j = cc + c;
+          float cv[8], sv[8];
+          *reinterpret_cast<float4*>(cv) = *reinterpret_cast<const float4*>(cs + pos * 64 + j);
+          *reinterpret_cast<float4*>(cv + 4) =
+              *reinterpret_cast<const float4*>(cs + pos * 64 + j + 4);
+          *reinterpret_cast<float4*>(sv) = *reinterpret_cast<const float4*>(sn + pos * 64 + j);
+          *reinterpret_cast<float4*>(sv + 4) =
+              *reinterpret_cast<const float4*>(sn + pos * 64 + j + 4);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float2 a = bf2_to_f2(lo[e]), b = bf2_to_f2(hi[e]);
+            const float c0 = cv[2 * e], c1 = cv[2 * e + 1], s0 = sv[2 * e], s1 = sv[2 * e + 1];
+            lo[e] = pack2(a.x * c0 - b.x * s0, a.y * c1 - b.y * s1);
+            hi[e] = pack2(b.x * c0 + a.x * s0, b.y * c1 + a.y * s1);
+          }
+        }
+        *reinterpret_cast<uint4*>(srow + c) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+        *reinterpret_cast<uint4*>(srow + 32 + c) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+      }
+      __syncwarp();
+#pragma unroll
+      for (int it = 0; it < 8; ++it) {  // 32 rows x (first 4 | second 4) units of 16 bytes
+        const int u = it * 32 + lane, rr = u >> 3, part = u & 7;
+        const int row = row0 + rr, col = colh + (part >> 2) * 64 + cc + (part & 3) * 8;
+        if (row < p.M && col < p.N)
+          *reinterpret_cast<uint4*>(C + (long long)row * p.ldc + col) =
+              *reinterpret_cast<const uint4*>(stage + rr * SW_PITCH + part * 16);
+      }
+      __syncwarp();
+    }
+  }
+}
+
 // epi 4 (GPT fc2 dgrad): acc = d(act) (rounded to bf16 as the unfused dgrad stores it),
 // aux = saved pre; C = d(pre) = d(act) * gelu'(pre + bias).  64-column chunks: pre loaded
 // coalesced into smem, transformed in place per row, stored coalesced.
@@ -894,6 +960,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
         epilogue_bias_gelu_bwd(p, tmem + acc * BN + ((uint32_t)(q * 32) << 16),
                                mt * 256 + (int)cr * 128 + q * 32, nt * BN,
                                staging + q * 32 * Cfg2<false>::STAGE_PITCH);
+      else if (p.epi == 5)
+        epilogue_rope_qkv(p, tmem + acc * BN + ((uint32_t)(q * 32) << 16),
+                          mt * 256 + (int)cr * 128 + q * 32, nt * BN,
+                          staging + q * 32 * Cfg2<false>::STAGE_PITCH);
       else if (p.splits > 1) {  // fp32 partial tile of this K-split -> workspace
         Params w = p;
         w.C = p.ws + (long long)(u / p.num_tiles) * p.M * p.N;
@@ -1106,7 +1176,8 @@ int32_t gemm_bf16_sm100(const void* A, const void* B, void* C, const void* bias,
                          ((reinterpret_cast<uintptr_t>(C) & 15) == 0 || peer_c != nullptr);
   if (epi != 0) {  // fused SwiGLU epilogues exist on the 2-CTA path only (callers check)
     GALV_CHECK_ARG(epilogue_fusable(A, B, C, aux, M, ldc, aux_ld, ff, trans_b, epi) &&
-                       peer_c == nullptr && (bias == nullptr || epi >= 3) && !accumulate &&
+                       peer_c == nullptr && (bias == nullptr || epi == 3 || epi == 4) &&
+                       !accumulate &&
                        c_dtype == GALV_BF16 && alpha == 1.0f,
                    "fused activation epilogue: unsupported operands");
   }

@@ -77,6 +77,8 @@ _SIGS = {
     "galv_bias_gelu_fwd": ([_P, _P, _P, _I64, _I64, _I32, _P], _I32),
     "galv_bias_gelu_bwd": ([_P, _P, _P, _P, _I64, _I64, _I32, _P], _I32),
     "galv_bias_gelu_bwd_colsum": ([_P, _P, _P, _P, _P, _I64, _I64, _I32, _P], _I32),
+    "galv_gemm_rope_qkv": ([_P, _P, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _I64,
+                            _P], _I32),
     "galv_bias_add": ([_P, _P, _I64, _I64, _I32, _P], _I32),
     "galv_colsum": ([_P, _P, _I64, _I64, _I32, _I32, _P, _P], _I32),
     "galv_embed_fwd": ([_P, _P, _P, _I64, _I64, _I64, _I64, _I32, _P], _I32),
@@ -276,6 +278,22 @@ def gemm_swiglu_fwd(x, w_gu, gu=None, h=None):
                 _ptr(w_gu), _ptr(gu), _ptr(h), T, F, Kd, x.stride(0), w_gu.stride(0),
                 gu.stride(0), h.stride(0), _stream())
     return gu, h
+
+
+def gemm_rope_qkv(x, w_qkv, seq_len, n_rot, *, theta=10000.0, out=None):
+    """qkv = x @ w_qkv^T with RoPE (head_dim 128) applied to the first n_rot columns (the q
+    and k heads) in the GEMM epilogue (galv_gemm_rope_qkv)."""
+    _bf16_rows(x, w_qkv)
+    T, Kd = x.shape
+    N = w_qkv.shape[0]
+    if w_qkv.shape[1] != Kd:
+        raise RuntimeError("gemm_rope_qkv shape mismatch")
+    out = torch.empty(T, N, device=x.device, dtype=x.dtype) if out is None else out
+    table = rope_table(seq_len, 128, theta, x.device)
+    _timed_call(2.0 * T * N * Kd, (T, N, Kd), "galv_gemm_rope_qkv", _ptr(x), _ptr(w_qkv),
+                _ptr(out), _ptr(table), T, N, Kd, x.stride(0), w_qkv.stride(0), out.stride(0),
+                n_rot, seq_len, _stream())
+    return out
 
 
 def gemm_swiglu_bwd(dy, w_down, gu, dgu=None):

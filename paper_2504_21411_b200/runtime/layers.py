@@ -298,12 +298,19 @@ class DecoderLayer:
         n1, st1, _ = self._norm_fwd(x, w, "attn_norm")
         n1f = self._gather_seq(n1)
         T = n1f.shape[0]
-        qkv = _linear(n1f, w["qkv.weight"], bias=w["qkv.bias"] if gpt else None)
+        # Llama: RoPE on the q|k heads inside the QKV GEMM epilogue (Ulysses rotates after
+        # its head all-to-all, so it keeps the standalone kernel)
+        rope_fused = (not gpt and not self.uly and cfg.head_dim == 128
+                      and n1f.dtype == torch.bfloat16)
+        if rope_fused:
+            qkv = K.gemm_rope_qkv(n1f, w["qkv.weight"], S, 2 * self.ahl, theta=cfg.rope_theta)
+        else:
+            qkv = _linear(n1f, w["qkv.weight"], bias=w["qkv.bias"] if gpt else None)
         if self.uly:
             qkv = self._uly_qkv_to_heads(qkv)
             T = qkv.shape[0]
         q, k, v = self._attn_views(qkv, B, S)
-        if not gpt:
+        if not gpt and not rope_fused:
             # q and k heads are adjacent in the qkv row ([q | k | v], ahl = Hl*D each):
             # one launch rotates all 2*Hl of them
             K.rope_(qkv.as_strided((T, 2 * self.Hl, cfg.head_dim),

@@ -143,3 +143,37 @@ def test_gemm_splitk(shape, acc):
         assert K._gemm_splits(M, N, Kd) > 1
     out32 = K.gemm(a, b, trans_a=True, out_dtype=torch.float32)
     assert ((out32 - a.float().t() @ b.float()).norm() / ref.norm()).item() < 1e-5
+
+
+@pytest.mark.parametrize("M,heads,Kd,S", [(1024, 2, 512, 256), (300, 3, 256, 100),
+                                          (128, 2, 128, 64), (4096, 4, 1024, 4096)])
+def test_gemm_rope_qkv_fused(M, heads, Kd, S):
+    """QKV GEMM with RoPE in the tcgen05 epilogue == the plain GEMM followed by the
+    standalone RoPE kernel on the q|k heads (the same fp32 arithmetic on the stored bf16
+    values; at most a 1-ulp bf16 difference where FMA contraction differs), and against a
+    torch fp32 RoPE of the GEMM output.  M = 300 leaves a partial pair tile; M = 128 takes
+    the unfused fallback; S = 100 is not a multiple of 8 (fallback too)."""
+    from paper_2504_21411_b200 import kernels as K
+    torch.manual_seed(M + heads)
+    D = 128
+    x = (torch.randn(M, Kd, device="cuda") / Kd ** 0.5).to(torch.bfloat16)
+    w = torch.randn(3 * heads * D, Kd, device="cuda").to(torch.bfloat16)
+    got = K.gemm_rope_qkv(x, w, S, 2 * heads * D)
+    ref = K.gemm(x, w, trans_b=True)
+    K.rope_(ref[:, :2 * heads * D].unflatten(1, (2 * heads, D)), S)
+    diff = (got.float() - ref.float()).abs()
+    ulp = ref.float().abs().clamp_min(1e-30) * 2.0 ** -7
+    assert bool((diff <= ulp).all()), diff.max().item()
+    assert (got == ref).float().mean().item() > 0.99
+    assert torch.equal(got[:, 2 * heads * D:], ref[:, 2 * heads * D:])  # v untouched
+    # torch fp32 RoPE of the stored GEMM output
+    plain = K.gemm(x, w, trans_b=True).float()
+    qk = plain[:, :2 * heads * D].unflatten(1, (2 * heads, D))
+    pos = (torch.arange(M, device="cuda") % S).float()
+    inv = 1.0 / 10000.0 ** (torch.arange(0, D, 2, device="cuda").float() / D)
+    ang = pos[:, None] * inv[None, :]
+    c, s = ang.cos()[:, None, :], ang.sin()[:, None, :]
+    a, b = qk[..., :D // 2], qk[..., D // 2:]
+    want = torch.cat([a * c - b * s, b * c + a * s], -1).flatten(1)
+    err = ((got[:, :2 * heads * D].float() - want).norm() / want.norm()).item()
+    assert err < 1e-2
