@@ -2,6 +2,8 @@
 // GEMM writes; no transposes), lse [B, H, S] fp32 natural-log logsumexp.
 //   bf16 -> tcgen05/TMEM flash attention (attn_sm100.cu)
 //   fp32 -> exact SIMT kernels below (thread per row), for the fp32 parity configuration.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace galv {
@@ -216,7 +218,8 @@ int64_t attn_bwd_ws_sm100(int64_t B, int64_t S, int64_t H);
 int32_t attn_bwd_sm100(const void* q, const void* k, const void* v, const void* o,
                        const void* dout, const float* lse, void* dq, void* dk, void* dv,
                        int64_t B, int64_t S, int64_t H, int64_t D, int64_t st, int64_t sh,
-                       int64_t ost, float scale, int32_t causal, void* ws, cudaStream_t stream);
+                       int64_t ost, float scale, int32_t causal, void* ws, cudaStream_t stream,
+                       const float* rope_table);
 }
 
 extern "C" {
@@ -250,6 +253,34 @@ int64_t galv_attn_bwd_workspace(int64_t B, int64_t S, int64_t H, int64_t D, int3
   return B * H * S * (int64_t)sizeof(float);
 }
 
+// galv_attn_bwd with the inverse RoPE of q and k applied to dq / dk in the kernels' store
+// epilogues (bf16, head_dim 128): replaces galv_attn_bwd + galv_rope_table(inverse=1) on
+// dq|dk.  rope_table: fp32 [2][S][D/2] cos|sin planes, positions = token index mod S.
+int32_t galv_attn_bwd_rope(const void* q, const void* k, const void* v, const void* o,
+                           const void* dout, const float* lse, void* dq, void* dk, void* dv,
+                           int64_t B, int64_t S, int64_t H, int64_t D, int64_t st, int64_t sh,
+                           int64_t ost, float scale, int32_t causal, const float* rope_table,
+                           int32_t dtype, void* ws, void* stream) {
+  GALV_CHECK_ARG(q && k && v && o && dout && lse && dq && dk && dv && ws && rope_table,
+                 "bad arguments");
+  GALV_CHECK_ARG(dtype == GALV_BF16 && D == 128, "fused RoPE backward: bf16, head_dim 128");
+  GALV_CHECK_ARG(st % 8 == 0 && sh % 8 == 0 && ost % 8 == 0, "strides must be multiples of 8");
+  // GALV_ROPE_UNFUSED=1 (A/B): the plain backward, then the standalone inverse RoPE on dq, dk
+  static const bool unfused = [] {
+    const char* e = getenv("GALV_ROPE_UNFUSED");
+    return e && e[0] == '1';
+  }();
+  if (!unfused && (reinterpret_cast<uintptr_t>(rope_table) & 15) == 0)
+    return attn_bwd_sm100(q, k, v, o, dout, lse, dq, dk, dv, B, S, H, D, st, sh, ost, scale,
+                          causal, ws, as_stream(stream), rope_table);
+  int32_t rc = attn_bwd_sm100(q, k, v, o, dout, lse, dq, dk, dv, B, S, H, D, st, sh, ost, scale,
+                              causal, ws, as_stream(stream), nullptr);
+  if (rc) return rc;
+  rc = galv_rope_table(dq, rope_table, B * S, S, H, D, st, sh, 0, 1, dtype, stream);
+  if (rc) return rc;
+  return galv_rope_table(dk, rope_table, B * S, S, H, D, st, sh, 0, 1, dtype, stream);
+}
+
 int32_t galv_attn_bwd(const void* q, const void* k, const void* v, const void* o,
                       const void* dout, const float* lse, void* dq, void* dk, void* dv, int64_t B,
                       int64_t S, int64_t H, int64_t D, int64_t st, int64_t sh, int64_t ost,
@@ -263,7 +294,7 @@ int32_t galv_attn_bwd(const void* q, const void* k, const void* v, const void* o
   if (dtype == GALV_BF16) {
     GALV_CHECK_ARG(st % 8 == 0 && sh % 8 == 0 && ost % 8 == 0, "strides must be multiples of 8");
     return attn_bwd_sm100(q, k, v, o, dout, lse, dq, dk, dv, B, S, H, D, st, sh, ost, scale,
-                          causal, ws, s);
+                          causal, ws, s, nullptr);
   } else {
     GALV_CHECK_ARG(dtype == GALV_F32 && D == 64, "fp32 attention supports head_dim 64");
     attn::bwd_dot_f32<<<gdot, 128, 0, s>>>((const float*)o, (const float*)dout, dvec, (int)S,

@@ -445,6 +445,7 @@ struct BwdParams {
   __nv_bfloat16* g0;   // dkdv: dk ; dq: dq
   __nv_bfloat16* g1;   // dkdv: dv
   long long st, sh;    // output (q layout) strides
+  const float* rope;   // optional fp32 [2][S][D/2] cos|sin planes: inverse RoPE on dq / dk
 };
 
 template <int D>
@@ -503,6 +504,48 @@ __device__ __forceinline__ void store_row_out(__nv_bfloat16* dst, uint32_t taddr
     w.y = pack2(__uint_as_float(ov[u * 8 + 2]) * mul, __uint_as_float(ov[u * 8 + 3]) * mul);
     w.z = pack2(__uint_as_float(ov[u * 8 + 4]) * mul, __uint_as_float(ov[u * 8 + 5]) * mul);
     w.w = pack2(__uint_as_float(ov[u * 8 + 6]) * mul, __uint_as_float(ov[u * 8 + 7]) * mul);
+    *reinterpret_cast<uint4*>(dst + u * 8) = w;
+  }
+}
+
+// Inverse rotate-half RoPE fused into the dq / dk store (replaces the standalone
+// rope_table_kernel pass over dq|dk, rope.cu): the warp's 32 columns [c0, c0+32) pair with
+// the partner chunk c0 +- D/2, loaded from TMEM by the same warp (same lanes = same rows).
+// Angles come from the fp32 table cs (cos plane, sin plane at +S*D/2) at the row's position.
+//   j <  D/2:  out_j = x_j cos + x_{j+D/2} sin;   j >= D/2:  out_j = x_j cos - x_{j-D/2} sin
+template <int D>
+__device__ __forceinline__ void store_row_out_rope(__nv_bfloat16* dst, uint32_t t_self,
+                                                   uint32_t t_pair, float mul, bool write,
+                                                   const float* cs, int S, int pos, int c0) {
+  uint32_t xv[32], yv[32];
+  tmem_ld32_nowait(t_self, xv);
+  tmem_ld32_nowait(t_pair, yv);
+  tmem_wait_ld();
+  if (!write) return;
+  constexpr int HALF = D / 2;
+  const float sgn = c0 < HALF ? 1.f : -1.f;
+  const float* cr = cs + (long long)pos * HALF + (c0 & (HALF - 1));
+  const float* sr = cr + (long long)S * HALF;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    float o[8];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const float4 c = __ldg(reinterpret_cast<const float4*>(cr + u * 8 + h * 4));
+      const float4 sn = __ldg(reinterpret_cast<const float4*>(sr + u * 8 + h * 4));
+      const float cc[4] = {c.x, c.y, c.z, c.w}, ss[4] = {sn.x, sn.y, sn.z, sn.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int i = u * 8 + h * 4 + e;
+        const float x = __uint_as_float(xv[i]) * mul, y = __uint_as_float(yv[i]) * mul;
+        o[h * 4 + e] = x * cc[e] + sgn * y * ss[e];
+      }
+    }
+    uint4 w;
+    w.x = pack2(o[0], o[1]);
+    w.y = pack2(o[2], o[3]);
+    w.z = pack2(o[4], o[5]);
+    w.w = pack2(o[6], o[7]);
     *reinterpret_cast<uint4*>(dst + u * 8) = w;
   }
 }
@@ -716,8 +759,14 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       if constexpr (OC >= 32) {
 #pragma unroll 1
         for (int c = 0; c < OC / 32; ++c) {
-          store_row_out(p.g1 + off + c * 32, t_dv + part * OC + c * 32 + lane_off, 1.f, ok);
-          store_row_out(p.g0 + off + c * 32, t_dk + part * OC + c * 32 + lane_off, p.scale, ok);
+          const int c0 = part * OC + c * 32;
+          store_row_out(p.g1 + off + c * 32, t_dv + c0 + lane_off, 1.f, ok);
+          if (p.rope != nullptr)
+            store_row_out_rope<D>(p.g0 + off + c * 32, t_dk + c0 + lane_off,
+                                  t_dk + ((c0 + D / 2) & (D - 1)) + lane_off, p.scale, ok,
+                                  p.rope, p.S, ok ? key : 0, c0);
+          else
+            store_row_out(p.g0 + off + c * 32, t_dk + c0 + lane_off, p.scale, ok);
         }
       } else {
         store_row_out16(p.g1 + off, t_dv + part * OC + lane_off, 1.f, ok);
@@ -947,8 +996,15 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         (long long)(tok0 + (ok ? qi : 0)) * p.st + (long long)h * p.sh + part * OC;
     if constexpr (OC >= 32) {
 #pragma unroll 1
-      for (int c = 0; c < OC / 32; ++c)
-        store_row_out(p.g0 + off + c * 32, t_dq + part * OC + c * 32 + lane_off, p.scale, ok);
+      for (int c = 0; c < OC / 32; ++c) {
+        const int c0 = part * OC + c * 32;
+        if (p.rope != nullptr)
+          store_row_out_rope<D>(p.g0 + off + c * 32, t_dq + c0 + lane_off,
+                                t_dq + ((c0 + D / 2) & (D - 1)) + lane_off, p.scale, ok, p.rope,
+                                p.S, ok ? qi : 0, c0);
+        else
+          store_row_out(p.g0 + off + c * 32, t_dq + c0 + lane_off, p.scale, ok);
+      }
     } else {
       store_row_out16(p.g0 + off, t_dq + part * OC + lane_off, p.scale, ok);
     }
@@ -1059,7 +1115,8 @@ int64_t attn_bwd_ws_sm100(int64_t B, int64_t S, int64_t H) {
 int32_t attn_bwd_sm100(const void* q, const void* k, const void* v, const void* o,
                        const void* dout, const float* lse, void* dq, void* dk, void* dv,
                        int64_t B, int64_t S, int64_t H, int64_t D, int64_t st, int64_t sh,
-                       int64_t ost, float scale, int32_t causal, void* ws, cudaStream_t stream) {
+                       int64_t ost, float scale, int32_t causal, void* ws, cudaStream_t stream,
+                       const float* rope_table) {
   using namespace fa;
   const int64_t S_pad = (S + 127) / 128 * 128;
   float* lse2 = reinterpret_cast<float*>(ws);
@@ -1088,6 +1145,8 @@ int32_t attn_bwd_sm100(const void* q, const void* k, const void* v, const void* 
   p.dvec = dvec;
   p.st = st;
   p.sh = sh;
+  p.rope = rope_table;
+  GALV_CHECK_ARG(rope_table == nullptr || D == 128, "fused inverse RoPE needs head_dim 128");
   const dim3 g_kv((unsigned)((S + 127) / 128), (unsigned)(B * H));
   const dim3 g_q((unsigned)((S + 127) / 128), (unsigned)(B * H));
 #define GALV_FA_BWD(DD)                                                                          \

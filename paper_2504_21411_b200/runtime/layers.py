@@ -429,11 +429,14 @@ class DecoderLayer:
         need = K.attn_bwd_workspace_bytes(B, S, self.Hl, cfg.head_dim, qkv.dtype)
         if self._ws is None or self._ws.numel() < need:
             self._ws = torch.empty(need, dtype=torch.uint8, device=qkv.device)
+        # Llama, head_dim 128: the inverse RoPE of q/k rides in the dq / dk store epilogues
+        rope_fused = not gpt and cfg.head_dim == 128 and qkv.dtype == torch.bfloat16
         K.attn_bwd(q, k, v, sv["o_full"].view(B, S, self.Hl, cfg.head_dim),
                    do.view(B, S, self.Hl, cfg.head_dim), sv["lse"], dq, dk, dv,
-                   scale=self.scale, causal=True, workspace=self._ws)
+                   scale=self.scale, causal=True, workspace=self._ws,
+                   rope_theta=cfg.rope_theta if rope_fused else None)
         del do
-        if not gpt:
+        if not gpt and not rope_fused:
             K.rope_(dqkv.as_strided((T, 2 * self.Hl, cfg.head_dim),
                                     (dqkv.stride(0), cfg.head_dim, 1), dqkv.storage_offset()),
                     S, theta=cfg.rope_theta, inverse=True)

@@ -83,3 +83,48 @@ def test_attention_fwd_repeatable_rescale_heavy():
         else:
             assert torch.equal(o, first)
     torch.cuda.synchronize()
+
+
+def _rope_fp32(x, cs):
+    # rotate-half RoPE on [B, S, H, D]; cs = kernels.rope_table(S, D) [2, S, D/2]
+    c, s = cs[0][None, :, None, :], cs[1][None, :, None, :]
+    h = x.shape[-1] // 2
+    x1, x2 = x[..., :h], x[..., h:]
+    return torch.cat([x1 * c - x2 * s, x2 * c + x1 * s], -1)
+
+
+@pytest.mark.parametrize("S", [128, 200, 512])
+@pytest.mark.parametrize("causal", [True, False])
+def test_attention_bwd_fused_inverse_rope(S, causal):
+    """galv_attn_bwd_rope (inverse RoPE of q/k in the dq/dk store epilogues) against
+    (a) the unfused pair galv_attn_bwd + galv_rope_table(inverse=1), which rounds dq/dk to
+    bf16 once more, and (b) a torch fp32 autograd reference through RoPE + attention."""
+    from paper_2504_21411_b200 import kernels as K
+    torch.manual_seed(2)
+    B, H, D, theta = 2, 3, 128, 10000.0
+    cs = K.rope_table(S, D, theta, "cuda")
+    raw = torch.randn(B, S, 3, H, D, device="cuda")
+    qkv = torch.stack([_rope_fp32(raw[:, :, 0], cs), _rope_fp32(raw[:, :, 1], cs),
+                       raw[:, :, 2]], 2).bfloat16()
+    q, k, v = qkv[:, :, 0], qkv[:, :, 1], qkv[:, :, 2]
+    o = torch.empty(B, S, H, D, device="cuda", dtype=torch.bfloat16)
+    lse = torch.empty(B, H, S, device="cuda")
+    scale = 1 / math.sqrt(D)
+    K.attn_fwd(q, k, v, o, lse, scale=scale, causal=causal)
+    do = torch.randn(B, S, H, D, device="cuda").bfloat16()
+    fused = torch.empty_like(qkv)
+    K.attn_bwd(q, k, v, o, do, lse, fused[:, :, 0], fused[:, :, 1], fused[:, :, 2],
+               scale=scale, causal=causal, rope_theta=theta)
+    pair = torch.empty_like(qkv)
+    K.attn_bwd(q, k, v, o, do, lse, pair[:, :, 0], pair[:, :, 1], pair[:, :, 2],
+               scale=scale, causal=causal)
+    K.rope_(pair.view(B * S, 3 * H, D)[:, :2 * H], S, theta=theta, inverse=True)
+    assert torch.equal(fused[:, :, 2], pair[:, :, 2])  # dv untouched by the epilogue
+    assert rel(fused, pair) < 8e-3
+    # fp32 reference: gradients w.r.t. the pre-RoPE q and k
+    rq, rk, rv = (t.float().clone().requires_grad_(True)
+                  for t in (raw[:, :, 0], raw[:, :, 1], raw[:, :, 2]))
+    o_ref, _ = ref_attn(_rope_fp32(rq, cs), _rope_fp32(rk, cs), rv, causal)
+    o_ref.backward(do.float())
+    for i, want in enumerate((rq.grad, rk.grad, rv.grad)):
+        assert rel(fused[:, :, i], want) < 2e-2
