@@ -129,16 +129,17 @@ class ClockSampler:
 
 def cluster_profile(n: int, path: str):
     from paper_2504_21411_b200.planner import profiles as P
+    shown = os.path.relpath(path, ROOT) if os.path.isabs(path) else path
     if os.path.exists(path):
         c = P.load_cluster_profile(path)
         if c.n_devices == n:
-            return c, path
+            return c, shown
         # re-scope a measured 8-GPU table to n devices
         table = tuple(e for e in c.bandwidth_table if e.group_size <= n)
         c = P.ClusterProfile(n, min(c.devices_per_node, n), c.device_flops,
                              c.device_memory_bytes, c.memory_reserve_fraction, table)
         c.validate()
-        return c, path + f" (rescoped to {n})"
+        return c, shown + f" (rescoped to {n})"
     table = tuple(P.BandwidthEntry("intra_node", g, 700e9, 5e-6) for g in (2, 4, 8) if g <= n)
     c = P.ClusterProfile(n, min(n, 8), 1.2e15, 180_000_000_000, 0.1, table)
     c.validate()
