@@ -43,7 +43,9 @@ def parse():
     ap.add_argument("--impl", choices=("galv", "reference"), default="galv")
     ap.add_argument("--model", default="llama2-7b")
     ap.add_argument("--seqs-per-gpu", type=int, default=8)
-    ap.add_argument("--cluster-profile", default=os.path.join(ROOT, "profiles", "b200_cluster.json"))
+    ap.add_argument("--cluster-profile", default=None,
+                    help="default: the profile calibrated on --model's layer "
+                         "(CLUSTER_PROFILES), else profiles/b200_cluster.json")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--plan-out", default=None)
     ap.add_argument("--trace-out", default=None,
@@ -125,6 +127,16 @@ class ClockSampler:
                     reasons.add(n)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
                 "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# cluster profiles calibrated on each model's own layer (profiles/*.meta.json); llama2-13b's
+# at seq 32K (config C5), gpt2-medium's at seq 1024 (C2); everything else uses the 7B one
+CLUSTER_PROFILES = {"llama2-13b": "b200_cluster_llama13b.json",
+                    "gpt2-medium": "b200_cluster_gpt2m.json"}
+
+
+def default_cluster_profile(model: str) -> str:
+    return os.path.join(ROOT, "profiles", CLUSTER_PROFILES.get(model, "b200_cluster.json"))
 
 
 def cluster_profile(n: int, path: str):
@@ -289,7 +301,8 @@ def main():
     from paper_2504_21411_b200.runtime.engine import construct_hybrid_parallel_model
     from paper_2504_21411_b200.runtime.init import synthetic_tokens
 
-    cluster, cluster_src = cluster_profile(n, args.cluster_profile)
+    cluster, cluster_src = cluster_profile(
+        n, args.cluster_profile or default_cluster_profile(args.model))
     if args.layer_pattern:
         plan, hc, training = explicit_plan(cfg, n, gb, cluster, args.layer_pattern,
                                            args.microbatch or max(n // args.pp, 1), args.pp)
