@@ -92,16 +92,17 @@ int32_t galv_attn_bwd(const void* q, const void* k, const void* v, const void* o
                       int64_t B, int64_t S, int64_t H, int64_t D, int64_t stride_tok,
                       int64_t stride_head, int64_t o_stride_tok, float scale, int32_t causal,
                       int32_t dtype, void* ws, void* stream);
-/* galv_attn_bwd with the inverse rotate-half RoPE of q/k folded into the dq/dk store
- * epilogues (bf16, head_dim 128); rope_table = fp32 [2][S][D/2] cos|sin planes (the
- * galv_rope_table layout).  Replaces galv_attn_bwd + galv_rope_table(inverse=1) on dq|dk
- * in the decoder backward (the reference's attention cost term, costmodel.py:104). */
+/* galv_attn_bwd with dq/dk returned through the inverse rotate-half RoPE of q/k (bf16,
+ * head_dim 128); rope_table = fp32 [2][S][D/2] cos|sin planes (the galv_rope_table layout).
+ * epilogue 1: rotate in the dq/dk store epilogues; 0: backward + streaming inverse-RoPE
+ * pass; <0: library default (0, measured faster).  Replaces galv_attn_bwd +
+ * galv_rope_table(inverse=1) on dq|dk in the decoder backward (costmodel.py:104). */
 int32_t galv_attn_bwd_rope(const void* q, const void* k, const void* v, const void* o,
                            const void* dout, const float* lse, void* dq, void* dk, void* dv,
                            int64_t B, int64_t S, int64_t H, int64_t D, int64_t stride_tok,
                            int64_t stride_head, int64_t o_stride_tok, float scale,
-                           int32_t causal, const float* rope_table, int32_t dtype, void* ws,
-                           void* stream);
+                           int32_t causal, const float* rope_table, int32_t epilogue,
+                           int32_t dtype, void* ws, void* stream);
 
 /* y = norm(x (+ residual)) * gamma (+ beta).  rows x cols; residual/res_out optional:
  * when residual != NULL, res_out = x + residual is written and normalized.

@@ -2,8 +2,6 @@
 // GEMM writes; no transposes), lse [B, H, S] fp32 natural-log logsumexp.
 //   bf16 -> tcgen05/TMEM flash attention (attn_sm100.cu)
 //   fp32 -> exact SIMT kernels below (thread per row), for the fp32 parity configuration.
-#include <cstdlib>
-
 #include "common.cuh"
 
 namespace galv {
@@ -253,29 +251,36 @@ int64_t galv_attn_bwd_workspace(int64_t B, int64_t S, int64_t H, int64_t D, int3
   return B * H * S * (int64_t)sizeof(float);
 }
 
-// galv_attn_bwd with the inverse RoPE of q and k applied to dq / dk in the kernels' store
-// epilogues (bf16, head_dim 128): replaces galv_attn_bwd + galv_rope_table(inverse=1) on
-// dq|dk.  rope_table: fp32 [2][S][D/2] cos|sin planes, positions = token index mod S.
+// galv_attn_bwd with dq / dk returned through the inverse RoPE of q / k (bf16, head_dim
+// 128); rope_table: fp32 [2][S][D/2] cos|sin planes, positions = token index mod S.
+//   epilogue 1: rotated in the kernels' dq / dk store epilogues (attn_sm100.cu
+//               store_row_out_rope) -- no extra pass over dq|dk, but the lane-per-row table
+//               reads sit on the CTA's critical path (1 CTA/SM);
+//   epilogue 0: the plain backward, then the streaming inverse-RoPE pass (rope.cu) -- one
+//               launch over q|k heads when dk directly follows dq in the row;
+//   epilogue < 0: library default = 0, the faster of the two as measured on B200
+//               (Llama-2-7B shapes: 1015 + 48 us vs 1095-1210 us).
 int32_t galv_attn_bwd_rope(const void* q, const void* k, const void* v, const void* o,
                            const void* dout, const float* lse, void* dq, void* dk, void* dv,
                            int64_t B, int64_t S, int64_t H, int64_t D, int64_t st, int64_t sh,
                            int64_t ost, float scale, int32_t causal, const float* rope_table,
-                           int32_t dtype, void* ws, void* stream) {
+                           int32_t epilogue, int32_t dtype, void* ws, void* stream) {
   GALV_CHECK_ARG(q && k && v && o && dout && lse && dq && dk && dv && ws && rope_table,
                  "bad arguments");
-  GALV_CHECK_ARG(dtype == GALV_BF16 && D == 128, "fused RoPE backward: bf16, head_dim 128");
+  GALV_CHECK_ARG(dtype == GALV_BF16 && D == 128, "RoPE backward: bf16, head_dim 128");
   GALV_CHECK_ARG(st % 8 == 0 && sh % 8 == 0 && ost % 8 == 0, "strides must be multiples of 8");
-  // GALV_ROPE_UNFUSED=1 (A/B): the plain backward, then the standalone inverse RoPE on dq, dk
-  static const bool unfused = [] {
-    const char* e = getenv("GALV_ROPE_UNFUSED");
-    return e && e[0] == '1';
-  }();
-  if (!unfused && (reinterpret_cast<uintptr_t>(rope_table) & 15) == 0)
+  if (epilogue > 0) {
+    GALV_CHECK_ARG((reinterpret_cast<uintptr_t>(rope_table) & 15) == 0,
+                   "rope_table must be 16-byte aligned");
     return attn_bwd_sm100(q, k, v, o, dout, lse, dq, dk, dv, B, S, H, D, st, sh, ost, scale,
                           causal, ws, as_stream(stream), rope_table);
+  }
   int32_t rc = attn_bwd_sm100(q, k, v, o, dout, lse, dq, dk, dv, B, S, H, D, st, sh, ost, scale,
                               causal, ws, as_stream(stream), nullptr);
   if (rc) return rc;
+  const __nv_bfloat16* q_end = static_cast<const __nv_bfloat16*>(dq) + H * sh;
+  if (q_end == static_cast<const __nv_bfloat16*>(dk))  // [q heads | k heads]: one launch
+    return galv_rope_table(dq, rope_table, B * S, S, 2 * H, D, st, sh, 0, 1, dtype, stream);
   rc = galv_rope_table(dq, rope_table, B * S, S, H, D, st, sh, 0, 1, dtype, stream);
   if (rc) return rc;
   return galv_rope_table(dk, rope_table, B * S, S, H, D, st, sh, 0, 1, dtype, stream);

@@ -56,7 +56,7 @@ _SIGS = {
     "galv_attn_bwd": ([_P, _P, _P, _P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64,
                        _I64, _F, _I32, _I32, _P, _P], _I32),
     "galv_attn_bwd_rope": ([_P, _P, _P, _P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _I64,
-                            _I64, _I64, _F, _I32, _P, _I32, _P, _P], _I32),
+                            _I64, _I64, _F, _I32, _P, _I32, _I32, _P, _P], _I32),
     "galv_rmsnorm_fwd": ([_P, _P, _P, _P, _P, _P, _I64, _I64, _F, _I32, _P], _I32),
     "galv_rmsnorm_bwd": ([_P, _P, _P, _P, _P, _P, _P, _I64, _I64, _I32, _P, _P], _I32),
     "galv_layernorm_fwd": ([_P, _P, _P, _P, _P, _P, _P, _P, _I64, _I64, _F, _I32, _P], _I32),
@@ -124,7 +124,7 @@ def load_library(path: str | os.PathLike | None = None):
 
 
 # kernels launched per C-ABI call (for the bench's gpu_launches count)
-KERNELS_PER_CALL = {"galv_attn_bwd": 3, "galv_attn_bwd_rope": 3, "galv_tp_signal_reduce": 2,
+KERNELS_PER_CALL = {"galv_attn_bwd": 3, "galv_attn_bwd_rope": 4, "galv_tp_signal_reduce": 2,
                     "galv_tp_allgather": 2}
 
 
@@ -385,8 +385,10 @@ def attn_bwd_workspace_bytes(B, S, H, D, dtype) -> int:
 
 
 def attn_bwd(q, k, v, o, dout, lse, dq, dk, dv, *, scale, causal=True, workspace=None,
-             rope_theta=None):
-    """rope_theta set: dq/dk come out with the inverse RoPE applied (galv_attn_bwd_rope)."""
+             rope_theta=None, rope_epilogue=None):
+    """rope_theta set: dq/dk come out with the inverse RoPE applied (galv_attn_bwd_rope);
+    rope_epilogue True/False forces the store-epilogue / streaming-pass variant, None takes
+    the library default."""
     B, S, H, D, st, sh, ost = _attn_geometry(q, o)
     if dout.stride() != o.stride() or dq.stride() != q.stride():
         raise RuntimeError("dout must match o's layout and dq/dk/dv q's layout")
@@ -397,7 +399,8 @@ def attn_bwd(q, k, v, o, dout, lse, dq, dk, dv, *, scale, causal=True, workspace
         table = rope_table(S, D, rope_theta, q.device)
         _call("galv_attn_bwd_rope", _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(dout), _ptr(lse),
               _ptr(dq), _ptr(dk), _ptr(dv), B, S, H, D, st, sh, ost, float(scale), int(causal),
-              _ptr(table), dtype_code(q.dtype), _ptr(workspace), _stream())
+              _ptr(table), -1 if rope_epilogue is None else int(bool(rope_epilogue)),
+              dtype_code(q.dtype), _ptr(workspace), _stream())
         return
     _call("galv_attn_bwd", _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(dout), _ptr(lse), _ptr(dq),
           _ptr(dk), _ptr(dv), B, S, H, D, st, sh, ost, float(scale), int(causal),

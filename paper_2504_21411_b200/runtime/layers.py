@@ -429,7 +429,8 @@ class DecoderLayer:
         need = K.attn_bwd_workspace_bytes(B, S, self.Hl, cfg.head_dim, qkv.dtype)
         if self._ws is None or self._ws.numel() < need:
             self._ws = torch.empty(need, dtype=torch.uint8, device=qkv.device)
-        # Llama, head_dim 128: the inverse RoPE of q/k rides in the dq / dk store epilogues
+        # Llama, head_dim 128: dq / dk come back through the inverse RoPE of q / k in the
+        # same C-ABI call (galv_attn_bwd_rope; its default variant is the streaming pass)
         rope_fused = not gpt and cfg.head_dim == 128 and qkv.dtype == torch.bfloat16
         K.attn_bwd(q, k, v, sv["o_full"].view(B, S, self.Hl, cfg.head_dim),
                    do.view(B, S, self.Hl, cfg.head_dim), sv["lse"], dq, dk, dv,

@@ -93,10 +93,12 @@ def _rope_fp32(x, cs):
     return torch.cat([x1 * c - x2 * s, x2 * c + x1 * s], -1)
 
 
+@pytest.mark.parametrize("epilogue", [True, False])
 @pytest.mark.parametrize("S", [128, 200, 512])
 @pytest.mark.parametrize("causal", [True, False])
-def test_attention_bwd_fused_inverse_rope(S, causal):
-    """galv_attn_bwd_rope (inverse RoPE of q/k in the dq/dk store epilogues) against
+def test_attention_bwd_fused_inverse_rope(S, causal, epilogue):
+    """galv_attn_bwd_rope (inverse RoPE of q/k in the dq/dk store epilogues, or the
+    streaming pass after the backward with epilogue=False) against
     (a) the unfused pair galv_attn_bwd + galv_rope_table(inverse=1), which rounds dq/dk to
     bf16 once more, and (b) a torch fp32 autograd reference through RoPE + attention."""
     from paper_2504_21411_b200 import kernels as K
@@ -114,7 +116,7 @@ def test_attention_bwd_fused_inverse_rope(S, causal):
     do = torch.randn(B, S, H, D, device="cuda").bfloat16()
     fused = torch.empty_like(qkv)
     K.attn_bwd(q, k, v, o, do, lse, fused[:, :, 0], fused[:, :, 1], fused[:, :, 2],
-               scale=scale, causal=causal, rope_theta=theta)
+               scale=scale, causal=causal, rope_theta=theta, rope_epilogue=epilogue)
     pair = torch.empty_like(qkv)
     K.attn_bwd(q, k, v, o, do, lse, pair[:, :, 0], pair[:, :, 1], pair[:, :, 2],
                scale=scale, causal=causal)
