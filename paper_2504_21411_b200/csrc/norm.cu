@@ -350,7 +350,8 @@ __global__ void __launch_bounds__(NT) bwd_fused_rows(
 static int forced_nt() {
   static const int nt = [] {
     const char* e = getenv("GALV_NORM_NT");
-    return e ? atoi(e) : 0;
+    const int v = e ? atoi(e) : 0;
+    return (v == 128 || v == 256) ? v : 0;  // the only instantiated widths; else default
   }();
   return nt;
 }

@@ -123,9 +123,9 @@ def load_library(path: str | os.PathLike | None = None):
     return lib
 
 
-# kernels launched per C-ABI call (for the bench's gpu_launches count)
-KERNELS_PER_CALL = {"galv_attn_bwd": 3, "galv_attn_bwd_rope": 4, "galv_tp_signal_reduce": 2,
-                    "galv_tp_allgather": 2}
+# kernels launched per C-ABI call (for the bench's gpu_launches count); calls whose count
+# depends on their arguments pass it to _call(launches=...) instead
+KERNELS_PER_CALL = {"galv_attn_bwd": 3, "galv_tp_signal_reduce": 2, "galv_tp_allgather": 2}
 
 
 class KernelStats:
@@ -133,12 +133,14 @@ class KernelStats:
 
     def __init__(self, time_gemm: bool = False):
         self.calls: dict = {}
+        self.extra_launches = 0       # calls that reported their own launch count
         self.time_gemm = time_gemm
         self.gemm_events: list = []   # (flops, start_event, end_event, shape)
 
     @property
     def launches(self) -> int:
-        return sum(n * KERNELS_PER_CALL.get(k, 1) for k, n in self.calls.items())
+        return self.extra_launches + sum(n * KERNELS_PER_CALL.get(k, 1)
+                                         for k, n in self.calls.items())
 
     def gemm_summary(self) -> dict:
         torch.cuda.synchronize()
@@ -164,9 +166,12 @@ def stop_stats() -> KernelStats | None:
     return s
 
 
-def _call(name: str, *args) -> None:
+def _call(name: str, *args, launches: int | None = None) -> None:
     if _stats is not None:
-        _stats.calls[name] = _stats.calls.get(name, 0) + 1
+        if launches is None:
+            _stats.calls[name] = _stats.calls.get(name, 0) + 1
+        else:
+            _stats.extra_launches += launches
     rc = getattr(load_library(), name)(*args)
     if rc != 0:
         msg = load_library().galv_last_error().decode(errors="replace")
@@ -397,10 +402,16 @@ def attn_bwd(q, k, v, o, dout, lse, dq, dk, dv, *, scale, causal=True, workspace
         workspace = torch.empty(need, dtype=torch.uint8, device=q.device)
     if rope_theta is not None:
         table = rope_table(S, D, rope_theta, q.device)
+        # 3 backward kernels; the streaming variant adds one inverse-RoPE launch over q|k
+        # when dk directly follows dq's heads in memory, else one each
+        if rope_epilogue:
+            n = 3
+        else:
+            n = 4 if dk.data_ptr() == dq.data_ptr() + H * sh * dq.element_size() else 5
         _call("galv_attn_bwd_rope", _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(dout), _ptr(lse),
               _ptr(dq), _ptr(dk), _ptr(dv), B, S, H, D, st, sh, ost, float(scale), int(causal),
               _ptr(table), -1 if rope_epilogue is None else int(bool(rope_epilogue)),
-              dtype_code(q.dtype), _ptr(workspace), _stream())
+              dtype_code(q.dtype), _ptr(workspace), _stream(), launches=n)
         return
     _call("galv_attn_bwd", _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(dout), _ptr(lse), _ptr(dq),
           _ptr(dk), _ptr(dv), B, S, H, D, st, sh, ost, float(scale), int(causal),

@@ -61,6 +61,12 @@ class ModelConfig:
         L, h, s, V = self.n_layers, self.hidden, self.seq_len, self.vocab
         return 6.0 * L * self.layer_params() + 12.0 * L * h * s + 6.0 * h * V
 
+    def train_flops_per_token_causal(self) -> float:
+        """Same with the causal half of the attention score/PV FLOPs only (the work the
+        causal attention kernels actually do): 6*L*P + 6*L*h*s + 6*h*V."""
+        L, h, s, V = self.n_layers, self.hidden, self.seq_len, self.vocab
+        return 6.0 * L * self.layer_params() + 6.0 * L * h * s + 6.0 * h * V
+
     def with_(self, **kw) -> "ModelConfig":
         return replace(self, **kw)
 
@@ -76,6 +82,13 @@ MODEL_PRESETS = {
     "tiny-llama": ModelConfig("llama", 4, 512, 8, 1408, 8192, 256, name="tiny-llama"),
     "micro-llama": ModelConfig("llama", 2, 256, 4, 704, 1024, 128, name="micro-llama"),
     "micro-gpt": ModelConfig("gpt", 2, 256, 4, 1024, 1024, 128, name="micro-gpt"),
+    # head_dim 128 (the Llama-2-7B/13B head): exercises the RoPE-fused QKV GEMM epilogue
+    # and galv_attn_bwd_rope exactly as the headline runs them
+    "micro-llama128": ModelConfig("llama", 2, 256, 2, 704, 1024, 256, name="micro-llama128"),
+    "mini-llama128": ModelConfig("llama", 2, 512, 4, 1408, 1024, 256, name="mini-llama128"),
+    # one decoder layer at Llama-2-7B width and sequence length (h4096, 32x128, ffn 11008,
+    # s4096, V 32000): the production shapes of every kernel of the headline step
+    "llama2-7b-1l": ModelConfig("llama", 1, 4096, 32, 11008, 32000, 4096, name="llama2-7b-1l"),
 }
 
 
@@ -145,8 +158,17 @@ class HybridConfig:
 
 
 def get_hybrid_parallel_configs(plan, model_cfg: ModelConfig | None = None, *,
-                                sp_mode: str = "megatron") -> HybridConfig:
-    """Plan object, Plan dict, or path to a Plan JSON -> HybridConfig (validated)."""
+                                sp_mode: str = "megatron", model_profile=None, cluster=None,
+                                training=None, transitions: bool = True) -> HybridConfig:
+    """Plan object, Plan dict, or path to a Plan JSON -> HybridConfig (validated).
+
+    With the profiles the plan was searched under (``model_profile`` / ``cluster`` /
+    ``training``), the plan is first re-checked by ``validate_plan`` (reference
+    search.py:823-913: partition, degrees, divisibility, re-costed time within 1e-9
+    relative, stage peaks within the memory budget) and refused with ``InvalidPlan``
+    on any violation -- a plan produced under another profile, or one that no longer
+    fits, does not run silently."""
+    from ..planner.errors import InvalidPlan
     if isinstance(plan, (str, bytes)) or hasattr(plan, "__fspath__"):
         with open(plan, "r", encoding="utf-8") as fh:
             plan = json.load(fh)
@@ -154,6 +176,15 @@ def get_hybrid_parallel_configs(plan, model_cfg: ModelConfig | None = None, *,
         plan = Plan.from_dict(plan)
     if not isinstance(plan, Plan):
         raise ValidationError("expected a Plan, plan dict, or plan path")
+    given = [x is not None for x in (model_profile, cluster, training)]
+    if any(given) and not all(given):
+        raise ValidationError("plan validation needs model_profile, cluster and training")
+    if all(given):
+        from ..planner.search import validate_plan
+        problems = validate_plan(plan, model_profile, cluster, training,
+                                 transitions=transitions)
+        if problems:
+            raise InvalidPlan(problems)
     hc = HybridConfig(pp=plan.pp, microbatch=plan.microbatch,
                       n_microbatches=plan.n_microbatches,
                       stage_ranges=tuple(tuple(r) for r in plan.stage_ranges),

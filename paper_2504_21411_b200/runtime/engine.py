@@ -311,6 +311,11 @@ class HybridParallelModel:
                 ev.record()
                 store.ready_event = ev
 
+    def wait_optimizer(self):
+        """Make the current stream wait for the optimizer side stream (timing edges)."""
+        if self._opt_stream is not None:
+            torch.cuda.current_stream().wait_stream(self._opt_stream)
+
     def zero_grads(self):
         for _, store, _ in self.stores():
             store.zero_grads()

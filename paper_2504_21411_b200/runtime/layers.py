@@ -91,6 +91,9 @@ def tp_unslice(cfg, name: str, parts: list) -> torch.Tensor:
 # the backward (which also streams the saved pre-activation) from K >= 4096.
 FUSE_ACT_FWD_MIN_K = 2048
 FUSE_ACT_BWD_MIN_K = 4096
+# galv_attn_bwd_rope variant: None = library default (backward + one streaming inverse-RoPE
+# pass), True = rotation in the dq/dk store epilogues
+ROPE_BWD_EPILOGUE = None
 
 
 def _fuse_fwd(x):
@@ -435,7 +438,8 @@ class DecoderLayer:
         K.attn_bwd(q, k, v, sv["o_full"].view(B, S, self.Hl, cfg.head_dim),
                    do.view(B, S, self.Hl, cfg.head_dim), sv["lse"], dq, dk, dv,
                    scale=self.scale, causal=True, workspace=self._ws,
-                   rope_theta=cfg.rope_theta if rope_fused else None)
+                   rope_theta=cfg.rope_theta if rope_fused else None,
+                   rope_epilogue=ROPE_BWD_EPILOGUE)
         del do
         if not gpt and not rope_fused:
             K.rope_(dqkv.as_strided((T, 2 * self.Hl, cfg.head_dim),

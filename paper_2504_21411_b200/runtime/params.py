@@ -285,6 +285,12 @@ class ParamStore:
     # ------------------------------------------------------------------ optimizer
     def step(self, *, lr, beta1, beta2, eps, weight_decay, step, grad_scale=1.0) -> None:
         g = self._owned_grad
+        if g is not None and self.zero == 1:
+            # the z1 shard grad was allocated on the compute stream and is read here on the
+            # optimizer side stream; zero_grads() drops the last reference right after this
+            # call is queued, so tell the caching allocator not to hand the block back to
+            # the compute stream before the update has consumed it
+            g.record_stream(torch.cuda.current_stream())
         if self.zero == 3:
             out = self.p_shard
         elif self.zero == 0:

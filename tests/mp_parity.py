@@ -95,6 +95,29 @@ SCENARIOS = {
     "tp2dp2_bf16_opt": (4, "tiny-llama", hc([PS(2, 2, 1, True, False), PS(2, 2, 2, True, False),
                                              PS(1, 4, 0, False, False), PS(1, 4, 2, False, True)],
                                             mb=4), BF16, BF16_OPT, 2),
+    # head_dim 128 (the Llama-2-7B/13B path): RoPE in the QKV GEMM epilogue + the fused
+    # inverse-RoPE attention backward under every tp/sp/dp mode the headline plans use
+    "tp2_hd128_bf16": (2, "micro-llama128", hc([PS(2, 1, 0, False, False)] * 2), BF16, 2e-2),
+    "tp2_sp_hd128_bf16": (2, "micro-llama128", hc([PS(2, 1, 0, True, False)] * 2), BF16, 2e-2),
+    "tp2_sp_hd128_bf16_rc": (2, "micro-llama128", hc([PS(2, 1, 0, True, True)] * 2), BF16,
+                             2e-2),
+    "uly2_hd128_bf16": (2, "micro-llama128", hc([PS(2, 1, 0, True, False)] * 2,
+                                                sp_mode="ulysses"), BF16, 2e-2),
+    "dp2_z2_hd128_bf16": (2, "micro-llama128", hc([PS(1, 2, 2, False, False)] * 2, mb=2),
+                          BF16, 2e-2, 2),
+    "dp2_z1_hd128_bf16_opt": (2, "micro-llama128", hc([PS(1, 2, 1, False, False)] * 2, mb=2),
+                              BF16, BF16_OPT, 2),
+    "pp2_hd128_bf16": (2, "micro-llama128", hc([PS(1, 1, 0, False, False)] * 2, pp=2, m=4),
+                       BF16, 2e-2),
+    "tp4_sp_hd128_bf16": (4, "mini-llama128", hc([PS(4, 1, 0, True, False)] * 2, mb=2), BF16,
+                          2e-2),
+    "tp2dp2_hd128_bf16_opt": (4, "mini-llama128", hc([PS(2, 2, 1, True, False),
+                                                      PS(2, 2, 2, False, True)], mb=2),
+                              BF16, BF16_OPT, 2),
+    "dp4_z2_hd128_bf16": (4, "mini-llama128", hc([PS(1, 4, 2, False, False)] * 2, mb=4), BF16,
+                          2e-2, 2),
+    "uly4_hd128_bf16": (4, "mini-llama128", hc([PS(4, 1, 0, True, False)] * 2, mb=1,
+                                               sp_mode="ulysses"), BF16, 2e-2),
     "tp2dp2": (4, "micro-llama", hc([PS(2, 2, 1, True, False)] * 2, mb=2), F32, 1e-5),
     "pp2_tp2": (4, "tiny-llama", hc([PS(2, 1, 0, False, False), PS(1, 2, 2, False, False),
                                      PS(2, 1, 0, True, True), PS(2, 1, 0, False, False)],

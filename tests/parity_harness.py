@@ -31,7 +31,8 @@ def oracle_after_steps(cfg, w, tokens, steps: int, optim):
 
 
 def run_parity(name: str, hc: HybridConfig, dtype, *, grad_bytes: int = 4, seed: int = 1234,
-               oracle_cache: dict | None = None, opt_steps: int = 0):
+               oracle_cache: dict | None = None, opt_steps: int = 0,
+               oracle_dtype=torch.float64):
     """Returns (loss_err, {param: grad_err}) for this rank's stage params, after `opt_steps`
     optimizer steps (fused AdamW + ZeRO sharding) on the same batch."""
     cfg = MODEL_PRESETS[name]
@@ -54,7 +55,7 @@ def run_parity(name: str, hc: HybridConfig, dtype, *, grad_bytes: int = 4, seed:
     elif opt_steps:
         ref_loss, ref_grads = oracle_after_steps(cfg, w, tokens, opt_steps, optim)
     else:
-        ref_loss, ref_grads = model_ref.loss_and_grads(cfg, w, tokens, dtype=torch.float64)
+        ref_loss, ref_grads = model_ref.loss_and_grads(cfg, w, tokens, dtype=oracle_dtype)
         if oracle_cache is not None:
             oracle_cache[key] = (ref_loss, ref_grads)
     errs = {n: rel(g.float(), ref_grads[n]) for n, g in grads.items()}

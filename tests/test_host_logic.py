@@ -177,3 +177,49 @@ def test_committed_model_profiles_carry_the_fold(name):
     prof = load_model_profile(str(ROOT / "profiles" / f"b200_model_{name}.json"))
     assert prof == calibrated_model_profile(MODEL_PRESETS[name], meta["activation"])
     assert sum(lp.param_count for lp in prof.layers) == MODEL_PRESETS[name].total_params()
+
+
+def _plan_inputs(n=4, mem=180_000_000_000):
+    from paper_2504_21411_b200.planner import profiles as P
+    from paper_2504_21411_b200.runtime.config import MODEL_PRESETS, profile_for
+    cfg = MODEL_PRESETS["gpt2-medium"]
+    table = tuple(P.BandwidthEntry("intra_node", g, 7e11, 5e-6) for g in (2, 4) if g <= n)
+    cluster = P.ClusterProfile(n, n, 1.2e15, mem, 0.0, table)
+    return cfg, profile_for(cfg), cluster, P.TrainingConfig(global_batch=16 * n)
+
+
+def test_runtime_accepts_a_fresh_searched_plan():
+    from paper_2504_21411_b200.planner.search import optimize
+    from paper_2504_21411_b200.runtime.config import get_hybrid_parallel_configs
+    cfg, mp, cluster, training = _plan_inputs()
+    plan = optimize(mp, cluster, training)
+    hc = get_hybrid_parallel_configs(plan.to_dict(), cfg, model_profile=mp, cluster=cluster,
+                                     training=training)
+    assert hc.layer_strategies == tuple(plan.layer_strategies)
+
+
+def test_runtime_refuses_stale_and_over_budget_plans():
+    """ref search.py:823-913 (validate_plan) -- the runtime raises InvalidPlan instead of
+    running a plan searched under other profiles (CLI exit 5, cli.py:21-25)."""
+    import dataclasses
+    from paper_2504_21411_b200.planner.errors import InvalidPlan, ValidationError
+    from paper_2504_21411_b200.planner.search import optimize
+    from paper_2504_21411_b200.runtime.config import get_hybrid_parallel_configs
+    cfg, mp, cluster, training = _plan_inputs()
+    plan = optimize(mp, cluster, training)
+    # stale: costed under a 2x faster device
+    fast = dataclasses.replace(cluster, device_flops=cluster.device_flops * 2)
+    with pytest.raises(InvalidPlan) as ei:
+        get_hybrid_parallel_configs(plan, cfg, model_profile=mp, cluster=fast,
+                                    training=training)
+    assert any("predicted" in p or "stale" in p for p in ei.value.problems), ei.value.problems
+    # over budget: the same plan on a device with 1 GB
+    small = dataclasses.replace(cluster, device_memory_bytes=1_000_000_000)
+    with pytest.raises(InvalidPlan) as ei:
+        get_hybrid_parallel_configs(plan, cfg, model_profile=mp, cluster=small,
+                                    training=training)
+    assert any("budget" in p or "memory" in p for p in ei.value.problems), ei.value.problems
+    assert isinstance(ei.value, ValidationError)
+    # partial profile sets are a usage error
+    with pytest.raises(ValidationError):
+        get_hybrid_parallel_configs(plan, cfg, cluster=cluster)

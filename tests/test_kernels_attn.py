@@ -130,3 +130,99 @@ def test_attention_bwd_fused_inverse_rope(S, causal, epilogue):
     o_ref.backward(do.float())
     for i, want in enumerate((rq.grad, rk.grad, rv.grad)):
         assert rel(fused[:, :, i], want) < 2e-2
+
+
+def test_attention_bwd_rope_separate_dq_dk():
+    """Streaming variant with dq and dk in separate buffers (two inverse-RoPE launches)."""
+    from paper_2504_21411_b200 import kernels as K
+    torch.manual_seed(5)
+    B, S, H, D, theta = 1, 256, 2, 128, 10000.0
+    qkv = torch.randn(B, S, 3, H, D, device="cuda").bfloat16()
+    q, k, v = qkv[:, :, 0], qkv[:, :, 1], qkv[:, :, 2]
+    o = torch.empty(B, S, H, D, device="cuda", dtype=torch.bfloat16)
+    lse = torch.empty(B, H, S, device="cuda")
+    scale = 1 / math.sqrt(D)
+    K.attn_fwd(q, k, v, o, lse, scale=scale, causal=True)
+    do = torch.randn(B, S, H, D, device="cuda").bfloat16()
+    a, b = torch.empty_like(qkv), torch.empty_like(qkv)
+    dq, dk, dv = a[:, :, 0], b[:, :, 1], a[:, :, 2]
+    stats = K.start_stats()
+    K.attn_bwd(q, k, v, o, do, lse, dq, dk, dv, scale=scale, causal=True, rope_theta=theta)
+    K.stop_stats()
+    assert stats.launches == 5
+    pair = torch.empty_like(qkv)
+    K.attn_bwd(q, k, v, o, do, lse, pair[:, :, 0], pair[:, :, 1], pair[:, :, 2],
+               scale=scale, causal=True)
+    K.rope_(pair.view(B * S, 3 * H, D)[:, :2 * H], S, theta=theta, inverse=True)
+    assert torch.equal(dq, pair[:, :, 0]) and torch.equal(dk, pair[:, :, 1])
+    assert torch.equal(dv, pair[:, :, 2])
+
+
+def _chunked_ref(q, k, v, o, do, scale, chunk):
+    """fp32 causal attention forward (o, lse) and backward (dq, dk, dv) of bf16 inputs,
+    one head at a time in query blocks of `chunk` rows, so S = 32K fits: the standard
+    definitions P = exp(s - lse), dV = P^T dO, dS = P * (dO V^T - rowsum(dO * O)),
+    dQ = scale dS K, dK = scale dS^T Q.  O in the backward is the kernel's (as the
+    backward sees it); dO is the given upstream gradient."""
+    B, S, H, D = q.shape
+    o_ref = torch.empty(B, S, H, D, device=q.device)
+    lse_ref = torch.empty(B, H, S, device=q.device)
+    dq = torch.empty(B, S, H, D, device=q.device)
+    dk = torch.zeros(B, S, H, D, device=q.device)
+    dv = torch.zeros(B, S, H, D, device=q.device)
+    ar = torch.arange(S, device=q.device)
+    for b in range(B):
+        for h in range(H):
+            qh, kh, vh = (t[b, :, h].float() for t in (q, k, v))
+            oh, doh = o[b, :, h].float(), do[b, :, h].float()
+            for lo in range(0, S, chunk):
+                hi = min(S, lo + chunk)
+                n = hi  # causal: keys < hi only
+                s = (qh[lo:hi] @ kh[:n].t()) * scale
+                s.masked_fill_(ar[None, :n] > ar[lo:hi, None], float("-inf"))
+                lse = torch.logsumexp(s, -1)
+                p = torch.exp(s - lse[:, None])
+                o_ref[b, lo:hi, h] = p @ vh[:n]
+                lse_ref[b, h, lo:hi] = lse
+                dvec = (doh[lo:hi] * oh[lo:hi]).sum(-1)
+                dp = doh[lo:hi] @ vh[:n].t()
+                ds = p * (dp - dvec[:, None])
+                dq[b, lo:hi, h] = (ds @ kh[:n]) * scale
+                dk[b, :n, h] += (ds.t() @ qh[lo:hi]) * scale
+                dv[b, :n, h] += p.t() @ doh[lo:hi]
+    return o_ref, lse_ref, dq, dk, dv
+
+
+@pytest.mark.parametrize("B,S,H", [(2, 4096, 32), (1, 32768, 8)])
+def test_attention_production_shapes(B, S, H):
+    """Causal bf16 attention at the Llama-2-7B step shape (mb 2 x 4096, 32 heads) and the
+    Llama-2-13B 32K context (one sequence of 32768, 8 heads of a tp/Ulysses shard), inside
+    a fused [B, S, 3, H, D] qkv buffer as the runtime lays it out, against a chunked fp32
+    reference; plus the fused inverse-RoPE backward at the same shape."""
+    from paper_2504_21411_b200 import kernels as K
+    D, theta = 128, 10000.0
+    torch.manual_seed(7)
+    qkv = torch.randn(B, S, 3, H, D, device="cuda").bfloat16()
+    q, k, v = qkv[:, :, 0], qkv[:, :, 1], qkv[:, :, 2]
+    o = torch.empty(B, S, H, D, device="cuda", dtype=torch.bfloat16)
+    lse = torch.empty(B, H, S, device="cuda")
+    scale = 1 / math.sqrt(D)
+    K.attn_fwd(q, k, v, o, lse, scale=scale, causal=True)
+    do = torch.randn(B, S, H, D, device="cuda").bfloat16()
+    dqkv = torch.empty_like(qkv)
+    K.attn_bwd(q, k, v, o, do, lse, dqkv[:, :, 0], dqkv[:, :, 1], dqkv[:, :, 2], scale=scale,
+               causal=True)
+    o_ref, lse_ref, dq, dk, dv = _chunked_ref(q, k, v, o, do, scale, 2048)
+    assert rel(o, o_ref) < 1e-2
+    assert rel(lse, lse_ref) < 1e-4
+    for got, want in ((dqkv[:, :, 0], dq), (dqkv[:, :, 1], dk), (dqkv[:, :, 2], dv)):
+        assert rel(got, want) < 2e-2
+    # fused inverse RoPE (both variants) == backward then the standalone inverse rotation
+    ref = dqkv.clone()
+    K.rope_(ref.view(B * S, 3 * H, D)[:, :2 * H], S, theta=theta, inverse=True)
+    for epi in (False, True):
+        fused = torch.empty_like(qkv)
+        K.attn_bwd(q, k, v, o, do, lse, fused[:, :, 0], fused[:, :, 1], fused[:, :, 2],
+                   scale=scale, causal=True, rope_theta=theta, rope_epilogue=epi)
+        assert torch.equal(fused[:, :, 2], dqkv[:, :, 2])
+        assert rel(fused, ref) < 8e-3

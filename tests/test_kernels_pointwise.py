@@ -128,12 +128,16 @@ def test_rope_roundtrip(dt):
     from paper_2504_21411_b200 import kernels as K
     torch.manual_seed(2)
     qkv = torch.randn(2 * 128, 3 * 4 * 64, device="cuda").to(dt)
+    orig = qkv.clone()  # unaliased copy of the input
     view = qkv[:, : 4 * 64].view(256, 4, 64)
     ref = rope_ref(view.clone(), 128)
     K.rope_(view, 128)
     assert rel(view, ref) < tol(dt)
+    # the rotated values are rounded to dt, so the round trip is exact only in fp32
     K.rope_(view, 128, inverse=True)
-    assert rel(view, qkv[:, :256].view(256, 4, 64).clone()) < 1e-9 or True
+    assert rel(view, orig[:, : 4 * 64].view(256, 4, 64)) < (1e-6 if dt == torch.float32
+                                                            else 1e-2)
+    assert torch.equal(qkv[:, 4 * 64:], orig[:, 4 * 64:])  # v columns untouched
 
 
 @pytest.mark.parametrize("dt", DT)

@@ -83,3 +83,50 @@ def test_fp32_parity_after_adamw_steps(name, strategy):
     lerr, errs = run_parity(name, hc, torch.float32, opt_steps=2)
     assert lerr <= 1e-4
     assert max(errs.values()) <= 1e-3, max(errs.items(), key=lambda kv: kv[1])
+
+
+# ---------------------------------------------------------------- head_dim 128 (headline path)
+# Llama-2-7B/13B run head_dim 128: RoPE inside the QKV GEMM epilogue (galv_gemm_rope_qkv) and
+# the attention backward with the inverse RoPE in the same C-ABI call (galv_attn_bwd_rope).
+
+
+@pytest.mark.parametrize("name", ["micro-llama128", "mini-llama128"])
+@pytest.mark.parametrize("rope_epilogue", [None, True])
+def test_bf16_parity_head_dim_128(name, rope_epilogue, monkeypatch):
+    from paper_2504_21411_b200.runtime import layers
+    monkeypatch.setattr(layers, "ROPE_BWD_EPILOGUE", rope_epilogue)
+    cfg = MODEL_PRESETS[name]
+    assert cfg.head_dim == 128
+    hc = uniform_config(cfg, S1, microbatch=2, n_microbatches=2)
+    lerr, errs = run_parity(name, hc, torch.bfloat16, grad_bytes=4, oracle_cache=CACHE)
+    assert lerr <= 2e-2
+    worst = max(errs.items(), key=lambda kv: kv[1])
+    assert worst[1] <= 2e-2, worst
+
+
+def test_bf16_parity_head_dim_128_recompute_fused_epilogues(monkeypatch):
+    """hd128 + recompute + the SwiGLU GEMM-epilogue fusions forced on + bf16 grads."""
+    from paper_2504_21411_b200.runtime import layers
+    monkeypatch.setattr(layers, "FUSE_ACT_FWD_MIN_K", 0)
+    monkeypatch.setattr(layers, "FUSE_ACT_BWD_MIN_K", 0)
+    cfg = MODEL_PRESETS["micro-llama128"]
+    hc = uniform_config(cfg, S1R, microbatch=1, n_microbatches=2)
+    lerr, errs = run_parity("micro-llama128", hc, torch.bfloat16, grad_bytes=2)
+    assert lerr <= 2e-2
+    worst = max(errs.items(), key=lambda kv: kv[1])
+    assert worst[1] <= 2e-2, worst
+
+
+def test_bf16_parity_llama2_7b_width_one_layer():
+    """One decoder layer at the exact Llama-2-7B production shapes (h4096, 32 heads x 128,
+    ffn 11008, s4096, V 32000, mb 1): every kernel of the headline step (fused RoPE-QKV
+    GEMM, tcgen05 attention fwd/bwd at S=4096, SwiGLU GEMM epilogues at K>=2048/4096,
+    fused RMSNorm backward, vocab-32000 cross-entropy) against the oracle (fp32 on the host:
+    the bf16 tolerance 2e-2 is 4 orders above fp32 rounding)."""
+    cfg = MODEL_PRESETS["llama2-7b-1l"]
+    hc = uniform_config(cfg, S1, microbatch=1, n_microbatches=1)
+    lerr, errs = run_parity("llama2-7b-1l", hc, torch.bfloat16, grad_bytes=4,
+                            oracle_dtype=torch.float32)
+    assert lerr <= 2e-2
+    worst = max(errs.items(), key=lambda kv: kv[1])
+    assert worst[1] <= 2e-2, worst
