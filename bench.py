@@ -231,6 +231,31 @@ def describe(hc) -> str:
     return f"pp{hc.pp} mb{hc.microbatch}x{hc.n_microbatches} [{layers}]"
 
 
+def memory_breakdown(plan, model, cluster, training, peak_gb, persistent_bytes):
+    """This rank's stage: the cost model's terms (costmodel.py:137-176) next to the
+    runtime's persistent bytes (after construction, symmetric pools included) and peak."""
+    from paper_2504_21411_b200.planner import costmodel
+    cfg = model.cfg
+    prof = model_profile(cfg)
+    st = model.stage
+    lo, hi = plan.stage_ranges[st]
+    infl = costmodel.in_flight_microbatches(plan.pp, st, plan.n_microbatches)
+    tot = {"param": 0.0, "grad": 0.0, "optimizer": 0.0, "activation": 0.0}
+    for li in range(lo, hi):
+        m = costmodel.layer_memory(prof.layers[li], plan.layer_strategies[li], plan.microbatch,
+                                   prof.seq_len, infl, training)
+        tot["param"] += m.param_bytes
+        tot["grad"] += m.grad_bytes
+        tot["optimizer"] += m.optimizer_bytes
+        tot["activation"] += m.activation_bytes
+    state = tot["param"] + tot["grad"] + tot["optimizer"]
+    return {"stage": st, "model_state_gb": state / 1e9, "model_activation_gb":
+            tot["activation"] / 1e9, "runtime_persistent_gb": persistent_bytes / 1e9,
+            "runtime_peak_gb": peak_gb, "predicted_gb": plan.predicted_stage_peak_memory[st] / 1e9,
+            "budget_gb": cluster.memory_budget_bytes() / 1e9,
+            "peak_within_prediction": peak_gb * 1e9 <= plan.predicted_stage_peak_memory[st]}
+
+
 # ----------------------------------------------------------------------------- CPU arm
 
 
@@ -322,6 +347,8 @@ def main():
             fh.write(dumps_canonical(plan.to_dict(), sort_keys=False))
     model = construct_hybrid_parallel_model(cfg, hc, training=training, dtype=torch.bfloat16,
                                             init="fast")
+    torch.cuda.synchronize()
+    persistent_bytes = torch.cuda.memory_allocated() + sum(p.nbytes for p in model.dp_pools)
     tokens_host = synthetic_tokens(cfg, gb).pin_memory()
     tokens_dev = tokens_host.to("cuda")
     torch.cuda.synchronize()
@@ -455,6 +482,7 @@ def main():
                             "multicast": all(bool(p.mc) for p in model.dp_pools)}
                            if model.dp_pools else {"impl": "nccl" if n > 1 else "none"}),
         "predicted_peak_mem_gb": max(plan.predicted_stage_peak_memory) / 1e9,
+        "memory": memory_breakdown(plan, model, cluster, training, mem, persistent_bytes),
     }
     if args.trace_out:
         model.record_trace = True

@@ -30,6 +30,17 @@ def all_gather(t: torch.Tensor, g, out: torch.Tensor | None = None) -> torch.Ten
     return out
 
 
+def all_gather_async(t: torch.Tensor, g):
+    """all_gather launched on NCCL's stream: (out, work); work.wait() orders the current
+    stream after it (None work for single-rank groups)."""
+    if g is None or g.size == 1:
+        return t, None
+    out = torch.empty((t.shape[0] * g.size,) + tuple(t.shape[1:]), dtype=t.dtype,
+                      device=t.device)
+    work = dist.all_gather_into_tensor(out, t.contiguous(), group=g.group, async_op=True)
+    return out, work
+
+
 def reduce_scatter(t: torch.Tensor, g, out: torch.Tensor | None = None) -> torch.Tensor:
     """Sum over ranks, keep this rank's dim-0 chunk."""
     if g is None or g.size == 1:

@@ -291,8 +291,14 @@ class DecoderLayer:
         mk = lambda j: qkv.as_strided((B, S, self.Hl, D), (S * st, st, D, 1), base + j * hl)
         return mk(0), mk(1), mk(2)
 
-    def forward_impl(self, x, B, save: bool):
-        """x: [T_in, h] in this layer's layout; B = samples in this dp replica."""
+    def forward_impl(self, x, B, save: bool, keep_gathered: bool = False):
+        """x: [T_in, h] in this layer's layout; B = samples in this dp replica.
+
+        Under Megatron-SP the saved norm outputs are this rank's token shards (n1, n2),
+        as the cost model counts them (replicated activations / tp, costmodel.py:162-175);
+        the backward all-gathers them again, overlapped with its dgrad GEMMs (Megatron
+        does the same).  A recompute replay (keep_gathered) keeps the gathered copies:
+        only one layer's activations are alive then."""
         cfg = self.cfg
         S = cfg.seq_len
         flat = self.store.materialize()
@@ -353,8 +359,10 @@ class DecoderLayer:
             K.bias_add_(m, w["fc2.bias"])
         y = K.axpby(h1, m, 1.0, 1.0)
         if save:
-            saved = dict(x=x, st1=st1, n1f=n1f, qkv=qkv, o=o, o_full=o_full, lse=lse, h1=h1,
-                         st2=st2, n2f=n2f, act=act, B=B)
+            regather = self.s.sp and not self.uly and self.tp > 1 and not keep_gathered
+            saved = dict(x=x, st1=st1, n1f=n1 if regather else n1f, qkv=qkv, o=o,
+                         o_full=o_full, lse=lse, h1=h1, st2=st2,
+                         n2f=n2 if regather else n2f, act=act, B=B, regather=regather)
             saved["pre"] = f1 if gpt else gu
             return y, saved
         return y, None
@@ -374,7 +382,7 @@ class DecoderLayer:
         cfg = self.cfg
         if ctx.saved is None:
             x, B = ctx.x
-            _, sv = self.forward_impl(x, B, save=True)
+            _, sv = self.forward_impl(x, B, save=True, keep_gathered=True)
         else:
             sv = ctx.saved
         ctx.saved = ctx.x = None
@@ -388,6 +396,11 @@ class DecoderLayer:
         B = sv["B"]
         # ---- MLP
         dmf = self._gather_seq(dy)
+        n2f = n2_work = n1f = n1_work = None
+        if sv["regather"]:  # SP: re-gather the norm-2 output behind the dgrad GEMM
+            n2f, n2_work = comm.all_gather_async(sv["n2f"], self.tpg)
+        else:
+            n2f = sv["n2f"]
         if gpt:
             K.colsum(dy, sg["fc2.bias"])
             if _fuse_bwd(dmf):  # GeLU bwd fused into the fc2 dgrad epilogue
@@ -401,7 +414,9 @@ class DecoderLayer:
             if _fuse_bwd(dmf):
                 K.colsum(dpre, sg["fc1.bias"])
             dn2 = self._row_gemm(dpre, w["fc1.weight"], trans_b=False)
-            _wgrad(dpre, sv["n2f"], gw["fc1.weight"])
+            if n2_work is not None:
+                n2_work.wait()
+            _wgrad(dpre, n2f, gw["fc1.weight"])
         else:
             if _fuse_bwd(dmf):  # SwiGLU bwd fused into the down dgrad epilogue
                 dpre = K.gemm_swiglu_bwd(dmf, w["down.weight"], sv["pre"])
@@ -411,12 +426,18 @@ class DecoderLayer:
                 del dact
             _wgrad(dmf, sv["act"], gw["down.weight"])
             dn2 = self._row_gemm(dpre, w["gate_up.weight"], trans_b=False)
-            _wgrad(dpre, sv["n2f"], gw["gate_up.weight"])
-        del dpre, dmf
+            if n2_work is not None:
+                n2_work.wait()
+            _wgrad(dpre, n2f, gw["gate_up.weight"])
+        del dpre, dmf, n2f
         dh1 = self._norm_bwd(sv["h1"], w, sv["st2"], dn2, "mlp_norm", sg, dres=dy)
         del dn2
         # ---- attention
         daf = self._gather_seq(dh1)
+        if sv["regather"]:  # norm-1 output, behind the attention backward
+            n1f, n1_work = comm.all_gather_async(sv["n1f"], self.tpg)
+        else:
+            n1f = sv["n1f"]
         if gpt:
             K.colsum(dh1, sg["proj.bias"])
         do = _dgrad(daf, w["proj.weight"])
@@ -450,8 +471,10 @@ class DecoderLayer:
         if gpt:
             K.colsum(dqkv, sg["qkv.bias"])
         dn1 = self._row_gemm(dqkv, w["qkv.weight"], trans_b=False)
-        _wgrad(dqkv, sv["n1f"], gw["qkv.weight"])
-        del dqkv
+        if n1_work is not None:
+            n1_work.wait()
+        _wgrad(dqkv, n1f, gw["qkv.weight"])
+        del dqkv, n1f
         dx = self._norm_bwd(sv["x"], w, sv["st1"], dn1, "attn_norm", sg, dres=dh1)
         self.store.release()
         self.store.finish_microbatch(gflat, self.tp_partial, self.tpg)
