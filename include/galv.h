@@ -210,6 +210,13 @@ int32_t galv_embed_fwd(const int64_t* ids, const void* table, void* out, int64_t
 int32_t galv_embed_bwd(const int64_t* ids, const void* dout, float* dtable_acc, int64_t T,
                        int64_t V_local, int64_t vocab_lo, int64_t Hd, int32_t dtype,
                        void* stream);
+/* Deterministic embedding backward: ids sorted (stable) with their token order; grad rows
+ * of this vocab shard += the fp32 sum of their dout rows, stored in grad_dtype (bf16/f32).
+ * Replaces the fp32 scatter table + atomics of galv_embed_bwd on the training path. */
+int32_t galv_embed_bwd_sorted(const int64_t* sorted_ids, const int64_t* order,
+                              const void* dout, void* grad, int64_t T, int64_t V_local,
+                              int64_t vocab_lo, int64_t Hd, int32_t dtype, int32_t grad_dtype,
+                              void* stream);
 
 /* Vocab-parallel cross entropy over a logits shard [T, V_local].
  *  stage 0: row max -> stats[T*3+0] ; (caller all-reduces MAX over tp)

@@ -36,6 +36,60 @@ __global__ void embed_bwd(const int64_t* __restrict__ ids, const T* __restrict__
     atomicAdd(&dtable[id * Hd + c], to_f(dout[t * Hd + c]));
 }
 
+// Deterministic embedding backward over token ids sorted by id (stable): the CTA at the
+// first position of each id's run sums that id's dout rows in fp32 registers (each thread
+// owns 8 columns per 2048-column chunk) and adds the sum once into the gradient row, in the
+// gradient's own dtype (bf16 or fp32).  No fp32 [V, h] scratch table, no atomics: dout is
+// read once and each touched gradient row is read and written once.
+template <typename T, typename G>
+__global__ void __launch_bounds__(256) embed_bwd_sorted(const int64_t* __restrict__ sorted,
+                                                        const int64_t* __restrict__ order,
+                                                        const T* __restrict__ dout,
+                                                        G* __restrict__ grad, int64_t T_,
+                                                        int64_t V_local, int64_t lo,
+                                                        int64_t Hd) {
+  const int64_t t = blockIdx.x;
+  const int64_t key = sorted[t];
+  if (t > 0 && sorted[t - 1] == key) return;  // not the first of its run
+  const int64_t id = key - lo;
+  if (id < 0 || id >= V_local) return;        // another rank's vocab shard
+  int64_t end = t + 1;
+  while (end < T_ && sorted[end] == key) ++end;
+  for (int64_t c0 = threadIdx.x * 8; c0 < Hd; c0 += 256 * 8) {
+    float acc[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[i] = 0.f;
+    for (int64_t r = t; r < end; ++r) {
+      const T* row = dout + order[r] * Hd + c0;
+      float v[8];
+      if constexpr (sizeof(T) == 2) {
+        load16(row, v);
+      } else {
+        load16(row, v);
+        load16(row + 4, v + 4);
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[i] += v[i];
+    }
+    G* g = grad + id * Hd + c0;
+    float cur[8];
+    if constexpr (sizeof(G) == 2) {
+      load16(g, cur);
+    } else {
+      load16(g, cur);
+      load16(g + 4, cur + 4);
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) cur[i] += acc[i];
+    if constexpr (sizeof(G) == 2) {
+      store16(g, cur);
+    } else {
+      store16(g, cur);
+      store16(g + 4, cur + 4);
+    }
+  }
+}
+
 }  // namespace emb
 
 namespace xent {
@@ -122,6 +176,28 @@ int32_t galv_embed_bwd(const int64_t* ids, const void* dout, float* dtable, int6
   GALV_DISPATCH(dtype, T, {
     emb::embed_bwd<T><<<(unsigned)T_, 256, 0, as_stream(stream)>>>(ids, (const T*)dout, dtable,
                                                                   T_, V_local, vocab_lo, Hd);
+  });
+  GALV_LAUNCH_CHECK();
+  return 0;
+}
+
+int32_t galv_embed_bwd_sorted(const int64_t* sorted_ids, const int64_t* order, const void* dout,
+                              void* grad, int64_t T_, int64_t V_local, int64_t vocab_lo,
+                              int64_t Hd, int32_t dtype, int32_t grad_dtype, void* stream) {
+  GALV_CHECK_ARG(sorted_ids && order && dout && grad && T_ > 0 && Hd % 8 == 0, "bad arguments");
+  GALV_CHECK_ARG((reinterpret_cast<uintptr_t>(dout) & 15) == 0 &&
+                     (reinterpret_cast<uintptr_t>(grad) & 15) == 0,
+                 "dout and grad must be 16-byte aligned");
+  cudaStream_t s = as_stream(stream);
+  GALV_DISPATCH(dtype, T, {
+    if (grad_dtype == GALV_BF16)
+      emb::embed_bwd_sorted<T, __nv_bfloat16><<<(unsigned)T_, 256, 0, s>>>(
+          sorted_ids, order, (const T*)dout, (__nv_bfloat16*)grad, T_, V_local, vocab_lo, Hd);
+    else if (grad_dtype == GALV_F32)
+      emb::embed_bwd_sorted<T, float><<<(unsigned)T_, 256, 0, s>>>(
+          sorted_ids, order, (const T*)dout, (float*)grad, T_, V_local, vocab_lo, Hd);
+    else
+      GALV_CHECK_ARG(false, "grad dtype must be bf16 or f32");
   });
   GALV_LAUNCH_CHECK();
   return 0;

@@ -85,6 +85,7 @@ _SIGS = {
     "galv_colsum": ([_P, _P, _I64, _I64, _I32, _I32, _P, _P], _I32),
     "galv_embed_fwd": ([_P, _P, _P, _I64, _I64, _I64, _I64, _I32, _P], _I32),
     "galv_embed_bwd": ([_P, _P, _P, _I64, _I64, _I64, _I64, _I32, _P], _I32),
+    "galv_embed_bwd_sorted": ([_P, _P, _P, _P, _I64, _I64, _I64, _I64, _I32, _I32, _P], _I32),
     "galv_xent": ([_P, _P, _P, _P, _P, _I64, _I64, _I64, _F, _I64, _I32, _I32, _P], _I32),
     "galv_adamw": ([_P, _P, _P, _P, _P, _I64, _F, _F, _F, _F, _F, _F, _I64, _I32, _I32, _P],
                    _I32),
@@ -548,6 +549,15 @@ def embed_bwd(ids, dout, dtable_acc, vocab_lo=0):
     V, Hd = dtable_acc.shape
     _call("galv_embed_bwd", _ptr(ids), _ptr(dout), _ptr(dtable_acc), T, V, vocab_lo, Hd,
           dtype_code(dout.dtype), _stream())
+
+
+def embed_bwd_sorted(ids, dout, grad, vocab_lo=0):
+    """grad[V_local, h] (bf16 or fp32) += per-id sums of dout rows (deterministic)."""
+    sorted_ids, order = torch.sort(ids.reshape(-1), stable=True)
+    T = sorted_ids.numel()
+    V, Hd = grad.shape
+    _call("galv_embed_bwd_sorted", _ptr(sorted_ids), _ptr(order), _ptr(dout), _ptr(grad), T, V,
+          vocab_lo, Hd, dtype_code(dout.dtype), dtype_code(grad.dtype), _stream())
 
 
 def xent(logits, labels, stats, stage, *, loss=None, dlogits=None, vocab_lo=0, grad_scale=1.0,

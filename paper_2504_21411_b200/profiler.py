@@ -129,7 +129,65 @@ def measure_activation_bytes(cfg, microbatch: int) -> dict:
             "bytes_per_token_recompute": out["recompute"], "microbatch": microbatch}
 
 
-def fold_embedding_head(prof: P.ModelProfile, cfg) -> P.ModelProfile:
+def measure_working_set(cfg, microbatch: int) -> dict:
+    """Per-token bytes the step holds *beyond* the saved activations at its memory peak
+    (tp=1, pp=1): the peak is either the head (logits chunks, cross-entropy stats, dlogits
+    -> dx) on top of every layer's saved activations, or the last layer's backward (its
+    dy plus the backward temporaries: dgrads, dq|dk|dv, re-gathered inputs) while its own
+    saved activations are still alive.  Folded into the last layer's activation term
+    (fold_embedding_head) so the unchanged cost model's stage peak covers it."""
+    from .runtime.config import HybridConfig
+    from .runtime.init import layer_param_shapes
+    from .runtime.layers import DecoderLayer, Head
+    from .runtime.topology import Topology
+    one = cfg.with_(n_layers=1)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    T = microbatch * cfg.seq_len
+    s = ParallelStrategy(1, 1, 0, False, False)
+    hc = HybridConfig(pp=1, microbatch=microbatch, n_microbatches=1, stage_ranges=((0, 1),),
+                      layer_strategies=(s,))
+    topo = Topology(hc, rank=0, world=1)
+    kw = dict(dtype=torch.bfloat16, grad_dtype=torch.bfloat16, device=dev)
+    layer = DecoderLayer(one, 0, s, topo, **kw)
+    layer.store.load({n: 0.02 * torch.ones(shp, device=dev)
+                      for n, shp in layer_param_shapes(one).items()})
+    x = torch.randn(T, cfg.hidden, device=dev, dtype=torch.bfloat16)
+    for _ in range(2):  # the second pass runs with warm allocator / tables / workspaces
+        y, ctx = layer.forward(x, microbatch)
+        del y
+        torch.cuda.synchronize()
+        m_saved = torch.cuda.memory_allocated()
+        dy = torch.randn_like(x) * 1e-3
+        torch.cuda.reset_peak_memory_stats()
+        dx = layer.backward(dy, ctx)
+        torch.cuda.synchronize()
+        layer_ws = torch.cuda.max_memory_allocated() - m_saved  # dy + temporaries (+ dx)
+        del dx, ctx, dy
+    del layer
+    head = Head(cfg, s, topo, **kw)
+    head.store.load({n: (0.02 if n == "lm_head.weight" else 1.0) *
+                     torch.ones(shp, device=dev) for n, (_, shp) in head.store.layout.items()})
+    labels = torch.randint(0, cfg.vocab, (T,), device=dev)
+    for _ in range(2):
+        torch.cuda.synchronize()
+        m0 = torch.cuda.memory_allocated()
+        torch.cuda.reset_peak_memory_stats()
+        loss, dx = head.forward_backward(x, labels, 1.0 / T)
+        torch.cuda.synchronize()
+        # logits chunk, stats, dn, dx + the head's input (the last layer's output y, which
+        # no layer saves)
+        head_ws = torch.cuda.max_memory_allocated() - m0 + x.numel() * x.element_size()
+        del loss, dx
+    del head
+    torch.cuda.synchronize()
+    return {"layer_backward_bytes_per_token": layer_ws / T,
+            "head_bytes_per_token": head_ws / T,
+            "working_set_bytes_per_token": max(layer_ws, head_ws) / T,
+            "microbatch": microbatch}
+
+
+def fold_embedding_head(prof: P.ModelProfile, cfg, working_set_per_token: float = 0.0
+                        ) -> P.ModelProfile:
     """Charge the embedding and the LM head to the planned layers that share their
     strategy (the runtime builds them on layer 0's / layer L-1's tp and dp groups,
     runtime/engine.py): layer 0 gains the embedding tables' parameters, layer L-1 the
@@ -138,22 +196,29 @@ def fold_embedding_head(prof: P.ModelProfile, cfg) -> P.ModelProfile:
     embedding/head layers, so without this the cost model under-predicts
     by the head's share of the step (13% on GPT-2-medium, 9% on GPT-1.3B) and the
     memory prediction misses 16 B/param of vocab tables.  Approximation: the tables
-    are dp-replicated (z0) in the runtime but inherit the layer's zero stage here."""
+    are dp-replicated (z0) in the runtime but inherit the layer's zero stage here.
+
+    ``working_set_per_token`` (measure_working_set) is added to the last layer's
+    tp-shardable activation bytes: the step's peak is the saved activations plus this
+    working set, and the last layer's stage is where it occurs (pp=1: every stage is the
+    last; pp>1: the head's stage holds one microbatch in flight).  Residual: when the last
+    layer itself recomputes, the cost model charges it boundary bytes only and the
+    working set (and the replayed layer's activations) fall outside the prediction."""
     L, h, V = cfg.n_layers, cfg.hidden, cfg.vocab
     emb = V * h + (cfg.seq_len * h if cfg.arch == "gpt" else 0)
     head = V * h + h * (2 if cfg.arch == "gpt" else 1)
     layers = list(prof.layers)
 
-    def bump(lp, params, fpt):
+    def bump(lp, params, fpt, ws=0.0):
         return P.LayerProfile(
             param_count=lp.param_count + params, flops_per_token=lp.flops_per_token + fpt,
             flops_per_token_sq=lp.flops_per_token_sq,
-            act_shardable_bytes_per_token=lp.act_shardable_bytes_per_token,
+            act_shardable_bytes_per_token=lp.act_shardable_bytes_per_token + ws,
             act_replicated_bytes_per_token=lp.act_replicated_bytes_per_token,
             boundary_bytes_per_token=lp.boundary_bytes_per_token)
 
     layers[0] = bump(layers[0], emb, 0)
-    layers[L - 1] = bump(layers[L - 1], head, 2 * h * V)
+    layers[L - 1] = bump(layers[L - 1], head, 2 * h * V, float(working_set_per_token))
     out = P.ModelProfile(n_layers=prof.n_layers, hidden_size=prof.hidden_size,
                          seq_len=prof.seq_len, layers=tuple(layers))
     out.validate()
@@ -185,7 +250,7 @@ def calibrated_model_profile(cfg, act: dict) -> P.ModelProfile:
     prof = P.ModelProfile(n_layers=base.n_layers, hidden_size=base.hidden_size,
                           seq_len=base.seq_len, layers=(layer,) * base.n_layers)
     prof.validate()
-    return fold_embedding_head(prof, cfg)
+    return fold_embedding_head(prof, cfg, act.get("working_set_bytes_per_token", 0.0))
 
 
 def measure_collectives(sizes=(2 ** 20, 2 ** 24, 2 ** 28)) -> dict:
@@ -220,9 +285,10 @@ def measure_collectives(sizes=(2 ** 20, 2 ** 24, 2 ** 28)) -> dict:
 
 
 def build_cluster(n_devices: int, device_flops: float, table: dict, *,
-                  reserve: float = 0.1) -> P.ClusterProfile:
-    mem = torch.cuda.get_device_properties(0).total_memory if torch.cuda.is_available() \
-        else 180_000_000_000
+                  reserve: float = 0.1, memory: int | None = None) -> P.ClusterProfile:
+    mem = memory if memory is not None else (
+        torch.cuda.get_device_properties(0).total_memory if torch.cuda.is_available()
+        else 180_000_000_000)
     entries = tuple(P.BandwidthEntry("intra_node", g, v["bus_bandwidth"], v["latency"])
                     for g, v in sorted(table.items()))
     c = P.ClusterProfile(n_devices, min(n_devices, 8), float(device_flops), int(mem), reserve,
@@ -238,6 +304,11 @@ def main(argv=None) -> int:
     ap.add_argument("--microbatch", type=int, default=2)
     ap.add_argument("--devices", type=int, default=8, help="n_devices written to the profile")
     ap.add_argument("--reserve", type=float, default=0.1)
+    ap.add_argument("--device-memory", type=int, default=None,
+                    help="device_memory_bytes to write (default: this GPU's total HBM); "
+                         "BASELINE C5 plans under 180e9 with --reserve 0")
+    ap.add_argument("--flops-from", default=None,
+                    help="reuse device_flops of this cluster profile (skip the layer timing)")
     ap.add_argument("--table-from", default=None, help="reuse the bandwidth table of a profile")
     ap.add_argument("--model-out", default=None,
                     help="also write the activation-calibrated ModelProfile of --model here")
@@ -260,6 +331,7 @@ def main(argv=None) -> int:
     if rank == 0 and args.model_out:
         cfg = MODEL_PRESETS[args.model]
         act = measure_activation_bytes(cfg, args.microbatch)
+        act.update(measure_working_set(cfg, args.microbatch))
         P.save_profiles(args.model_out, model=calibrated_model_profile(cfg, act))
         with open(os.path.splitext(args.model_out)[0] + ".meta.json", "w") as fh:
             json.dump({"model": args.model, "activation": act}, fh, indent=1)
@@ -267,13 +339,20 @@ def main(argv=None) -> int:
         if args.skip_flops:
             return 0
     if rank == 0:
-        lay = measure_layer_flops(MODEL_PRESETS[args.model], args.microbatch)
+        if args.flops_from:
+            lay = {"device_flops": P.load_cluster_profile(args.flops_from).device_flops,
+                   "from": args.flops_from}
+        else:
+            lay = measure_layer_flops(MODEL_PRESETS[args.model], args.microbatch)
         if not table:  # single GPU: NVLink table from the pool's published measurements
             table = {g: {"bus_bandwidth": 725e9, "latency": 5e-6} for g in (2, 4, 8)}
-        cluster = build_cluster(args.devices, lay["device_flops"], table, reserve=args.reserve)
+        cluster = build_cluster(args.devices, lay["device_flops"], table, reserve=args.reserve,
+                                memory=args.device_memory)
         P.save_profiles(args.output, cluster=cluster)
         meta = {"layer": lay, "table": {str(k): v for k, v in table.items()},
-                "model": args.model, "microbatch": args.microbatch, "world": world}
+                "model": args.model, "microbatch": args.microbatch, "world": world,
+                "device_memory_bytes": cluster.device_memory_bytes,
+                "memory_reserve_fraction": cluster.memory_reserve_fraction}
         with open(os.path.splitext(args.output)[0] + ".meta.json", "w") as fh:
             json.dump(meta, fh, indent=1)
         print(json.dumps(meta))

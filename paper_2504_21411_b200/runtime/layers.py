@@ -497,7 +497,6 @@ class Embedding:
             entries.append(("pos_embed.weight", (cfg.seq_len, cfg.hidden)))
         self.store = ParamStore(entries, dtype=dtype, grad_dtype=grad_dtype, device=device,
                                 dp=self.dpg, zero=0)
-        self.dtable = None
 
     def forward(self, ids):
         """ids: [T_rep] int64 (this dp replica's tokens) -> [T_in, h] in layer-0 layout."""
@@ -519,11 +518,9 @@ class Embedding:
         dxf = comm.all_gather(dx, self.tpg) if (self.s.sp and self.tp > 1) else dx
         gflat = self.store.grad_target()
         gw = self.store.views(gflat)
-        if self.dtable is None:
-            self.dtable = torch.zeros(self.vl, cfg.hidden, dtype=torch.float32, device=dx.device)
-        K.embed_bwd(ids, dxf, self.dtable, vocab_lo=self.tpr * self.vl)
-        K.axpby(self.dtable, gw["embed.weight"], 1.0, 1.0)
-        self.dtable.zero_()
+        # deterministic sorted segment-sum straight into the (bf16 or fp32) grad rows: no
+        # fp32 [V, h] scratch table (it would sit outside the cost model's grad bytes)
+        K.embed_bwd_sorted(ids, dxf, gw["embed.weight"], vocab_lo=self.tpr * self.vl)
         if cfg.arch == "gpt":
             S = cfg.seq_len
             T = dx.shape[0]
@@ -538,6 +535,18 @@ class Embedding:
 
 
 # ---------------------------------------------------------------------------- head
+
+
+HEAD_CHUNKS = 4
+
+
+def _head_chunks(T: int, v_local: int, elt: int):
+    """HEAD_CHUNKS token ranges (multiples of 128 rows, so each chunk's GEMMs keep whole
+    128-row tiles): the [rows, V/tp] logits working set is a fixed fraction of the tokens,
+    i.e. a per-token constant, which is how the cost model's activation terms scale."""
+    step = -(-T // HEAD_CHUNKS)
+    step = -(-step // 128) * 128
+    return [(a, min(T, a + step)) for a in range(0, T, step)]
 
 
 class Head:
@@ -574,29 +583,33 @@ class Head:
         sp = self.s.sp and self.tp > 1
         nf = comm.all_gather(n, self.tpg) if sp else n
         T = nf.shape[0]
-        logits = _linear(nf, w["lm_head.weight"])
         stats = torch.empty(T, 3, dtype=torch.float32, device=x.device)
         loss = torch.empty(T, dtype=torch.float32, device=x.device)
+        dnf = torch.empty_like(nf)
         lo = self.tpr * self.vl
-        if self.tp == 1:
-            K.xent(logits, labels, stats, 3, loss=loss, dlogits=logits, vocab_lo=lo,
-                   grad_scale=grad_scale)
-        else:
-            import torch.distributed as dist
-            K.xent(logits, labels, stats, 0, vocab_lo=lo)
-            mx = stats[:, 0].contiguous()
-            comm.all_reduce(mx, self.tpg, op=dist.ReduceOp.MAX)
-            stats[:, 0] = mx
-            K.xent(logits, labels, stats, 1, vocab_lo=lo)
-            part = stats[:, 1:3].contiguous()
-            comm.all_reduce(part, self.tpg)
-            stats[:, 1:3] = part
-            K.xent(logits, labels, stats, 2, loss=loss, dlogits=logits, vocab_lo=lo,
-                   grad_scale=grad_scale)
-        dlogits = logits
-        dnf = _dgrad(dlogits, w["lm_head.weight"])
-        _wgrad(dlogits, nf, gw["lm_head.weight"])
-        del logits, dlogits
+        # token chunks bound the [tokens, V/tp] logits working set (HEAD_CHUNK_BYTES): each
+        # chunk runs GEMM -> cross-entropy (dlogits in place) -> dgrad -> wgrad accumulate
+        for a, b in _head_chunks(T, self.vl, nf.element_size()):
+            logits = _linear(nf[a:b], w["lm_head.weight"])
+            st, ls, lab = stats[a:b], loss[a:b], labels[a:b]
+            if self.tp == 1:
+                K.xent(logits, lab, st, 3, loss=ls, dlogits=logits, vocab_lo=lo,
+                       grad_scale=grad_scale)
+            else:
+                import torch.distributed as dist
+                K.xent(logits, lab, st, 0, vocab_lo=lo)
+                mx = st[:, 0].contiguous()
+                comm.all_reduce(mx, self.tpg, op=dist.ReduceOp.MAX)
+                st[:, 0] = mx
+                K.xent(logits, lab, st, 1, vocab_lo=lo)
+                part = st[:, 1:3].contiguous()
+                comm.all_reduce(part, self.tpg)
+                st[:, 1:3] = part
+                K.xent(logits, lab, st, 2, loss=ls, dlogits=logits, vocab_lo=lo,
+                       grad_scale=grad_scale)
+            _dgrad(logits, w["lm_head.weight"], out=dnf[a:b])
+            _wgrad(logits, nf[a:b], gw["lm_head.weight"])
+            del logits
         if self.tp > 1:
             dn = comm.reduce_scatter(dnf, self.tpg) if sp else comm.all_reduce(dnf, self.tpg)
         else:

@@ -267,3 +267,29 @@ def test_bias_gelu_bwd_colsum(dt, rows, cols):
     torch.nn.functional.gelu(xf, approximate="tanh").backward(dy.float())
     assert rel(dx, xf.grad) < tol(dt)
     assert rel(db - 0.25, xf.grad.sum(0)) < tol(dt)
+
+
+@pytest.mark.parametrize("gdt", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("dt", DT)
+def test_embed_bwd_sorted(dt, gdt):
+    """Deterministic sorted segment-sum embedding backward into a vocab shard's grad rows
+    (bf16 or fp32), vs an fp64 index_add; repeated ids (runs) and ids of other shards."""
+    from paper_2504_21411_b200 import kernels as K
+    torch.manual_seed(11)
+    T, V, Hd, lo, Vl = 3000, 512, 4096 + 8 * 3, 128, 256
+    ids = torch.randint(0, V, (T,), device="cuda")
+    ids[:100] = 200  # a long run of one id
+    dout = torch.randn(T, Hd, device="cuda").to(dt)
+    base = torch.randn(Vl, Hd, device="cuda")
+    grad = base.to(gdt).clone()
+    K.embed_bwd_sorted(ids, dout, grad, vocab_lo=lo)
+    ref = base.to(gdt).double().clone()
+    mine = (ids >= lo) & (ids < lo + Vl)
+    ref.index_add_(0, (ids[mine] - lo), dout[mine].double())
+    assert rel(grad, ref) < (1e-6 if gdt == torch.float32 else 5e-3)
+    untouched = torch.ones(Vl, dtype=torch.bool, device="cuda")
+    untouched[(ids[mine] - lo).unique()] = False
+    assert torch.equal(grad[untouched], base.to(gdt)[untouched])
+    again = base.to(gdt).clone()
+    K.embed_bwd_sorted(ids, dout, again, vocab_lo=lo)
+    assert torch.equal(again, grad)  # deterministic
