@@ -131,7 +131,7 @@ class ClockSampler:
 
 # cluster profiles calibrated on each model's own layer (profiles/*.meta.json); llama2-13b's
 # at seq 32K (config C5), gpt2-medium's at seq 1024 (C2); everything else uses the 7B one
-CLUSTER_PROFILES = {"llama2-13b": "b200_cluster_llama13b.json",
+CLUSTER_PROFILES = {"llama2-13b": "b200_cluster_llama13b_180g.json",  # C5: 180e9, reserve 0
                     "gpt2-medium": "b200_cluster_gpt2m.json"}
 
 

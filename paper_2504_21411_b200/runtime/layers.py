@@ -169,7 +169,6 @@ class DecoderLayer:
                 T = topo.hc.microbatch // strategy.dp * cfg.seq_len
                 self.peer = nvlink.peer_buffers(self.tpg, T * max(cfg.hidden, 1) * 2, device)
         self.scale = 1.0 / math.sqrt(cfg.head_dim)
-        self._ws = None
 
     def param_prefix(self) -> str:
         return f"layers.{self.index}."
@@ -450,15 +449,16 @@ class DecoderLayer:
         dqkv = torch.empty_like(qkv)
         q, k, v = self._attn_views(qkv, B, S)
         dq, dk, dv = self._attn_views(dqkv, B, S)
-        need = K.attn_bwd_workspace_bytes(B, S, self.Hl, cfg.head_dim, qkv.dtype)
-        if self._ws is None or self._ws.numel() < need:
-            self._ws = torch.empty(need, dtype=torch.uint8, device=qkv.device)
+        # transient (caching allocator): part of the measured backward working set, not a
+        # per-layer resident buffer outside the cost model
+        ws = torch.empty(K.attn_bwd_workspace_bytes(B, S, self.Hl, cfg.head_dim, qkv.dtype),
+                         dtype=torch.uint8, device=qkv.device)
         # Llama, head_dim 128: dq / dk come back through the inverse RoPE of q / k in the
         # same C-ABI call (galv_attn_bwd_rope; its default variant is the streaming pass)
         rope_fused = not gpt and cfg.head_dim == 128 and qkv.dtype == torch.bfloat16
         K.attn_bwd(q, k, v, sv["o_full"].view(B, S, self.Hl, cfg.head_dim),
                    do.view(B, S, self.Hl, cfg.head_dim), sv["lse"], dq, dk, dv,
-                   scale=self.scale, causal=True, workspace=self._ws,
+                   scale=self.scale, causal=True, workspace=ws,
                    rope_theta=cfg.rope_theta if rope_fused else None,
                    rope_epilogue=ROPE_BWD_EPILOGUE)
         del do
