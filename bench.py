@@ -50,6 +50,9 @@ def parse():
     ap.add_argument("--plan-out", default=None)
     ap.add_argument("--trace-out", default=None,
                     help="write the measured step timeline (pipesim JSONL schema) + sim diff")
+    ap.add_argument("--report-out", default=None,
+                    help="write the measured-vs-predicted per-layer/per-stage report "
+                         "(reference build_report bundle + measured columns) to PATH.json/.csv")
     ap.add_argument("--layer-pattern", default=None,
                     help="explicit per-layer strategies instead of the search, cycled over "
                          "layers, e.g. 'tp8,dp8z3,tp4dp2' (BASELINE config 4)")
@@ -171,11 +174,30 @@ def model_profile(cfg):
     return planned_profile(cfg)
 
 
+def training_config(cfg, n: int, global_batch: int):
+    """TrainingConfig for the search: bytes per param/grad/optimizer state at the cost-model
+    defaults and comm_overlap_fraction as measured by the profiler for this model at this
+    world size (profiles/b200_training_<model>_n<N>.json, `profiler --overlap-out`); N
+    beyond the largest measured world uses that world's fraction; none measured -> 0."""
+    from paper_2504_21411_b200.planner.profiles import TrainingConfig, load_training_config
+    best = None
+    for k in (1, 2, 4, 8, 16):
+        path = os.path.join(ROOT, "profiles", f"b200_training_{cfg.name}_n{k}.json")
+        if k <= n and os.path.exists(path):
+            best = path
+    if n == 1 or best is None:
+        return TrainingConfig(global_batch=global_batch), "comm_overlap_fraction 0 (no dp sync)" \
+            if n == 1 else "comm_overlap_fraction 0 (not measured)"
+    f = load_training_config(best).comm_overlap_fraction
+    return (TrainingConfig(global_batch=global_batch, comm_overlap_fraction=f),
+            f"comm_overlap_fraction {f:.4f} measured ({os.path.relpath(best, ROOT)})")
+
+
 def plan_for(cfg, n: int, global_batch: int, cluster):
     from paper_2504_21411_b200.planner.profiles import TrainingConfig
     from paper_2504_21411_b200.planner.search import SearchConfig, optimize
     from paper_2504_21411_b200.runtime.config import get_hybrid_parallel_configs, profile_for
-    training = TrainingConfig(global_batch=global_batch)
+    training, _ = training_config(cfg, n, global_batch)
     mp = model_profile(cfg)
     plan = optimize(mp, cluster, training, SearchConfig())
     return plan, get_hybrid_parallel_configs(plan, cfg, model_profile=mp, cluster=cluster,
@@ -204,7 +226,7 @@ def explicit_plan(cfg, n, global_batch, cluster, pattern, microbatch, pp=1):
     from paper_2504_21411_b200.runtime.config import get_hybrid_parallel_configs, profile_for
     strats = parse_pattern(pattern, n // pp)
     layers = [strats[i % len(strats)] for i in range(cfg.n_layers)]
-    training = TrainingConfig(global_batch=global_batch)
+    training, _ = training_config(cfg, n, global_batch)
     mp = model_profile(cfg)
     plan = make_plan(mp, cluster, training, pp, microbatch, layers)
     # hand-written plans are validated like searched ones: over budget -> InvalidPlan
@@ -256,7 +278,116 @@ def memory_breakdown(plan, model, cluster, training, peak_gb, persistent_bytes):
             "peak_within_prediction": peak_gb * 1e9 <= plan.predicted_stage_peak_memory[st]}
 
 
+def write_report(path, plan, model, cluster, training, tokens, rank):
+    """One instrumented step (per-layer CUDA events + step marks) -> report.py bundle."""
+    import torch
+    from paper_2504_21411_b200.report import measured_report, report_to_csv
+    from paper_2504_21411_b200.planner.serialize import dumps_canonical
+    model.layer_events.clear()
+    model.trace.clear()
+    model.record_layers = model.record_trace = True
+    torch.cuda.reset_peak_memory_stats()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    model.train_step(tokens)
+    model.wait_optimizer()
+    b.record()
+    torch.cuda.synchronize()
+    model.record_layers = model.record_trace = False
+    marks = {kind: ev for kind, _, ev in model.trace}
+    exposed = marks["dp_sync"].elapsed_time(marks["end"]) / 1e3 if "dp_sync" in marks else None
+    peak = torch.cuda.max_memory_allocated() + sum(p.nbytes for p in model.dp_pools)
+    bundle = measured_report(plan, model_profile(model.cfg), cluster, training,
+                             stage=model.stage, layer_times=model.layer_times(),
+                             iteration_s=a.elapsed_time(b) / 1e3, dp_sync_exposed_s=exposed,
+                             peak_memory_bytes=peak)
+    out = f"{path}.rank{rank}" if rank else path
+    if rank == 0 or model.topo.stage_group.index == 0:
+        with open(out + ".json", "w") as fh:
+            fh.write(dumps_canonical(bundle, sort_keys=False))
+        with open(out + ".csv", "w") as fh:
+            fh.write(report_to_csv(bundle))
+    st = [r for r in bundle["stages"] if r["stage"] == model.stage][0]
+    return {"file": out + ".json", "stage": model.stage,
+            "stage_per_microbatch_error": st.get("relative_error"),
+            "iteration_error": bundle["total"]["relative_error"],
+            "max_abs_layer_error": bundle["total"]["max_abs_layer_error"],
+            "layers_within_10pct": f"{bundle['total']['layers_within_10pct']}/"
+                                   f"{bundle['total']['layers_measured']}"}
+
+
 # ----------------------------------------------------------------------------- CPU arm
+
+_REF_PLANNER = r"""
+import hashlib, json, os, sys, time
+import hybridplan
+from hybridplan import profiles as P, search, pipesim
+from hybridplan.serialize import dumps_canonical
+args = json.loads(sys.argv[1])
+assert os.path.realpath(hybridplan.__file__).startswith(os.path.realpath(args["ref_dir"]))
+model = P.load_model_profile(args["model"])
+cluster = P.load_cluster_profile(args["cluster"])
+training = P.TrainingConfig(global_batch=args["global_batch"],
+                            comm_overlap_fraction=args["overlap"])
+out = {"hybridplan": os.path.dirname(hybridplan.__file__)}
+for jobs in args["jobs"]:
+    t0 = time.perf_counter()
+    plan = search.optimize(model, cluster, training, search.SearchConfig(jobs=jobs))
+    out[f"optimize_s_jobs{jobs}"] = time.perf_counter() - t0
+text = dumps_canonical(plan.to_dict(), sort_keys=False)
+out["plan_sha256"] = hashlib.sha256(text.encode()).hexdigest()
+out["predicted_iteration_time"] = plan.predicted_iteration_time
+t0 = time.perf_counter()
+sim = pipesim.simulate(plan, model, cluster, training)
+out["simulate_s"] = time.perf_counter() - t0
+out["sim_makespan"] = sim.makespan
+print(json.dumps(out))
+"""
+
+
+def reference_planner_timing(cfg, n: int, global_batch: int, cluster_path: str) -> dict:
+    """the reference's own optimize() (ref search.py:663; --jobs pool at
+    search.py:605-610) and simulate() (pipesim.py:132), run from the unmodified package
+    installed in baseline/_ref, timed on this host's cores -- single-threaded and with
+    jobs = cores -- on the exact committed B200 profile JSON, next to this repository's
+    planner on the same inputs (the plans must be byte-identical)."""
+    import hashlib
+    import tempfile
+    from paper_2504_21411_b200.planner import profiles as P
+    from paper_2504_21411_b200.planner.search import SearchConfig, optimize
+    from paper_2504_21411_b200.planner.serialize import dumps_canonical
+    ref_dir = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref_dir, "hybridplan")):
+        return {"unavailable": "baseline/_ref not installed (see DESIGN.md §6)"}
+    model_path = os.path.join(ROOT, "profiles", f"b200_model_{cfg.name}.json")
+    if not os.path.exists(model_path):
+        return {"unavailable": f"no committed model profile for {cfg.name}"}
+    cluster, shown = cluster_profile(n, cluster_path)
+    cores = len(os.sched_getaffinity(0))
+    with tempfile.TemporaryDirectory() as td:
+        cpath = os.path.join(td, "cluster.json")
+        P.save_profiles(cpath, cluster=cluster)
+        training, tsrc = training_config(cfg, n, global_batch)
+        arg = json.dumps({"ref_dir": ref_dir, "model": model_path, "cluster": cpath,
+                          "global_batch": global_batch, "jobs": [1, cores],
+                          "overlap": training.comm_overlap_fraction})
+        r = subprocess.run([sys.executable, "-c", _REF_PLANNER, arg], cwd=ref_dir,
+                           capture_output=True, text=True, timeout=600,
+                           env={**os.environ, "PYTHONPATH": ref_dir})
+    if r.returncode != 0:
+        return {"unavailable": "reference planner failed: " + r.stderr.strip()[-300:]}
+    ref = json.loads(r.stdout.strip().splitlines()[-1])
+    mp = P.load_model_profile(model_path)
+    t0 = time.perf_counter()
+    plan = optimize(mp, cluster, training, SearchConfig())
+    ours_s = time.perf_counter() - t0
+    sha = hashlib.sha256(dumps_canonical(plan.to_dict(), sort_keys=False).encode()).hexdigest()
+    return {"inputs": {"model": os.path.relpath(model_path, ROOT), "cluster": shown,
+                       "n_devices": n, "global_batch": global_batch, "training": tsrc},
+            "cores": cores, "reference": ref, "ours_optimize_s_jobs1": ours_s,
+            "plans_byte_identical": sha == ref.get("plan_sha256")}
+
+
 
 
 def cpu_reference(cfg, steps: int, warmup: int):
@@ -307,6 +438,11 @@ def main():
             return 0
         steps, warm = max(1, min(args.steps, 3)), min(args.warmup, 3)  # ~5 s per CPU step
         tok_s, t1, cores, sample = cpu_reference(cfg, steps, warm)
+        # the search at this run's N and at the north star's 8 B200s
+        planner = {f"n{k}": reference_planner_timing(
+            cfg, k, args.seqs_per_gpu * k,
+            args.cluster_profile or default_cluster_profile(args.model))
+            for k in sorted({args.gpus, 8})}
         line = {"metric": metric, "value": tok_s, "unit": "tokens/s", "n_gpus": args.gpus,
                 "steps": steps, "warmup": warm, "ms_per_step": t1 * 1e3,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
@@ -317,7 +453,8 @@ def main():
                 "cpu_baseline": {"value": tok_s, "unit": "tokens/s", "cores": cores,
                                  "kind": "port", "sample": sample},
                 "e2e": {"value": tok_s, "unit": "tokens/s", "h2d_bytes_per_step": 0,
-                        "d2h_bytes_per_step": 0}}
+                        "d2h_bytes_per_step": 0},
+                "planner_cpu": planner}
         print(json.dumps(line), flush=True)
         return 0
 
@@ -460,6 +597,7 @@ def main():
         "measured_iteration_time_s": ms / 1e3,
         "prediction_error": (ms / 1e3 - plan.predicted_iteration_time) / plan.predicted_iteration_time,
         "cluster_profile": cluster_src,
+        "training_config": training_config(cfg, n, gb)[1],
         "model_profile": ("profiles/b200_model_%s.json (activation-calibrated)" % cfg.name
                           if os.path.exists(os.path.join(ROOT, "profiles",
                                                          "b200_model_%s.json" % cfg.name))
@@ -484,6 +622,9 @@ def main():
         "predicted_peak_mem_gb": max(plan.predicted_stage_peak_memory) / 1e9,
         "memory": memory_breakdown(plan, model, cluster, training, mem, persistent_bytes),
     }
+    if args.report_out:
+        line["report"] = write_report(args.report_out, plan, model, cluster, training,
+                                      tokens_dev, rank)
     if args.trace_out:
         model.record_trace = True
         model.trace.clear()
@@ -512,6 +653,10 @@ def main():
         tok_s, t1, cores, sample = cpu_reference(cfg, 1, 0)
         line["cpu_baseline"] = {"value": tok_s, "unit": "tokens/s", "cores": cores,
                                 "kind": "port", "sample": sample}
+        # the reference planner itself (baseline/_ref) on the committed profiles, N=8
+        line["planner_cpu"] = {"n8": reference_planner_timing(
+            cfg, 8, args.seqs_per_gpu * 8,
+            args.cluster_profile or default_cluster_profile(args.model))}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -284,6 +284,73 @@ def measure_collectives(sizes=(2 ** 20, 2 ** 24, 2 ** 28)) -> dict:
     return out
 
 
+def measure_dp_overlap(cfg, cluster, global_batch: int, *, steps: int = 4,
+                       warmup: int = 2) -> dict:
+    """Measured ``comm_overlap_fraction`` (reference profiles.py:187, costmodel.py:265,
+    search.py:193): how much of the cost model's dp-sync time the runtime hides behind
+    compute.  Under torchrun, the searched plan for this world is run twice with the same
+    per-rank work -- with its dp collectives (reduce-scatter / all-reduce overlapped with
+    the backward, parameter all-gather fused into AdamW) and with them skipped
+    (params.SKIP_DP_SYNC, timing only) -- and
+
+        exposed = T_step(sync) - T_step(no sync)        (device time, max over ranks)
+        overlap = clamp(1 - exposed / max_stage(dp_sync_time), 0, 1)
+
+    with dp_sync_time the plan's modeled per-stage sync (overlap 0)."""
+    from .planner.search import SearchConfig, optimize
+    from .runtime import params as params_mod
+    from .runtime.config import get_hybrid_parallel_configs
+    from .runtime.engine import construct_hybrid_parallel_model
+    from .runtime.init import synthetic_tokens
+    model_prof = load_or_plan_profile(cfg)
+    training = P.TrainingConfig(global_batch=global_batch)
+    plan = optimize(model_prof, cluster, training, SearchConfig())
+    hc = get_hybrid_parallel_configs(plan, cfg)
+    model = construct_hybrid_parallel_model(cfg, hc, training=training, dtype=torch.bfloat16,
+                                            init="fast")
+    tokens = synthetic_tokens(cfg, global_batch).cuda()
+
+    def timed() -> float:
+        for _ in range(warmup):
+            model.train_step(tokens)
+        model.wait_optimizer()
+        torch.cuda.synchronize()
+        dist.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(steps):
+            model.train_step(tokens)
+        model.wait_optimizer()
+        b.record()
+        torch.cuda.synchronize()
+        t = torch.tensor([a.elapsed_time(b) / steps / 1e3], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.item()
+
+    t_sync = timed()
+    params_mod.SKIP_DP_SYNC = True
+    try:
+        t_nosync = timed()
+    finally:
+        params_mod.SKIP_DP_SYNC = False
+    modeled = max(c.dp_sync_time for c in plan.cost_breakdown)
+    exposed = t_sync - t_nosync
+    overlap = min(max(1.0 - exposed / modeled, 0.0), 1.0) if modeled > 0 else 0.0
+    return {"t_step_sync_s": t_sync, "t_step_nosync_s": t_nosync, "exposed_s": exposed,
+            "modeled_dp_sync_s": modeled, "comm_overlap_fraction": overlap,
+            "plan": [s.to_dict() for s in plan.layer_strategies[:1]],
+            "plan_microbatch": plan.microbatch, "world": dist.get_world_size()}
+
+
+def load_or_plan_profile(cfg) -> P.ModelProfile:
+    """The committed activation-calibrated model profile, else the analytic one."""
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                        "profiles", f"b200_model_{cfg.name}.json")
+    if os.path.exists(path):
+        return P.load_model_profile(path)
+    return planned_profile(cfg)
+
+
 def build_cluster(n_devices: int, device_flops: float, table: dict, *,
                   reserve: float = 0.1, memory: int | None = None) -> P.ClusterProfile:
     mem = memory if memory is not None else (
@@ -312,6 +379,12 @@ def main(argv=None) -> int:
     ap.add_argument("--table-from", default=None, help="reuse the bandwidth table of a profile")
     ap.add_argument("--model-out", default=None,
                     help="also write the activation-calibrated ModelProfile of --model here")
+    ap.add_argument("--overlap-out", default=None,
+                    help="under torchrun: measure comm_overlap_fraction of the searched "
+                         "plan for --model at this world size (--cluster-in) and write a "
+                         "TrainingConfig JSON here")
+    ap.add_argument("--cluster-in", default=None, help="cluster profile for --overlap-out")
+    ap.add_argument("--seqs-per-gpu", type=int, default=8)
     ap.add_argument("--skip-flops", action="store_true",
                     help="with --table-from + --model-out: only measure activations")
     args = ap.parse_args(argv)
@@ -322,12 +395,32 @@ def main(argv=None) -> int:
     table = {}
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        table = measure_collectives()
+        if not args.overlap_out:
+            table = measure_collectives()
     elif args.table_from:
         c = P.load_cluster_profile(args.table_from)
         table = {e.group_size: {"bus_bandwidth": e.bus_bandwidth, "latency": e.latency}
                  for e in c.bandwidth_table if e.span == "intra_node"}
     rank = dist.get_rank() if world > 1 else 0
+    if args.overlap_out:
+        if world < 2:
+            raise SystemExit("--overlap-out needs torchrun with >= 2 ranks")
+        c = P.load_cluster_profile(args.cluster_in)
+        table = tuple(e for e in c.bandwidth_table if e.group_size <= world)
+        c = P.ClusterProfile(world, min(c.devices_per_node, world), c.device_flops,
+                             c.device_memory_bytes, c.memory_reserve_fraction, table)
+        gb = args.seqs_per_gpu * world
+        res = measure_dp_overlap(MODEL_PRESETS[args.model], c, gb)
+        if rank == 0:
+            P.save_profiles(args.overlap_out, training=P.TrainingConfig(
+                global_batch=gb, comm_overlap_fraction=res["comm_overlap_fraction"]))
+            with open(os.path.splitext(args.overlap_out)[0] + ".meta.json", "w") as fh:
+                json.dump({"model": args.model, "cluster": args.cluster_in, **res}, fh,
+                          indent=1)
+            print(json.dumps(res))
+        dist.barrier()
+        dist.destroy_process_group()
+        return 0
     if rank == 0 and args.model_out:
         cfg = MODEL_PRESETS[args.model]
         act = measure_activation_bytes(cfg, args.microbatch)

@@ -66,6 +66,9 @@ class HybridParallelModel:
         self._opt_stream = None
         self.trace: list = []
         self.record_trace = False
+        # per-layer CUDA events (report.measured_report): (kind, layer, mb, start, end)
+        self.layer_events: list = []
+        self.record_layers = False
         self._init_params(seed, init, perturb, weights)
         # dp collectives of bf16 ZeRO-0/1/2 stores over NVLink/NVSwitch (symmetric pools)
         self.dp_pools = dp_nvlink.attach([st for _, st, _ in self.stores()], self.device)
@@ -116,13 +119,15 @@ class HybridParallelModel:
         cfg, hc = self.cfg, self.hc
         S = cfg.seq_len
         T = hc.microbatch * S
-        rec = {"ctxs": []}
+        rec = {"ctxs": [], "mb": k}
         if self.first:
             s0 = hc.layer_strategies[0]
             a, b = self._replica_slice(s0, T)
             ids = tokens[k, a:b, :S].reshape(-1)
             rec["ids"] = ids
+            ev = self._ev_start()
             x = self.embed.forward(ids)
+            self._ev_end(ev, "embed_fwd", 0, k)
         else:
             x = x_in
         prev = None
@@ -131,10 +136,14 @@ class HybridParallelModel:
                 self.layers[idx + 1].store.prefetch()
             lay = Layout.of(layer.s)
             if prev is not None and prev != lay:
+                ev = self._ev_start()
                 x = self.resharder(x, prev, lay, T)
+                self._ev_end(ev, "transition_fwd", layer.index, k)
                 rec["ctxs"].append(("reshard", prev, lay))
             B = hc.microbatch // layer.s.dp
+            ev = self._ev_start()
             x, ctx = layer.forward(x, B)
+            self._ev_end(ev, "fwd", layer.index, k)
             rec["ctxs"].append(("layer", layer, ctx))
             prev = lay
         if not self.last:
@@ -147,7 +156,9 @@ class HybridParallelModel:
         a, b = self._replica_slice(sl, T)
         labels = tokens[k, a:b, 1:S + 1].reshape(-1)
         scale = 1.0 / (hc.global_batch * S)
+        ev = self._ev_start()
         loss_sum, dx = self.head.forward_backward(x, labels, scale)
+        self._ev_end(ev, "head", self.cfg.n_layers - 1, k)
         rec["head_dx"] = dx
         rec["loss"] = loss_sum
         return None, rec
@@ -160,18 +171,27 @@ class HybridParallelModel:
         if layer_items:
             layer_items[0][1].store.prefetch()
         nxt_layer = {id(a[1]): b[1] for a, b in zip(layer_items, layer_items[1:])}
+        last = -1
         for item in items:
             if item[0] == "layer" and id(item[1]) in nxt_layer:
                 nxt_layer[id(item[1])].store.prefetch()
             if item[0] == "reshard":
                 _, src, dst = item
+                ev = self._ev_start()
                 dx = self.resharder(dx, dst, src, T)
+                # the transition into layer `last` (recorded under that layer, as in fwd)
+                self._ev_end(ev, "transition_bwd", last, rec.get("mb", -1))
             else:
                 _, layer, ctx = item
+                ev = self._ev_start()
                 dx = layer.backward(dx, ctx)
+                self._ev_end(ev, "bwd", layer.index, rec.get("mb", -1))
+                last = layer.index
         rec["ctxs"] = []
         if self.first:
+            ev = self._ev_start()
             self.embed.backward(rec["ids"], dx)
+            self._ev_end(ev, "embed_bwd", 0, rec.get("mb", -1))
             return None
         return dx
 
@@ -258,6 +278,25 @@ class HybridParallelModel:
             dist.all_reduce(loss_acc)
         self.last_step_time = time.perf_counter() - t0
         return loss_acc / (hc.global_batch * cfg.seq_len)
+
+    def _ev_start(self):
+        if not self.record_layers:
+            return None
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record()
+        return ev
+
+    def _ev_end(self, start, kind, layer, mb):
+        if start is None:
+            return
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record()
+        self.layer_events.append((kind, layer, mb, start, ev))
+
+    def layer_times(self) -> list:
+        """[(kind, layer, microbatch, seconds)] of the recorded layer events."""
+        torch.cuda.synchronize()
+        return [(k, li, mb, a.elapsed_time(b) / 1e3) for k, li, mb, a, b in self.layer_events]
 
     def _mark(self, kind, mb):
         if self.record_trace:

@@ -47,6 +47,12 @@ def _async(fn, *args, **kw):
 
 ALIGN = 64
 
+# Timing-only switch for the profiler's dp-sync exposure measurement
+# (profiler.measure_dp_overlap): when True, every dp gradient reduction and parameter
+# all-gather of ZeRO-0/1/2 is skipped (each rank updates its own shard from its local
+# gradients).  The numbers are wrong by construction; never set it for training.
+SKIP_DP_SYNC = False
+
 
 def _roundup(x: int, m: int) -> int:
     return (x + m - 1) // m * m
@@ -213,6 +219,9 @@ class ParamStore:
         self.acc32.zero_()
         if self.zero >= 2:
             comm.all_reduce(target, self.extra)
+            if SKIP_DP_SYNC:
+                self._slot = None
+                return
             if self.nvl is not None:
                 self.pending.append((self.nvl.reduce_scatter_slot(self, self._slot), None, ()))
                 self._slot = None
@@ -229,6 +238,12 @@ class ParamStore:
         if self._synced:
             return
         self._synced = True
+        if SKIP_DP_SYNC:
+            if self.zero < 2:
+                comm.all_reduce(self.g_full, self.extra)
+            self._owned_grad = (self.g_full if self.zero == 0 else self.g_shard if
+                                self.zero >= 2 else self.g_full[self.lo:self.lo + self.shard])
+            return
         if self.zero < 2:
             comm.all_reduce(self.g_full, self.extra)
         if self.zero == 0:
@@ -297,6 +312,10 @@ class ParamStore:
             out = self.p_full
         else:
             out = self.p_full[self.lo:self.lo + self.shard]
+        if SKIP_DP_SYNC and self.zero in (1, 2):
+            K.adamw(self.master, self.m, self.v, g, out, lr=lr, beta1=beta1, beta2=beta2,
+                    eps=eps, weight_decay=weight_decay, step=step, grad_scale=grad_scale)
+            return
         if self.nvl is not None and self.zero in (1, 2):
             # fused AdamW + parameter all-gather over NVSwitch (dp_nvlink.py)
             self._param_epoch = self.nvl.adamw_bcast(

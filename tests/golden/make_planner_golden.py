@@ -2,7 +2,8 @@
 
 Run in the build container (where /root/reference exists):
 
-    python tests/golden/make_planner_golden.py
+    python tests/golden/make_planner_golden.py               # random + BASELINE instances
+    python tests/golden/make_planner_golden.py --committed   # the committed B200 profiles
 
 It imports the reference ``hybridplan`` read-only from /root/reference/pkg/src
 (never copied into this repo) and writes ``planner_golden.jsonl``: one line
@@ -95,8 +96,56 @@ def _b200_configs(ref):
     return out
 
 
+# committed B200 profiles (profiles/*.json) x the headline device counts: the exact plan
+# inputs bench.py searches on, pinned to the reference's choice
+COMMITTED = (("llama2-7b", "b200_cluster.json", 8, (1, 2, 4, 8)),
+             ("llama2-13b", "b200_cluster_llama13b_180g.json", 2, (4, 8)),
+             ("gpt2-medium", "b200_cluster_gpt2m.json", 16, (1, 2, 4, 8)),
+             ("gpt-1.3b", "b200_cluster.json", 16, (4, 8)))
+OUT_B200 = Path(__file__).with_name("planner_golden_b200.jsonl")
+
+
+def _committed(ref):
+    """(tag, cluster, model, training) for every COMMITTED profile pair, the cluster
+    re-scoped to n devices exactly as bench.cluster_profile does."""
+    P = ref.profiles
+    prof = Path(__file__).resolve().parents[2] / "profiles"
+    for name, cl_file, per_gpu, ns in COMMITTED:
+        model = P.load_model_profile(str(prof / f"b200_model_{name}.json"))
+        base = P.load_cluster_profile(str(prof / cl_file))
+        for n in ns:
+            table = tuple(e for e in base.bandwidth_table if e.group_size <= n)
+            cl = P.ClusterProfile(n, min(base.devices_per_node, n), base.device_flops,
+                                  base.device_memory_bytes, base.memory_reserve_fraction, table)
+            yield f"committed-{name}-n{n}", cl, model, P.TrainingConfig(global_batch=per_gpu * n)
+
+
+def main_committed(ref) -> None:
+    from hybridplan import pipesim as refsim
+    with open(OUT_B200, "w") as fh:
+        for tag, cl, mo, tr in _committed(ref):
+            plan = ref.search.optimize(mo, cl, tr)
+            sim = refsim.simulate(plan, mo, cl, tr)
+            doc = {"tag": tag, "cluster": ref.profiles.cluster_to_dict(cl),
+                   "model": ref.profiles.model_to_dict(mo),
+                   "training": ref.profiles.training_to_dict(tr),
+                   "plan": ref.serialize.dumps_canonical(plan.to_dict(), sort_keys=False),
+                   "sim": {"makespan": sim.makespan, "peaks": list(sim.stage_peak_memory),
+                           "trace_sha256": hashlib.sha256(
+                               refsim.trace_to_jsonl(sim).encode()).hexdigest()}}
+            fh.write(json.dumps(doc, sort_keys=True) + "\n")
+            print(tag, plan.pp, plan.microbatch, plan.predicted_iteration_time)
+    print(f"wrote {OUT_B200}")
+
+
 def main() -> None:
     sys.path.insert(0, REF)
+    if "--committed" in sys.argv:
+        import hybridplan as ref  # noqa: E402
+        import hybridplan.profiles  # noqa: F401,E402
+        import hybridplan.search  # noqa: F401,E402
+        main_committed(ref)
+        return
     import hybridplan as ref  # noqa: E402
     from hybridplan import cli as refcli, pipesim as refsim  # noqa: E402
     import hybridplan.profiles  # noqa: F401,E402

@@ -223,3 +223,34 @@ def test_runtime_refuses_stale_and_over_budget_plans():
     # partial profile sets are a usage error
     with pytest.raises(ValidationError):
         get_hybrid_parallel_configs(plan, cfg, cluster=cluster)
+
+
+def test_measured_report_bundle_and_csv():
+    """report.measured_report: the reference build_report bundle (cli.py:213-292) with the
+    measured per-layer / per-stage / total columns from layer events."""
+    from paper_2504_21411_b200.planner.search import optimize
+    from paper_2504_21411_b200.report import COLUMNS, measured_report, report_to_csv
+    cfg, mp, cluster, training = _plan_inputs(n=1)
+    plan = optimize(mp, cluster, training)
+    L = mp.n_layers
+    times = []
+    for mb in range(plan.n_microbatches):
+        for li in range(L):
+            times += [("fwd", li, mb, 0.001), ("bwd", li, mb, 0.002)]
+        times += [("head", L - 1, mb, 0.0005), ("embed_fwd", 0, mb, 0.0001),
+                  ("embed_bwd", 0, mb, 0.0001)]
+    b = measured_report(plan, mp, cluster, training, stage=0, layer_times=times,
+                        iteration_s=0.5, dp_sync_exposed_s=0.0, peak_memory_bytes=10)
+    mid = b["layers"][1]
+    assert mid["measured_time_total"] == pytest.approx(0.003)
+    assert mid["relative_error"] == pytest.approx((0.003 - mid["time_total"]) / mid["time_total"])
+    assert b["layers"][-1]["measured_time_total"] == pytest.approx(0.0035)
+    assert b["layers"][0]["measured_time_total"] == pytest.approx(0.0032)
+    st = b["stages"][0]
+    assert st["measured_per_microbatch_time"] == pytest.approx(0.003 * L + 0.0007)
+    assert st["peak_within_prediction"] is True
+    assert b["total"]["measured_iteration_time"] == 0.5
+    csv = report_to_csv(b).splitlines()
+    assert csv[0].split(",") == COLUMNS
+    assert len(csv) == 1 + L + plan.pp + 1
+    assert all(len(r.split(",")) == len(COLUMNS) for r in csv)

@@ -71,3 +71,37 @@ def test_search_matches_reference(doc):
                               transitions=knobs["transitions"])
     blob = dumps_canonical(bundle, sort_keys=False) + cli.report_to_csv(bundle)
     assert hashlib.sha256(blob.encode()).hexdigest() == doc["report_sha256"]
+
+
+B200_LINES = [json.loads(l) for l in
+              (GOLDEN / "planner_golden_b200.jsonl").read_text().splitlines()]
+
+
+@pytest.mark.parametrize("doc", B200_LINES, ids=[d["tag"] for d in B200_LINES])
+def test_committed_b200_profiles_pick_the_reference_plan(doc):
+    """The exact inputs bench.py searches on (committed profiles/*.json, re-scoped to N):
+    byte-identical Plan JSON and identical simulated schedule vs the reference planner
+    (tests/golden/make_planner_golden.py --committed)."""
+    cluster = profiles.cluster_from_dict(doc["cluster"])
+    model = profiles.model_from_dict(doc["model"])
+    training = profiles.training_from_dict(doc["training"])
+    plan = search.optimize(model, cluster, training)
+    assert dumps_canonical(plan.to_dict(), sort_keys=False) == doc["plan"]
+    sim = pipesim.simulate(plan, model, cluster, training)
+    assert sim.makespan == doc["sim"]["makespan"]
+    assert list(sim.stage_peak_memory) == doc["sim"]["peaks"]
+    assert hashlib.sha256(pipesim.trace_to_jsonl(sim).encode()).hexdigest() == \
+        doc["sim"]["trace_sha256"]
+
+
+def test_committed_golden_covers_the_committed_profiles():
+    """The golden inputs are the files bench.py loads (regenerate on recalibration)."""
+    import sys
+    sys.path.insert(0, str(GOLDEN))
+    from make_planner_golden import COMMITTED
+    root = GOLDEN.parents[1] / "profiles"
+    by_tag = {d["tag"]: d for d in B200_LINES}
+    for name, cl_file, _, ns in COMMITTED:
+        want = profiles.load_model_profile(str(root / f"b200_model_{name}.json"))
+        for n in ns:
+            assert profiles.model_from_dict(by_tag[f"committed-{name}-n{n}"]["model"]) == want
