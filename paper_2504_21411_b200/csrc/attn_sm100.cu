@@ -285,18 +285,20 @@ __global__ void __launch_bounds__(384, 1)
       if (warp == 4 && lane == 0) TRACE(6144 + j * 8 + 3);
       const int k0 = j * BKV + half * HC;
       const bool mask = (k0 + HC > p.S) || (p.causal && k0 + HC - 1 > q0);
-      float mx = -INFINITY;
       if (mask) {  // diagonal / tail block: keys >= lim are invisible to this row
         const int lim = (p.causal ? min(p.S, qi + 1) : p.S) - k0;
 #pragma unroll
-        for (int i = 0; i < HC; ++i) {
-          s[i] = i < lim ? s[i] : -INFINITY;
-          mx = fmaxf(mx, s[i]);
-        }
-      } else {
-#pragma unroll
-        for (int i = 0; i < HC; ++i) mx = fmaxf(mx, s[i]);
+        for (int i = 0; i < HC; ++i) s[i] = i < lim ? s[i] : -INFINITY;
       }
+      // row max as a tree (8 independent chains): a serial fmax chain over 64 columns is
+      // ~256 cycles of dependent latency per block on the softmax critical path
+      float m8[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) m8[u] = s[u];
+#pragma unroll
+      for (int i = 8; i < HC; ++i) m8[i & 7] = fmaxf(m8[i & 7], s[i]);
+      float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
+                       fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
       // combine the two halves' row maxima (pair barrier: 64 threads of this quarter)
       xch[(j & 1) * 256 + half * 128 + r] = mx;
       asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
@@ -308,7 +310,7 @@ __global__ void __launch_bounds__(384, 1)
         m_used = mx;
       }
       const float mu = (m_used == -INFINITY) ? 0.f : m_used;
-      float rs = 0.f;
+      float r4[4] = {0.f, 0.f, 0.f, 0.f};  // 4 independent partial row sums
       uint32_t pk[HC / 2];
 #pragma unroll
       for (int i = 0; i < HC; i += 2) {
@@ -323,9 +325,10 @@ __global__ void __launch_bounds__(384, 1)
           p0 = exp2_mufu(x0);
           p1 = exp2_mufu(x1);
         }
-        rs += p0 + p1;
+        r4[(i >> 1) & 3] += p0 + p1;
         pk[i / 2] = pack2(p0, p1);
       }
+      const float rs = (r4[0] + r4[1]) + (r4[2] + r4[3]);
       l = l * alpha + rs;
       if (warp == 4 && lane == 0) TRACE(6144 + j * 8 + 4);
       // lazy rescale: O must hold PV(j-1) first.  When S(j) completed, PV(j-2) had too and

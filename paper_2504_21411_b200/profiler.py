@@ -195,8 +195,8 @@ def fold_embedding_head(prof: P.ModelProfile, cfg, working_set_per_token: float 
     costmodel.py:106, i.e. the dgrad + wgrad GEMMs).  The reference has no
     embedding/head layers, so without this the cost model under-predicts
     by the head's share of the step (13% on GPT-2-medium, 9% on GPT-1.3B) and the
-    memory prediction misses 16 B/param of vocab tables.  Approximation: the tables
-    are dp-replicated (z0) in the runtime but inherit the layer's zero stage here.
+    memory prediction misses 16 B/param of vocab tables.  The runtime shards the tables
+    with the layer's ZeRO stage too (layers.Embedding / Head), so the fold is exact.
 
     ``working_set_per_token`` (measure_working_set) is added to the last layer's
     tp-shardable activation bytes: the step's peak is the saved activations plus this

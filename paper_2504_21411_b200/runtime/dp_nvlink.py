@@ -33,7 +33,10 @@ import torch
 from .. import kernels as K
 
 _FLAGS = 512                  # [ch0 flags: 64 x u32][ch1 flags: 64 x u32][pad]
-RING = 3                      # ZeRO-2 grad-target slots in flight (written / reducing / free)
+# ZeRO-2 grad-target slots: one being written by the current layer's backward while the
+# previous layer's is reduced on the comm stream (a 400 MB pull-reduce takes ~0.6 ms, a
+# layer backward ~20 ms, so a third slot only costs memory)
+RING = int(os.environ.get("GALV_DP_RING", "2"))
 MAX_CTAS = int(os.environ.get("GALV_DP_NVLINK_CTAS", "16"))
 
 

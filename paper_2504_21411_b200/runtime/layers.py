@@ -495,8 +495,10 @@ class Embedding:
         entries = [("embed.weight", (self.vl, cfg.hidden))]
         if cfg.arch == "gpt":
             entries.append(("pos_embed.weight", (cfg.seq_len, cfg.hidden)))
+        # the tables follow layer 0's ZeRO stage: the cost model charges them to layer 0
+        # (profiler.fold_embedding_head), so params / grads / optimizer state shard alike
         self.store = ParamStore(entries, dtype=dtype, grad_dtype=grad_dtype, device=device,
-                                dp=self.dpg, zero=0)
+                                dp=self.dpg, zero=strategy.zero_stage)
 
     def forward(self, ids):
         """ids: [T_rep] int64 (this dp replica's tokens) -> [T_in, h] in layer-0 layout."""
@@ -511,6 +513,7 @@ class Embedding:
             pos = w["pos_embed.weight"]
             rows = (torch.arange(lo, lo + T, device=x.device) % S)
             x.add_(pos.index_select(0, rows))
+        self.store.release()
         return x
 
     def backward(self, ids, dx):
@@ -561,8 +564,9 @@ class Head:
         if cfg.arch == "gpt":
             entries.append(("final_norm.bias", (cfg.hidden,)))
         entries.append(("lm_head.weight", (self.vl, cfg.hidden)))
+        # follows the last layer's ZeRO stage (charged to it by fold_embedding_head)
         self.store = ParamStore(entries, dtype=dtype, grad_dtype=grad_dtype, device=device,
-                                dp=self.dpg, zero=0,
+                                dp=self.dpg, zero=strategy.zero_stage,
                                 small_names=("final_norm.weight", "final_norm.bias"))
         self.tp_partial = ["final_norm.weight", "final_norm.bias"] if strategy.sp else []
 
@@ -619,5 +623,6 @@ class Head:
                                  sg["final_norm.weight"], sg["final_norm.bias"])
         else:
             dx = K.rmsnorm_bwd(x, w["final_norm.weight"], rstd, dn, sg["final_norm.weight"])
+        self.store.release()
         self.store.finish_microbatch(gflat, self.tp_partial, self.tpg)
         return loss.sum(), dx
