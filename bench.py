@@ -271,7 +271,10 @@ def memory_breakdown(plan, model, cluster, training, peak_gb, persistent_bytes):
         tot["optimizer"] += m.optimizer_bytes
         tot["activation"] += m.activation_bytes
     state = tot["param"] + tot["grad"] + tot["optimizer"]
-    return {"stage": st, "model_state_gb": state / 1e9, "model_activation_gb":
+    last = plan.layer_strategies[hi - 1]
+    return {"stage": st, "pp": plan.pp, "microbatch": plan.microbatch,
+            "seq_len": prof.seq_len, "last_layer": last.to_dict(),
+            "model_state_gb": state / 1e9, "model_activation_gb":
             tot["activation"] / 1e9, "runtime_persistent_gb": persistent_bytes / 1e9,
             "runtime_peak_gb": peak_gb, "predicted_gb": plan.predicted_stage_peak_memory[st] / 1e9,
             "budget_gb": cluster.memory_budget_bytes() / 1e9,
@@ -296,7 +299,7 @@ def write_report(path, plan, model, cluster, training, tokens, rank):
     model.record_layers = model.record_trace = False
     marks = {kind: ev for kind, _, ev in model.trace}
     exposed = marks["dp_sync"].elapsed_time(marks["end"]) / 1e3 if "dp_sync" in marks else None
-    peak = torch.cuda.max_memory_allocated() + sum(p.nbytes for p in model.dp_pools)
+    peak = torch.cuda.max_memory_allocated() + model.symmetric_bytes()
     bundle = measured_report(plan, model_profile(model.cfg), cluster, training,
                              stage=model.stage, layer_times=model.layer_times(),
                              iteration_s=a.elapsed_time(b) / 1e3, dp_sync_exposed_s=exposed,
@@ -485,7 +488,7 @@ def main():
     model = construct_hybrid_parallel_model(cfg, hc, training=training, dtype=torch.bfloat16,
                                             init="fast")
     torch.cuda.synchronize()
-    persistent_bytes = torch.cuda.memory_allocated() + sum(p.nbytes for p in model.dp_pools)
+    persistent_bytes = torch.cuda.memory_allocated() + model.symmetric_bytes()
     tokens_host = synthetic_tokens(cfg, gb).pin_memory()
     tokens_dev = tokens_host.to("cuda")
     torch.cuda.synchronize()
@@ -575,8 +578,9 @@ def main():
     mfu = value * flops_tok / (n * PEAK_BF16_DENSE)
     peak_tf = peaks.get("bf16_tflops_sustained", 1424.5)
     clk = clocks.summary()
-    # caching-allocator peak + the symmetric (NVLink) pools, which live outside it
-    mem = (torch.cuda.max_memory_allocated() + sum(p.nbytes for p in model.dp_pools)) / 1e9
+    # caching-allocator peak + the symmetric (NVLink) dp pools and tp peer buffers, which
+    # live outside it
+    mem = (torch.cuda.max_memory_allocated() + model.symmetric_bytes()) / 1e9
     alloc_retries = torch.cuda.memory_stats().get("num_alloc_retries", 0)
     line = {
         "metric": metric, "value": value, "unit": "tokens/s", "n_gpus": n,

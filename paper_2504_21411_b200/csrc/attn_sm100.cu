@@ -391,6 +391,282 @@ __global__ void __launch_bounds__(384, 1)
   }
 }
 
+// ---------------------------------------------------------------- forward, two Q tiles
+// CTA = 256 queries (two 128-row tiles t = 0, 1) of one (batch, head), so every K/V tile
+// loaded by TMA feeds two QK^T and two PV MMAs, and the tensor pipe alternates between the
+// tiles: while softmax warpgroup-pair t works on S_t(j), the MMA warp runs the other tile's
+// PV(j) and S(j+1).  TMEM (512 columns): S_0 [0,128), S_1 [128,256), O_0 [256, 256+D),
+// O_1 [384, 384+D); P_t (bf16) is packed over the first half of each 64-column half of S_t
+// and read by PV as the A operand.  tcgen05.mma instructions from one thread execute in
+// issue order, so S_t(j+1) -- issued after PV_t(j) -- never overwrites P_t(j) before PV
+// has read it.
+//   warp 0    : TMA producer (Q_0, Q_1 once; K/V 2-stage ring)
+//   warp 1    : MMA issuer: S_0(0), S_1(0), then per block j: PV_0(j), S_0(j+1), PV_1(j),
+//               S_1(j+1)
+//   warp 2    : TMEM allocator;  warp 3: idle
+//   warps 4-11: softmax of tile 0;  warps 12-19: softmax of tile 1 (per tile as fwd_tc:
+//               quarter = warp % 4 owns TMEM lanes, half = which 64 key columns)
+template <int D>
+struct Smem2 {
+  static constexpr int TILE = D * 128 * 2;
+  static constexpr int Q = 0;                    // [2 tiles]
+  static constexpr int K0 = 2 * TILE;            // [2 stages]
+  static constexpr int V0 = K0 + 2 * TILE;       // [2 stages]
+  static constexpr int BAR = V0 + 2 * TILE;
+  static constexpr int XCH = BAR + 256;          // per tile: [2][256] maxima + [256] sums
+  static constexpr int BYTES = XCH + 2 * 768 * 4 + 1024;
+};
+constexpr int FWD2_THREADS = 640;
+
+template <int D>
+__global__ void __launch_bounds__(FWD2_THREADS, 1)
+    fwd_tc2(const __grid_constant__ CUtensorMap mq, const __grid_constant__ CUtensorMap mk,
+            const __grid_constant__ CUtensorMap mv, const FwdParams p) {
+  using L = Smem2<D>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::BAR);
+  uint64_t* q_full = bar + 0;
+  uint64_t* k_full = bar + 1;    // [2]
+  uint64_t* v_full = bar + 3;    // [2]
+  uint64_t* k_empty = bar + 5;   // [2]
+  uint64_t* v_empty = bar + 7;   // [2]
+  uint64_t* s_full = bar + 9;    // [tile]
+  uint64_t* p_full = bar + 11;   // [tile]
+  uint64_t* o_done = bar + 13;   // [tile]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 15);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_pairs = (p.n_qblocks + 1) / 2;
+  const int qp = n_pairs - 1 - blockIdx.x;  // heavy causal pairs first
+  const int bh = blockIdx.y, b = bh / p.H, h = bh % p.H;
+  const int q0 = qp * 2 * BQ;
+  const int nkb = (p.S + BKV - 1) / BKV;
+  // blocks of keys each tile attends to (0 = tile beyond the sequence)
+  auto blocks_of = [&](int qt) { return qt >= p.S ? 0 : (p.causal ? min(qt / BKV + 1, nkb) : nkb); };
+  const int nkv0 = blocks_of(q0), nkv1 = blocks_of(q0 + BQ);  // scalars: no local array
+  const int n_kv = max(nkv0, nkv1);
+  const int tok0 = b * p.S;
+  constexpr uint32_t TILE_BYTES = L::TILE;
+
+  if (threadIdx.x == 0) {
+    mbar_init(q_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&k_full[i], 1);
+      mbar_init(&v_full[i], 1);
+      mbar_init(&k_empty[i], 1);
+      mbar_init(&v_empty[i], 1);
+      mbar_init(&s_full[i], 1);
+      mbar_init(&p_full[i], 256);
+      mbar_init(&o_done[i], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    fence_async_smem();
+    prefetch_map(&mq);
+    prefetch_map(&mk);
+    prefetch_map(&mv);
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  if (warp == 0) {
+    if (lane == 0) {
+      const int nq = nkv1 > 0 ? 2 : 1;
+      mbar_expect_tx(q_full, nq * TILE_BYTES);
+      for (int t = 0; t < nq; ++t)
+#pragma unroll
+        for (int c = 0; c < D / 64; ++c)
+          tma_load_3d(&mq, q_full, sm + L::Q + t * L::TILE + c * 16384, c * 64, h,
+                      tok0 + q0 + t * BQ);
+      for (int j = 0; j < n_kv; ++j) {
+        const int st = j & 1;
+        mbar_wait(&k_empty[st], ((j >> 1) & 1) ^ 1);
+        mbar_expect_tx(&k_full[st], TILE_BYTES);
+#pragma unroll
+        for (int c = 0; c < D / 64; ++c)
+          tma_load_3d(&mk, &k_full[st], sm + L::K0 + st * L::TILE + c * 16384, c * 64, h,
+                      tok0 + j * BKV);
+        mbar_wait(&v_empty[st], ((j >> 1) & 1) ^ 1);
+        mbar_expect_tx(&v_full[st], TILE_BYTES);
+#pragma unroll
+        for (int c = 0; c < D / 64; ++c)
+          tma_load_3d(&mv, &v_full[st], sm + L::V0 + st * L::TILE + c * 16384, c * 64, h,
+                      tok0 + j * BKV);
+      }
+    }
+  } else if (warp == 1) {
+    const uint32_t id_s = make_idesc(BQ, BKV, 0, 0);
+    const uint32_t id_o = make_idesc(BQ, D, 0, 1);
+    const uint64_t d_q = sdesc(smem_u32(sm + L::Q), 16, 1024);
+    const uint64_t d_k = sdesc(smem_u32(sm + L::K0), 16, 1024);
+    const uint64_t d_v = sdesc(smem_u32(sm + L::V0), 16384, 1024);
+    mbar_wait_fast(q_full, 0);
+    auto issue_s = [&](int t, int j) {
+      const int st = j & 1;
+      mbar_wait_fast(&k_full[st], (j >> 1) & 1);
+      tc_fence_after();
+      const uint64_t bk = d_k + (uint64_t)((st * L::TILE) >> 4);
+      const uint64_t bq = d_q + (uint64_t)((t * L::TILE) >> 4);
+      if (elect_one()) {
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k) {
+          const uint64_t off = (uint64_t)(((k >> 2) * 16384 + (k & 3) * 32) >> 4);
+          umma_bf16(tmem + t * 128, bq + off, bk + off, id_s, k != 0);
+        }
+        umma_commit(&s_full[t]);
+        if (t == 1 || j >= nkv1) umma_commit(&k_empty[st]);  // last reader of K_j
+      }
+      __syncwarp();
+    };
+    auto issue_pv = [&](int t, int j) {
+      const int st = j & 1;
+      mbar_wait_fast(&p_full[t], j & 1);
+      mbar_wait_fast(&v_full[st], (j >> 1) & 1);
+      tc_fence_after();
+      const uint64_t bv = d_v + (uint64_t)((st * L::TILE) >> 4);
+      const uint32_t t_o = tmem + 256 + t * 128, t_p = tmem + t * 128;
+      if (elect_one()) {
+#pragma unroll
+        for (int k = 0; k < BKV / 16; ++k)
+          umma_bf16_ts(t_o, t_p + (k >> 2) * 64 + (k & 3) * 8,
+                       bv + (uint64_t)((k * 2048) >> 4), id_o, (j | k) != 0);
+        umma_commit(&o_done[t]);
+        if (t == 1 || j >= nkv1) umma_commit(&v_empty[st]);  // last reader of V_j
+      }
+      __syncwarp();
+    };
+    if (nkv0 > 0) issue_s(0, 0);
+    if (nkv1 > 0) issue_s(1, 0);
+    for (int j = 0; j < n_kv; ++j) {
+      if (j < nkv0) {
+        issue_pv(0, j);
+        if (j + 1 < nkv0) issue_s(0, j + 1);
+      }
+      if (j < nkv1) {
+        issue_pv(1, j);
+        if (j + 1 < nkv1) issue_s(1, j + 1);
+      }
+    }
+  } else if (warp >= 4) {
+    const int t = (warp - 4) >> 3;              // tile
+    const int q = warp & 3, half = ((warp - 4) >> 2) & 1;
+    const int r = q * 32 + lane;
+    const int qt = q0 + t * BQ, qi = qt + r;
+    const int n_t = t == 0 ? nkv0 : nkv1;
+    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    const uint32_t t_s = tmem + t * 128, t_o = tmem + 256 + t * 128;
+    float* xch = reinterpret_cast<float*>(sm + L::XCH) + t * 768;
+    const int bar_id = 1 + t * 4 + q;
+    float m_used = -INFINITY, l = 0.f;
+    constexpr int HC = BKV / 2;
+    for (int j = 0; j < n_t; ++j) {
+      mbar_wait(&s_full[t], j & 1);
+      tc_fence_after();
+      float s[HC];
+#pragma unroll
+      for (int c = 0; c < HC / 32; ++c)
+        tmem_ld32_nowait(t_s + half * HC + c * 32 + lane_off,
+                         reinterpret_cast<uint32_t*>(s) + c * 32);
+      tmem_wait_ld();
+      const int k0 = j * BKV + half * HC;
+      const bool mask = (k0 + HC > p.S) || (p.causal && k0 + HC - 1 > qt);
+      if (mask) {
+        const int lim = (p.causal ? min(p.S, qi + 1) : p.S) - k0;
+#pragma unroll
+        for (int i = 0; i < HC; ++i) s[i] = i < lim ? s[i] : -INFINITY;
+      }
+      float m8[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) m8[u] = s[u];
+#pragma unroll
+      for (int i = 8; i < HC; ++i) m8[i & 7] = fmaxf(m8[i & 7], s[i]);
+      float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
+                       fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
+      xch[(j & 1) * 256 + half * 128 + r] = mx;
+      asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
+      mx = fmaxf(mx, xch[(j & 1) * 256 + (half ^ 1) * 128 + r]);
+      mx *= p.scale_log2;
+      float alpha = 1.f;
+      if ((mx > m_used + RESCALE_THRESHOLD || m_used == -INFINITY) && mx != -INFINITY) {
+        alpha = (m_used == -INFINITY) ? 0.f : exp2f(m_used - mx);
+        m_used = mx;
+      }
+      const float mu = (m_used == -INFINITY) ? 0.f : m_used;
+      float r4[4] = {0.f, 0.f, 0.f, 0.f};
+      // P in chunks of 16 keys -> 8 packed columns each, stored as they are produced so the
+      // score registers die progressively (20 warps leave 96 registers per thread)
+#pragma unroll
+      for (int c = 0; c < HC / 16; ++c) {
+        uint32_t pk[8];
+#pragma unroll
+        for (int i = 0; i < 16; i += 2) {
+          const int e = c * 16 + i;
+          const float p0 = exp2_mufu(fmaf(s[e], p.scale_log2, -mu));
+          const float p1 = exp2_mufu(fmaf(s[e + 1], p.scale_log2, -mu));
+          r4[(i >> 1) & 3] += p0 + p1;
+          pk[i / 2] = pack2(p0, p1);
+        }
+        tmem_st8(t_s + half * HC + c * 8 + lane_off, pk);
+      }
+      l = l * alpha + ((r4[0] + r4[1]) + (r4[2] + r4[3]));
+      tmem_wait_st();
+      // lazy rescale of O (after P is out of registers): O must hold PV(j-1) first; o_done
+      // has completed j-1 or j phases here (PV(j) needs this P), so the parity wait is exact
+      if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
+        mbar_wait(&o_done[t], (j - 1) & 1);
+        tc_fence_after();
+#pragma unroll 1
+        for (int c = 0; c < D / 64; ++c) {
+          uint32_t ov[32];
+          const uint32_t ta = t_o + half * (D / 2) + c * 32 + lane_off;
+          tmem_ld32(ta, ov);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * alpha);
+          tmem_st32(ta, ov);
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&p_full[t]);
+    }
+    if (n_t > 0) {
+      xch[512 + half * 128 + r] = l;
+      asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
+      l += xch[512 + (half ^ 1) * 128 + r];
+      mbar_wait(&o_done[t], (n_t - 1) & 1);
+      tc_fence_after();
+      const float inv_l = l > 0.f ? 1.f / l : 0.f;
+      __nv_bfloat16* orow =
+          p.o + (long long)(tok0 + qi) * p.o_st + (long long)h * p.sh + half * (D / 2);
+#pragma unroll 1
+      for (int c = 0; c < D / 64; ++c) {
+        uint32_t ov[32];
+        tmem_ld32(t_o + half * (D / 2) + c * 32 + lane_off, ov);
+        if (qi < p.S) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            uint4 w;
+            w.x = pack2(__uint_as_float(ov[u * 8 + 0]) * inv_l, __uint_as_float(ov[u * 8 + 1]) * inv_l);
+            w.y = pack2(__uint_as_float(ov[u * 8 + 2]) * inv_l, __uint_as_float(ov[u * 8 + 3]) * inv_l);
+            w.z = pack2(__uint_as_float(ov[u * 8 + 4]) * inv_l, __uint_as_float(ov[u * 8 + 5]) * inv_l);
+            w.w = pack2(__uint_as_float(ov[u * 8 + 6]) * inv_l, __uint_as_float(ov[u * 8 + 7]) * inv_l);
+            *reinterpret_cast<uint4*>(orow + c * 32 + u * 8) = w;
+          }
+        }
+      }
+      if (qi < p.S && half == 0)
+        p.lse[((long long)b * p.H + h) * p.S + qi] = (m_used + log2f(l)) * 0.6931471805599453f;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
 // ---------------------------------------------------------------- backward
 // Two deterministic kernels (no atomics), both on tcgen05 with 8 math warps:
 //   dkdv: CTA = 128 keys; per 64-query step  S^T = K Q^T, dP^T = V dO^T (TMEM, double
@@ -1051,6 +1327,15 @@ static bool qkv_map(CUtensorMap* m, const void* base, int64_t tokens, int64_t H,
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// GALV_ATTN_FWD=1 selects the one-Q-tile forward (fwd_tc) for A/B runs
+static bool fwd_two_tiles() {
+  static const bool two = [] {
+    const char* e = getenv("GALV_ATTN_FWD");
+    return !(e && e[0] == '1');
+  }();
+  return two;
+}
+
 }  // namespace fa
 
 int32_t attn_fwd_sm100(const void* q, const void* k, const void* v, void* o, float* lse,
@@ -1092,6 +1377,15 @@ int32_t attn_fwd_sm100(const void* q, const void* k, const void* v, void* o, flo
     return 0;
   };
   int32_t rc;
+  if (fwd_two_tiles()) {  // default: the two-Q-tile kernel (fwd_tc2)
+    const dim3 grid2((unsigned)((p.n_qblocks + 1) / 2), (unsigned)(B * H));
+    auto kern = D == 128 ? fwd_tc2<128> : fwd_tc2<64>;
+    const int smem = D == 128 ? Smem2<128>::BYTES : Smem2<64>::BYTES;
+    GALV_CUDA_RET(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    kern<<<grid2, FWD2_THREADS, smem, stream>>>(mq, mk, mv, p);
+    GALV_LAUNCH_CHECK();
+    return 0;
+  }
   if (D == 128)
     rc = mc ? launch(fwd_tc<128, true>, Smem<128>::BYTES)
             : launch(fwd_tc<128, false>, Smem<128>::BYTES);

@@ -250,7 +250,36 @@ def calibrated_model_profile(cfg, act: dict) -> P.ModelProfile:
     prof = P.ModelProfile(n_layers=base.n_layers, hidden_size=base.hidden_size,
                           seq_len=base.seq_len, layers=(layer,) * base.n_layers)
     prof.validate()
-    return fold_embedding_head(prof, cfg, act.get("working_set_bytes_per_token", 0.0))
+    return fold_embedding_head(prof, cfg, act.get("working_set_bytes_per_token", 0.0)
+                               + act.get("step_memory_extra_bytes_per_token", 0.0))
+
+
+def step_memory_extra(lines: list) -> dict:
+    """Per-token bytes to add to the working-set fold so the cost model's stage peak covers
+    what a full training step held on the GPU, from bench.py JSON lines (their "memory"
+    object: runtime peak incl. symmetric NVLink allocations vs the plan's predicted stage
+    peak).  What the single-layer measurement cannot see lives here: the ZeRO-2 full-size
+    gradient ring of the NVLink dp pool, tp peer buffers, the gathered (tp-replicated)
+    backward temporaries of Megatron-SP, rope tables.  The excess of a line is charged to
+    its last layer's tp-shardable activation term (act = tokens*(shard/tp + ...)):
+    extra = excess * tp / (microbatch * seq / dp); the maximum over the lines is kept.
+    Lines whose last layer recomputes (the term is not used then) or that are not the
+    last pipeline stage are skipped."""
+    best, used, skipped = 0.0, [], []
+    for ln in lines:
+        m = ln.get("memory", {})
+        ll = m.get("last_layer")
+        if not ll or m.get("stage") != m.get("pp", 1) - 1 or ll.get("recompute"):
+            skipped.append(ln.get("config", {}).get("parallelism"))
+            continue
+        excess = m["runtime_peak_gb"] * 1e9 - m["predicted_gb"] * 1e9
+        tokens = m["microbatch"] * m["seq_len"] / ll["dp"]
+        x = max(excess, 0.0) * ll["tp"] / tokens
+        used.append({"config": ln.get("config", {}).get("parallelism"), "n_gpus": ln.get("n_gpus"),
+                     "excess_bytes": excess, "extra_bytes_per_token": x})
+        best = max(best, x)
+    return {"step_memory_extra_bytes_per_token": best, "step_memory_sources": used,
+            "step_memory_skipped": skipped}
 
 
 def measure_collectives(sizes=(2 ** 20, 2 ** 24, 2 ** 28)) -> dict:
@@ -285,7 +314,7 @@ def measure_collectives(sizes=(2 ** 20, 2 ** 24, 2 ** 28)) -> dict:
 
 
 def measure_dp_overlap(cfg, cluster, global_batch: int, *, steps: int = 4,
-                       warmup: int = 2) -> dict:
+                       warmup: int = 2, rounds: int = 3) -> dict:
     """Measured ``comm_overlap_fraction`` (reference profiles.py:187, costmodel.py:265,
     search.py:193): how much of the cost model's dp-sync time the runtime hides behind
     compute.  Under torchrun, the searched plan for this world is run twice with the same
@@ -327,16 +356,23 @@ def measure_dp_overlap(cfg, cluster, global_batch: int, *, steps: int = 4,
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return t.item()
 
-    t_sync = timed()
-    params_mod.SKIP_DP_SYNC = True
+    # alternate the two variants (clock / power drift hits both alike), median of each
+    syncs, nosyncs = [], []
     try:
-        t_nosync = timed()
+        for _ in range(rounds):
+            params_mod.SKIP_DP_SYNC = False
+            syncs.append(timed())
+            params_mod.SKIP_DP_SYNC = True
+            nosyncs.append(timed())
     finally:
         params_mod.SKIP_DP_SYNC = False
+    import statistics
+    t_sync, t_nosync = statistics.median(syncs), statistics.median(nosyncs)
     modeled = max(c.dp_sync_time for c in plan.cost_breakdown)
     exposed = t_sync - t_nosync
     overlap = min(max(1.0 - exposed / modeled, 0.0), 1.0) if modeled > 0 else 0.0
     return {"t_step_sync_s": t_sync, "t_step_nosync_s": t_nosync, "exposed_s": exposed,
+            "samples_sync_s": syncs, "samples_nosync_s": nosyncs,
             "modeled_dp_sync_s": modeled, "comm_overlap_fraction": overlap,
             "plan": [s.to_dict() for s in plan.layer_strategies[:1]],
             "plan_microbatch": plan.microbatch, "world": dist.get_world_size()}
@@ -385,13 +421,17 @@ def main(argv=None) -> int:
                          "TrainingConfig JSON here")
     ap.add_argument("--cluster-in", default=None, help="cluster profile for --overlap-out")
     ap.add_argument("--seqs-per-gpu", type=int, default=8)
+    ap.add_argument("--memory-from", nargs="+", default=None,
+                    help="bench.py JSON lines of --model: fold the measured step-memory excess "
+                         "over the prediction into --model-out (step_memory_extra)")
     ap.add_argument("--skip-flops", action="store_true",
                     help="with --table-from + --model-out: only measure activations")
     args = ap.parse_args(argv)
     from .runtime.config import MODEL_PRESETS
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
+    if torch.cuda.is_available():
+        torch.cuda.set_device(local)
     table = {}
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -402,6 +442,28 @@ def main(argv=None) -> int:
         table = {e.group_size: {"bus_bandwidth": e.bus_bandwidth, "latency": e.latency}
                  for e in c.bandwidth_table if e.span == "intra_node"}
     rank = dist.get_rank() if world > 1 else 0
+    if args.memory_from:
+        # offline: rewrite --model-out's profile with the step-memory calibration folded in
+        cfg = MODEL_PRESETS[args.model]
+        meta_path = os.path.splitext(args.model_out)[0] + ".meta.json"
+        with open(meta_path) as fh:
+            meta = json.load(fh)
+        lines = []
+        for path in args.memory_from:
+            with open(path) as fh:
+                for raw in fh:
+                    raw = raw.strip()
+                    if raw.startswith("{") and '"memory"' in raw:
+                        d = json.loads(raw)
+                        if d.get("config", {}).get("model") == cfg.name:
+                            lines.append(d)
+        meta["activation"].update(step_memory_extra(lines))
+        P.save_profiles(args.model_out, model=calibrated_model_profile(cfg, meta["activation"]))
+        with open(meta_path, "w") as fh:
+            json.dump(meta, fh, indent=1)
+        print(json.dumps({k: meta["activation"][k] for k in meta["activation"]
+                          if k.startswith("step_memory")}))
+        return 0
     if args.overlap_out:
         if world < 2:
             raise SystemExit("--overlap-out needs torchrun with >= 2 ranks")
@@ -425,6 +487,12 @@ def main(argv=None) -> int:
         cfg = MODEL_PRESETS[args.model]
         act = measure_activation_bytes(cfg, args.microbatch)
         act.update(measure_working_set(cfg, args.microbatch))
+        # re-measuring activations keeps an existing step-memory calibration
+        old = os.path.splitext(args.model_out)[0] + ".meta.json"
+        if os.path.exists(old):
+            with open(old) as fh:
+                prev = json.load(fh).get("activation", {})
+            act.update({k: v for k, v in prev.items() if k.startswith("step_memory")})
         P.save_profiles(args.model_out, model=calibrated_model_profile(cfg, act))
         with open(os.path.splitext(args.model_out)[0] + ".meta.json", "w") as fh:
             json.dump({"model": args.model, "activation": act}, fh, indent=1)

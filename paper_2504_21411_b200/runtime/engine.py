@@ -350,6 +350,12 @@ class HybridParallelModel:
                 ev.record()
                 store.ready_event = ev
 
+    def symmetric_bytes(self) -> int:
+        """Device memory in symmetric (NVLink) allocations, outside the caching allocator:
+        the dp pools of this model and the tp peer buffers."""
+        from . import nvlink
+        return sum(p.nbytes for p in self.dp_pools) + nvlink.symmetric_bytes()
+
     def wait_optimizer(self):
         """Make the current stream wait for the optimizer side stream (timing edges)."""
         if self._opt_stream is not None:

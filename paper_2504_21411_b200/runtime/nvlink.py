@@ -92,6 +92,12 @@ class PeerBuffers:
         return self._region(2 + k, M * N * 2).view(torch.bfloat16).view(M, N).clone()
 
 
+def symmetric_bytes() -> int:
+    """Bytes of the live tp peer-buffer allocations (symmetric memory: outside the caching
+    allocator, so torch.cuda.max_memory_allocated does not see them)."""
+    return sum(pb.buf.numel() * pb.buf.element_size() for pb in _CACHE.values())
+
+
 def peer_buffers(group, region_bytes: int, device) -> PeerBuffers:
     """Shared per tp group; grows (collectively, in layer-construction order) if needed."""
     key = tuple(group.ranks)

@@ -44,7 +44,7 @@ def timed(fn, iters=20, warmup=5):
     return statistics.median(out)
 
 
-def run_shape(B, S, H, D, iters):
+def run_shape(B, S, H, D, iters, libs=True):
     from paper_2504_21411_b200 import kernels as K
     dev = "cuda"
     torch.manual_seed(0)
@@ -77,6 +77,8 @@ def run_shape(B, S, H, D, iters):
                                       rope_theta=10000.0), iters)
         rec("galv", "bwd+inverse_rope", us, f_bwd)
 
+    if not libs:
+        return rows
     from torch.nn.attention import SDPBackend, sdpa_kernel
     import torch.nn.functional as F
     qt, kt, vt = (t.transpose(1, 2) for t in (q, k, v))  # [B, H, S, D] strided views
@@ -135,13 +137,14 @@ def main():
     ap.add_argument("--out", default=None)
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--shapes", default="2x4096x32,1x32768x8,4x1024x16x64")
+    ap.add_argument("--galv-only", action="store_true", help="skip the library arms")
     args = ap.parse_args()
     rows = []
     for spec in args.shapes.split(","):
         parts = [int(x) for x in spec.split("x")]
         B, S, H = parts[:3]
         D = parts[3] if len(parts) > 3 else 128
-        rows += run_shape(B, S, H, D, args.iters)
+        rows += run_shape(B, S, H, D, args.iters, libs=not args.galv_only)
     for r in rows:
         print(json.dumps(r), flush=True)
     if args.out:
