@@ -540,14 +540,19 @@ class Embedding:
 # ---------------------------------------------------------------------------- head
 
 
-HEAD_CHUNKS = 4
+# logits above HEAD_CHUNK_BYTES are processed in token chunks of >= HEAD_CHUNK_MIN_ROWS rows
+# (tools/head_bench.py, B200, 8192 tokens x V 32000: 1 chunk 4.90 ms, 2 chunks 5.85 ms, 4
+# chunks 7.07 ms -- a K=2048 wgrad is epilogue-bound), so chunking only bounds the memory of
+# long-context microbatches (Llama-2-13B at 32K: 2 GB of logits per sequence)
+HEAD_CHUNK_BYTES = 1 << 30
+HEAD_CHUNK_MIN_ROWS = 8192
 
 
 def _head_chunks(T: int, v_local: int, elt: int):
-    """HEAD_CHUNKS token ranges (multiples of 128 rows, so each chunk's GEMMs keep whole
-    128-row tiles): the [rows, V/tp] logits working set is a fixed fraction of the tokens,
-    i.e. a per-token constant, which is how the cost model's activation terms scale."""
-    step = -(-T // HEAD_CHUNKS)
+    """Token ranges (multiples of 128 rows) whose [rows, V/tp] logits stay within
+    HEAD_CHUNK_BYTES, never shorter than HEAD_CHUNK_MIN_ROWS."""
+    n = max(1, -(-T * v_local * elt // HEAD_CHUNK_BYTES))
+    step = max(-(-T // n), min(T, HEAD_CHUNK_MIN_ROWS))
     step = -(-step // 128) * 128
     return [(a, min(T, a + step)) for a in range(0, T, step)]
 

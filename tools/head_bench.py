@@ -19,7 +19,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--tokens", type=int, default=8192)
-    ap.add_argument("--chunks", default="1,2,4")
+    ap.add_argument("--chunk-bytes", default="1073741824,268435456")
     ap.add_argument("--model", default="llama2-7b")
     args = ap.parse_args()
     from paper_2504_21411_b200 import kernels as K
@@ -39,8 +39,9 @@ def main():
     x = torch.randn(T, cfg.hidden, device=dev, dtype=torch.bfloat16)
     labels = torch.randint(0, cfg.vocab, (T,), device=dev)
     flops = 3 * 2.0 * T * cfg.hidden * cfg.vocab
-    for c in [int(v) for v in args.chunks.split(",")]:
-        layers.HEAD_CHUNKS = c
+    layers.HEAD_CHUNK_MIN_ROWS = 128
+    for c in [int(v) for v in args.chunk_bytes.split(",")]:
+        layers.HEAD_CHUNK_BYTES = c
         for _ in range(3):
             head.forward_backward(x, labels, 1.0 / T)
         torch.cuda.synchronize()
@@ -56,7 +57,7 @@ def main():
         K.stop_stats()
         g = st.gemm_summary()
         shapes = [(shp, round(s0.elapsed_time(s1) * 1e3, 1)) for _, s0, s1, shp in st.gemm_events]
-        print(json.dumps({"chunks": c, "tokens": T, "ms": ms, "tflops_gemm_flops": flops / ms / 1e9,
+        print(json.dumps({"chunk_bytes": c, "tokens": T, "ms": ms, "tflops_gemm_flops": flops / ms / 1e9,
                           "gemm_ms": g["ms"], "gemm_tflops": g["tflops"],
                           "gemms_us": shapes[:6]}), flush=True)
 
