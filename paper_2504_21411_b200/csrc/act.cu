@@ -48,14 +48,28 @@ __global__ void swiglu_bwd(const T* gu, const T* dh, T* dgu, int64_t T_, int64_t
   }
 }
 
+// tanh: bf16 activations use the MUFU tanh.approx.f32 (max rel err ~2^-11, below the bf16
+// rounding of the result); fp32 (the exact-parity config) keeps tanhf
+template <bool FAST>
+__device__ __forceinline__ float tanh_sel(float u) {
+  if constexpr (FAST) {
+    float t;
+    asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(u));
+    return t;
+  } else {
+    return tanhf(u);
+  }
+}
+template <bool FAST = false>
 __device__ __forceinline__ float gelu_tanh(float x) {
   const float k0 = 0.7978845608028654f, k1 = 0.044715f;
-  return 0.5f * x * (1.f + tanhf(k0 * (x + k1 * x * x * x)));
+  return 0.5f * x * (1.f + tanh_sel<FAST>(k0 * (x + k1 * x * x * x)));
 }
+template <bool FAST = false>
 __device__ __forceinline__ float gelu_tanh_grad(float x) {
   const float k0 = 0.7978845608028654f, k1 = 0.044715f;
   const float u = k0 * (x + k1 * x * x * x);
-  const float th = tanhf(u);
+  const float th = tanh_sel<FAST>(u);
   return 0.5f * (1.f + th) + 0.5f * x * (1.f - th * th) * k0 * (1.f + 3.f * k1 * x * x);
 }
 
@@ -63,16 +77,23 @@ template <typename T>
 __global__ void bias_gelu_fwd(const T* __restrict__ x, const T* __restrict__ b, T* __restrict__ y,
                               int64_t T_, int64_t F) {
   constexpr int V = 16 / sizeof(T);
+  constexpr bool FAST = sizeof(T) == 2;
   const int64_t nvec = T_ * F / V;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nvec;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t e = i * V, f = e % F;
+  const int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  // column of the vector: one 64-bit modulo per thread, then stepped (stride*V mod F < F)
+  const int64_t fstep = (stride * V) % F;
+  int64_t f = (i0 * V) % F;
+  for (int64_t i = i0; i < nvec; i += stride) {
+    const int64_t e = i * V;
     float v[V], bb[V];
     load16(x + e, v);
     if (b) load16(b + f, bb);
 #pragma unroll
-    for (int k = 0; k < V; ++k) v[k] = gelu_tanh(v[k] + (b ? bb[k] : 0.f));
+    for (int k = 0; k < V; ++k) v[k] = gelu_tanh<FAST>(v[k] + (b ? bb[k] : 0.f));
     store16(y + e, v);
+    f += fstep;
+    if (f >= F) f -= F;
   }
 }
 
@@ -81,17 +102,23 @@ __global__ void bias_gelu_bwd(const T* __restrict__ x, const T* __restrict__ b,
                               const T* __restrict__ dy, T* __restrict__ dx, int64_t T_,
                               int64_t F) {
   constexpr int V = 16 / sizeof(T);
+  constexpr bool FAST = sizeof(T) == 2;
   const int64_t nvec = T_ * F / V;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nvec;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t e = i * V, f = e % F;
+  const int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t fstep = (stride * V) % F;
+  int64_t f = (i0 * V) % F;
+  for (int64_t i = i0; i < nvec; i += stride) {
+    const int64_t e = i * V;
     float v[V], bb[V], d[V];
     load16(x + e, v);
     load16(dy + e, d);
     if (b) load16(b + f, bb);
 #pragma unroll
-    for (int k = 0; k < V; ++k) v[k] = d[k] * gelu_tanh_grad(v[k] + (b ? bb[k] : 0.f));
+    for (int k = 0; k < V; ++k) v[k] = d[k] * gelu_tanh_grad<FAST>(v[k] + (b ? bb[k] : 0.f));
     store16(dx + e, v);
+    f += fstep;
+    if (f >= F) f -= F;
   }
 }
 
@@ -178,7 +205,7 @@ __global__ void __launch_bounds__(256) bias_gelu_bwd_colsum(
       load16(x + r * cols + c, v);
       load16(dy + r * cols + c, d);
 #pragma unroll
-      for (int e = 0; e < V; ++e) v[e] = d[e] * gelu_tanh_grad(v[e] + bb[e]);
+      for (int e = 0; e < V; ++e) v[e] = d[e] * gelu_tanh_grad<sizeof(T) == 2>(v[e] + bb[e]);
       store16(dx + r * cols + c, v);
 #pragma unroll
       for (int e = 0; e < V; ++e) s[e] += to_f(from_f<T>(v[e]));  // sum what was stored

@@ -150,6 +150,122 @@ __global__ void __launch_bounds__(256) xent_kernel(T* __restrict__ logits,
   }
 }
 
+// Vectorized variant (rows 16-byte aligned, V_local a multiple of the 16-byte vector):
+// stage 3 makes ONE pass over the logits for the row statistics -- an online (max, sum of
+// exp) per thread, merged across the CTA -- and a second pass (an L2 hit: the row was just
+// read) writing the gradient in place, so HBM sees the logits read once and written once;
+// the scalar kernel above read them three times with 2-byte loads.
+constexpr float XLOG2E = 1.4426950408889634f;
+
+__device__ __forceinline__ void online_merge(float& m, float& s, float m2, float s2) {
+  const float mm = fmaxf(m, m2);
+  if (mm == -INFINITY) return;
+  s = s * exp2f((m - mm) * XLOG2E) + s2 * exp2f((m2 - mm) * XLOG2E);
+  m = mm;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) xent_vec(T* __restrict__ logits,
+                                                const int64_t* __restrict__ labels,
+                                                float* __restrict__ stats,
+                                                float* __restrict__ loss, T* __restrict__ dl,
+                                                int64_t V_local, int64_t lo, float gscale,
+                                                int64_t ignore, int stage) {
+  constexpr int VEC = 16 / sizeof(T);
+  __shared__ float red_m[8], red_s[8], bc[2];
+  const int64_t row = blockIdx.x;
+  const T* x = logits + row * V_local;
+  const int64_t lab = labels[row];
+  const int64_t tgt = lab - lo;
+  float* st = stats + row * 3;
+  const int nvec = (int)(V_local / VEC);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float m = -INFINITY, sum = 0.f;
+  if (stage == 0 || stage == 3) {
+    for (int v = threadIdx.x; v < nvec; v += 256) {
+      float e[VEC];
+      load16(x + (int64_t)v * VEC, e);
+      float mv = e[0];
+#pragma unroll
+      for (int i = 1; i < VEC; ++i) mv = fmaxf(mv, e[i]);
+      if (stage == 3) {
+        const float mn = fmaxf(m, mv);
+        float acc = 0.f;
+#pragma unroll
+        for (int i = 0; i < VEC; ++i) acc += exp2f((e[i] - mn) * XLOG2E);
+        sum = (m == -INFINITY ? 0.f : sum * exp2f((m - mn) * XLOG2E)) + acc;
+      }
+      m = fmaxf(m, mv);
+    }
+    // merge (max, sum) across the warp, then across warps
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float m2 = __shfl_xor_sync(0xffffffffu, m, o);
+      const float s2 = __shfl_xor_sync(0xffffffffu, sum, o);
+      online_merge(m, sum, m2, s2);
+    }
+    if (lane == 0) {
+      red_m[warp] = m;
+      red_s[warp] = sum;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      float mm = red_m[0], ss = red_s[0];
+      for (int w = 1; w < 8; ++w) online_merge(mm, ss, red_m[w], red_s[w]);
+      bc[0] = mm;
+      bc[1] = ss;
+      st[0] = mm;
+      if (stage == 3) {
+        st[1] = ss;
+        st[2] = (tgt >= 0 && tgt < V_local) ? to_f(x[tgt]) : 0.f;
+      }
+    }
+    __syncthreads();
+    if (stage == 0) return;
+    m = bc[0];
+    sum = bc[1];
+  }
+  if (stage == 1) {
+    const float mg = st[0];
+    float acc = 0.f;
+    for (int v = threadIdx.x; v < nvec; v += 256) {
+      float e[VEC];
+      load16(x + (int64_t)v * VEC, e);
+#pragma unroll
+      for (int i = 0; i < VEC; ++i) acc += exp2f((e[i] - mg) * XLOG2E);
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) red_s[warp] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      float t = 0.f;
+      for (int w = 0; w < 8; ++w) t += red_s[w];
+      st[1] = t;
+      st[2] = (tgt >= 0 && tgt < V_local) ? to_f(x[tgt]) : 0.f;
+    }
+    return;
+  }
+  // stage 2 (or 3): loss + gradient, in place over the logits
+  if (stage == 2) {
+    m = st[0];
+    sum = st[1];
+  }
+  const bool ign = lab == ignore;
+  if (threadIdx.x == 0) loss[row] = ign ? 0.f : (logf(sum) + m - st[2]);
+  T* d = dl + row * V_local;
+  const float scale = ign ? 0.f : gscale / sum;
+  for (int v = threadIdx.x; v < nvec; v += 256) {
+    float e[VEC];
+    load16(x + (int64_t)v * VEC, e);
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) {
+      e[i] = exp2f((e[i] - m) * XLOG2E) * scale;
+      if (!ign && (int64_t)v * VEC + i == tgt) e[i] -= gscale;
+    }
+    store16(d + (int64_t)v * VEC, e);
+  }
+}
+
 }  // namespace xent
 }  // namespace galv
 
@@ -210,9 +326,17 @@ int32_t galv_xent(void* logits, const int64_t* labels, float* stats, float* loss
   GALV_CHECK_ARG(stage >= 0 && stage <= 3, "stage must be 0..3");
   GALV_CHECK_ARG(stage < 2 || (loss && dlogits), "stage 2/3 need loss and dlogits");
   GALV_DISPATCH(dtype, T, {
-    xent::xent_kernel<T><<<(unsigned)T_, 256, 0, as_stream(stream)>>>(
-        (T*)logits, labels, stats, loss, (T*)dlogits, V_local, vocab_lo, grad_scale, ignore_index,
-        stage);
+    const bool vec = (V_local * (int64_t)sizeof(T)) % 16 == 0 &&
+                     (reinterpret_cast<uintptr_t>(logits) & 15) == 0 &&
+                     (dlogits == nullptr || (reinterpret_cast<uintptr_t>(dlogits) & 15) == 0);
+    if (vec)
+      xent::xent_vec<T><<<(unsigned)T_, 256, 0, as_stream(stream)>>>(
+          (T*)logits, labels, stats, loss, (T*)dlogits, V_local, vocab_lo, grad_scale,
+          ignore_index, stage);
+    else
+      xent::xent_kernel<T><<<(unsigned)T_, 256, 0, as_stream(stream)>>>(
+          (T*)logits, labels, stats, loss, (T*)dlogits, V_local, vocab_lo, grad_scale,
+          ignore_index, stage);
   });
   GALV_LAUNCH_CHECK();
   return 0;

@@ -11,6 +11,14 @@ namespace norm {
 constexpr int WARPS = 8;
 
 // GALV_NORM_UNFUSED=1 selects the two-kernel backward (dx pass, then dgamma pass) for A/B.
+// GALV_NORM_WARP=0: narrow rows fall back to the dx + dgamma kernel pair (A/B)
+static bool warp_rows_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("GALV_NORM_WARP");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 static bool fused_disabled() {
   static const bool off = [] {
     const char* e = getenv("GALV_NORM_UNFUSED");
@@ -342,6 +350,132 @@ __global__ void __launch_bounds__(NT) bwd_fused_rows(
   }
 }
 
+// Narrow rows (<= 1024 bf16 / 512 fp32 columns): a WARP per row instead of a CTA per row.
+// Each lane owns VPL fixed 16-byte column vectors (columns lane*V + j*32*V), so its dgamma
+// (/dbeta) partials stay in registers across all the rows the warp visits; the row
+// reductions are warp shuffles (no CTA barrier per row, which is what starved the
+// CTA-per-row kernel at width 1024: one short row per barrier interval).  x and dy are read
+// once; the partials are summed over the CTA's warps through smem and flushed with one
+// atomic per column per CTA.
+template <typename T, bool LAYER, int VPL>
+__global__ void __launch_bounds__(256) bwd_fused_warp_rows(
+    const T* __restrict__ x, const T* __restrict__ gamma, const float* __restrict__ mean,
+    const float* __restrict__ rstd, const T* __restrict__ dy, const T* __restrict__ dres,
+    T* __restrict__ dx, float* __restrict__ dgamma, float* __restrict__ dbeta, int64_t rows,
+    int cols) {
+  constexpr int V = 16 / sizeof(T);
+  constexpr int NW = 8;
+  extern __shared__ float sred[];  // [NW][cols] dgamma (+ [NW][cols] dbeta)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float ga[VPL][V], ba[VPL][V], g[VPL][V];
+#pragma unroll
+  for (int j = 0; j < VPL; ++j) {
+    const int c = (j * 32 + lane) * V;
+#pragma unroll
+    for (int i = 0; i < V; ++i) ga[j][i] = ba[j][i] = 0.f;
+    if (c < cols) load16(gamma + c, g[j]);
+  }
+  const float inv_cols = 1.f / cols;
+  for (int64_t row = (int64_t)blockIdx.x * NW + warp; row < rows; row += (int64_t)gridDim.x * NW) {
+    const T* xr = x + row * cols;
+    const T* dyr = dy + row * cols;
+    const float mu = LAYER ? mean[row] : 0.f, rs = rstd[row];
+    float v[VPL][V], d[VPL][V];
+#pragma unroll
+    for (int j = 0; j < VPL; ++j) {
+      const int c = (j * 32 + lane) * V;
+      if (c < cols) {
+        const uint4 xv = __ldcs(reinterpret_cast<const uint4*>(xr + c));
+        const uint4 dv = __ldcs(reinterpret_cast<const uint4*>(dyr + c));
+        load16(reinterpret_cast<const T*>(&xv), v[j]);
+        load16(reinterpret_cast<const T*>(&dv), d[j]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < V; ++i) v[j][i] = d[j][i] = 0.f;
+      }
+    }
+    float a1 = 0.f, a2 = 0.f;
+#pragma unroll
+    for (int j = 0; j < VPL; ++j)
+#pragma unroll
+      for (int i = 0; i < V; ++i) {
+        const float xh = (v[j][i] - mu) * rs;
+        const float gd = g[j][i] * d[j][i];
+        a1 += gd * xh;
+        a2 += gd;
+        ga[j][i] += d[j][i] * xh;
+        if (LAYER) ba[j][i] += d[j][i];
+      }
+    a1 = warp_sum(a1) * inv_cols;
+    a2 = warp_sum(a2) * inv_cols;
+    T* dxr = dx + row * cols;
+    const T* drr = dres ? dres + row * cols : nullptr;
+#pragma unroll
+    for (int j = 0; j < VPL; ++j) {
+      const int c = (j * 32 + lane) * V;
+      if (c >= cols) continue;
+      float r[V];
+      if (drr) load16(drr + c, r);
+#pragma unroll
+      for (int i = 0; i < V; ++i) {
+        const float xh = (v[j][i] - mu) * rs;
+        float o = rs * (g[j][i] * d[j][i] - xh * a1 - (LAYER ? a2 : 0.f));
+        if (drr) o += r[i];
+        v[j][i] = o;
+      }
+      store16(dxr + c, v[j]);
+    }
+  }
+  // CTA reduction of the per-warp partials, one atomic per column
+#pragma unroll
+  for (int j = 0; j < VPL; ++j) {
+    const int c = (j * 32 + lane) * V;
+    if (c >= cols) continue;
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+      sred[warp * cols + c + i] = ga[j][i];
+      if (LAYER) sred[(NW + warp) * cols + c + i] = ba[j][i];
+    }
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < cols; c += blockDim.x) {
+    float sg = 0.f, sb = 0.f;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+      sg += sred[w * cols + c];
+      if (LAYER) sb += sred[(NW + w) * cols + c];
+    }
+    atomicAdd(dgamma + c, sg);
+    if (LAYER) atomicAdd(dbeta + c, sb);
+  }
+}
+
+template <typename T, bool LAYER>
+bool launch_fused_warp(const void* x, const void* gamma, const float* mean, const float* rstd,
+                       const void* dy, const void* dres, void* dx, float* dgamma, float* dbeta,
+                       int64_t rows, int64_t cols, void* stream) {
+  constexpr int V = 16 / (int)sizeof(T);
+  if (cols % V != 0 || cols > 32 * V * 4) return false;
+  const int64_t vpl = (cols / V + 31) / 32;
+  auto go = [&](auto kernel) {
+    const size_t smem = (size_t)(LAYER ? 2 : 1) * 8 * cols * sizeof(float);
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 256, smem);
+    const int64_t grid =
+        std::min<int64_t>((rows + 7) / 8, (int64_t)sm_count() * std::max(per_sm, 1));
+    kernel<<<(unsigned)grid, 256, smem, as_stream(stream)>>>(
+        (const T*)x, (const T*)gamma, mean, rstd, (const T*)dy, (const T*)dres, (T*)dx, dgamma,
+        dbeta, rows, (int)cols);
+  };
+  if (vpl <= 1) go(bwd_fused_warp_rows<T, LAYER, 1>);
+  else if (vpl <= 2) go(bwd_fused_warp_rows<T, LAYER, 2>);
+  else if (vpl <= 3) go(bwd_fused_warp_rows<T, LAYER, 3>);
+  else go(bwd_fused_warp_rows<T, LAYER, 4>);
+  return true;
+}
+
 // GALV_NORM_NT=128|256 forces the CTA width (A/B).  Default (B200 A/B, scratch/norm_ab.py,
 // profiles/r01/kernels_ab/norm_bwd_ab.jsonl): 256 threads, and the fused kernel only for rows of
 // >= 256 vectors (bf16 width >= 2048): 8192x4096 RMS 89.9 -> 65.3 us, 8192x5120 145.9 ->
@@ -500,6 +634,11 @@ static int32_t norm_bwd(const void* x, const void* gamma, const float* mean, con
   GALV_DISPATCH(dtype, T, {
     if (norm::launch_fused<T, LAYER>(x, gamma, mean, rstd, dy, dres, dx, dgamma, dbeta, rows,
                                      cols, stream))
+      break;
+    if (!norm::fused_disabled() && norm::warp_rows_enabled() &&
+        (reinterpret_cast<uintptr_t>(gamma) & 15) == 0 &&
+        norm::launch_fused_warp<T, LAYER>(x, gamma, mean, rstd, dy, dres, dx, dgamma, dbeta,
+                                          rows, cols, stream))
       break;
     if (!norm::launch_dx_row<T, LAYER>(x, gamma, mean, rstd, dy, dres, dx, rows, cols, stream))
       norm::bwd_dx_kernel<T, LAYER><<<grid, norm::WARPS * 32, 0, as_stream(stream)>>>(

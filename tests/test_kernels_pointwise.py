@@ -74,7 +74,10 @@ def test_layernorm(dt):
 
 @pytest.mark.parametrize("layer", [False, True])
 @pytest.mark.parametrize("rows,cols,off", [(3, 4096, 0), (2000, 4096, 1), (1500, 5120, 0),
-                                           (700, 2048, 3), (5000, 1024, 0), (64, 8192, 2)])
+                                           (700, 2048, 3), (5000, 1024, 0), (64, 8192, 2),
+                                           # warp-per-row kernel (<= 1024 columns)
+                                           (16384, 1024, 0), (999, 512, 1), (7, 768, 0),
+                                           (100, 256, 2)])
 def test_norm_bwd_fused_shapes(layer, rows, cols, off):
     """Fused dx+dgamma backward (persistent rows, smem partials, one atomic flush per CTA)
     across the model widths, rows not a multiple of the grid, and dgamma/dbeta views at
@@ -293,3 +296,44 @@ def test_embed_bwd_sorted(dt, gdt):
     again = base.to(gdt).clone()
     K.embed_bwd_sorted(ids, dout, again, vocab_lo=lo)
     assert torch.equal(again, grad)  # deterministic
+
+
+@pytest.mark.parametrize("V", [1001, 50304])
+@pytest.mark.parametrize("dt", DT)
+def test_xent_vocab_parallel_stages(dt, V):
+    """Vocab-parallel cross-entropy as the tp>1 head runs it: stage 0 (row max per shard),
+    max over shards, stage 1 (sum of exp + target logit per shard), sum over shards,
+    stage 2 (loss + in-place gradient); vectorized (V/2 a multiple of 8) and scalar rows."""
+    from paper_2504_21411_b200 import kernels as K
+    torch.manual_seed(12)
+    T = 257
+    logits = (4 * torch.randn(T, V, device="cuda")).to(dt)
+    labels = torch.randint(0, V, (T,), device="cuda")
+    labels[3] = -100
+    lr = logits.float().clone().requires_grad_(True)
+    l_ref = torch.nn.functional.cross_entropy(lr, labels, reduction="none", ignore_index=-100)
+    (l_ref.sum() / T).backward()
+    loss = torch.empty(T, device="cuda")
+    # fused single-launch path on the whole row (V = 1001: the scalar kernel)
+    d = logits.clone()
+    st = torch.empty(T, 3, device="cuda")
+    K.xent(d, labels, st, 3, loss=loss, dlogits=d, grad_scale=1.0 / T)
+    assert rel(loss, l_ref) < tol(dt)
+    assert rel(d, lr.grad) < tol(dt) * 2
+    if V % 2:
+        return
+    Vl = V // 2
+    shards = [logits[:, :Vl].contiguous(), logits[:, Vl:].contiguous()]
+    stats = [torch.empty(T, 3, device="cuda") for _ in shards]
+    for sh, st, r in zip(shards, stats, range(2)):
+        K.xent(sh, labels, st, 0, vocab_lo=r * Vl)
+    mx = torch.maximum(stats[0][:, 0], stats[1][:, 0])
+    for sh, st, r in zip(shards, stats, range(2)):
+        st[:, 0] = mx
+        K.xent(sh, labels, st, 1, vocab_lo=r * Vl)
+    tot = stats[0][:, 1:3] + stats[1][:, 1:3]
+    for sh, st, r in zip(shards, stats, range(2)):
+        st[:, 1:3] = tot
+        K.xent(sh, labels, st, 2, loss=loss, dlogits=sh, vocab_lo=r * Vl, grad_scale=1.0 / T)
+    assert rel(loss, l_ref) < tol(dt)
+    assert rel(torch.cat(shards, 1), lr.grad) < tol(dt) * 2
