@@ -77,18 +77,6 @@ __device__ __forceinline__ float exp2_fma(float x) {
   const int bits = __float_as_int(p) + (__float_as_int(r) << 23);
   return x < -125.f ? 0.f : __int_as_float(bits);
 }
-// 2^x for x <= 0 on the FMA/ALU pipes: x = n + f (n = floor x, f in [0,1)), 2^f by a
-// degree-3 minimax (max rel err 8.6e-5, far below the bf16 rounding of P), exponent by an
-// integer add.  ~8 FP32/INT ops; offloads part of the softmax from the MUFU (XU) pipe.
-__device__ __forceinline__ float exp2_poly3(float x) {
-  const float xc = fmaxf(x, -126.f);
-  const float n = floorf(xc);
-  const float f = xc - n;
-  float p = fmaf(0.07706213f, f, 0.22764884f);
-  p = fmaf(p, f, 0.69511681f);
-  p = fmaf(p, f, 1.0f);
-  return __int_as_float(__float_as_int(p) + (static_cast<int>(n) << 23));
-}
 __device__ __forceinline__ float exp2_mufu(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -430,7 +418,7 @@ struct Smem2 {
 };
 constexpr int FWD2_THREADS = 640;
 
-template <int D, int POLY>
+template <int D>
 __global__ void __launch_bounds__(FWD2_THREADS, 1)
     fwd_tc2(const __grid_constant__ CUtensorMap mq, const __grid_constant__ CUtensorMap mk,
             const __grid_constant__ CUtensorMap mv, const FwdParams p) {
@@ -615,11 +603,10 @@ __global__ void __launch_bounds__(FWD2_THREADS, 1)
 #pragma unroll
         for (int i = 0; i < 16; i += 2) {
           const int e = c * 16 + i;
-          const float x0 = fmaf(s[e], p.scale_log2, -mu), x1 = fmaf(s[e + 1], p.scale_log2, -mu);
-          // POLY > 0: every POLY-th pair on the FMA pipe (exp2_poly3), the rest on MUFU
-          const bool poly = POLY > 0 && ((i >> 1) % (POLY > 0 ? POLY : 1)) == (POLY > 0 ? POLY : 1) - 1;
-          const float p0 = poly ? exp2_poly3(x0) : exp2_mufu(x0);
-          const float p1 = poly ? exp2_poly3(x1) : exp2_mufu(x1);
+          // all exponentials on MUFU: moving 1/4 or 1/2 of them to an FMA-pipe polynomial
+          // measured 4-14 % slower here (D 64 and 128) -- the loop is latency-, not XU-bound
+          const float p0 = exp2_mufu(fmaf(s[e], p.scale_log2, -mu));
+          const float p1 = exp2_mufu(fmaf(s[e + 1], p.scale_log2, -mu));
           r4[(i >> 1) & 3] += p0 + p1;
           pk[i / 2] = pack2(p0, p1);
         }
@@ -1351,16 +1338,6 @@ static bool fwd_two_tiles() {
   return two;
 }
 
-// GALV_ATTN_POLY=k: every k-th exponential pair of the two-tile forward on the FMA pipe
-static int fwd_poly() {
-  static const int k = [] {
-    const char* e = getenv("GALV_ATTN_POLY");
-    const int v = e ? atoi(e) : 0;
-    return (v == 2 || v == 3 || v == 4) ? v : 0;
-  }();
-  return k;
-}
-
 }  // namespace fa
 
 int32_t attn_fwd_sm100(const void* q, const void* k, const void* v, void* o, float* lse,
@@ -1404,11 +1381,7 @@ int32_t attn_fwd_sm100(const void* q, const void* k, const void* v, void* o, flo
   int32_t rc;
   if (fwd_two_tiles()) {  // default: the two-Q-tile kernel (fwd_tc2)
     const dim3 grid2((unsigned)((p.n_qblocks + 1) / 2), (unsigned)(B * H));
-    const int poly = fwd_poly();
-    auto kern = D == 128 ? (poly == 4 ? fwd_tc2<128, 4> : poly == 2 ? fwd_tc2<128, 2>
-                            : poly == 3 ? fwd_tc2<128, 3> : fwd_tc2<128, 0>)
-                         : (poly == 4 ? fwd_tc2<64, 4> : poly == 2 ? fwd_tc2<64, 2>
-                            : poly == 3 ? fwd_tc2<64, 3> : fwd_tc2<64, 0>);
+    auto kern = D == 128 ? fwd_tc2<128> : fwd_tc2<64>;
     const int smem = D == 128 ? Smem2<128>::BYTES : Smem2<64>::BYTES;
     GALV_CUDA_RET(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     kern<<<grid2, FWD2_THREADS, smem, stream>>>(mq, mk, mv, p);

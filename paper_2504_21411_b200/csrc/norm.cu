@@ -358,54 +358,66 @@ __global__ void __launch_bounds__(NT) bwd_fused_rows(
 // once; the partials are summed over the CTA's warps through smem and flushed with one
 // atomic per column per CTA.
 template <typename T, bool LAYER, int VPL>
-__global__ void __launch_bounds__(256) bwd_fused_warp_rows(
+__global__ void __launch_bounds__(256, 2) bwd_fused_warp_rows(
     const T* __restrict__ x, const T* __restrict__ gamma, const float* __restrict__ mean,
     const float* __restrict__ rstd, const T* __restrict__ dy, const T* __restrict__ dres,
     T* __restrict__ dx, float* __restrict__ dgamma, float* __restrict__ dbeta, int64_t rows,
     int cols) {
   constexpr int V = 16 / sizeof(T);
   constexpr int NW = 8;
-  extern __shared__ float sred[];  // [NW][cols] dgamma (+ [NW][cols] dbeta)
+  // per-warp dgamma (/dbeta) partials in smem ([NW][cols] each): every lane owns its
+  // columns, so read-modify-write needs no atomics; x / dy / gamma stay packed in registers
+  // (a register-resident version used 223 registers: one CTA per SM, latency-bound)
+  extern __shared__ float sred[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  float ga[VPL][V], ba[VPL][V], g[VPL][V];
+  float* ga = sred + warp * cols;
+  float* ba = sred + (NW + warp) * cols;
+  uint4 gv[VPL];
 #pragma unroll
   for (int j = 0; j < VPL; ++j) {
     const int c = (j * 32 + lane) * V;
+    if (c < cols) {
+      gv[j] = *reinterpret_cast<const uint4*>(gamma + c);
 #pragma unroll
-    for (int i = 0; i < V; ++i) ga[j][i] = ba[j][i] = 0.f;
-    if (c < cols) load16(gamma + c, g[j]);
+      for (int i = 0; i < V; ++i) {
+        ga[c + i] = 0.f;
+        if (LAYER) ba[c + i] = 0.f;
+      }
+    }
   }
   const float inv_cols = 1.f / cols;
   for (int64_t row = (int64_t)blockIdx.x * NW + warp; row < rows; row += (int64_t)gridDim.x * NW) {
     const T* xr = x + row * cols;
     const T* dyr = dy + row * cols;
     const float mu = LAYER ? mean[row] : 0.f, rs = rstd[row];
-    float v[VPL][V], d[VPL][V];
+    uint4 xv[VPL], dv[VPL];
 #pragma unroll
     for (int j = 0; j < VPL; ++j) {
       const int c = (j * 32 + lane) * V;
       if (c < cols) {
-        const uint4 xv = __ldcs(reinterpret_cast<const uint4*>(xr + c));
-        const uint4 dv = __ldcs(reinterpret_cast<const uint4*>(dyr + c));
-        load16(reinterpret_cast<const T*>(&xv), v[j]);
-        load16(reinterpret_cast<const T*>(&dv), d[j]);
-      } else {
-#pragma unroll
-        for (int i = 0; i < V; ++i) v[j][i] = d[j][i] = 0.f;
+        xv[j] = __ldcs(reinterpret_cast<const uint4*>(xr + c));
+        dv[j] = __ldcs(reinterpret_cast<const uint4*>(dyr + c));
       }
     }
     float a1 = 0.f, a2 = 0.f;
 #pragma unroll
-    for (int j = 0; j < VPL; ++j)
+    for (int j = 0; j < VPL; ++j) {
+      const int c = (j * 32 + lane) * V;
+      if (c >= cols) continue;
+      float v[V], d[V], g[V];
+      load16(reinterpret_cast<const T*>(&xv[j]), v);
+      load16(reinterpret_cast<const T*>(&dv[j]), d);
+      load16(reinterpret_cast<const T*>(&gv[j]), g);
 #pragma unroll
       for (int i = 0; i < V; ++i) {
-        const float xh = (v[j][i] - mu) * rs;
-        const float gd = g[j][i] * d[j][i];
+        const float xh = (v[i] - mu) * rs;
+        const float gd = g[i] * d[i];
         a1 += gd * xh;
         a2 += gd;
-        ga[j][i] += d[j][i] * xh;
-        if (LAYER) ba[j][i] += d[j][i];
+        ga[c + i] += d[i] * xh;
+        if (LAYER) ba[c + i] += d[i];
       }
+    }
     a1 = warp_sum(a1) * inv_cols;
     a2 = warp_sum(a2) * inv_cols;
     T* dxr = dx + row * cols;
@@ -414,27 +426,19 @@ __global__ void __launch_bounds__(256) bwd_fused_warp_rows(
     for (int j = 0; j < VPL; ++j) {
       const int c = (j * 32 + lane) * V;
       if (c >= cols) continue;
-      float r[V];
+      float v[V], d[V], g[V], r[V];
+      load16(reinterpret_cast<const T*>(&xv[j]), v);
+      load16(reinterpret_cast<const T*>(&dv[j]), d);
+      load16(reinterpret_cast<const T*>(&gv[j]), g);
       if (drr) load16(drr + c, r);
 #pragma unroll
       for (int i = 0; i < V; ++i) {
-        const float xh = (v[j][i] - mu) * rs;
-        float o = rs * (g[j][i] * d[j][i] - xh * a1 - (LAYER ? a2 : 0.f));
+        const float xh = (v[i] - mu) * rs;
+        float o = rs * (g[i] * d[i] - xh * a1 - (LAYER ? a2 : 0.f));
         if (drr) o += r[i];
-        v[j][i] = o;
+        v[i] = o;
       }
-      store16(dxr + c, v[j]);
-    }
-  }
-  // CTA reduction of the per-warp partials, one atomic per column
-#pragma unroll
-  for (int j = 0; j < VPL; ++j) {
-    const int c = (j * 32 + lane) * V;
-    if (c >= cols) continue;
-#pragma unroll
-    for (int i = 0; i < V; ++i) {
-      sred[warp * cols + c + i] = ga[j][i];
-      if (LAYER) sred[(NW + warp) * cols + c + i] = ba[j][i];
+      store16(dxr + c, v);
     }
   }
   __syncthreads();
