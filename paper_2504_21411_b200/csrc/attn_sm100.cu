@@ -505,8 +505,10 @@ __global__ void __launch_bounds__(FWD2_THREADS, 1)
     mbar_wait_fast(q_full, 0);
     auto issue_s = [&](int t, int j) {
       const int st = j & 1;
+      if (lane == 0) TRACE(4096 + t * 1024 + j * 8 + 0);
       mbar_wait_fast(&k_full[st], (j >> 1) & 1);
       tc_fence_after();
+      if (lane == 0) TRACE(4096 + t * 1024 + j * 8 + 1);
       const uint64_t bk = d_k + (uint64_t)((st * L::TILE) >> 4);
       const uint64_t bq = d_q + (uint64_t)((t * L::TILE) >> 4);
       if (elect_one()) {
@@ -522,9 +524,12 @@ __global__ void __launch_bounds__(FWD2_THREADS, 1)
     };
     auto issue_pv = [&](int t, int j) {
       const int st = j & 1;
+      if (lane == 0) TRACE(4096 + t * 1024 + j * 8 + 2);
       mbar_wait_fast(&p_full[t], j & 1);
+      if (lane == 0) TRACE(4096 + t * 1024 + j * 8 + 3);
       mbar_wait_fast(&v_full[st], (j >> 1) & 1);
       tc_fence_after();
+      if (lane == 0) TRACE(4096 + t * 1024 + j * 8 + 4);
       const uint64_t bv = d_v + (uint64_t)((st * L::TILE) >> 4);
       const uint32_t t_o = tmem + 256 + t * 128, t_p = tmem + t * 128;
       if (elect_one()) {
@@ -561,9 +566,12 @@ __global__ void __launch_bounds__(FWD2_THREADS, 1)
     const int bar_id = 1 + t * 4 + q;
     float m_used = -INFINITY, l = 0.f;
     constexpr int HC = BKV / 2;
+    const bool tr = (warp == 4 || warp == 12) && lane == 0;
     for (int j = 0; j < n_t; ++j) {
+      if (tr) TRACE(t * 1024 + j * 8 + 0);
       mbar_wait(&s_full[t], j & 1);
       tc_fence_after();
+      if (tr) TRACE(t * 1024 + j * 8 + 1);
       float s[HC];
 #pragma unroll
       for (int c = 0; c < HC / 32; ++c)
@@ -584,9 +592,11 @@ __global__ void __launch_bounds__(FWD2_THREADS, 1)
       for (int i = 8; i < HC; ++i) m8[i & 7] = fmaxf(m8[i & 7], s[i]);
       float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
                        fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
+      if (tr) TRACE(t * 1024 + j * 8 + 2);
       xch[(j & 1) * 256 + half * 128 + r] = mx;
       asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
       mx = fmaxf(mx, xch[(j & 1) * 256 + (half ^ 1) * 128 + r]);
+      if (tr) TRACE(t * 1024 + j * 8 + 3);
       mx *= p.scale_log2;
       float alpha = 1.f;
       if ((mx > m_used + RESCALE_THRESHOLD || m_used == -INFINITY) && mx != -INFINITY) {
@@ -614,6 +624,7 @@ __global__ void __launch_bounds__(FWD2_THREADS, 1)
       }
       l = l * alpha + ((r4[0] + r4[1]) + (r4[2] + r4[3]));
       tmem_wait_st();
+      if (tr) TRACE(t * 1024 + j * 8 + 4);
       // lazy rescale of O (after P is out of registers): O must hold PV(j-1) first; o_done
       // has completed j-1 or j phases here (PV(j) needs this P), so the parity wait is exact
       if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
@@ -631,6 +642,7 @@ __global__ void __launch_bounds__(FWD2_THREADS, 1)
       }
       tc_fence_before();
       mbar_arrive(&p_full[t]);
+      if (tr) TRACE(t * 1024 + j * 8 + 5);
     }
     if (n_t > 0) {
       xch[512 + half * 128 + r] = l;

@@ -11,11 +11,14 @@ namespace norm {
 constexpr int WARPS = 8;
 
 // GALV_NORM_UNFUSED=1 selects the two-kernel backward (dx pass, then dgamma pass) for A/B.
-// GALV_NORM_WARP=0: narrow rows fall back to the dx + dgamma kernel pair (A/B)
+// GALV_NORM_WARP=1 opts narrow rows into the warp-per-row kernel.  Off by default: B200,
+// 16384 x 1024 LayerNorm backward 77.1 us vs 48.3 us for the dx + dgamma pair
+// (tools/pointwise_bench.py, profiles/r02/kernels_ab/pointwise.jsonl) -- the per-element
+// smem read-modify-write of the partials costs more than the pair's second read.
 static bool warp_rows_enabled() {
   static const bool on = [] {
     const char* e = getenv("GALV_NORM_WARP");
-    return !(e && e[0] == '0');
+    return e && e[0] == '1';
   }();
   return on;
 }
