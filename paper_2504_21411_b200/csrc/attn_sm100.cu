@@ -404,8 +404,8 @@ __global__ void __launch_bounds__(384, 1)
 //   warp 1    : MMA issuer: S_0(0), S_1(0), then per block j: PV_0(j), S_0(j+1), PV_1(j),
 //               S_1(j+1)
 //   warp 2    : TMEM allocator;  warp 3: idle
-//   warps 4-11: softmax of tile 0;  warps 12-19: softmax of tile 1 (per tile as fwd_tc:
-//               quarter = warp % 4 owns TMEM lanes, half = which 64 key columns)
+//   warps 4-7 : softmax of tile 0;  warps 8-11: softmax of tile 1 (one thread per query
+//               row = TMEM lane, quarter = warp % 4, all 128 key columns in registers)
 template <int D>
 struct Smem2 {
   static constexpr int TILE = D * 128 * 2;
@@ -416,7 +416,7 @@ struct Smem2 {
   static constexpr int XCH = BAR + 256;          // per tile: [2][256] maxima + [256] sums
   static constexpr int BYTES = XCH + 2 * 768 * 4 + 1024;
 };
-constexpr int FWD2_THREADS = 640;
+constexpr int FWD2_THREADS = 384;
 
 template <int D>
 __global__ void __launch_bounds__(FWD2_THREADS, 1)
@@ -457,7 +457,7 @@ __global__ void __launch_bounds__(FWD2_THREADS, 1)
       mbar_init(&k_empty[i], 1);
       mbar_init(&v_empty[i], 1);
       mbar_init(&s_full[i], 1);
-      mbar_init(&p_full[i], 256);
+      mbar_init(&p_full[i], 128);
       mbar_init(&o_done[i], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -555,48 +555,43 @@ __global__ void __launch_bounds__(FWD2_THREADS, 1)
       }
     }
   } else if (warp >= 4) {
-    const int t = (warp - 4) >> 3;              // tile
-    const int q = warp & 3, half = ((warp - 4) >> 2) & 1;
+    // softmax: one thread per query row (warp % 4 = TMEM lane quarter), all 128 key columns
+    // of a block in registers -- no cross-warp row-max exchange (the two-threads-per-row
+    // split spent ~300 of ~1800 cycles per block in that smem exchange + named barrier)
+    const int t = (warp - 4) >> 2;              // tile
+    const int q = warp & 3;
     const int r = q * 32 + lane;
     const int qt = q0 + t * BQ, qi = qt + r;
     const int n_t = t == 0 ? nkv0 : nkv1;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     const uint32_t t_s = tmem + t * 128, t_o = tmem + 256 + t * 128;
-    float* xch = reinterpret_cast<float*>(sm + L::XCH) + t * 768;
-    const int bar_id = 1 + t * 4 + q;
     float m_used = -INFINITY, l = 0.f;
-    constexpr int HC = BKV / 2;
-    const bool tr = (warp == 4 || warp == 12) && lane == 0;
+    const bool tr = (warp == 4 || warp == 8) && lane == 0;
     for (int j = 0; j < n_t; ++j) {
       if (tr) TRACE(t * 1024 + j * 8 + 0);
       mbar_wait(&s_full[t], j & 1);
       tc_fence_after();
       if (tr) TRACE(t * 1024 + j * 8 + 1);
-      float s[HC];
+      float s[BKV];
 #pragma unroll
-      for (int c = 0; c < HC / 32; ++c)
-        tmem_ld32_nowait(t_s + half * HC + c * 32 + lane_off,
-                         reinterpret_cast<uint32_t*>(s) + c * 32);
+      for (int c = 0; c < BKV / 32; ++c)
+        tmem_ld32_nowait(t_s + c * 32 + lane_off, reinterpret_cast<uint32_t*>(s) + c * 32);
       tmem_wait_ld();
-      const int k0 = j * BKV + half * HC;
-      const bool mask = (k0 + HC > p.S) || (p.causal && k0 + HC - 1 > qt);
-      if (mask) {
+      const int k0 = j * BKV;
+      const bool mask = (k0 + BKV > p.S) || (p.causal && k0 + BKV - 1 > qt);
+      if (mask) {  // diagonal / tail block: keys >= lim are invisible to this row
         const int lim = (p.causal ? min(p.S, qi + 1) : p.S) - k0;
 #pragma unroll
-        for (int i = 0; i < HC; ++i) s[i] = i < lim ? s[i] : -INFINITY;
+        for (int i = 0; i < BKV; ++i) s[i] = i < lim ? s[i] : -INFINITY;
       }
       float m8[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) m8[u] = s[u];
 #pragma unroll
-      for (int i = 8; i < HC; ++i) m8[i & 7] = fmaxf(m8[i & 7], s[i]);
+      for (int i = 8; i < BKV; ++i) m8[i & 7] = fmaxf(m8[i & 7], s[i]);
       float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
                        fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
       if (tr) TRACE(t * 1024 + j * 8 + 2);
-      xch[(j & 1) * 256 + half * 128 + r] = mx;
-      asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
-      mx = fmaxf(mx, xch[(j & 1) * 256 + (half ^ 1) * 128 + r]);
-      if (tr) TRACE(t * 1024 + j * 8 + 3);
       mx *= p.scale_log2;
       float alpha = 1.f;
       if ((mx > m_used + RESCALE_THRESHOLD || m_used == -INFINITY) && mx != -INFINITY) {
@@ -605,22 +600,22 @@ __global__ void __launch_bounds__(FWD2_THREADS, 1)
       }
       const float mu = (m_used == -INFINITY) ? 0.f : m_used;
       float r4[4] = {0.f, 0.f, 0.f, 0.f};
-      // P in chunks of 16 keys -> 8 packed columns each, stored as they are produced so the
-      // score registers die progressively (20 warps leave 96 registers per thread)
+      // P in chunks of 16 keys -> 8 packed bf16x2 columns, placed where the PV MMA reads
+      // its A operand: keys 16c.. at column 64*(c/4) + 8*(c%4) of the tile's S columns
 #pragma unroll
-      for (int c = 0; c < HC / 16; ++c) {
+      for (int c = 0; c < BKV / 16; ++c) {
         uint32_t pk[8];
 #pragma unroll
         for (int i = 0; i < 16; i += 2) {
           const int e = c * 16 + i;
           // all exponentials on MUFU: moving 1/4 or 1/2 of them to an FMA-pipe polynomial
-          // measured 4-14 % slower here (D 64 and 128) -- the loop is latency-, not XU-bound
+          // measured 4-14 % slower (D 64 and 128, two-threads-per-row variant)
           const float p0 = exp2_mufu(fmaf(s[e], p.scale_log2, -mu));
           const float p1 = exp2_mufu(fmaf(s[e + 1], p.scale_log2, -mu));
           r4[(i >> 1) & 3] += p0 + p1;
           pk[i / 2] = pack2(p0, p1);
         }
-        tmem_st8(t_s + half * HC + c * 8 + lane_off, pk);
+        tmem_st8(t_s + (c >> 2) * 64 + (c & 3) * 8 + lane_off, pk);
       }
       l = l * alpha + ((r4[0] + r4[1]) + (r4[2] + r4[3]));
       tmem_wait_st();
@@ -631,9 +626,9 @@ __global__ void __launch_bounds__(FWD2_THREADS, 1)
         mbar_wait(&o_done[t], (j - 1) & 1);
         tc_fence_after();
 #pragma unroll 1
-        for (int c = 0; c < D / 64; ++c) {
+        for (int c = 0; c < D / 32; ++c) {
           uint32_t ov[32];
-          const uint32_t ta = t_o + half * (D / 2) + c * 32 + lane_off;
+          const uint32_t ta = t_o + c * 32 + lane_off;
           tmem_ld32(ta, ov);
 #pragma unroll
           for (int i = 0; i < 32; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * alpha);
@@ -645,18 +640,14 @@ __global__ void __launch_bounds__(FWD2_THREADS, 1)
       if (tr) TRACE(t * 1024 + j * 8 + 5);
     }
     if (n_t > 0) {
-      xch[512 + half * 128 + r] = l;
-      asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
-      l += xch[512 + (half ^ 1) * 128 + r];
       mbar_wait(&o_done[t], (n_t - 1) & 1);
       tc_fence_after();
       const float inv_l = l > 0.f ? 1.f / l : 0.f;
-      __nv_bfloat16* orow =
-          p.o + (long long)(tok0 + qi) * p.o_st + (long long)h * p.sh + half * (D / 2);
+      __nv_bfloat16* orow = p.o + (long long)(tok0 + qi) * p.o_st + (long long)h * p.sh;
 #pragma unroll 1
-      for (int c = 0; c < D / 64; ++c) {
+      for (int c = 0; c < D / 32; ++c) {
         uint32_t ov[32];
-        tmem_ld32(t_o + half * (D / 2) + c * 32 + lane_off, ov);
+        tmem_ld32(t_o + c * 32 + lane_off, ov);
         if (qi < p.S) {
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
@@ -669,7 +660,7 @@ __global__ void __launch_bounds__(FWD2_THREADS, 1)
           }
         }
       }
-      if (qi < p.S && half == 0)
+      if (qi < p.S)
         p.lse[((long long)b * p.H + h) * p.S + qi] = (m_used + log2f(l)) * 0.6931471805599453f;
     }
   }
