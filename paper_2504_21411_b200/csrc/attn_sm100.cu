@@ -600,23 +600,23 @@ __global__ void __launch_bounds__(FWD2_THREADS, 1)
       }
       const float mu = (m_used == -INFINITY) ? 0.f : m_used;
       float r4[4] = {0.f, 0.f, 0.f, 0.f};
-      // P as packed bf16x2 where the PV MMA reads its A operand: keys 0-63 -> columns 0-31,
-      // keys 64-127 -> columns 64-95 of the tile's S columns.  One straight-line loop over
-      // all 64 pairs, then two stores: the scores die as the packed pairs fill in, and the
-      // 128 MUFU ops form one scheduling region (per-chunk stores drained the MUFU pipe
-      // between chunks: ~1500 instead of ~1024 cycles per block)
-      uint32_t pk[BKV / 2];
+      // P in chunks of 16 keys -> 8 packed bf16x2 columns, placed where the PV MMA reads
+      // its A operand: keys 16c.. at column 64*(c/4) + 8*(c%4) of the tile's S columns
 #pragma unroll
-      for (int i = 0; i < BKV; i += 2) {
-        // all exponentials on MUFU: moving 1/4 or 1/2 of them to an FMA-pipe polynomial
-        // measured 4-14 % slower (D 64 and 128, two-threads-per-row variant)
-        const float p0 = exp2_mufu(fmaf(s[i], p.scale_log2, -mu));
-        const float p1 = exp2_mufu(fmaf(s[i + 1], p.scale_log2, -mu));
-        r4[(i >> 1) & 3] += p0 + p1;
-        pk[i / 2] = pack2(p0, p1);
+      for (int c = 0; c < BKV / 16; ++c) {
+        uint32_t pk[8];
+#pragma unroll
+        for (int i = 0; i < 16; i += 2) {
+          const int e = c * 16 + i;
+          // all exponentials on MUFU: moving 1/4 or 1/2 of them to an FMA-pipe polynomial
+          // measured 4-14 % slower (D 64 and 128, two-threads-per-row variant)
+          const float p0 = exp2_mufu(fmaf(s[e], p.scale_log2, -mu));
+          const float p1 = exp2_mufu(fmaf(s[e + 1], p.scale_log2, -mu));
+          r4[(i >> 1) & 3] += p0 + p1;
+          pk[i / 2] = pack2(p0, p1);
+        }
+        tmem_st8(t_s + (c >> 2) * 64 + (c & 3) * 8 + lane_off, pk);
       }
-      tmem_st32_async(t_s + lane_off, pk);
-      tmem_st32_async(t_s + 64 + lane_off, pk + 32);
       l = l * alpha + ((r4[0] + r4[1]) + (r4[2] + r4[3]));
       tmem_wait_st();
       if (tr) TRACE(t * 1024 + j * 8 + 4);

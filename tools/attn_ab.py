@@ -138,7 +138,11 @@ def main():
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--shapes", default="2x4096x32,1x32768x8,4x1024x16x64")
     ap.add_argument("--galv-only", action="store_true", help="skip the library arms")
+    ap.add_argument("--lib", default=None, help="load this libgalv build instead (A/B)")
     args = ap.parse_args()
+    if args.lib:
+        from paper_2504_21411_b200 import kernels as K
+        K._lib = K.load_library(args.lib)
     rows = []
     for spec in args.shapes.split(","):
         parts = [int(x) for x in spec.split("x")]
