@@ -103,6 +103,31 @@ int32_t galv_attn_bwd_rope(const void* q, const void* k, const void* v, const vo
                            int64_t stride_head, int64_t o_stride_tok, float scale,
                            int32_t causal, const float* rope_table, int32_t epilogue,
                            int32_t dtype, void* ws, void* stream);
+/* Softmax-dropout variants (SURVEY.md §8(b) attn_fwd / attn_bwd with p, seed, offset;
+ * north_star (1) softmax-dropout).  Attention probabilities are dropped with probability
+ * dropout_p and the kept ones scaled by 1/(1-p); the keep mask is Philox4x32-10 of
+ * (counter = (key/4, query, (b0+b)*H_total + h0+h, offset), key = seed) -- csrc/dropout.cuh,
+ * regenerated identically by the forward and both backward kernels (nothing stored).
+ * b0 / h0 / H_total place this call's local (b, h) in the global batch / head grid, so the
+ * mask does not depend on how dp / tp / Ulysses shard the call.  dropout_p = 0: exactly
+ * galv_attn_fwd / galv_attn_bwd(_rope).  rope_table NULL: no inverse RoPE. */
+int32_t galv_attn_fwd_dropout(const void* q, const void* k, const void* v, void* o, float* lse,
+                              int64_t B, int64_t S, int64_t H, int64_t D, int64_t stride_tok,
+                              int64_t stride_head, int64_t o_stride_tok, float scale,
+                              int32_t causal, float dropout_p, uint64_t seed, uint64_t offset,
+                              int64_t b0, int64_t h0, int64_t H_total, int32_t dtype,
+                              void* stream);
+int32_t galv_attn_bwd_dropout(const void* q, const void* k, const void* v, const void* o,
+                              const void* dout, const float* lse, void* dq, void* dk, void* dv,
+                              int64_t B, int64_t S, int64_t H, int64_t D, int64_t stride_tok,
+                              int64_t stride_head, int64_t o_stride_tok, float scale,
+                              int32_t causal, float dropout_p, uint64_t seed, uint64_t offset,
+                              int64_t b0, int64_t h0, int64_t H_total, const float* rope_table,
+                              int32_t epilogue, int32_t dtype, void* ws, void* stream);
+/* The keep mask itself, uint8 [B][H][S][S] (tests: cross-checked against the CPU Philox). */
+int32_t galv_dropout_mask(uint8_t* mask, int64_t B, int64_t S, int64_t H, float dropout_p,
+                          uint64_t seed, uint64_t offset, int64_t b0, int64_t h0,
+                          int64_t H_total, void* stream);
 
 /* y = norm(x (+ residual)) * gamma (+ beta).  rows x cols; residual/res_out optional:
  * when residual != NULL, res_out = x + residual is written and normalized.

@@ -9,7 +9,8 @@ GPT-2 block (pre-LN):  x += proj(attn(LN1(x))) ; x += fc2(gelu_tanh(fc1(LN2(x)))
 Llama-2 block:         x += proj(attn(rope(RMSNorm1(x)))) ; x += down(silu(gate)*up)
   RMSNorm eps 1e-5 (weight * x * rsqrt(mean(x^2)+eps)), rotate-half RoPE theta 1e4,
   no biases, final RMSNorm, untied LM head.
-Causal softmax attention with scale 1/sqrt(head_dim).  Loss = mean token
+Causal softmax attention with scale 1/sqrt(head_dim); optional dropout of the attention
+probabilities (cfg.attn_dropout) with the Philox4x32-10 mask of oracle/dropout_ref.py.  Loss = mean token
 cross-entropy over all B*S positions of the global batch, labels = tokens shifted by
 one (inputs tokens[:, :S], labels tokens[:, 1:S+1]).
 
@@ -66,18 +67,33 @@ def _rope(x, theta):
     return torch.cat([x1 * cos - x2 * sin, x2 * cos + x1 * sin], dim=-1)
 
 
-def _attention(q, k, v):
-    # [B, S, H, D] -> [B, S, H, D], causal
+def _attention(q, k, v, keep=None, p=0.0):
+    # [B, S, H, D] -> [B, S, H, D], causal; keep: bool [B, H, S, S] dropout mask of the
+    # attention probabilities (kept ones scaled by 1/(1-p)), oracle/dropout_ref.py
     B, S, H, D = q.shape
     qt, kt, vt = (t.transpose(1, 2) for t in (q, k, v))
     scores = qt @ kt.transpose(-1, -2) / math.sqrt(D)
     mask = torch.triu(torch.ones(S, S, dtype=torch.bool), diagonal=1)
     scores = scores.masked_fill(mask, float("-inf"))
-    return (torch.softmax(scores, dim=-1) @ vt).transpose(1, 2)
+    probs = torch.softmax(scores, dim=-1)
+    if keep is not None:
+        probs = probs * torch.as_tensor(keep).to(probs.dtype) / (1.0 - p)
+    return (probs @ vt).transpose(1, 2)
 
 
-def forward(cfg, w: dict, tokens: torch.Tensor):
-    """Mean next-token loss of tokens [B, S+1] (int64) under weights ``w``."""
+def attention_keep_mask(cfg, B: int, layer: int, *, seed: int, step: int = 0):
+    """The runtime's attention-dropout mask of decoder `layer` for a global batch of B
+    sequences (Philox counter offset = (step << 16) | layer; sample / head indices global)."""
+    from oracle.dropout_ref import keep_mask
+    return keep_mask(B, cfg.seq_len, cfg.heads, cfg.attn_dropout, seed,
+                     (step << 16) | layer)
+
+
+def forward(cfg, w: dict, tokens: torch.Tensor, *, dropout_seed: int | None = None,
+            dropout_step: int = 0):
+    """Mean next-token loss of tokens [B, S+1] (int64) under weights ``w``; with
+    cfg.attn_dropout > 0 and a dropout_seed, the attention probabilities are dropped with
+    the runtime's Philox mask (attention_keep_mask)."""
     B = tokens.shape[0]
     S, h, H = cfg.seq_len, cfg.hidden, cfg.heads
     D = h // H
@@ -98,7 +114,10 @@ def forward(cfg, w: dict, tokens: torch.Tensor):
         q, k, v = (t.reshape(B, S, H, D) for t in (q, k, v))
         if cfg.arch == "llama":
             q, k = _rope(q, cfg.rope_theta), _rope(k, cfg.rope_theta)
-        a = _attention(q, k, v).reshape(B, S, h)
+        p_drop = getattr(cfg, "attn_dropout", 0.0)
+        keep = (attention_keep_mask(cfg, B, i, seed=dropout_seed, step=dropout_step)
+                if p_drop > 0 and dropout_seed is not None else None)
+        a = _attention(q, k, v, keep, p_drop).reshape(B, S, h)
         a = a @ w[p + "proj.weight"].t()
         if cfg.arch == "gpt":
             a = a + w[p + "proj.bias"]
@@ -121,9 +140,10 @@ def forward(cfg, w: dict, tokens: torch.Tensor):
     return F.cross_entropy(logits.reshape(-1, cfg.vocab), labels.reshape(-1))
 
 
-def loss_and_grads(cfg, weights: dict, tokens: torch.Tensor, dtype=torch.float64):
+def loss_and_grads(cfg, weights: dict, tokens: torch.Tensor, dtype=torch.float64, *,
+                   dropout_seed: int | None = None, dropout_step: int = 0):
     """(loss, {name: grad}) for one fwd+bwd on CPU in ``dtype``."""
     w = {k: v.detach().to("cpu", dtype).clone().requires_grad_(True) for k, v in weights.items()}
-    loss = forward(cfg, w, tokens.cpu())
+    loss = forward(cfg, w, tokens.cpu(), dropout_seed=dropout_seed, dropout_step=dropout_step)
     loss.backward()
     return loss.detach(), {k: v.grad for k, v in w.items()}

@@ -10,6 +10,7 @@
 //              rescale (O in TMEM is rescaled only when a row max grows by > 2^8),
 //              P written to smem as a 128B-swizzled K-major bf16 operand, epilogue.
 #include "common.cuh"
+#include "dropout.cuh"
 #include "sm100.cuh"
 
 namespace galv {
@@ -60,6 +61,7 @@ struct FwdParams {
   float* lse;
   long long o_st;  // o token stride (elements)
   long long sh;    // head stride (elements)
+  DropoutParams drop;  // attention-probability dropout (fwd_tc2 only; thresh 0 = off)
 };
 
 // 2^x on the FMA/ALU pipes (Cody-Waite split + degree-4 minimax, rel err 5e-6): used for
@@ -418,7 +420,7 @@ struct Smem2 {
 };
 constexpr int FWD2_THREADS = 384;
 
-template <int D>
+template <int D, bool DROP>
 __global__ void __launch_bounds__(FWD2_THREADS, 1)
     fwd_tc2(const __grid_constant__ CUtensorMap mq, const __grid_constant__ CUtensorMap mk,
             const __grid_constant__ CUtensorMap mv, const FwdParams p) {
@@ -605,6 +607,13 @@ __global__ void __launch_bounds__(FWD2_THREADS, 1)
 #pragma unroll
       for (int c = 0; c < BKV / 16; ++c) {
         uint32_t pk[8];
+        uint32_t keep = 0xFFFFu;  // dropout: keep bits of the chunk's 16 keys
+        if constexpr (DROP) {
+          keep = 0;
+#pragma unroll
+          for (int g = 0; g < 4; ++g)
+            keep |= dropout_keep4(p.drop, b, h, qi, k0 + c * 16 + g * 4) << (4 * g);
+        }
 #pragma unroll
         for (int i = 0; i < 16; i += 2) {
           const int e = c * 16 + i;
@@ -612,8 +621,11 @@ __global__ void __launch_bounds__(FWD2_THREADS, 1)
           // measured 4-14 % slower (D 64 and 128, two-threads-per-row variant)
           const float p0 = exp2_mufu(fmaf(s[e], p.scale_log2, -mu));
           const float p1 = exp2_mufu(fmaf(s[e + 1], p.scale_log2, -mu));
-          r4[(i >> 1) & 3] += p0 + p1;
-          pk[i / 2] = pack2(p0, p1);
+          r4[(i >> 1) & 3] += p0 + p1;  // the normalizer uses the undropped probabilities
+          if constexpr (DROP)
+            pk[i / 2] = pack2((keep >> i) & 1u ? p0 : 0.f, (keep >> (i + 1)) & 1u ? p1 : 0.f);
+          else
+            pk[i / 2] = pack2(p0, p1);
         }
         tmem_st8(t_s + (c >> 2) * 64 + (c & 3) * 8 + lane_off, pk);
       }
@@ -642,7 +654,8 @@ __global__ void __launch_bounds__(FWD2_THREADS, 1)
     if (n_t > 0) {
       mbar_wait(&o_done[t], (n_t - 1) & 1);
       tc_fence_after();
-      const float inv_l = l > 0.f ? 1.f / l : 0.f;
+      // dropout: kept probabilities carry 1 / (1 - p)
+      const float inv_l = l > 0.f ? (DROP ? p.drop.inv_keep : 1.f) / l : 0.f;
       __nv_bfloat16* orow = p.o + (long long)(tok0 + qi) * p.o_st + (long long)h * p.sh;
 #pragma unroll 1
       for (int c = 0; c < D / 32; ++c) {
@@ -730,6 +743,7 @@ struct BwdParams {
   __nv_bfloat16* g1;   // dkdv: dv
   long long st, sh;    // output (q layout) strides
   const float* rope;   // optional fp32 [2][S][D/2] cos|sin planes: inverse RoPE on dq / dk
+  DropoutParams drop;  // attention-probability dropout (thresh 0 = off)
 };
 
 template <int D>
@@ -852,7 +866,7 @@ __device__ __forceinline__ void store_row_out16(__nv_bfloat16* dst, uint32_t tad
   }
 }
 
-template <int D>
+template <int D, bool DROP>
 __global__ void __launch_bounds__(BWD_THREADS, 1)
     bwd_dkdv_tc(const __grid_constant__ CUtensorMap mq, const __grid_constant__ CUtensorMap mk,
                 const __grid_constant__ CUtensorMap mv, const __grid_constant__ CUtensorMap mdo,
@@ -1004,7 +1018,17 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       const float* dd = reinterpret_cast<const float*>(sm + L::DV + st * 256) + part * BWD_CP;
       const int qbase = q0 + part * BWD_CP;
       const float sl2 = p.scale_log2;
-      if (p.causal && key > qbase) {  // diagonal: queries < key are masked
+      if constexpr (DROP) {
+        // dropout: dV uses the kept, 1/(1-p)-scaled P; dS = P * (dP * mask / (1-p) - D)
+        const int first = p.causal ? key - qbase : -1;
+#pragma unroll
+        for (int i = 0; i < BWD_CP; ++i) {
+          const float pv = i >= first ? exp2_mufu(fmaf(s[i], sl2, -l2[i])) : 0.f;
+          const float kp = dropout_keep(p.drop, b, h, qbase + i, key) ? p.drop.inv_keep : 0.f;
+          s[i] = pv * kp;
+          dp[i] = pv * (dp[i] * kp - dd[i]);
+        }
+      } else if (p.causal && key > qbase) {  // diagonal: queries < key are masked
         const int first = key - qbase;
 #pragma unroll
         for (int i = 0; i < BWD_CP; ++i) {
@@ -1082,7 +1106,7 @@ struct SmemQ {
   static constexpr int BYTES = BAR + 256 + 1024;
 };
 
-template <int D>
+template <int D, bool DROP>
 __global__ void __launch_bounds__(BWD_THREADS, 1)
     bwd_dq_tc(const __grid_constant__ CUtensorMap mq, const __grid_constant__ CUtensorMap mk,
               const __grid_constant__ CUtensorMap mv, const __grid_constant__ CUtensorMap mdo,
@@ -1247,7 +1271,20 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       mbar_arrive(dp_free);
       if (warp == 4 && lane == 0) TRACE(it * 8 + 5);
       const int kbase = it * 128 + part * 32;
-      if ((kbase + 32 > p.S) || (p.causal && kbase + 31 > qi)) {
+      if constexpr (DROP) {
+        const int lim = (p.causal ? min(p.S, qi + 1) : p.S) - kbase;
+#pragma unroll
+        for (int g = 0; g < 8; ++g) {
+          const uint32_t keep = dropout_keep4(p.drop, b, h, qi, kbase + g * 4);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int i = g * 4 + e;
+            const float pv = i < lim ? exp2_mufu(fmaf(s[i], sl2, -l2)) : 0.f;
+            const float kp = (keep >> e) & 1u ? p.drop.inv_keep : 0.f;
+            dp[i] = pv * (dp[i] * kp - dd);
+          }
+        }
+      } else if ((kbase + 32 > p.S) || (p.causal && kbase + 31 > qi)) {
         const int lim = (p.causal ? min(p.S, qi + 1) : p.S) - kbase;
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
@@ -1345,7 +1382,8 @@ static bool fwd_two_tiles() {
 
 int32_t attn_fwd_sm100(const void* q, const void* k, const void* v, void* o, float* lse,
                        int64_t B, int64_t S, int64_t H, int64_t D, int64_t st, int64_t sh,
-                       int64_t ost, float scale, int32_t causal, cudaStream_t stream) {
+                       int64_t ost, float scale, int32_t causal, cudaStream_t stream,
+                       const DropoutParams& drop) {
   using namespace fa;
   CUtensorMap mq, mk, mv;
   const int64_t tokens = B * S;
@@ -1362,6 +1400,7 @@ int32_t attn_fwd_sm100(const void* q, const void* k, const void* v, void* o, flo
   p.lse = lse;
   p.o_st = ost;
   p.sh = sh;
+  p.drop = drop;
   const dim3 grid((unsigned)p.n_qblocks, (unsigned)(B * H));
   const bool mc = ATTN_FWD_MC && (p.n_qblocks % 2) == 0;  // cluster pairs share K/V loads
   auto launch = [&](auto kernel, int smem) -> int32_t {
@@ -1382,9 +1421,12 @@ int32_t attn_fwd_sm100(const void* q, const void* k, const void* v, void* o, flo
     return 0;
   };
   int32_t rc;
-  if (fwd_two_tiles()) {  // default: the two-Q-tile kernel (fwd_tc2)
+  // default: the two-Q-tile kernel (fwd_tc2); dropout is implemented there only
+  if (fwd_two_tiles() || p.drop.thresh != 0) {
     const dim3 grid2((unsigned)((p.n_qblocks + 1) / 2), (unsigned)(B * H));
-    auto kern = D == 128 ? fwd_tc2<128> : fwd_tc2<64>;
+    const bool drop = p.drop.thresh != 0;
+    auto kern = D == 128 ? (drop ? fwd_tc2<128, true> : fwd_tc2<128, false>)
+                         : (drop ? fwd_tc2<64, true> : fwd_tc2<64, false>);
     const int smem = D == 128 ? Smem2<128>::BYTES : Smem2<64>::BYTES;
     GALV_CUDA_RET(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     kern<<<grid2, FWD2_THREADS, smem, stream>>>(mq, mk, mv, p);
@@ -1418,7 +1460,7 @@ int32_t attn_bwd_sm100(const void* q, const void* k, const void* v, const void* 
                        const void* dout, const float* lse, void* dq, void* dk, void* dv,
                        int64_t B, int64_t S, int64_t H, int64_t D, int64_t st, int64_t sh,
                        int64_t ost, float scale, int32_t causal, void* ws, cudaStream_t stream,
-                       const float* rope_table) {
+                       const float* rope_table, const DropoutParams& drop) {
   using namespace fa;
   const int64_t S_pad = (S + 127) / 128 * 128;
   float* lse2 = reinterpret_cast<float*>(ws);
@@ -1448,34 +1490,45 @@ int32_t attn_bwd_sm100(const void* q, const void* k, const void* v, const void* 
   p.st = st;
   p.sh = sh;
   p.rope = rope_table;
+  p.drop = drop;
   GALV_CHECK_ARG(rope_table == nullptr || D == 128, "fused inverse RoPE needs head_dim 128");
   const dim3 g_kv((unsigned)((S + 127) / 128), (unsigned)(B * H));
   const dim3 g_q((unsigned)((S + 127) / 128), (unsigned)(B * H));
-#define GALV_FA_BWD(DD)                                                                          \
+#define GALV_FA_BWD(DD, DR)                                                                      \
   do {                                                                                           \
     static bool set = false;                                                                     \
     if (!set) {                                                                                  \
-      GALV_CUDA_RET(cudaFuncSetAttribute(bwd_dkdv_tc<DD>,                                        \
+      GALV_CUDA_RET(cudaFuncSetAttribute(bwd_dkdv_tc<DD, DR>,                                    \
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,            \
                                          SmemKV<DD>::BYTES));                                    \
-      GALV_CUDA_RET(cudaFuncSetAttribute(bwd_dq_tc<DD>,                                          \
+      GALV_CUDA_RET(cudaFuncSetAttribute(bwd_dq_tc<DD, DR>,                                      \
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,            \
                                          SmemQ<DD>::BYTES));                                     \
       set = true;                                                                                \
     }                                                                                            \
     p.g0 = (__nv_bfloat16*)dk;                                                                   \
     p.g1 = (__nv_bfloat16*)dv;                                                                   \
-    bwd_dkdv_tc<DD><<<g_kv, BWD_THREADS, SmemKV<DD>::BYTES, stream>>>(mq64, mk128, mv128, mdo64, p);     \
+    bwd_dkdv_tc<DD, DR><<<g_kv, BWD_THREADS, SmemKV<DD>::BYTES, stream>>>(mq64, mk128, mv128,    \
+                                                                         mdo64, p);              \
     GALV_LAUNCH_CHECK();                                                                         \
     p.g0 = (__nv_bfloat16*)dq;                                                                   \
     p.g1 = nullptr;                                                                              \
-    bwd_dq_tc<DD><<<g_q, BWD_THREADS, SmemQ<DD>::BYTES, stream>>>(mq128, mk128, mv128, mdo128, p);       \
+    bwd_dq_tc<DD, DR><<<g_q, BWD_THREADS, SmemQ<DD>::BYTES, stream>>>(mq128, mk128, mv128,       \
+                                                                     mdo128, p);                 \
     GALV_LAUNCH_CHECK();                                                                         \
   } while (0)
-  if (D == 128)
-    GALV_FA_BWD(128);
-  else
-    GALV_FA_BWD(64);
+  const bool drp = drop.thresh != 0;
+  if (D == 128) {
+    if (drp)
+      GALV_FA_BWD(128, true);
+    else
+      GALV_FA_BWD(128, false);
+  } else {
+    if (drp)
+      GALV_FA_BWD(64, true);
+    else
+      GALV_FA_BWD(64, false);
+  }
 #undef GALV_FA_BWD
   return 0;
 }

@@ -10,6 +10,7 @@ device the call fails loudly.
 from __future__ import annotations
 
 import ctypes as C
+from dataclasses import dataclass
 import os
 from pathlib import Path
 
@@ -57,6 +58,14 @@ _SIGS = {
                        _I64, _F, _I32, _I32, _P, _P], _I32),
     "galv_attn_bwd_rope": ([_P, _P, _P, _P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _I64,
                             _I64, _I64, _F, _I32, _P, _I32, _I32, _P, _P], _I32),
+    "galv_attn_fwd_dropout": ([_P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _F,
+                               _I32, _F, C.c_uint64, C.c_uint64, _I64, _I64, _I64, _I32, _P],
+                              _I32),
+    "galv_attn_bwd_dropout": ([_P, _P, _P, _P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _I64,
+                               _I64, _I64, _F, _I32, _F, C.c_uint64, C.c_uint64, _I64, _I64,
+                               _I64, _P, _I32, _I32, _P, _P], _I32),
+    "galv_dropout_mask": ([_P, _I64, _I64, _I64, _F, C.c_uint64, C.c_uint64, _I64, _I64, _I64,
+                           _P], _I32),
     "galv_rmsnorm_fwd": ([_P, _P, _P, _P, _P, _P, _I64, _I64, _F, _I32, _P], _I32),
     "galv_rmsnorm_bwd": ([_P, _P, _P, _P, _P, _P, _P, _I64, _I64, _I32, _P, _P], _I32),
     "galv_layernorm_fwd": ([_P, _P, _P, _P, _P, _P, _P, _P, _I64, _I64, _F, _I32, _P], _I32),
@@ -378,12 +387,42 @@ def _attn_geometry(q, o):
     return B, S, H, D, q.stride(1), q.stride(2), o.stride(1)
 
 
-def attn_fwd(q, k, v, o, lse, *, scale, causal=True):
+@dataclass(frozen=True)
+class Dropout:
+    """Attention-probability dropout of one call (csrc/dropout.cuh): probability p, Philox
+    seed, per-call counter offset, and where this call's (b, h) sit in the global
+    batch / head grid (b0, h0, H_total) so the mask is independent of the sharding."""
+    p: float
+    seed: int
+    offset: int
+    b0: int = 0
+    h0: int = 0
+    H_total: int = 0
+
+    def args(self, H):
+        return (float(self.p), int(self.seed) & 0xFFFFFFFFFFFFFFFF,
+                int(self.offset) & 0xFFFFFFFFFFFFFFFF, int(self.b0), int(self.h0),
+                int(self.H_total or H))
+
+
+def attn_fwd(q, k, v, o, lse, *, scale, causal=True, dropout: Dropout | None = None):
     B, S, H, D, st, sh, ost = _attn_geometry(q, o)
     if k.stride() != q.stride() or v.stride() != q.stride():
         raise RuntimeError("q, k, v must share strides")
+    if dropout is not None and dropout.p > 0:
+        _call("galv_attn_fwd_dropout", _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse), B, S, H,
+              D, st, sh, ost, float(scale), int(causal), *dropout.args(H), dtype_code(q.dtype),
+              _stream())
+        return
     _call("galv_attn_fwd", _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse), B, S, H, D, st, sh,
           ost, float(scale), int(causal), dtype_code(q.dtype), _stream())
+
+
+def dropout_mask(B, S, H, dropout: Dropout, device="cuda"):
+    """uint8 [B, H, S, S] keep mask the attention kernels apply for `dropout`."""
+    m = torch.empty(B, H, S, S, dtype=torch.uint8, device=device)
+    _call("galv_dropout_mask", _ptr(m), B, S, H, *dropout.args(H), _stream())
+    return m
 
 
 def attn_bwd_workspace_bytes(B, S, H, D, dtype) -> int:
@@ -391,7 +430,7 @@ def attn_bwd_workspace_bytes(B, S, H, D, dtype) -> int:
 
 
 def attn_bwd(q, k, v, o, dout, lse, dq, dk, dv, *, scale, causal=True, workspace=None,
-             rope_theta=None, rope_epilogue=None):
+             rope_theta=None, rope_epilogue=None, dropout: Dropout | None = None):
     """rope_theta set: dq/dk come out with the inverse RoPE applied (galv_attn_bwd_rope);
     rope_epilogue True/False forces the store-epilogue / streaming-pass variant, None takes
     the library default."""
@@ -401,6 +440,18 @@ def attn_bwd(q, k, v, o, dout, lse, dq, dk, dv, *, scale, causal=True, workspace
     need = load_library().galv_attn_bwd_workspace(B, S, H, D, dtype_code(q.dtype))
     if workspace is None or workspace.numel() * workspace.element_size() < need:
         workspace = torch.empty(need, dtype=torch.uint8, device=q.device)
+    if dropout is not None and dropout.p > 0:
+        table = rope_table(S, D, rope_theta, q.device) if rope_theta is not None else None
+        epi = -1 if rope_epilogue is None else int(bool(rope_epilogue))
+        if table is None or epi > 0:
+            n = 3
+        else:
+            n = 4 if dk.data_ptr() == dq.data_ptr() + H * sh * dq.element_size() else 5
+        _call("galv_attn_bwd_dropout", _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(dout),
+              _ptr(lse), _ptr(dq), _ptr(dk), _ptr(dv), B, S, H, D, st, sh, ost, float(scale),
+              int(causal), *dropout.args(H), _ptr(table), epi, dtype_code(q.dtype),
+              _ptr(workspace), _stream(), launches=n)
+        return
     if rope_theta is not None:
         table = rope_table(S, D, rope_theta, q.device)
         # 3 backward kernels; the streaming variant adds one inverse-RoPE launch over q|k

@@ -31,6 +31,9 @@ class ModelConfig:
     norm_eps: float = 1e-5
     rope_theta: float = 10000.0
     name: str = ""
+    # dropout probability of the attention probabilities (softmax-dropout, north_star (1));
+    # the BASELINE configs train with 0
+    attn_dropout: float = 0.0
 
     @property
     def head_dim(self) -> int:
@@ -43,6 +46,8 @@ class ModelConfig:
             raise ValidationError("hidden must be divisible by heads")
         if self.head_dim not in (64, 128):
             raise ValidationError("head_dim must be 64 or 128 (attention kernels)")
+        if not 0.0 <= self.attn_dropout < 1.0:
+            raise ValidationError("attn_dropout must be in [0, 1)")
 
     def layer_params(self) -> int:
         h, f = self.hidden, self.ffn

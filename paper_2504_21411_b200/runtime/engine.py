@@ -70,6 +70,9 @@ class HybridParallelModel:
         self.layer_events: list = []
         self.record_layers = False
         self._init_params(seed, init, perturb, weights)
+        self.dropout_step = 0  # attention-dropout Philox counter: advanced per train_step
+        for layer in self.layers:
+            layer.dropout_seed = seed
         # dp collectives of bf16 ZeRO-0/1/2 stores over NVLink/NVSwitch (symmetric pools)
         self.dp_pools = dp_nvlink.attach([st for _, st, _ in self.stores()], self.device)
 
@@ -141,8 +144,9 @@ class HybridParallelModel:
                 self._ev_end(ev, "transition_fwd", layer.index, k)
                 rec["ctxs"].append(("reshard", prev, lay))
             B = hc.microbatch // layer.s.dp
+            b0 = k * hc.microbatch + self._replica_slice(layer.s, T)[0]
             ev = self._ev_start()
-            x, ctx = layer.forward(x, B)
+            x, ctx = layer.forward(x, B, b0)
             self._ev_end(ev, "fwd", layer.index, k)
             rec["ctxs"].append(("layer", layer, ctx))
             prev = lay
@@ -212,6 +216,8 @@ class HybridParallelModel:
         m = hc.n_microbatches
         tok = tokens.to(self.device, non_blocking=True).view(m, hc.microbatch, cfg.seq_len + 1)
         ops = one_f_one_b_order(hc.pp, self.stage, m)
+        for layer in self.layers:
+            layer.dropout_step = self.dropout_step
         recs, inputs, grads = {}, {}, {}
         first_layer = hc.stage_ranges[self.stage][0]
         prev_rank, next_rank = self.topo.prev_stage_rank(), self.topo.next_stage_rank()
@@ -277,6 +283,7 @@ class HybridParallelModel:
                 loss_acc.zero_()
             dist.all_reduce(loss_acc)
         self.last_step_time = time.perf_counter() - t0
+        self.dropout_step += 1
         return loss_acc / (hc.global_batch * cfg.seq_len)
 
     def _ev_start(self):

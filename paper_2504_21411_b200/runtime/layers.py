@@ -169,6 +169,9 @@ class DecoderLayer:
                 T = topo.hc.microbatch // strategy.dp * cfg.seq_len
                 self.peer = nvlink.peer_buffers(self.tpg, T * max(cfg.hidden, 1) * 2, device)
         self.scale = 1.0 / math.sqrt(cfg.head_dim)
+        # attention dropout (cfg.attn_dropout): Philox seed and the step counter the engine
+        # advances per train_step; the counter offset is (step << 16) | layer index
+        self.dropout_seed, self.dropout_step = 0, 0
 
     def param_prefix(self) -> str:
         return f"layers.{self.index}."
@@ -290,7 +293,16 @@ class DecoderLayer:
         mk = lambda j: qkv.as_strided((B, S, self.Hl, D), (S * st, st, D, 1), base + j * hl)
         return mk(0), mk(1), mk(2)
 
-    def forward_impl(self, x, B, save: bool, keep_gathered: bool = False):
+    def _dropout(self, b0: int):
+        """Dropout of this layer's attention call: global sample b0 of its first sequence,
+        global head h0 of its first head (tp / Ulysses ranks own contiguous head blocks)."""
+        if self.cfg.attn_dropout <= 0:
+            return None
+        return K.Dropout(self.cfg.attn_dropout, self.dropout_seed,
+                         (self.dropout_step << 16) | self.index, b0=b0, h0=self.tpr * self.Hl,
+                         H_total=self.cfg.heads)
+
+    def forward_impl(self, x, B, save: bool, keep_gathered: bool = False, b0: int = 0):
         """x: [T_in, h] in this layer's layout; B = samples in this dp replica.
 
         Under Megatron-SP the saved norm outputs are this rank's token shards (n1, n2),
@@ -326,8 +338,9 @@ class DecoderLayer:
                     S, theta=cfg.rope_theta)
         o = torch.empty(T, self.ahl, device=x.device, dtype=x.dtype)
         lse = torch.empty(B, self.Hl, S, device=x.device, dtype=torch.float32)
+        drop = self._dropout(b0)
         K.attn_fwd(q, k, v, o.view(B, S, self.Hl, cfg.head_dim), lse, scale=self.scale,
-                   causal=True)
+                   causal=True, dropout=drop)
         o_full = o
         if self.uly:
             o = self._uly_o_to_tokens(o_full)
@@ -361,18 +374,20 @@ class DecoderLayer:
             regather = self.s.sp and not self.uly and self.tp > 1 and not keep_gathered
             saved = dict(x=x, st1=st1, n1f=n1 if regather else n1f, qkv=qkv, o=o,
                          o_full=o_full, lse=lse, h1=h1, st2=st2,
-                         n2f=n2 if regather else n2f, act=act, B=B, regather=regather)
+                         n2f=n2 if regather else n2f, act=act, B=B, regather=regather,
+                         drop=drop)
             saved["pre"] = f1 if gpt else gu
             return y, saved
         return y, None
 
-    def forward(self, x, B):
+    def forward(self, x, B, b0: int = 0):
+        """b0: global index of this replica's first sample (attention-dropout coordinates)."""
         ctx = _Ctx()
         if self.s.recompute:
-            y, _ = self.forward_impl(x, B, save=False)
-            ctx.x, ctx.saved = (x, B), None
+            y, _ = self.forward_impl(x, B, save=False, b0=b0)
+            ctx.x, ctx.saved = (x, B, b0), None
         else:
-            y, ctx.saved = self.forward_impl(x, B, save=True)
+            y, ctx.saved = self.forward_impl(x, B, save=True, b0=b0)
         self.store.release()
         return y, ctx
 
@@ -380,8 +395,8 @@ class DecoderLayer:
     def backward(self, dy, ctx):
         cfg = self.cfg
         if ctx.saved is None:
-            x, B = ctx.x
-            _, sv = self.forward_impl(x, B, save=True, keep_gathered=True)
+            x, B, b0 = ctx.x
+            _, sv = self.forward_impl(x, B, save=True, keep_gathered=True, b0=b0)
         else:
             sv = ctx.saved
         ctx.saved = ctx.x = None
@@ -460,7 +475,7 @@ class DecoderLayer:
                    do.view(B, S, self.Hl, cfg.head_dim), sv["lse"], dq, dk, dv,
                    scale=self.scale, causal=True, workspace=ws,
                    rope_theta=cfg.rope_theta if rope_fused else None,
-                   rope_epilogue=ROPE_BWD_EPILOGUE)
+                   rope_epilogue=ROPE_BWD_EPILOGUE, dropout=sv["drop"])
         del do
         if not gpt and not rope_fused:
             K.rope_(dqkv.as_strided((T, 2 * self.Hl, cfg.head_dim),

@@ -118,6 +118,12 @@ SCENARIOS = {
                           2e-2, 2),
     "uly4_hd128_bf16": (4, "mini-llama128", hc([PS(4, 1, 0, True, False)] * 2, mb=1,
                                                sp_mode="ulysses"), BF16, 2e-2),
+    # softmax-dropout (p = 0.1, Philox mask keyed on global sample / head indices): the mask
+    # must not depend on the dp / tp / Ulysses sharding of the attention call
+    "dp2_drop": (2, "micro-llama", hc([PS(1, 2, 0, False, False)] * 2), F32, 1e-5),
+    "tp2_drop_gpt": (2, "micro-gpt", hc([PS(2, 1, 0, False, True)] * 2), F32, 1e-5),
+    "uly2_hd128_bf16_drop": (2, "micro-llama128", hc([PS(2, 1, 0, True, False)] * 2,
+                                                     sp_mode="ulysses"), BF16, 2e-2),
     "tp2dp2": (4, "micro-llama", hc([PS(2, 2, 1, True, False)] * 2, mb=2), F32, 1e-5),
     "pp2_tp2": (4, "tiny-llama", hc([PS(2, 1, 0, False, False), PS(1, 2, 2, False, False),
                                      PS(2, 1, 0, True, True), PS(2, 1, 0, False, False)],
@@ -147,7 +153,8 @@ def main():
         try:
             lerr, errs = run_parity(model, cfg_hc, dtype, grad_bytes=rest[0] if rest else 4,
                                     oracle_cache=cache,
-                                    opt_steps=2 if "_opt" in name else 0)
+                                    opt_steps=2 if "_opt" in name else 0,
+                                    attn_dropout=0.1 if "_drop" in name else 0.0)
         finally:
             for k, v in saved.items():
                 if v is None:

@@ -226,3 +226,55 @@ def test_attention_production_shapes(B, S, H):
                    scale=scale, causal=True, rope_theta=theta, rope_epilogue=epi)
         assert torch.equal(fused[:, :, 2], dqkv[:, :, 2])
         assert rel(fused, ref) < 8e-3
+
+
+def test_dropout_mask_matches_cpu_philox():
+    """galv_dropout_mask (the device Philox every attention kernel calls) == the CPU
+    restatement oracle/dropout_ref.py, including global (b0, h0) placement."""
+    import numpy as np
+    from oracle.dropout_ref import keep_mask
+    from paper_2504_21411_b200 import kernels as K
+    for B, S, H, p, seed, off, b0, h0, Ht in [(2, 67, 3, 0.1, 1234, 5, 0, 0, 3),
+                                              (1, 130, 2, 0.5, 2**40 + 17, 65539, 3, 4, 8)]:
+        d = K.Dropout(p, seed, off, b0=b0, h0=h0, H_total=Ht)
+        got = K.dropout_mask(B, S, H, d).cpu().numpy().astype(bool)
+        want = keep_mask(B, S, H, p, seed, off, b0=b0, h0=h0, H_total=Ht)
+        assert (got == want).all()
+
+
+@pytest.mark.parametrize("dt,D", [(torch.bfloat16, 128), (torch.bfloat16, 64),
+                                  (torch.float32, 64)])
+@pytest.mark.parametrize("S", [200, 512])
+def test_attention_dropout_fwd_bwd(dt, D, S):
+    """Softmax-dropout attention (tcgen05 bf16 / SIMT fp32) vs a torch fp32 reference that
+    applies the CPU Philox mask: O, dQ, dK, dV; b0/h0 place the call in a larger grid."""
+    from oracle.dropout_ref import keep_mask
+    from paper_2504_21411_b200 import kernels as K
+    torch.manual_seed(3)
+    B, H, p = 2, 3, 0.2
+    drop = K.Dropout(p, 4321, 9, b0=1, h0=2, H_total=8)
+    qkv = torch.randn(B, S, 3, H, D, device="cuda").to(dt)
+    q, k, v = qkv[:, :, 0], qkv[:, :, 1], qkv[:, :, 2]
+    o = torch.empty(B, S, H, D, device="cuda", dtype=dt)
+    lse = torch.empty(B, H, S, device="cuda")
+    scale = 1 / math.sqrt(D)
+    K.attn_fwd(q, k, v, o, lse, scale=scale, causal=True, dropout=drop)
+    keep = torch.as_tensor(keep_mask(B, S, H, p, 4321, 9, b0=1, h0=2, H_total=8), device="cuda")
+    qr, kr, vr = (t.float().clone().requires_grad_(True) for t in (q, k, v))
+    qt, kt, vt = (t.permute(0, 2, 1, 3) for t in (qr, kr, vr))
+    sc = (qt @ kt.transpose(-1, -2)) * scale
+    sc = sc.masked_fill(torch.triu(torch.ones(S, S, dtype=torch.bool, device="cuda"), 1),
+                        float("-inf"))
+    ref_lse = torch.logsumexp(sc, -1)
+    probs = torch.softmax(sc, -1) * keep.float() / (1 - p)
+    o_ref = (probs @ vt).permute(0, 2, 1, 3)
+    tol = 1e-5 if dt == torch.float32 else 1e-2
+    assert rel(o, o_ref) < tol
+    assert rel(lse, ref_lse) < (1e-5 if dt == torch.float32 else 1e-3)
+    do = torch.randn_like(o_ref)
+    o_ref.backward(do)
+    d = torch.empty_like(qkv)
+    K.attn_bwd(q, k, v, o, do.to(dt).contiguous(), lse, d[:, :, 0], d[:, :, 1], d[:, :, 2],
+               scale=scale, causal=True, dropout=drop)
+    for i, want in enumerate((qr.grad, kr.grad, vr.grad)):
+        assert rel(d[:, :, i], want) < (1e-5 if dt == torch.float32 else 2e-2), i

@@ -79,3 +79,29 @@ def test_oracle_matches_live_hf(name):
     loss_hf, _ = hf_loss_and_grad_norms(cfg, w, tokens)
     loss, _ = model_ref.loss_and_grads(cfg, w, tokens)
     assert abs(loss.item() - loss_hf) < 1e-8 * abs(loss_hf)
+
+
+def test_dropout_philox_known_answers():
+    """oracle/dropout_ref.philox4x32_10 against the Random123 known-answer vectors for
+    philox4x32-10 (the generator csrc/dropout.cuh implements)."""
+    import numpy as np
+    from oracle.dropout_ref import philox4x32_10
+    kat = [((0, 0, 0, 0), (0, 0), (0x6627e8d5, 0xe169c58d, 0xbc57ac4c, 0x9b00dbd8)),
+           ((0xffffffff,) * 4, (0xffffffff, 0xffffffff),
+            (0x408f276d, 0x41c83b0e, 0xa20bc7c6, 0x6d5451fd)),
+           ((0x243f6a88, 0x85a308d3, 0x13198a2e, 0x03707344), (0xa4093822, 0x299f31d0),
+            (0xd16cfe09, 0x94fdcceb, 0x5001e420, 0x24126ea1))]
+    for ctr, key, want in kat:
+        got = philox4x32_10(np.array(ctr, dtype=np.uint32), key)
+        assert tuple(int(x) for x in got) == want
+
+
+def test_dropout_mask_statistics_and_sharding_invariance():
+    """Keep rate ~ 1-p; the mask of a (b0, h0)-offset block equals the matching slice of the
+    global mask (why the runtime can shard attention over dp / tp / Ulysses)."""
+    from oracle.dropout_ref import keep_mask
+    full = keep_mask(4, 64, 6, 0.25, 99, 7)
+    assert abs(full.mean() - 0.75) < 0.01
+    part = keep_mask(2, 64, 3, 0.25, 99, 7, b0=1, h0=2, H_total=6)
+    assert (part == full[1:3, 2:5]).all()
+    assert not (keep_mask(4, 64, 6, 0.25, 99, 8) == full).all()

@@ -130,3 +130,19 @@ def test_bf16_parity_llama2_7b_width_one_layer():
     assert lerr <= 2e-2
     worst = max(errs.items(), key=lambda kv: kv[1])
     assert worst[1] <= 2e-2, worst
+
+
+@pytest.mark.parametrize("name,dtype,tol", [("tiny-gpt", torch.float32, 1e-5),
+                                            ("micro-llama128", torch.bfloat16, 2e-2),
+                                            ("micro-gpt", torch.bfloat16, 2e-2)])
+def test_parity_with_attention_dropout(name, dtype, tol):
+    """Softmax-dropout p = 0.1 end to end: the runtime's Philox mask (every layer, both
+    microbatches, recompute replay included) and the oracle's CPU Philox mask agree, so loss
+    and every gradient match at the no-dropout tolerances."""
+    cfg = MODEL_PRESETS[name]
+    hc = uniform_config(cfg, S1R if dtype == torch.float32 else S1, microbatch=2,
+                        n_microbatches=2)
+    lerr, errs = run_parity(name, hc, dtype, attn_dropout=0.1)
+    assert lerr <= tol
+    worst = max(errs.items(), key=lambda kv: kv[1])
+    assert worst[1] <= tol, worst
