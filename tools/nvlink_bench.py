@@ -69,9 +69,11 @@ def main():
     peers = torch.tensor([int(p) for p in hdl.buffer_ptrs], dtype=torch.int64, device="cuda")
     nbytes = n * 2
     if mc:
-        us = timed(lambda: K.dp_reduce(n=shard, t=t, mc_src=mc + me * shard * 2, out=out,
-                                       max_ctas=16))
-        res["galv_dp_reduce_multimem"] = {"us": us, "busbw_GBps": (t - 1) / t * nbytes / us / 1e3}
+        for ctas in (16, 32, 64, 148):
+            us = timed(lambda: K.dp_reduce(n=shard, t=t, mc_src=mc + me * shard * 2, out=out,
+                                           max_ctas=ctas))
+            res[f"galv_dp_reduce_multimem_ctas{ctas}"] = {
+                "us": us, "busbw_GBps": (t - 1) / t * nbytes / us / 1e3}
     us = timed(lambda: K.dp_reduce(n=shard, t=t, peer_src=peers, offset=me * shard, out=out,
                                    max_ctas=16))
     res["galv_dp_reduce_unicast"] = {"us": us, "busbw_GBps": (t - 1) / t * nbytes / us / 1e3}
