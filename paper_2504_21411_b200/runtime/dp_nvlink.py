@@ -37,7 +37,11 @@ _FLAGS = 512                  # [ch0 flags: 64 x u32][ch1 flags: 64 x u32][pad]
 # previous layer's is reduced on the comm stream (a 400 MB pull-reduce takes ~0.6 ms, a
 # layer backward ~20 ms, so a third slot only costs memory)
 RING = int(os.environ.get("GALV_DP_RING", "2"))
-MAX_CTAS = int(os.environ.get("GALV_DP_NVLINK_CTAS", "16"))
+# CTAs of the pull-reduce kernels: B200, one 7B layer's gradients (405 MB) at N=2, alone
+# (tools/nvlink_bench.py, profiles/r02/nvlink): 16 CTAs 184 GB/s busbw, 32 316, 64 321, NCCL
+# 374; inside the step (profiler --overlap-out) the exposed dp sync fell from 60 / 48 ms
+# (16 CTAs, N=2 / 4) to 30 / 25 ms with 48 CTAs (NCCL 32 / 45 ms)
+MAX_CTAS = int(os.environ.get("GALV_DP_NVLINK_CTAS", "48"))
 
 
 def enabled() -> bool:
