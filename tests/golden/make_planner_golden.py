@@ -117,7 +117,15 @@ def _committed(ref):
             table = tuple(e for e in base.bandwidth_table if e.group_size <= n)
             cl = P.ClusterProfile(n, min(base.devices_per_node, n), base.device_flops,
                                   base.device_memory_bytes, base.memory_reserve_fraction, table)
-            yield f"committed-{name}-n{n}", cl, model, P.TrainingConfig(global_batch=per_gpu * n)
+            # bench.training_config: the measured comm_overlap_fraction of the largest
+            # measured world <= n (profiles/b200_training_<model>_n<k>.json), else 0
+            overlap = 0.0
+            for k in (2, 4, 8, 16):
+                tpath = prof / f"b200_training_{name}_n{k}.json"
+                if n > 1 and k <= n and tpath.exists():
+                    overlap = P.load_training_config(str(tpath)).comm_overlap_fraction
+            yield (f"committed-{name}-n{n}", cl, model,
+                   P.TrainingConfig(global_batch=per_gpu * n, comm_overlap_fraction=overlap))
 
 
 def main_committed(ref) -> None:
