@@ -561,17 +561,19 @@ def main():
 
     peaks, peak_src = measured_peaks()
     # DRAM traffic of the dominant kernel from the committed ncu --set full capture
+    # (tools/gemm_one.py under ncu: the gate|up GEMM + SwiGLU epilogue, the step's largest
+    # launch; profiles/r02/ncu/gemm_gateup_summary.json)
     traffic = None
     try:
-        with open(os.path.join(ROOT, "profiles", "r01", "ncu_full_summary_final.json")) as fh:
-            cap = json.load(fh)[0]  # gate|up GEMM + fused SwiGLU, the step's largest launch
+        with open(os.path.join(ROOT, "profiles", "r02", "ncu", "gemm_gateup_summary.json")) as fh:
+            cap = json.load(fh)
         rd = float(cap["dram__bytes_read.sum"].split()[0]) * 1e6
         wr = float(cap["dram__bytes_write.sum"].split()[0]) * 1e6
         traffic = {"bytes_per_launch": rd + wr,
                    "shape": "8192x22016x4096 gate|up fwd + SwiGLU epilogue (mb2)",
                    "algorithmic_bytes": 2 * (8192 * 4096 + 22016 * 4096 + 8192 * 22016
                                              + 8192 * 11008),
-                   "source": "profiles/r01/final_kernels.ncu-rep (launch 0)"}
+                   "source": "profiles/r02/ncu/gemm_gateup_summary.json (ncu --set full)"}
     except (OSError, KeyError, ValueError, IndexError):
         pass
     flops_tok = cfg.train_flops_per_token()
