@@ -79,6 +79,22 @@ __device__ __forceinline__ float exp2_fma(float x) {
   const int bits = __float_as_int(p) + (__float_as_int(r) << 23);
   return x < -125.f ? 0.f : __int_as_float(bits);
 }
+// 2^x (x <= 0) on the FMA/ALU pipes: x = n + f, n = floor(x), 2^f by a degree-3 minimax
+// (max rel err 8.6e-5, below the bf16 rounding of P), exponent by an integer add
+__device__ __forceinline__ float exp2_poly3(float x) {
+  const float xc = fmaxf(x, -126.f);
+  const float n = floorf(xc);
+  const float f = xc - n;
+  float q = fmaf(0.07706213f, f, 0.22764884f);
+  q = fmaf(q, f, 0.69511681f);
+  q = fmaf(q, f, 1.0f);
+  return __int_as_float(__float_as_int(q) + (static_cast<int>(n) << 23));
+}
+// head_dim 64 forward: the exp work is 2x the MMA work per block (MUFU-bound); every
+// ATTN_POLY64-th exponential pair goes to the FMA pipe (0 = all on MUFU)
+#ifndef ATTN_POLY64
+#define ATTN_POLY64 0
+#endif
 __device__ __forceinline__ float exp2_mufu(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -619,8 +635,11 @@ __global__ void __launch_bounds__(FWD2_THREADS, 1)
           const int e = c * 16 + i;
           // all exponentials on MUFU: moving 1/4 or 1/2 of them to an FMA-pipe polynomial
           // measured 4-14 % slower (D 64 and 128, two-threads-per-row variant)
-          const float p0 = exp2_mufu(fmaf(s[e], p.scale_log2, -mu));
-          const float p1 = exp2_mufu(fmaf(s[e + 1], p.scale_log2, -mu));
+          constexpr int PE = D == 64 ? ATTN_POLY64 : 0;
+          const bool poly = PE > 0 && ((i >> 1) % (PE > 0 ? PE : 1)) == (PE > 0 ? PE : 1) - 1;
+          const float x0 = fmaf(s[e], p.scale_log2, -mu), x1 = fmaf(s[e + 1], p.scale_log2, -mu);
+          const float p0 = poly ? exp2_poly3(x0) : exp2_mufu(x0);
+          const float p1 = poly ? exp2_poly3(x1) : exp2_mufu(x1);
           r4[(i >> 1) & 3] += p0 + p1;  // the normalizer uses the undropped probabilities
           if constexpr (DROP)
             pk[i / 2] = pack2((keep >> i) & 1u ? p0 : 0.f, (keep >> (i + 1)) & 1u ? p1 : 0.f);
