@@ -272,8 +272,9 @@ def memory_breakdown(plan, model, cluster, training, peak_gb, persistent_bytes):
         tot["activation"] += m.activation_bytes
     state = tot["param"] + tot["grad"] + tot["optimizer"]
     last = plan.layer_strategies[hi - 1]
-    return {"stage": st, "pp": plan.pp, "microbatch": plan.microbatch,
+    return {"stage": st, "pp": plan.pp, "microbatch": plan.microbatch, "in_flight": infl,
             "seq_len": prof.seq_len, "last_layer": last.to_dict(),
+            "first_layer": plan.layer_strategies[lo].to_dict(),
             "model_state_gb": state / 1e9, "model_activation_gb":
             tot["activation"] / 1e9, "runtime_persistent_gb": persistent_bytes / 1e9,
             "runtime_peak_gb": peak_gb, "predicted_gb": plan.predicted_stage_peak_memory[st] / 1e9,

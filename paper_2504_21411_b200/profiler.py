@@ -186,8 +186,8 @@ def measure_working_set(cfg, microbatch: int) -> dict:
             "microbatch": microbatch}
 
 
-def fold_embedding_head(prof: P.ModelProfile, cfg, working_set_per_token: float = 0.0
-                        ) -> P.ModelProfile:
+def fold_embedding_head(prof: P.ModelProfile, cfg, working_set_per_token: float = 0.0,
+                        first_working_set_per_token: float = 0.0) -> P.ModelProfile:
     """Charge the embedding and the LM head to the planned layers that share their
     strategy (the runtime builds them on layer 0's / layer L-1's tp and dp groups,
     runtime/engine.py): layer 0 gains the embedding tables' parameters, layer L-1 the
@@ -201,9 +201,11 @@ def fold_embedding_head(prof: P.ModelProfile, cfg, working_set_per_token: float 
     ``working_set_per_token`` (measure_working_set) is added to the last layer's
     tp-shardable activation bytes: the step's peak is the saved activations plus this
     working set, and the last layer's stage is where it occurs (pp=1: every stage is the
-    last; pp>1: the head's stage holds one microbatch in flight).  Residual: when the last
-    layer itself recomputes, the cost model charges it boundary bytes only and the
-    working set (and the replayed layer's activations) fall outside the prediction."""
+    last; pp>1: the head's stage holds one microbatch in flight).
+    ``first_working_set_per_token`` goes to layer 0 the same way: the first pipeline stage
+    (pp > 1) peaks in a layer backward too, with no head to carry it (pp = 1 charges both,
+    a conservative overlap).  Residual: middle stages of pp >= 3 carry no working set, and
+    when the last layer itself recomputes the cost model charges it boundary bytes only."""
     L, h, V = cfg.n_layers, cfg.hidden, cfg.vocab
     emb = V * h + (cfg.seq_len * h if cfg.arch == "gpt" else 0)
     head = V * h + h * (2 if cfg.arch == "gpt" else 1)
@@ -217,7 +219,7 @@ def fold_embedding_head(prof: P.ModelProfile, cfg, working_set_per_token: float 
             act_replicated_bytes_per_token=lp.act_replicated_bytes_per_token,
             boundary_bytes_per_token=lp.boundary_bytes_per_token)
 
-    layers[0] = bump(layers[0], emb, 0)
+    layers[0] = bump(layers[0], emb, 0, float(first_working_set_per_token))
     layers[L - 1] = bump(layers[L - 1], head, 2 * h * V, float(working_set_per_token))
     out = P.ModelProfile(n_layers=prof.n_layers, hidden_size=prof.hidden_size,
                          seq_len=prof.seq_len, layers=tuple(layers))
@@ -250,8 +252,12 @@ def calibrated_model_profile(cfg, act: dict) -> P.ModelProfile:
     prof = P.ModelProfile(n_layers=base.n_layers, hidden_size=base.hidden_size,
                           seq_len=base.seq_len, layers=(layer,) * base.n_layers)
     prof.validate()
-    return fold_embedding_head(prof, cfg, act.get("working_set_bytes_per_token", 0.0)
-                               + act.get("step_memory_extra_bytes_per_token", 0.0))
+    return fold_embedding_head(
+        prof, cfg,
+        act.get("working_set_bytes_per_token", 0.0)
+        + act.get("step_memory_extra_bytes_per_token", 0.0),
+        act.get("layer_backward_bytes_per_token", 0.0)
+        + act.get("step_memory_extra_first_bytes_per_token", 0.0))
 
 
 def step_memory_extra(lines: list) -> dict:
@@ -265,21 +271,31 @@ def step_memory_extra(lines: list) -> dict:
     extra = excess * tp / (microbatch * seq / dp); the maximum over the lines is kept.
     Lines whose last layer recomputes (the term is not used then) or that are not the
     last pipeline stage are skipped."""
-    best, used, skipped = 0.0, [], []
+    best, best_first, used, skipped = 0.0, 0.0, [], []
     for ln in lines:
         m = ln.get("memory", {})
-        ll = m.get("last_layer")
-        if not ll or m.get("stage") != m.get("pp", 1) - 1 or ll.get("recompute"):
+        pp, st = m.get("pp", 1), m.get("stage")
+        first = pp > 1 and st == 0
+        ll = m.get("first_layer" if first else "last_layer")
+        if not ll or (st != pp - 1 and not first) or ll.get("recompute"):
             skipped.append(ln.get("config", {}).get("parallelism"))
             continue
         excess = m["runtime_peak_gb"] * 1e9 - m["predicted_gb"] * 1e9
-        tokens = m["microbatch"] * m["seq_len"] / ll["dp"]
+        # the first stage holds min(m, pp) microbatches; its layer-0 fold counts once per
+        # microbatch in flight (costmodel.in_flight_microbatches)
+        inflight = m.get("in_flight", 1) if first else 1
+        tokens = m["microbatch"] * m["seq_len"] / ll["dp"] * inflight
         x = max(excess, 0.0) * ll["tp"] / tokens
         used.append({"config": ln.get("config", {}).get("parallelism"), "n_gpus": ln.get("n_gpus"),
+                     "stage": st, "fold": "layer 0" if first else "layer L-1",
                      "excess_bytes": excess, "extra_bytes_per_token": x})
-        best = max(best, x)
-    return {"step_memory_extra_bytes_per_token": best, "step_memory_sources": used,
-            "step_memory_skipped": skipped}
+        if first:
+            best_first = max(best_first, x)
+        else:
+            best = max(best, x)
+    return {"step_memory_extra_bytes_per_token": best,
+            "step_memory_extra_first_bytes_per_token": best_first,
+            "step_memory_sources": used, "step_memory_skipped": skipped}
 
 
 def measure_collectives(sizes=(2 ** 20, 2 ** 24, 2 ** 28)) -> dict:
@@ -457,7 +473,19 @@ def main(argv=None) -> int:
                         d = json.loads(raw)
                         if d.get("config", {}).get("model") == cfg.name:
                             lines.append(d)
-        meta["activation"].update(step_memory_extra(lines))
+        new = step_memory_extra(lines)
+        act = meta["activation"]
+        # a fold without new measurements keeps its previous calibration (the lines of an
+        # earlier bench generation were measured against a profile without the extra)
+        for key, fold in (("step_memory_extra_bytes_per_token", "layer L-1"),
+                          ("step_memory_extra_first_bytes_per_token", "layer 0")):
+            if any(src["fold"] == fold for src in new["step_memory_sources"]):
+                act[key] = new[key]
+        act["step_memory_sources"] = [s for s in act.get("step_memory_sources", [])
+                                      if s.get("fold", "layer L-1") not in
+                                      {x["fold"] for x in new["step_memory_sources"]}]
+        act["step_memory_sources"] += new["step_memory_sources"]
+        act["step_memory_skipped"] = new["step_memory_skipped"]
         P.save_profiles(args.model_out, model=calibrated_model_profile(cfg, meta["activation"]))
         with open(meta_path, "w") as fh:
             json.dump(meta, fh, indent=1)
