@@ -28,6 +28,25 @@ def hc(strats, *, pp=1, mb=2, m=2, sp_mode="megatron"):
                         layer_strategies=tuple(strats), sp_mode=sp_mode)
 
 
+def searched(model: str, n: int, global_batch: int) -> HybridConfig:
+    """BASELINE config 1 as the planner picks it for n GPUs: the unchanged search on the
+    analytic profile (embedding/head folded) and a B200 cluster table, loaded through the
+    runtime's validating entry point (get_hybrid_parallel_configs + validate_plan)."""
+    from paper_2504_21411_b200.planner import profiles as P
+    from paper_2504_21411_b200.planner.search import optimize
+    from paper_2504_21411_b200.profiler import planned_profile
+    from paper_2504_21411_b200.runtime.config import MODEL_PRESETS, get_hybrid_parallel_configs
+    cfg = MODEL_PRESETS[model]
+    table = tuple(P.BandwidthEntry("intra_node", g, 4.1e11, 2.4e-5) for g in (2, 4, 8) if g <= n)
+    cluster = P.ClusterProfile(n, n, 1.2e15, 191_502_876_672, 0.1, table)
+    prof = planned_profile(cfg)
+    training = P.TrainingConfig(global_batch=global_batch, bytes_per_param=4.0,
+                                bytes_per_grad=4.0, optimizer_bytes_per_param=8.0)
+    plan = optimize(prof, cluster, training)
+    return get_hybrid_parallel_configs(plan, cfg, model_profile=prof, cluster=cluster,
+                                       training=training)
+
+
 F32, BF16 = torch.float32, torch.bfloat16
 BF16_OPT = 4e-2
 # name -> (world, model, hybrid config, dtype, tolerance)
@@ -124,6 +143,10 @@ SCENARIOS = {
     "tp2_drop_gpt": (2, "micro-gpt", hc([PS(2, 1, 0, False, True)] * 2), F32, 1e-5),
     "uly2_hd128_bf16_drop": (2, "micro-llama128", hc([PS(2, 1, 0, True, False)] * 2,
                                                      sp_mode="ulysses"), BF16, 2e-2),
+    # BASELINE config 1 (tiny GPT 4L h512 s256 b8 fp32) with the plan the search picks:
+    # pp2 x mb4 at 2 GPUs, pp4 x mb4 at 4 GPUs (1F1B, p2p between stages)
+    "c1_searched_n2": (2, "tiny-gpt", searched("tiny-gpt", 2, 8), F32, 1e-5),
+    "c1_searched_n4": (4, "tiny-gpt", searched("tiny-gpt", 4, 8), F32, 1e-5),
     "tp2dp2": (4, "micro-llama", hc([PS(2, 2, 1, True, False)] * 2, mb=2), F32, 1e-5),
     "pp2_tp2": (4, "tiny-llama", hc([PS(2, 1, 0, False, False), PS(1, 2, 2, False, False),
                                      PS(2, 1, 0, True, True), PS(2, 1, 0, False, False)],

@@ -19,10 +19,10 @@ TWO = ["dp2_z0", "dp2_z1", "dp2_z2", "dp2_z3_rc", "tp2", "tp2_sp", "tp2_gpt", "t
        "dp2_mixed_bf16_opt",
        "tp2_hd128_bf16", "tp2_sp_hd128_bf16", "tp2_sp_hd128_bf16_rc", "uly2_hd128_bf16",
        "dp2_z2_hd128_bf16", "dp2_z1_hd128_bf16_opt", "pp2_hd128_bf16",
-       "dp2_drop", "tp2_drop_gpt", "uly2_hd128_bf16_drop"]
+       "dp2_drop", "tp2_drop_gpt", "uly2_hd128_bf16_drop", "c1_searched_n2"]
 FOUR = ["tp2dp2", "pp2_tp2", "alt4", "uly4_z3", "tp4_sp_bf16", "tp4_bf16", "dp4_z2_bf16_opt",
         "tp2dp2_bf16_opt", "tp4_sp_hd128_bf16", "tp2dp2_hd128_bf16_opt", "dp4_z2_hd128_bf16",
-        "uly4_hd128_bf16"]
+        "uly4_hd128_bf16", "c1_searched_n4"]
 
 
 def _run(n, scenarios, port):
