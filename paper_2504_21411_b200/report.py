@@ -59,6 +59,8 @@ def measured_report(plan, model, cluster, training, *, stage: int, layer_times: 
                     "measured_embedding_head": extra, "measured_time_total": total,
                     "relative_error": (total - row["time_total"]) / row["time_total"]
                     if row["time_total"] else None})
+    for li, tr in transition_traffic(plan, model, hidden=model.hidden_size).items():
+        bundle["layers"][li].update(tr)
     for row in bundle["stages"]:
         if row["stage"] != stage:
             continue
@@ -79,6 +81,31 @@ def measured_report(plan, model, cluster, training, *, stage: int, layer_times: 
     tot["layers_within_10pct"] = sum(e <= 0.10 for e in errs)
     tot["layers_measured"] = len(errs)
     return bundle
+
+
+def transition_traffic(plan, model, *, hidden: int, act_bytes: int = 2) -> dict:
+    """Per layer with a layout change: the bytes the busiest rank sends in the runtime's
+    reshard (runtime/reshard.plan_transition: rows a rank already holds never move) next
+    to the volume the cost model charges (transition_time = all-gather of microbatch*s*
+    boundary bytes over the stage group, costmodel.py:179-196, i.e. (g-1)/g of it per rank
+    on the ring)."""
+    from .runtime.reshard import Layout, plan_transition
+    out = {}
+    T = plan.microbatch * model.seq_len
+    for i, (lo, hi) in enumerate(plan.stage_ranges):
+        for li in range(lo + 1, hi):
+            a, b = plan.layer_strategies[li - 1], plan.layer_strategies[li]
+            if a.same_layout(b):
+                continue
+            src, dst = Layout.of(a), Layout.of(b)
+            tp = plan_transition(src, dst, T)
+            g = src.tp * src.dp
+            sent = [sum(max(h - l, 0) for j, (l, h) in enumerate(tp.send_rows[r]) if j != r)
+                    for r in range(g)]
+            bound = (g - 1) / g * T * model.layers[li].boundary_bytes_per_token
+            out[li] = {"reshard_bytes_max_rank": max(sent) * hidden * act_bytes,
+                       "model_allgather_bytes_per_rank": bound}
+    return out
 
 
 COLUMNS = cli.CSV_COLUMNS + ["measured_time_total", "relative_error"]

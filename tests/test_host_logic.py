@@ -254,3 +254,27 @@ def test_measured_report_bundle_and_csv():
     assert csv[0].split(",") == COLUMNS
     assert len(csv) == 1 + L + plan.pp + 1
     assert all(len(r.split(",")) == len(COLUMNS) for r in csv)
+
+
+def test_reshard_traffic_within_the_cost_model_bound():
+    """a11 (costmodel.py:179-196): the reshard of every layout change of BASELINE config 4's
+    alternating TP4 / SDP4 / DP2xTP2 plan sends no more bytes from its busiest rank than the
+    all-gather volume the cost model charges for the transition; tp -> dp moves nothing."""
+    from paper_2504_21411_b200.planner import profiles as P
+    from paper_2504_21411_b200.planner.search import make_plan
+    from paper_2504_21411_b200.planner.strategy import ParallelStrategy as PS
+    from paper_2504_21411_b200.profiler import planned_profile
+    from paper_2504_21411_b200.report import transition_traffic
+    from paper_2504_21411_b200.runtime.config import MODEL_PRESETS
+    cfg = MODEL_PRESETS["gpt-1.3b"]
+    mp = planned_profile(cfg)
+    table = tuple(P.BandwidthEntry("intra_node", g, 4e11, 5e-6) for g in (2, 4))
+    cluster = P.ClusterProfile(4, 4, 1.2e15, 191_000_000_000, 0.1, table)
+    strs = [PS(4, 1, 0, False, False), PS(1, 4, 3, False, False), PS(2, 2, 0, False, False)]
+    plan = make_plan(mp, cluster, P.TrainingConfig(global_batch=64), 1, 8,
+                     [strs[i % 3] for i in range(cfg.n_layers)])
+    tt = transition_traffic(plan, mp, hidden=cfg.hidden)
+    assert len(tt) == cfg.n_layers - 1
+    for li, t in tt.items():
+        assert t["reshard_bytes_max_rank"] <= t["model_allgather_bytes_per_rank"], (li, t)
+    assert tt[1]["reshard_bytes_max_rank"] == 0  # TP4 -> DP4: every rank already holds it
