@@ -58,6 +58,9 @@ int32_t galv_gemm(const void* A, const void* B, void* C, const void* bias,
  * it is > 1 only for GEMMs whose tiles cannot fill the chip (narrow-layer wgrad).
  */
 int32_t galv_gemm_splits(int64_t M, int64_t N, int64_t K);
+/* Workspace queries (the caller owns all memory): bytes the matching call needs in `ws`. */
+int64_t galv_gemm_splitk_workspace(int64_t M, int64_t N, int64_t K);
+int64_t galv_colsum_workspace(int64_t rows, int64_t cols, int32_t dtype);
 int32_t galv_gemm_splitk(const void* A, const void* B, void* C, const void* bias, int64_t M,
                          int64_t N, int64_t K, int64_t lda, int64_t ldb, int64_t ldc,
                          int32_t trans_a, int32_t trans_b, float alpha, int32_t accumulate,

@@ -78,6 +78,21 @@ int32_t galv_gemm_splits(int64_t M, int64_t N, int64_t K) {
   return M > 0 && N > 0 && K > 0 ? galv::gemm_pick_splits(M, N, K) : 1;
 }
 
+// Workspace queries (the caller owns all memory; kernels never allocate).
+// split-K: splits * M * N fp32 partial tiles when galv_gemm_splits picks > 1, else 0.
+int64_t galv_gemm_splitk_workspace(int64_t M, int64_t N, int64_t K) {
+  const int64_t s = galv_gemm_splits(M, N, K);
+  return s > 1 ? s * M * N * (int64_t)sizeof(float) : 0;
+}
+// The column-sum kernels need no scratch (their `ws` argument is reserved): 0 bytes.
+// (galv_norm_bwd_workspace lives with the norm kernels, norm.cu.)
+int64_t galv_colsum_workspace(int64_t rows, int64_t cols, int32_t dtype) {
+  (void)rows;
+  (void)cols;
+  (void)dtype;
+  return 0;
+}
+
 int32_t galv_gemm_splitk(const void* A, const void* B, void* C, const void* bias, int64_t M,
                          int64_t N, int64_t K, int64_t lda, int64_t ldb, int64_t ldc,
                          int32_t trans_a, int32_t trans_b, float alpha, int32_t accumulate,

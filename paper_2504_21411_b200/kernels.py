@@ -54,6 +54,8 @@ _SIGS = {
     "galv_attn_fwd": ([_P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _F, _I32,
                        _I32, _P], _I32),
     "galv_attn_bwd_workspace": ([_I64, _I64, _I64, _I64, _I32], _I64),
+    "galv_gemm_splitk_workspace": ([_I64, _I64, _I64], _I64),
+    "galv_colsum_workspace": ([_I64, _I64, _I32], _I64),
     "galv_attn_bwd": ([_P, _P, _P, _P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64,
                        _I64, _F, _I32, _I32, _P, _P], _I32),
     "galv_attn_bwd_rope": ([_P, _P, _P, _P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _I64,
@@ -248,7 +250,8 @@ def gemm(a, b, out=None, *, trans_a=False, trans_b=False, alpha=1.0, accumulate=
         ev0.record()
     splits = _gemm_splits(M, N, K) if a.dtype == torch.bfloat16 else 1
     if splits > 1:  # narrow output, long K: K-split units + one fp32 reduction pass
-        ws = torch.empty(splits * M * N, device=a.device, dtype=torch.float32)
+        nbytes = int(load_library().galv_gemm_splitk_workspace(M, N, K))
+        ws = torch.empty(nbytes // 4, device=a.device, dtype=torch.float32)
         _call("galv_gemm_splitk", _ptr(a), _ptr(b), _ptr(out), _ptr(bias), M, N, K,
               a.stride(0), b.stride(0), out.stride(0), int(trans_a), int(trans_b),
               float(alpha), int(accumulate), dtype_code(out.dtype),

@@ -177,3 +177,15 @@ def test_gemm_rope_qkv_fused(M, heads, Kd, S):
     want = torch.cat([a * c - b * s, b * c + a * s], -1).flatten(1)
     err = ((got[:, :2 * heads * D].float() - want).norm() / want.norm()).item()
     assert err < 1e-2
+
+
+def test_splitk_workspace_query_matches_the_plan():
+    """galv_gemm_splitk_workspace reports splits*M*N fp32 bytes exactly when the split-K
+    planner splits (narrow-output long-K wgrad shapes), else 0."""
+    from paper_2504_21411_b200 import kernels as K
+    lib = K.load_library()
+    for M, N, Kd in [(1024, 1024, 16384), (3072, 1024, 16384), (8192, 8192, 4096)]:
+        s = K._gemm_splits(M, N, Kd)
+        want = s * M * N * 4 if s > 1 else 0
+        assert lib.galv_gemm_splitk_workspace(M, N, Kd) == want
+    assert lib.galv_colsum_workspace(100, 64, 1) == 0
