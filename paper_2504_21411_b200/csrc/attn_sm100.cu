@@ -741,11 +741,8 @@ __global__ void __launch_bounds__(FWD2_THREADS, 1)
   uint64_t* k_empty = v_full + NST3;       // [NST3]
   uint64_t* v_empty = k_empty + NST3;      // [NST3]
   uint64_t* s_full = v_empty + NST3;       // [tile][buffer]
-  // P_t(j) written -- per tile AND buffer: the softmax of a tile may finish blocks j and
-  // j+1 (both S buffers ready) before the MMA warp waits for block j's P; one barrier per
-  // tile would then have moved two phases and the parity wait would alias
-  uint64_t* p_full = s_full + 4;           // [tile][buffer]
-  uint64_t* o_done = p_full + 4;           // [tile]  every PV_t
+  uint64_t* p_full = s_full + 4;           // [tile]
+  uint64_t* o_done = p_full + 2;           // [tile]  every PV_t
   // the last PV_t: with S double-buffered, PV(n-2) may still be pending when the last
   // softmax ends, so a parity wait on o_done could alias two phases back
   uint64_t* o_last = o_done + 2;           // [tile]
@@ -772,11 +769,9 @@ __global__ void __launch_bounds__(FWD2_THREADS, 1)
       mbar_init(&k_empty[i], 1);
       mbar_init(&v_empty[i], 1);
     }
-    for (int i = 0; i < 4; ++i) {
-      mbar_init(&s_full[i], 1);
-      mbar_init(&p_full[i], 128);
-    }
+    for (int i = 0; i < 4; ++i) mbar_init(&s_full[i], 1);
     for (int i = 0; i < 2; ++i) {
+      mbar_init(&p_full[i], 128);
       mbar_init(&o_done[i], 1);
       mbar_init(&o_last[i], 1);
     }
@@ -844,7 +839,7 @@ __global__ void __launch_bounds__(FWD2_THREADS, 1)
     };
     auto issue_pv = [&](int t, int j) {
       const int st = j % NST3;
-      mbar_wait_fast(&p_full[t * 2 + (j & 1)], (j >> 1) & 1);
+      mbar_wait_fast(&p_full[t], j & 1);
       mbar_wait_fast(&v_full[st], (j / NST3) & 1);
       tc_fence_after();
       const uint64_t bv = d_v + (uint64_t)((st * L::KT) >> 4);
@@ -942,7 +937,7 @@ __global__ void __launch_bounds__(FWD2_THREADS, 1)
         }
       }
       tc_fence_before();
-      mbar_arrive(&p_full[t * 2 + (j & 1)]);
+      mbar_arrive(&p_full[t]);
     }
     if (n_t > 0) {
       mbar_wait(&o_last[t], 0);
