@@ -742,11 +742,8 @@ __global__ void __launch_bounds__(FWD2_THREADS, 1)
   uint64_t* v_empty = k_empty + NST3;      // [NST3]
   uint64_t* s_full = v_empty + NST3;       // [tile][buffer]
   uint64_t* p_full = s_full + 4;           // [tile]
-  uint64_t* o_done = p_full + 2;           // [tile]  every PV_t
-  // the last PV_t: with S double-buffered, PV(n-2) may still be pending when the last
-  // softmax ends, so a parity wait on o_done could alias two phases back
-  uint64_t* o_last = o_done + 2;           // [tile]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_last + 2);
+  uint64_t* o_done = p_full + 2;           // [tile]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_pairs = (p.n_qblocks + 1) / 2;
@@ -773,7 +770,6 @@ __global__ void __launch_bounds__(FWD2_THREADS, 1)
     for (int i = 0; i < 2; ++i) {
       mbar_init(&p_full[i], 128);
       mbar_init(&o_done[i], 1);
-      mbar_init(&o_last[i], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     fence_async_smem();
@@ -849,7 +845,6 @@ __global__ void __launch_bounds__(FWD2_THREADS, 1)
         for (int k = 0; k < BKV3 / 16; ++k)
           umma_bf16_ts(t_o, t_p + k * 8, bv + (uint64_t)((k * 2048) >> 4), id_o, (j | k) != 0);
         umma_commit(&o_done[t]);
-        if (j == (t == 0 ? nkv0 : nkv1) - 1) umma_commit(&o_last[t]);
         if (t == 1 || j >= nkv1) umma_commit(&v_empty[st]);  // last reader of V_j
       }
       __syncwarp();
@@ -940,7 +935,7 @@ __global__ void __launch_bounds__(FWD2_THREADS, 1)
       mbar_arrive(&p_full[t]);
     }
     if (n_t > 0) {
-      mbar_wait(&o_last[t], 0);
+      mbar_wait(&o_done[t], (n_t - 1) & 1);
       tc_fence_after();
       const float inv_l = l > 0.f ? 1.f / l : 0.f;
       __nv_bfloat16* orow = p.o + (long long)(tok0 + qi) * p.o_st + (long long)h * p.sh;
