@@ -704,269 +704,6 @@ __global__ void __launch_bounds__(FWD2_THREADS, 1)
   }
 }
 
-// ---------------------------------------------------------------- forward, 64-key blocks
-// fwd_tc3: as fwd_tc2 (two 128-row Q tiles per CTA, one softmax thread per row) with K/V in
-// 64-key blocks so each tile's S is DOUBLE-buffered in TMEM: per tile S_t[0] | S_t[1]
-// (64 fp32 columns each) | O_t (128 columns) = 256 columns, two tiles = 512.  S_t(j+2) is
-// issued right after PV_t(j) into the buffer PV_t(j) has just read P_t(j) from, while the
-// softmax of block j+1 -- whose S was computed a block earlier -- is already running: the
-// per-tile chain S(j) -> softmax -> PV(j) -> S(j+1) of fwd_tc2 (P over the single S buffer;
-// ~3300 SM cycles per 128 keys, 61 % of the tensor pipe) becomes a chain of softmaxes.
-// The price: the N=64 QK^T MMAs read 6 KB of smem per 32-cycle MMA, above the 128 B/cycle
-// smem port, so S runs at ~2/3 rate (384 instead of 256 cycles per block).
-//   warp 0: TMA (Q_0, Q_1; K/V 64-key ring of NST3 stages); warp 1: MMA; warp 2: TMEM
-//   alloc; warps 4-7 / 8-11: softmax of tile 0 / 1.
-constexpr int BKV3 = 64, NST3 = 4;
-template <int D>
-struct Smem3 {
-  static constexpr int QT = D * 128 * 2, KT = D * BKV3 * 2;
-  static constexpr int Q = 0;
-  static constexpr int K0 = 2 * QT;              // [NST3 stages]
-  static constexpr int V0 = K0 + NST3 * KT;      // [NST3 stages]
-  static constexpr int BAR = V0 + NST3 * KT;
-  static constexpr int BYTES = BAR + 512 + 1024;
-};
-
-template <int D>
-__global__ void __launch_bounds__(FWD2_THREADS, 1)
-    fwd_tc3(const __grid_constant__ CUtensorMap mq, const __grid_constant__ CUtensorMap mk,
-            const __grid_constant__ CUtensorMap mv, const FwdParams p) {
-  using L = Smem3<D>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::BAR);
-  uint64_t* q_full = bar + 0;
-  uint64_t* k_full = bar + 1;              // [NST3]
-  uint64_t* v_full = k_full + NST3;        // [NST3]
-  uint64_t* k_empty = v_full + NST3;       // [NST3]
-  uint64_t* v_empty = k_empty + NST3;      // [NST3]
-  uint64_t* s_full = v_empty + NST3;       // [tile][buffer]
-  uint64_t* p_full = s_full + 4;           // [tile]
-  uint64_t* o_done = p_full + 2;           // [tile]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n_pairs = (p.n_qblocks + 1) / 2;
-  const int qp = n_pairs - 1 - blockIdx.x;  // heavy causal pairs first
-  const int bh = blockIdx.y, b = bh / p.H, h = bh % p.H;
-  const int q0 = qp * 2 * BQ;
-  const int nkb = (p.S + BKV3 - 1) / BKV3;
-  auto blocks_of = [&](int qt) {
-    return qt >= p.S ? 0 : (p.causal ? min((qt + BQ - 1) / BKV3 + 1, nkb) : nkb);
-  };
-  const int nkv0 = blocks_of(q0), nkv1 = blocks_of(q0 + BQ);
-  const int n_kv = max(nkv0, nkv1);
-  const int tok0 = b * p.S;
-
-  if (threadIdx.x == 0) {
-    mbar_init(q_full, 1);
-    for (int i = 0; i < NST3; ++i) {
-      mbar_init(&k_full[i], 1);
-      mbar_init(&v_full[i], 1);
-      mbar_init(&k_empty[i], 1);
-      mbar_init(&v_empty[i], 1);
-    }
-    for (int i = 0; i < 4; ++i) mbar_init(&s_full[i], 1);
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&p_full[i], 128);
-      mbar_init(&o_done[i], 1);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    fence_async_smem();
-    prefetch_map(&mq);
-    prefetch_map(&mk);
-    prefetch_map(&mv);
-  }
-  if (warp == 2) tmem_alloc(tmem_slot, 512);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-
-  if (warp == 0) {
-    if (lane == 0) {
-      const int nq = nkv1 > 0 ? 2 : 1;
-      mbar_expect_tx(q_full, nq * L::QT);
-      for (int t = 0; t < nq; ++t)
-#pragma unroll
-        for (int c = 0; c < D / 64; ++c)
-          tma_load_3d(&mq, q_full, sm + L::Q + t * L::QT + c * 16384, c * 64, h,
-                      tok0 + q0 + t * BQ);
-      for (int j = 0; j < n_kv; ++j) {
-        const int st = j % NST3, ph = (j / NST3) & 1;
-        mbar_wait(&k_empty[st], ph ^ 1);
-        mbar_expect_tx(&k_full[st], L::KT);
-#pragma unroll
-        for (int c = 0; c < D / 64; ++c)
-          tma_load_3d(&mk, &k_full[st], sm + L::K0 + st * L::KT + c * (BKV3 * 128), c * 64, h,
-                      tok0 + j * BKV3);
-        mbar_wait(&v_empty[st], ph ^ 1);
-        mbar_expect_tx(&v_full[st], L::KT);
-#pragma unroll
-        for (int c = 0; c < D / 64; ++c)
-          tma_load_3d(&mv, &v_full[st], sm + L::V0 + st * L::KT + c * (BKV3 * 128), c * 64, h,
-                      tok0 + j * BKV3);
-      }
-    }
-  } else if (warp == 1) {
-    const uint32_t id_s = make_idesc(BQ, BKV3, 0, 0);
-    const uint32_t id_o = make_idesc(BQ, D, 0, 1);
-    const uint64_t d_q = sdesc(smem_u32(sm + L::Q), 16, 1024);
-    const uint64_t d_k = sdesc(smem_u32(sm + L::K0), 16, 1024);
-    const uint64_t d_v = sdesc(smem_u32(sm + L::V0), BKV3 * 128, 1024);
-    mbar_wait_fast(q_full, 0);
-    auto issue_s = [&](int t, int j) {
-      const int st = j % NST3;
-      mbar_wait_fast(&k_full[st], (j / NST3) & 1);
-      tc_fence_after();
-      const uint64_t bk = d_k + (uint64_t)((st * L::KT) >> 4);
-      const uint64_t bq = d_q + (uint64_t)((t * L::QT) >> 4);
-      if (elect_one()) {
-#pragma unroll
-        for (int k = 0; k < D / 16; ++k) {
-          const uint64_t oq = (uint64_t)(((k >> 2) * 16384 + (k & 3) * 32) >> 4);
-          const uint64_t ok = (uint64_t)(((k >> 2) * (BKV3 * 128) + (k & 3) * 32) >> 4);
-          umma_bf16(tmem + t * 256 + (j & 1) * BKV3, bq + oq, bk + ok, id_s, k != 0);
-        }
-        umma_commit(&s_full[t * 2 + (j & 1)]);
-        if (t == 1 || j >= nkv1) umma_commit(&k_empty[st]);  // last reader of K_j
-      }
-      __syncwarp();
-    };
-    auto issue_pv = [&](int t, int j) {
-      const int st = j % NST3;
-      mbar_wait_fast(&p_full[t], j & 1);
-      mbar_wait_fast(&v_full[st], (j / NST3) & 1);
-      tc_fence_after();
-      const uint64_t bv = d_v + (uint64_t)((st * L::KT) >> 4);
-      const uint32_t t_o = tmem + t * 256 + 128, t_p = tmem + t * 256 + (j & 1) * BKV3;
-      if (elect_one()) {
-#pragma unroll
-        for (int k = 0; k < BKV3 / 16; ++k)
-          umma_bf16_ts(t_o, t_p + k * 8, bv + (uint64_t)((k * 2048) >> 4), id_o, (j | k) != 0);
-        umma_commit(&o_done[t]);
-        if (t == 1 || j >= nkv1) umma_commit(&v_empty[st]);  // last reader of V_j
-      }
-      __syncwarp();
-    };
-    for (int j = 0; j < 2; ++j) {
-      if (j < nkv0) issue_s(0, j);
-      if (j < nkv1) issue_s(1, j);
-    }
-    for (int j = 0; j < n_kv; ++j) {
-      if (j < nkv0) {
-        issue_pv(0, j);
-        if (j + 2 < nkv0) issue_s(0, j + 2);
-      }
-      if (j < nkv1) {
-        issue_pv(1, j);
-        if (j + 2 < nkv1) issue_s(1, j + 2);
-      }
-    }
-  } else if (warp >= 4) {
-    const int t = (warp - 4) >> 2;
-    const int q = warp & 3;
-    const int r = q * 32 + lane;
-    const int qt = q0 + t * BQ, qi = qt + r;
-    const int n_t = t == 0 ? nkv0 : nkv1;
-    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-    const uint32_t t_o = tmem + t * 256 + 128;
-    float m_used = -INFINITY, l = 0.f;
-    for (int j = 0; j < n_t; ++j) {
-      const uint32_t t_s = tmem + t * 256 + (j & 1) * BKV3;
-      mbar_wait(&s_full[t * 2 + (j & 1)], (j >> 1) & 1);
-      tc_fence_after();
-      float s[BKV3];
-#pragma unroll
-      for (int c = 0; c < BKV3 / 32; ++c)
-        tmem_ld32_nowait(t_s + c * 32 + lane_off, reinterpret_cast<uint32_t*>(s) + c * 32);
-      tmem_wait_ld();
-      const int k0 = j * BKV3;
-      const bool mask = (k0 + BKV3 > p.S) || (p.causal && k0 + BKV3 - 1 > qt);
-      if (mask) {
-        const int lim = (p.causal ? min(p.S, qi + 1) : p.S) - k0;
-#pragma unroll
-        for (int i = 0; i < BKV3; ++i) s[i] = i < lim ? s[i] : -INFINITY;
-      }
-      float m8[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) m8[u] = s[u];
-#pragma unroll
-      for (int i = 8; i < BKV3; ++i) m8[i & 7] = fmaxf(m8[i & 7], s[i]);
-      float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
-                       fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
-      mx *= p.scale_log2;
-      float alpha = 1.f;
-      if ((mx > m_used + RESCALE_THRESHOLD || m_used == -INFINITY) && mx != -INFINITY) {
-        alpha = (m_used == -INFINITY) ? 0.f : exp2f(m_used - mx);
-        m_used = mx;
-      }
-      const float mu = (m_used == -INFINITY) ? 0.f : m_used;
-      float r4[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-      for (int c = 0; c < BKV3 / 16; ++c) {
-        uint32_t pk[8];
-#pragma unroll
-        for (int i = 0; i < 16; i += 2) {
-          const int e = c * 16 + i;
-          const float p0 = exp2_mufu(fmaf(s[e], p.scale_log2, -mu));
-          const float p1 = exp2_mufu(fmaf(s[e + 1], p.scale_log2, -mu));
-          r4[(i >> 1) & 3] += p0 + p1;
-          pk[i / 2] = pack2(p0, p1);
-        }
-        tmem_st8(t_s + c * 8 + lane_off, pk);
-      }
-      l = l * alpha + ((r4[0] + r4[1]) + (r4[2] + r4[3]));
-      tmem_wait_st();
-      if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
-        mbar_wait(&o_done[t], (j - 1) & 1);
-        tc_fence_after();
-#pragma unroll 1
-        for (int c = 0; c < D / 32; ++c) {
-          uint32_t ov[32];
-          const uint32_t ta = t_o + c * 32 + lane_off;
-          tmem_ld32(ta, ov);
-#pragma unroll
-          for (int i = 0; i < 32; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * alpha);
-          tmem_st32(ta, ov);
-        }
-      }
-      tc_fence_before();
-      mbar_arrive(&p_full[t]);
-    }
-    if (n_t > 0) {
-      mbar_wait(&o_done[t], (n_t - 1) & 1);
-      tc_fence_after();
-      const float inv_l = l > 0.f ? 1.f / l : 0.f;
-      __nv_bfloat16* orow = p.o + (long long)(tok0 + qi) * p.o_st + (long long)h * p.sh;
-#pragma unroll 1
-      for (int c = 0; c < D / 32; ++c) {
-        uint32_t ov[32];
-        tmem_ld32(t_o + c * 32 + lane_off, ov);
-        if (qi < p.S) {
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            uint4 w;
-            w.x = pack2(__uint_as_float(ov[u * 8 + 0]) * inv_l, __uint_as_float(ov[u * 8 + 1]) * inv_l);
-            w.y = pack2(__uint_as_float(ov[u * 8 + 2]) * inv_l, __uint_as_float(ov[u * 8 + 3]) * inv_l);
-            w.z = pack2(__uint_as_float(ov[u * 8 + 4]) * inv_l, __uint_as_float(ov[u * 8 + 5]) * inv_l);
-            w.w = pack2(__uint_as_float(ov[u * 8 + 6]) * inv_l, __uint_as_float(ov[u * 8 + 7]) * inv_l);
-            *reinterpret_cast<uint4*>(orow + c * 32 + u * 8) = w;
-          }
-        }
-      }
-      if (qi < p.S)
-        p.lse[((long long)b * p.H + h) * p.S + qi] = (m_used + log2f(l)) * 0.6931471805599453f;
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 2) {
-    tc_fence_after();
-    tmem_dealloc(tmem, 512);
-  }
-}
-
 // ---------------------------------------------------------------- backward
 // Two deterministic kernels (no atomics), both on tcgen05 with 8 math warps:
 //   dkdv: CTA = 128 keys; per 64-query step  S^T = K Q^T, dP^T = V dO^T (TMEM, double
@@ -1651,14 +1388,6 @@ static bool qkv_map(CUtensorMap* m, const void* base, int64_t tokens, int64_t H,
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// GALV_ATTN_FWD=3 selects the 64-key-block forward (fwd_tc3) for A/B runs
-static int fwd_variant() {
-  static const int v = [] {
-    const char* e = getenv("GALV_ATTN_FWD");
-    return e ? atoi(e) : 2;
-  }();
-  return v;
-}
 // GALV_ATTN_FWD=1 selects the one-Q-tile forward (fwd_tc) for A/B runs
 static bool fwd_two_tiles() {
   static const bool two = [] {
@@ -1711,17 +1440,6 @@ int32_t attn_fwd_sm100(const void* q, const void* k, const void* v, void* o, flo
     return 0;
   };
   int32_t rc;
-  if (fwd_variant() == 3 && p.drop.thresh == 0 && D == 128) {  // 64-key blocks, S double-buffered
-    CUtensorMap mk64, mv64;
-    ok = qkv_map(&mk64, k, tokens, H, D, st, sh, BKV3) && qkv_map(&mv64, v, tokens, H, D, st, sh, BKV3);
-    GALV_CHECK_ARG(ok, "tensor map encode failed (alignment?)");
-    const dim3 grid3((unsigned)((p.n_qblocks + 1) / 2), (unsigned)(B * H));
-    const int smem = Smem3<128>::BYTES;
-    GALV_CUDA_RET(cudaFuncSetAttribute(fwd_tc3<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    fwd_tc3<128><<<grid3, FWD2_THREADS, smem, stream>>>(mq, mk64, mv64, p);
-    GALV_LAUNCH_CHECK();
-    return 0;
-  }
   // default: the two-Q-tile kernel (fwd_tc2); dropout is implemented there only
   if (fwd_two_tiles() || p.drop.thresh != 0) {
     const dim3 grid2((unsigned)((p.n_qblocks + 1) / 2), (unsigned)(B * H));
