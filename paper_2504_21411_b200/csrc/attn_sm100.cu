@@ -456,8 +456,11 @@ __global__ void __launch_bounds__(FWD2_THREADS, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_pairs = (p.n_qblocks + 1) / 2;
-  const int qp = n_pairs - 1 - blockIdx.x;  // heavy causal pairs first
-  const int bh = blockIdx.y, b = bh / p.H, h = bh % p.H;
+  // blockIdx.x (fastest in launch order) runs over (batch, head) and blockIdx.y over query
+  // pairs from the heaviest causal one down, so the grid is issued heaviest-first as a whole
+  // (longest-first list scheduling: no long CTA starts in the last wave)
+  const int qp = n_pairs - 1 - blockIdx.y;
+  const int bh = blockIdx.x, b = bh / p.H, h = bh % p.H;
   const int q0 = qp * 2 * BQ;
   const int nkb = (p.S + BKV - 1) / BKV;
   // blocks of keys each tile attends to (0 = tile beyond the sequence)
@@ -1109,6 +1112,357 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
   }
 }
 
+// dkdv, 128-query steps (default): CTA = 128 keys.  The N=128 score MMAs read 8 KB of smem
+// per 64 tensor cycles (the N=64 ones of bwd_dkdv_tc read 6 KB per 32 and are smem-bound).
+// TMEM (512 columns at D=128): S^T [0,128), dP^T [128,256), dV [256,256+D), dK [256+D,..).
+// The scores are single-buffered; instead the MMA warp interleaves two steps so that each
+// softmax phase overlaps other MMAs:
+//     ... dV(it-1) S(it) dK(it-1) dP(it) | dV(it) S(it+1) dK(it) dP(it+1) | ...
+//   phase 1 (P^T = exp2(S^T - lse), packed bf16 over S^T) runs under dK(it-1), dP(it)
+//   phase 2 (dS^T = P^T (dP^T - D), packed over dP^T) runs under dV(it), S(it+1)
+// Both phases go in two query halves with their own barriers, so dV / dK over the first
+// 64 queries start while the second half is computed (phase 1 is MUFU-bound: 16K exp2 per
+// step = 1024 cycles at 16/clk/SM; measured period 2730 cycles per 128-query step vs 3400
+// for two 64-query steps of bwd_dkdv_tc).  tcgen05.mma from one thread execute in issue
+// order, so S(it+1) (issued after dV(it)) never overwrites P^T(it) before dV has read it;
+// likewise dP(it+1) after dK(it).  Q (+ lse, D vectors) and dO come through separate
+// 2-stage rings: dO(it) is released by dV(it), Q(it) by dK(it), the last reader of the
+// step's vectors being phase 2 (before dK(it) issues).  Splitting S(it+1) into two N=64
+// halves (so S half 0 can follow dV half 0) measured slower (period 3010): N=64 score MMAs
+// are smem-bound.
+// every DKDV_POLY-th phase-1 exponential on the FMA pipe: measured neutral to slower (poly 4:
+// 925-929 vs 907-934 us at B2 S4096 H32; poly 2: 993): the phase is issue-bound once the
+// polynomial's ~11 instructions are added.  0 = all on MUFU.
+#ifndef DKDV_POLY
+#define DKDV_POLY 0
+#endif
+// Grid order of the backward kernels.  1 = (batch, head) fastest, i.e. the whole grid issued
+// heaviest-first (what the forward does); measured slower for both backward kernels on B200
+// (B2 S4096 H32: 941-958 vs 921 us, B4 S8192 H16: 3785-4110 vs 3627 us): a key (query)
+// block sweeps every query (key) block of its head, and with the blocks of one head running
+// side by side those sweeps share L2.  0 = block index fastest (heaviest-first per head).
+#ifndef DKDV_GRID_BH_FAST
+#define DKDV_GRID_BH_FAST 0
+#endif
+#ifndef DQ_GRID_BH_FAST
+#define DQ_GRID_BH_FAST 0
+#endif
+template <int D>
+struct SmemKV2 {
+  static constexpr int NST = 2;
+  static constexpr int KT = D * 128 * 2;  // every tile is 128 rows x D
+  static constexpr int K = 0, V = KT, Q0 = 2 * KT, O0 = Q0 + NST * KT;
+  static constexpr int LSE = O0 + NST * KT, DV = LSE + NST * 512;
+  static constexpr int BAR = DV + NST * 512;
+  static constexpr int BYTES = BAR + 256 + 1024;
+};
+
+template <int D, bool DROP>
+__global__ void __launch_bounds__(BWD_THREADS, 1)
+    bwd_dkdv2_tc(const __grid_constant__ CUtensorMap mq, const __grid_constant__ CUtensorMap mk,
+                 const __grid_constant__ CUtensorMap mv, const __grid_constant__ CUtensorMap mdo,
+                 const BwdParams p) {
+  using L = SmemKV2<D>;
+  constexpr int NST = L::NST;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::BAR);
+  uint64_t* kv_full = bar + 0;
+  uint64_t* q_full = bar + 1;         // [NST] Q tile + lse2 / D vectors
+  uint64_t* q_empty = q_full + NST;   // [NST]
+  uint64_t* o_full = q_empty + NST;   // [NST] dO tile
+  uint64_t* o_empty = o_full + NST;   // [NST]
+  uint64_t* s_full = o_empty + NST;   // S^T(it) complete
+  uint64_t* dp_full = s_full + 1;     // dP^T(it) complete
+  uint64_t* p_full = dp_full + 1;     // [2] P^T(it) query half packed (all math threads)
+  uint64_t* ds_full = p_full + 2;     // [2] dS^T(it) query half packed (all math threads)
+  uint64_t* mm_done = ds_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mm_done + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // causal: low key blocks carry the most query blocks (see DKDV_GRID_BH_FAST)
+  const int kb = DKDV_GRID_BH_FAST ? blockIdx.y : blockIdx.x;
+  const int bh = DKDV_GRID_BH_FAST ? blockIdx.x : blockIdx.y, b = bh / p.H, h = bh % p.H;
+  const int k0 = kb * 128, tok0 = b * p.S;
+  const int n_qb = (p.S + 127) / 128;
+  const int i0 = p.causal ? kb : 0;
+  const int n_it = n_qb - i0;
+  if (threadIdx.x == 0) TRACE(4096 + 16 * 64 + 3);
+  if (threadIdx.x == 0) {
+    mbar_init(kv_full, 1);
+    for (int i = 0; i < NST; ++i) {
+      mbar_init(&q_full[i], 1);
+      mbar_init(&q_empty[i], 1);
+      mbar_init(&o_full[i], 1);
+      mbar_init(&o_empty[i], 1);
+    }
+    mbar_init(s_full, 1);
+    mbar_init(dp_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&p_full[i], 128 * BWD_SPLIT);
+      mbar_init(&ds_full[i], 128 * BWD_SPLIT);
+    }
+    mbar_init(mm_done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    fence_async_smem();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t t_dp = tmem + 128, t_dv = tmem + 256, t_dk = tmem + 256 + D;
+  const float* lse2_g = p.lse2 + (long long)bh * p.S_pad;
+  const float* dv_g = p.dvec + (long long)bh * p.S_pad;
+
+  if (warp == 0) {  // Q ring (+ vectors), then K / V once up front
+    if (lane == 0 && n_it > 0) {
+      mbar_expect_tx(kv_full, 2 * L::KT);
+#pragma unroll
+      for (int c = 0; c < D / 64; ++c) {
+        tma_load_3d(&mk, kv_full, sm + L::K + c * 16384, c * 64, h, tok0 + k0);
+        tma_load_3d(&mv, kv_full, sm + L::V + c * 16384, c * 64, h, tok0 + k0);
+      }
+      for (int it = 0; it < n_it; ++it) {
+        const int st = it % NST, q0 = (i0 + it) * 128;
+        mbar_wait(&q_empty[st], ((it / NST) & 1) ^ 1);
+        mbar_expect_tx(&q_full[st], L::KT + 1024);
+#pragma unroll
+        for (int c = 0; c < D / 64; ++c)
+          tma_load_3d(&mq, &q_full[st], sm + L::Q0 + st * L::KT + c * 16384, c * 64, h, tok0 + q0);
+        bulk_load(sm + L::LSE + st * 512, lse2_g + q0, 512, &q_full[st]);
+        bulk_load(sm + L::DV + st * 512, dv_g + q0, 512, &q_full[st]);
+      }
+    }
+  } else if (warp == 3) {  // dO ring
+    if (lane == 0) {
+      for (int it = 0; it < n_it; ++it) {
+        const int st = it % NST, q0 = (i0 + it) * 128;
+        mbar_wait(&o_empty[st], ((it / NST) & 1) ^ 1);
+        mbar_expect_tx(&o_full[st], L::KT);
+#pragma unroll
+        for (int c = 0; c < D / 64; ++c)
+          tma_load_3d(&mdo, &o_full[st], sm + L::O0 + st * L::KT + c * 16384, c * 64, h,
+                      tok0 + q0);
+      }
+    }
+  } else if (warp == 1) {
+    if (n_it > 0) {  // whole warp; elected lane issues
+      const uint32_t id_s = make_idesc(128, 128, 0, 0);
+      const uint32_t id_g = make_idesc(128, D, 0, 1);
+      const uint64_t d_k = sdesc(smem_u32(sm + L::K), 16, 1024);
+      const uint64_t d_v = sdesc(smem_u32(sm + L::V), 16, 1024);
+      const uint64_t d_q = sdesc(smem_u32(sm + L::Q0), 16, 1024);
+      const uint64_t d_o = sdesc(smem_u32(sm + L::O0), 16, 1024);
+      const uint64_t m_q = sdesc(smem_u32(sm + L::Q0), 16384, 1024);  // MN-major views
+      const uint64_t m_o = sdesc(smem_u32(sm + L::O0), 16384, 1024);
+      auto scores = [&](uint32_t dst, uint64_t da, uint64_t db) {
+        if (elect_one()) {
+#pragma unroll
+          for (int k = 0; k < D / 16; ++k) {
+            const uint64_t o = (uint64_t)(((k >> 2) * 16384 + (k & 3) * 32) >> 4);
+            umma_bf16(dst, da + o, db + o, id_s, k != 0);
+          }
+        }
+      };
+      // dst += A^T B over query half hf, A^T packed in TMEM (queries 16k.. at col 16k of src)
+      auto grad = [&](uint32_t dst, uint32_t src, uint64_t mb, int hf, bool acc) {
+        if (elect_one()) {
+#pragma unroll
+          for (int k = 4 * hf; k < 4 * hf + 4; ++k)
+            umma_bf16_ts(dst, src + k * 16, mb + (uint64_t)((k * 2048) >> 4), id_g, acc || k != 0);
+        }
+      };
+      auto so = [&](int it) { return (uint64_t)(((it % NST) * L::KT) >> 4); };
+      mbar_wait_fast(kv_full, 0);
+      if (lane == 0) TRACE(4096 + 16 * 64 + 2);
+      // prologue: S(0), dP(0)
+      mbar_wait_fast(&q_full[0], 0);
+      tc_fence_after();
+      scores(tmem, d_k, d_q);
+      if (elect_one()) umma_commit(s_full);
+      __syncwarp();
+      mbar_wait_fast(&o_full[0], 0);
+      tc_fence_after();
+      scores(t_dp, d_v, d_o);
+      if (elect_one()) umma_commit(dp_full);
+      __syncwarp();
+      for (int it = 0; it < n_it; ++it) {
+        const int st = it % NST;
+        // dV += P^T dO
+        if (lane == 0) TRACE(4096 + it * 16 + 0);
+        mbar_wait_fast(&p_full[0], it & 1);
+        tc_fence_after();
+        if (lane == 0) TRACE(4096 + it * 16 + 1);
+        grad(t_dv, tmem, m_o + so(it), 0, it != 0);
+        __syncwarp();
+        mbar_wait_fast(&p_full[1], it & 1);
+        tc_fence_after();
+        grad(t_dv, tmem, m_o + so(it), 1, true);
+        if (elect_one()) umma_commit(&o_empty[st]);
+        __syncwarp();
+        const bool more = it + 1 < n_it;
+        if (more) {  // S(it+1)
+          const int sn = (it + 1) % NST;
+          mbar_wait_fast(&q_full[sn], ((it + 1) / NST) & 1);
+          tc_fence_after();
+          if (lane == 0) TRACE(4096 + it * 16 + 2);
+          scores(tmem, d_k, d_q + so(it + 1));
+          if (elect_one()) umma_commit(s_full);
+          __syncwarp();
+        }
+        // dK += dS^T Q
+        mbar_wait_fast(&ds_full[0], it & 1);
+        tc_fence_after();
+        if (lane == 0) TRACE(4096 + it * 16 + 3);
+        grad(t_dk, t_dp, m_q + so(it), 0, it != 0);
+        __syncwarp();
+        mbar_wait_fast(&ds_full[1], it & 1);
+        tc_fence_after();
+        grad(t_dk, t_dp, m_q + so(it), 1, true);
+        if (elect_one()) {
+          if (!more) umma_commit(mm_done);
+          umma_commit(&q_empty[st]);
+        }
+        __syncwarp();
+        if (more) {  // dP(it+1)
+          const int sn = (it + 1) % NST;
+          mbar_wait_fast(&o_full[sn], ((it + 1) / NST) & 1);
+          tc_fence_after();
+          if (lane == 0) TRACE(4096 + it * 16 + 4);
+          scores(t_dp, d_v, d_o + so(it + 1));
+          if (elect_one()) umma_commit(dp_full);
+          __syncwarp();
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    // part p owns query columns [16p, 16p+16) (half 0) and [64+16p, 64+16p+16) (half 1), so
+    // the packed bf16 of query slice k lands on the thread's own columns 16k.. and the dV / dK
+    // MMAs of half 0 start while half 1 is still being computed
+    const int q = warp & 3, part = (warp - 4) >> 2;
+    const int r = q * 32 + lane, key = k0 + r;
+    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    const float sl2 = p.scale_log2;
+    for (int it = 0; it < n_it; ++it) {
+      const int st = it % NST, q0 = (i0 + it) * 128;
+      const float* l2 = reinterpret_cast<const float*>(sm + L::LSE + st * 512) + part * 16;
+      const float* dd = reinterpret_cast<const float*>(sm + L::DV + st * 512) + part * 16;
+      // ---- phase 1: P^T
+      mbar_wait(s_full, it & 1);
+      tc_fence_after();
+      if (warp == 4 && lane == 0) TRACE(4096 + it * 16 + 8);
+      float pv[32];
+      tmem_ld16_nowait(tmem + part * 16 + lane_off, reinterpret_cast<uint32_t*>(pv));
+      tmem_ld16_nowait(tmem + 64 + part * 16 + lane_off, reinterpret_cast<uint32_t*>(pv + 16));
+      tmem_wait_ld();
+      if (warp == 4 && lane == 0) TRACE(4096 + it * 16 + 13);
+      uint32_t keep = 0xffffffffu;
+      if constexpr (DROP) {
+        keep = 0;
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          keep |= (uint32_t)dropout_keep(p.drop, b, h, q0 + (i >> 4) * 64 + part * 16 + (i & 15),
+                                         key) << i;
+      }
+      // every DKDV_POLY-th exponential on the FMA pipe (exp2_fma, rel err 5e-6); 0 = MUFU only
+      auto ex = [](int i, float x) {
+        if constexpr (DKDV_POLY > 0) {
+          if (i % DKDV_POLY == DKDV_POLY - 1) return exp2_fma(x);
+        }
+        return exp2_mufu(x);
+      };
+      uint32_t pk[8];
+#pragma unroll
+      for (int hf = 0; hf < 2; ++hf) {
+        float* v = pv + hf * 16;
+        const float* lh = l2 + hf * 64;
+        const int qb = q0 + hf * 64 + part * 16;
+        if (p.causal && key > qb) {  // diagonal block: queries < key are masked
+          const int first = key - qb;
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] = i >= first ? ex(i, fmaf(v[i], sl2, -lh[i])) : 0.f;
+        } else {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] = ex(i, fmaf(v[i], sl2, -lh[i]));
+        }
+        if constexpr (DROP) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int c = hf * 16 + 2 * i;
+            pk[i] = pack2((keep >> c) & 1u ? v[2 * i] * p.drop.inv_keep : 0.f,
+                          (keep >> (c + 1)) & 1u ? v[2 * i + 1] * p.drop.inv_keep : 0.f);
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) pk[i] = pack2(v[2 * i], v[2 * i + 1]);
+        }
+        tmem_st8(tmem + hf * 64 + part * 16 + lane_off, pk);
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(&p_full[hf]);
+        if (warp == 4 && lane == 0) TRACE(4096 + it * 16 + 9 + hf);
+      }
+      // ---- phase 2: dS^T = P^T (dP^T * mask / (1-p) - D)
+      mbar_wait(dp_full, it & 1);
+      tc_fence_after();
+      if (warp == 4 && lane == 0) TRACE(4096 + it * 16 + 11);
+#pragma unroll
+      for (int hf = 0; hf < 2; ++hf) {
+        float dp[16];
+        tmem_ld16_nowait(t_dp + hf * 64 + part * 16 + lane_off, reinterpret_cast<uint32_t*>(dp));
+        tmem_wait_ld();
+        if (warp == 4 && lane == 0 && hf == 0) TRACE(4096 + it * 16 + 14);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int c = hf * 16 + i;
+          float g = dp[i];
+          if constexpr (DROP) g = (keep >> c) & 1u ? g * p.drop.inv_keep : 0.f;
+          dp[i] = pv[c] * (g - dd[hf * 64 + i]);
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) pk[i] = pack2(dp[2 * i], dp[2 * i + 1]);
+        tmem_st8(t_dp + hf * 64 + part * 16 + lane_off, pk);
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(&ds_full[hf]);
+      }
+      if (warp == 4 && lane == 0) TRACE(4096 + it * 16 + 12);
+    }
+    if (n_it > 0) {
+      mbar_wait(mm_done, 0);
+      tc_fence_after();
+      if (warp == 4 && lane == 0) TRACE(4096 + 16 * 64 + 0);
+      const bool ok = key < p.S;
+      constexpr int OC = D / BWD_SPLIT;  // output columns per warp
+      const long long off =
+          (long long)(tok0 + (ok ? key : 0)) * p.st + (long long)h * p.sh + part * OC;
+      if constexpr (OC >= 32) {
+#pragma unroll 1
+        for (int c = 0; c < OC / 32; ++c) {
+          const int c0 = part * OC + c * 32;
+          store_row_out(p.g1 + off + c * 32, t_dv + c0 + lane_off, 1.f, ok);
+          if (p.rope != nullptr)
+            store_row_out_rope<D>(p.g0 + off + c * 32, t_dk + c0 + lane_off,
+                                  t_dk + ((c0 + D / 2) & (D - 1)) + lane_off, p.scale, ok,
+                                  p.rope, p.S, ok ? key : 0, c0);
+          else
+            store_row_out(p.g0 + off + c * 32, t_dk + c0 + lane_off, p.scale, ok);
+        }
+      } else {
+        store_row_out16(p.g1 + off, t_dv + part * OC + lane_off, 1.f, ok);
+        store_row_out16(p.g0 + off, t_dk + part * OC + lane_off, p.scale, ok);
+      }
+      if (warp == 4 && lane == 0) TRACE(4096 + 16 * 64 + 1);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
 // dq kernel: CTA = 128 queries, 128-key steps.  TMEM: S double-buffered (cols 0-255), dP
 // single (256-383; released as soon as the math warps have loaded it), dQ (384-).  dS is
 // packed (bf16) over the first half of its own S columns and read from TMEM as the A
@@ -1147,8 +1501,8 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dq_done + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_q = (p.S + 127) / 128;
-  const int qb = n_q - 1 - blockIdx.x;  // heavy causal blocks first
-  const int bh = blockIdx.y, b = bh / p.H, h = bh % p.H;
+  const int qb = n_q - 1 - (DQ_GRID_BH_FAST ? blockIdx.y : blockIdx.x);  // heavy blocks first
+  const int bh = DQ_GRID_BH_FAST ? blockIdx.x : blockIdx.y, b = bh / p.H, h = bh % p.H;
   const int q0 = qb * 128, tok0 = b * p.S;
   const int n_kb = (p.S + 127) / 128;
   const int n_it = p.causal ? min(n_kb, qb + 1) : n_kb;
@@ -1397,6 +1751,15 @@ static bool fwd_two_tiles() {
   return two;
 }
 
+// GALV_ATTN_DKDV=1 selects the 64-query-step dK/dV kernel (bwd_dkdv_tc) for A/B runs
+static bool dkdv_64q_steps() {
+  static const bool old = [] {
+    const char* e = getenv("GALV_ATTN_DKDV");
+    return e && e[0] == '1';
+  }();
+  return old;
+}
+
 }  // namespace fa
 
 int32_t attn_fwd_sm100(const void* q, const void* k, const void* v, void* o, float* lse,
@@ -1442,7 +1805,7 @@ int32_t attn_fwd_sm100(const void* q, const void* k, const void* v, void* o, flo
   int32_t rc;
   // default: the two-Q-tile kernel (fwd_tc2); dropout is implemented there only
   if (fwd_two_tiles() || p.drop.thresh != 0) {
-    const dim3 grid2((unsigned)((p.n_qblocks + 1) / 2), (unsigned)(B * H));
+    const dim3 grid2((unsigned)(B * H), (unsigned)((p.n_qblocks + 1) / 2));
     const bool drop = p.drop.thresh != 0;
     auto kern = D == 128 ? (drop ? fwd_tc2<128, true> : fwd_tc2<128, false>)
                          : (drop ? fwd_tc2<64, true> : fwd_tc2<64, false>);
@@ -1512,7 +1875,8 @@ int32_t attn_bwd_sm100(const void* q, const void* k, const void* v, const void* 
   p.drop = drop;
   GALV_CHECK_ARG(rope_table == nullptr || D == 128, "fused inverse RoPE needs head_dim 128");
   const dim3 g_kv((unsigned)((S + 127) / 128), (unsigned)(B * H));
-  const dim3 g_q((unsigned)((S + 127) / 128), (unsigned)(B * H));
+  const dim3 g_q = DQ_GRID_BH_FAST ? dim3((unsigned)(B * H), (unsigned)((S + 127) / 128)) : g_kv;
+  const dim3 g_kv2 = DKDV_GRID_BH_FAST ? dim3((unsigned)(B * H), (unsigned)((S + 127) / 128)) : g_kv;
 #define GALV_FA_BWD(DD, DR)                                                                      \
   do {                                                                                           \
     static bool set = false;                                                                     \
@@ -1520,6 +1884,9 @@ int32_t attn_bwd_sm100(const void* q, const void* k, const void* v, const void* 
       GALV_CUDA_RET(cudaFuncSetAttribute(bwd_dkdv_tc<DD, DR>,                                    \
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,            \
                                          SmemKV<DD>::BYTES));                                    \
+      GALV_CUDA_RET(cudaFuncSetAttribute(bwd_dkdv2_tc<DD, DR>,                                   \
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,            \
+                                         SmemKV2<DD>::BYTES));                                   \
       GALV_CUDA_RET(cudaFuncSetAttribute(bwd_dq_tc<DD, DR>,                                      \
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,            \
                                          SmemQ<DD>::BYTES));                                     \
@@ -1527,8 +1894,12 @@ int32_t attn_bwd_sm100(const void* q, const void* k, const void* v, const void* 
     }                                                                                            \
     p.g0 = (__nv_bfloat16*)dk;                                                                   \
     p.g1 = (__nv_bfloat16*)dv;                                                                   \
-    bwd_dkdv_tc<DD, DR><<<g_kv, BWD_THREADS, SmemKV<DD>::BYTES, stream>>>(mq64, mk128, mv128,    \
-                                                                         mdo64, p);              \
+    if (dkdv_64q_steps())                                                                        \
+      bwd_dkdv_tc<DD, DR><<<g_kv, BWD_THREADS, SmemKV<DD>::BYTES, stream>>>(mq64, mk128, mv128,  \
+                                                                           mdo64, p);            \
+    else                                                                                         \
+      bwd_dkdv2_tc<DD, DR><<<g_kv2, BWD_THREADS, SmemKV2<DD>::BYTES, stream>>>(mq128, mk128,      \
+                                                                             mv128, mdo128, p);  \
     GALV_LAUNCH_CHECK();                                                                         \
     p.g0 = (__nv_bfloat16*)dq;                                                                   \
     p.g1 = nullptr;                                                                              \
