@@ -1147,6 +1147,16 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
 #ifndef DQ_GRID_BH_FAST
 #define DQ_GRID_BH_FAST 0
 #endif
+// dq kernel MMA issuers: 0 = one warp issuing S(it), dP(it), dQ(it-1) per step (dP(it) queues
+// behind the waits for S's buffer); 2 (default) = warp 1 issues S(it), dQ(it-1) and warp 2
+// issues dP(it) as soon as dP(it-1) is loaded.  Measured B2 S4096 H32 912-913 -> 895 us
+// (whole backward; period 2080 -> 1860 cycles per 128-key step, where the step's smem
+// traffic -- S and dP read A and B from smem, dQ reads B, TMA writes K and V, 224 KB -- is
+// 1750 cycles at 128 B/clk).  Issuing dQ(it-2) before dP(it) and S(it) from one warp
+// measured neutral (911-912 us).
+#ifndef DQ_ISSUE_ORDER
+#define DQ_ISSUE_ORDER 2
+#endif
 template <int D>
 struct SmemKV2 {
   static constexpr int NST = 2;
@@ -1367,7 +1377,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       // every DKDV_POLY-th exponential on the FMA pipe (exp2_fma, rel err 5e-6); 0 = MUFU only
       auto ex = [](int i, float x) {
         if constexpr (DKDV_POLY > 0) {
-          if (i % DKDV_POLY == DKDV_POLY - 1) return exp2_fma(x);
+          if (i % (DKDV_POLY > 0 ? DKDV_POLY : 1) == DKDV_POLY - 1) return exp2_fma(x);
         }
         return exp2_mufu(x);
       };
@@ -1498,7 +1508,8 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
   uint64_t* ds_full = s_free + 2;       // [2]  dS packed into the S buffer
   uint64_t* dp_free = ds_full + 2;      // dP loaded by every math thread
   uint64_t* dq_done = dp_free + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dq_done + 1);
+  uint64_t* dp_full = dq_done + 1;      // dP(it) complete (DQ_ISSUE_ORDER 2: own issuing warp)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dp_full + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_q = (p.S + 127) / 128;
   const int qb = n_q - 1 - (DQ_GRID_BH_FAST ? blockIdx.y : blockIdx.x);  // heavy blocks first
@@ -1523,6 +1534,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     }
     mbar_init(dp_free, 128 * BWD_SPLIT);
     mbar_init(dq_done, 1);
+    mbar_init(dp_full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     fence_async_smem();
   }
@@ -1563,6 +1575,29 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
                       tok0 + it * 128);
       }
     }
+  } else if (warp == 2 && DQ_ISSUE_ORDER == 2) {  // dP issuer (after the TMEM allocation)
+    const uint32_t id_s = make_idesc(128, 128, 0, 0);
+    const uint64_t d_o = sdesc(smem_u32(sm + L::O), 16, 1024);
+    const uint64_t d_v = sdesc(smem_u32(sm + L::V0), 16, 1024);
+    mbar_wait_fast(qo_full, 0);
+    for (int it = 0; it < n_it; ++it) {
+      const int sv = it % L::NV;
+      mbar_wait_fast(&v_full[sv], (it / L::NV) & 1);
+      if (it > 0) mbar_wait_fast(dp_free, (it - 1) & 1);
+      tc_fence_after();
+      if (lane == 0) TRACE(it * 8 + 2);
+      const uint64_t ov = (uint64_t)((sv * L::KT) >> 4);
+      if (elect_one()) {
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k) {
+          const uint64_t o = (uint64_t)(((k >> 2) * 16384 + (k & 3) * 32) >> 4);
+          umma_bf16(t_dp, d_o + o, d_v + ov + o, id_s, k != 0);
+        }
+        umma_commit(dp_full);
+        umma_commit(&v_empty[sv]);
+      }
+      __syncwarp();
+    }
   } else if (warp == 1) {  // whole warp; elected lane issues (see fwd_tc)
     const uint32_t id_s = make_idesc(128, 128, 0, 0);
     const uint32_t id_g = make_idesc(128, D, 0, 1);
@@ -1591,14 +1626,15 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       }
       __syncwarp();
     };
-    for (int it = 0; it < n_it; ++it) {
-      const int sk = it % L::NK, sv = it % L::NV, sb = it & 1;
-      if (lane == 0) TRACE(it * 8 + 0);
+    auto s_mma = [&](int it) {  // S(it) = Q K^T into buffer it&1
+      const int sk = it % L::NK, sb = it & 1;
       mbar_wait_fast(&k_full[sk], (it / L::NK) & 1);
-      mbar_wait_fast(&s_free[sb], ((it >> 1) & 1) ^ 1);
+      // order 2: this warp issued dQ(it-2) (the last reader of buffer sb) before S(it), and
+      // one thread's MMAs execute in issue order -- no completion wait needed
+      if constexpr (DQ_ISSUE_ORDER != 2) mbar_wait_fast(&s_free[sb], ((it >> 1) & 1) ^ 1);
       tc_fence_after();
       if (lane == 0) TRACE(it * 8 + 1);
-      const uint64_t ok = (uint64_t)((sk * L::KT) >> 4), ov = (uint64_t)((sv * L::KT) >> 4);
+      const uint64_t ok = (uint64_t)((sk * L::KT) >> 4);
       if (elect_one()) {
 #pragma unroll
         for (int k = 0; k < D / 16; ++k) {
@@ -1607,23 +1643,48 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         }
       }
       __syncwarp();
+    };
+    auto dp_mma = [&](int it) {  // dP(it) = dO V^T (single buffer)
+      const int sv = it % L::NV;
       mbar_wait_fast(&v_full[sv], (it / L::NV) & 1);
       if (it > 0) mbar_wait_fast(dp_free, (it - 1) & 1);
       tc_fence_after();
       if (lane == 0) TRACE(it * 8 + 2);
+      const uint64_t ov = (uint64_t)((sv * L::KT) >> 4);
       if (elect_one()) {
 #pragma unroll
         for (int k = 0; k < D / 16; ++k) {
           const uint64_t o = (uint64_t)(((k >> 2) * 16384 + (k & 3) * 32) >> 4);
           umma_bf16(t_dp, d_o + o, d_v + ov + o, id_s, k != 0);
         }
-        umma_commit(&st_full[sb]);
         umma_commit(&v_empty[sv]);
       }
       __syncwarp();
-      if (it > 0) grads(it - 1);
+    };
+    auto st_commit = [&](int it) {  // S(it) and dP(it) both complete
+      if (elect_one()) umma_commit(&st_full[it & 1]);
+      __syncwarp();
+    };
+    if constexpr (DQ_ISSUE_ORDER == 2) {
+      // S and dQ only; dP(it) is issued by warp 2 as soon as the math warps have loaded
+      // dP(it-1), so it never queues behind this warp's waits for dS
+      for (int it = 0; it < n_it; ++it) {
+        if (lane == 0) TRACE(it * 8 + 0);
+        s_mma(it);
+        st_commit(it);
+        if (it > 0) grads(it - 1);
+      }
+      grads(n_it - 1);
+    } else {
+      for (int it = 0; it < n_it; ++it) {
+        if (lane == 0) TRACE(it * 8 + 0);
+        s_mma(it);
+        dp_mma(it);
+        st_commit(it);
+        if (it > 0) grads(it - 1);
+      }
+      grads(n_it - 1);
     }
-    grads(n_it - 1);
   } else if (warp >= 4) {
     const int q = warp & 3, part = (warp - 4) >> 2;  // part: keys [32 part, 32 part + 32)
     const int r = q * 32 + lane, qi = q0 + r;
@@ -1634,6 +1695,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     for (int it = 0; it < n_it; ++it) {
       const int sb = it & 1;
       mbar_wait(&st_full[sb], (it >> 1) & 1);
+      if constexpr (DQ_ISSUE_ORDER == 2) mbar_wait(dp_full, it & 1);
       tc_fence_after();
       if (warp == 4 && lane == 0) TRACE(it * 8 + 4);
       float s[32], dp[32];
