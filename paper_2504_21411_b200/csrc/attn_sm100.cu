@@ -1141,6 +1141,12 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
 // (B2 S4096 H32: 941-958 vs 921 us, B4 S8192 H16: 3785-4110 vs 3627 us): a key (query)
 // block sweeps every query (key) block of its head, and with the blocks of one head running
 // side by side those sweeps share L2.  0 = block index fastest (heaviest-first per head).
+// Two MMA-issuing warps for the dK/dV kernel (see the chain comment in bwd_dkdv2_tc):
+// measured slower (B2 S4096 H32 936 vs 884 us, period 3196 vs ~2730 cycles) -- the tensor
+// pipe then interleaves dP(it+1) ahead of S(it+1) and phase 1 starts later.  Off.
+#ifndef DKDV_TWO_ISSUERS
+#define DKDV_TWO_ISSUERS 0
+#endif
 #ifndef DKDV_GRID_BH_FAST
 #define DKDV_GRID_BH_FAST 0
 #endif
@@ -1203,7 +1209,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       mbar_init(&q_full[i], 1);
       mbar_init(&q_empty[i], 1);
       mbar_init(&o_full[i], 1);
-      mbar_init(&o_empty[i], 1);
+      mbar_init(&o_empty[i], DKDV_TWO_ISSUERS ? 2 : 1);  // dV(it) [+ dP(it) from warp 2]
     }
     mbar_init(s_full, 1);
     mbar_init(dp_full, 1);
@@ -1211,7 +1217,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       mbar_init(&p_full[i], 128 * BWD_SPLIT);
       mbar_init(&ds_full[i], 128 * BWD_SPLIT);
     }
-    mbar_init(mm_done, 1);
+    mbar_init(mm_done, DKDV_TWO_ISSUERS ? 2 : 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     fence_async_smem();
   }
@@ -1255,7 +1261,12 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
                       tok0 + q0);
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == 1 || (DKDV_TWO_ISSUERS && warp == 2)) {
+    // chain A (S^T columns): dV(it) then S(it+1); chain B (dP^T columns): dK(it) then dP(it+1).
+    // The chains touch disjoint TMEM, so with DKDV_TWO_ISSUERS warp 1 issues A and warp 2
+    // (after its TMEM allocation) issues B, each waiting only on its own barriers; otherwise
+    // warp 1 issues both in the order dV(it) S(it+1) dK(it) dP(it+1).
+    const bool chain_a = warp == 1, chain_b = !DKDV_TWO_ISSUERS || warp == 2;
     if (n_it > 0) {  // whole warp; elected lane issues
       const uint32_t id_s = make_idesc(128, 128, 0, 0);
       const uint32_t id_g = make_idesc(128, D, 0, 1);
@@ -1265,6 +1276,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       const uint64_t d_o = sdesc(smem_u32(sm + L::O0), 16, 1024);
       const uint64_t m_q = sdesc(smem_u32(sm + L::Q0), 16384, 1024);  // MN-major views
       const uint64_t m_o = sdesc(smem_u32(sm + L::O0), 16384, 1024);
+      auto so = [&](int it) { return (uint64_t)(((it % NST) * L::KT) >> 4); };
       auto scores = [&](uint32_t dst, uint64_t da, uint64_t db) {
         if (elect_one()) {
 #pragma unroll
@@ -1282,66 +1294,64 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
             umma_bf16_ts(dst, src + k * 16, mb + (uint64_t)((k * 2048) >> 4), id_g, acc || k != 0);
         }
       };
-      auto so = [&](int it) { return (uint64_t)(((it % NST) * L::KT) >> 4); };
+      auto s_mma = [&](int it) {  // S^T(it)
+        mbar_wait_fast(&q_full[it % NST], (it / NST) & 1);
+        tc_fence_after();
+        scores(tmem, d_k, d_q + so(it));
+        if (elect_one()) umma_commit(s_full);
+        __syncwarp();
+      };
+      auto dp_mma = [&](int it) {  // dP^T(it); with two issuers this warp also frees dO(it)
+        mbar_wait_fast(&o_full[it % NST], (it / NST) & 1);
+        tc_fence_after();
+        scores(t_dp, d_v, d_o + so(it));
+        if (elect_one()) {
+          umma_commit(dp_full);
+          if (DKDV_TWO_ISSUERS) umma_commit(&o_empty[it % NST]);
+        }
+        __syncwarp();
+      };
       mbar_wait_fast(kv_full, 0);
       if (lane == 0) TRACE(4096 + 16 * 64 + 2);
-      // prologue: S(0), dP(0)
-      mbar_wait_fast(&q_full[0], 0);
-      tc_fence_after();
-      scores(tmem, d_k, d_q);
-      if (elect_one()) umma_commit(s_full);
-      __syncwarp();
-      mbar_wait_fast(&o_full[0], 0);
-      tc_fence_after();
-      scores(t_dp, d_v, d_o);
-      if (elect_one()) umma_commit(dp_full);
-      __syncwarp();
+      if (chain_a) s_mma(0);
+      if (chain_b) dp_mma(0);
       for (int it = 0; it < n_it; ++it) {
         const int st = it % NST;
-        // dV += P^T dO
-        if (lane == 0) TRACE(4096 + it * 16 + 0);
-        mbar_wait_fast(&p_full[0], it & 1);
-        tc_fence_after();
-        if (lane == 0) TRACE(4096 + it * 16 + 1);
-        grad(t_dv, tmem, m_o + so(it), 0, it != 0);
-        __syncwarp();
-        mbar_wait_fast(&p_full[1], it & 1);
-        tc_fence_after();
-        grad(t_dv, tmem, m_o + so(it), 1, true);
-        if (elect_one()) umma_commit(&o_empty[st]);
-        __syncwarp();
         const bool more = it + 1 < n_it;
-        if (more) {  // S(it+1)
-          const int sn = (it + 1) % NST;
-          mbar_wait_fast(&q_full[sn], ((it + 1) / NST) & 1);
+        if (chain_a) {  // dV += P^T dO, then S(it+1) over the columns dV has just read
+          if (lane == 0) TRACE(4096 + it * 16 + 0);
+          mbar_wait_fast(&p_full[0], it & 1);
           tc_fence_after();
+          if (lane == 0) TRACE(4096 + it * 16 + 1);
+          grad(t_dv, tmem, m_o + so(it), 0, it != 0);
+          __syncwarp();
+          mbar_wait_fast(&p_full[1], it & 1);
+          tc_fence_after();
+          grad(t_dv, tmem, m_o + so(it), 1, true);
+          if (elect_one()) {
+            umma_commit(&o_empty[st]);
+            if (DKDV_TWO_ISSUERS && !more) umma_commit(mm_done);
+          }
+          __syncwarp();
           if (lane == 0) TRACE(4096 + it * 16 + 2);
-          scores(tmem, d_k, d_q + so(it + 1));
-          if (elect_one()) umma_commit(s_full);
-          __syncwarp();
+          if (more) s_mma(it + 1);
         }
-        // dK += dS^T Q
-        mbar_wait_fast(&ds_full[0], it & 1);
-        tc_fence_after();
-        if (lane == 0) TRACE(4096 + it * 16 + 3);
-        grad(t_dk, t_dp, m_q + so(it), 0, it != 0);
-        __syncwarp();
-        mbar_wait_fast(&ds_full[1], it & 1);
-        tc_fence_after();
-        grad(t_dk, t_dp, m_q + so(it), 1, true);
-        if (elect_one()) {
-          if (!more) umma_commit(mm_done);
-          umma_commit(&q_empty[st]);
-        }
-        __syncwarp();
-        if (more) {  // dP(it+1)
-          const int sn = (it + 1) % NST;
-          mbar_wait_fast(&o_full[sn], ((it + 1) / NST) & 1);
+        if (chain_b) {  // dK += dS^T Q, then dP(it+1)
+          mbar_wait_fast(&ds_full[0], it & 1);
           tc_fence_after();
-          if (lane == 0) TRACE(4096 + it * 16 + 4);
-          scores(t_dp, d_v, d_o + so(it + 1));
-          if (elect_one()) umma_commit(dp_full);
+          if (lane == 0) TRACE(4096 + it * 16 + 3);
+          grad(t_dk, t_dp, m_q + so(it), 0, it != 0);
           __syncwarp();
+          mbar_wait_fast(&ds_full[1], it & 1);
+          tc_fence_after();
+          grad(t_dk, t_dp, m_q + so(it), 1, true);
+          if (elect_one()) {
+            if (!more) umma_commit(mm_done);
+            umma_commit(&q_empty[st]);
+          }
+          __syncwarp();
+          if (lane == 0) TRACE(4096 + it * 16 + 4);
+          if (more) dp_mma(it + 1);
         }
       }
     }
