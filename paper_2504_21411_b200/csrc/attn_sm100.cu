@@ -24,7 +24,29 @@ __device__ unsigned long long g_trace[8192];
   do {                                                                     \
     if (blockIdx.x == 0 && blockIdx.y == 0) g_trace[(slot)] = clock64();   \
   } while (0)
+// per-CTA [start, end, smid] in globaltimer ns (forward kernel only)
+__device__ unsigned long long g_cta[3 * 65536];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define CTA_TRACE(k)                                                                   \
+  do {                                                                                 \
+    const unsigned id = blockIdx.y * gridDim.x + blockIdx.x;                           \
+    if (id < 65536) {                                                                  \
+      g_cta[3 * id + (k)] = gtimer();                                                  \
+      if ((k) == 0) {                                                                  \
+        unsigned smid;                                                                 \
+        asm volatile("mov.u32 %0, %smid;" : "=r"(smid));                               \
+        g_cta[3 * id + 2] = smid;                                                      \
+      }                                                                                \
+    }                                                                                  \
+  } while (0)
 #else
+#define CTA_TRACE(k) \
+  do {               \
+  } while (0)
 #define TRACE(slot) \
   do {              \
   } while (0)
@@ -55,6 +77,7 @@ struct Smem {
 
 struct FwdParams {
   int S, H, n_qblocks;
+  int bh_total;  // batch * heads (fwd_tc2 work-item decode)
   int causal;
   float scale_log2;
   __nv_bfloat16* o;
@@ -140,6 +163,8 @@ __global__ void __launch_bounds__(384, 1)
   const int tok0 = b * p.S;
   constexpr uint32_t TILE_BYTES = L::TILE;
 
+  if (threadIdx.x == 0) CTA_TRACE(0);
+  if (threadIdx.x == 0) TRACE(8000);
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
     for (int i = 0; i < 2; ++i) {
@@ -418,7 +443,11 @@ __global__ void __launch_bounds__(384, 1)
 // and read by PV as the A operand.  tcgen05.mma instructions from one thread execute in
 // issue order, so S_t(j+1) -- issued after PV_t(j) -- never overwrites P_t(j) before PV
 // has read it.
-//   warp 0    : TMA producer (Q_0, Q_1 once; K/V 2-stage ring)
+// Work items (query pair, batch*head) go heaviest causal pair first; with fwd_ctas(S) > 0
+// each CTA loops over items c, c + gridDim.x, ... (persistent: TMEM and barriers set up once,
+// the next item's Q load and first S MMAs overlap this item's epilogue; q_empty and o_free
+// hand Q and O_t over between items).
+//   warp 0    : TMA producer (Q_0, Q_1 per item; K/V 2-stage ring)
 //   warp 1    : MMA issuer: S_0(0), S_1(0), then per block j: PV_0(j), S_0(j+1), PV_1(j),
 //               S_1(j+1)
 //   warp 2    : TMEM allocator;  warp 3: idle
@@ -435,6 +464,9 @@ struct Smem2 {
   static constexpr int BYTES = XCH + 2 * 768 * 4 + 1024;
 };
 constexpr int FWD2_THREADS = 384;
+#ifndef ATTN_FWD_PERSIST_MAX_S
+#define ATTN_FWD_PERSIST_MAX_S 2048
+#endif
 
 template <int D, bool DROP>
 __global__ void __launch_bounds__(FWD2_THREADS, 1)
@@ -452,26 +484,42 @@ __global__ void __launch_bounds__(FWD2_THREADS, 1)
   uint64_t* s_full = bar + 9;    // [tile]
   uint64_t* p_full = bar + 11;   // [tile]
   uint64_t* o_done = bar + 13;   // [tile]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 15);
+  uint64_t* q_empty = bar + 15;  // the item's last S MMA done: Q tiles reusable
+  uint64_t* o_free = bar + 16;   // [tile] the item's epilogue has read O_t out of TMEM
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 18);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_pairs = (p.n_qblocks + 1) / 2;
-  // blockIdx.x (fastest in launch order) runs over (batch, head) and blockIdx.y over query
-  // pairs from the heaviest causal one down, so the grid is issued heaviest-first as a whole
-  // (longest-first list scheduling: no long CTA starts in the last wave)
-  const int qp = n_pairs - 1 - blockIdx.y;
-  const int bh = blockIdx.x, b = bh / p.H, h = bh % p.H;
-  const int q0 = qp * 2 * BQ;
   const int nkb = (p.S + BKV - 1) / BKV;
-  // blocks of keys each tile attends to (0 = tile beyond the sequence)
-  auto blocks_of = [&](int qt) { return qt >= p.S ? 0 : (p.causal ? min(qt / BKV + 1, nkb) : nkb); };
-  const int nkv0 = blocks_of(q0), nkv1 = blocks_of(q0 + BQ);  // scalars: no local array
-  const int n_kv = max(nkv0, nkv1);
-  const int tok0 = b * p.S;
+  const int n_items = n_pairs * p.bh_total;
   constexpr uint32_t TILE_BYTES = L::TILE;
+  // Work item w = (query pair, batch*head), ordered heaviest causal pair first with
+  // (batch, head) fastest; CTA c runs items c, c + gridDim.x, ... (one item per CTA when the
+  // grid covers them all; persistent CTAs otherwise -- the next item's Q load and S MMAs then
+  // overlap this item's epilogue, and the CTA set-up is paid once).
+  struct Item {
+    int b, h, q0, nkv0, nkv1, tok0;
+  };
+  auto decode = [&](int w) {
+    Item it;
+    const int qp = n_pairs - 1 - w / p.bh_total, bh = w % p.bh_total;
+    it.b = bh / p.H;
+    it.h = bh % p.H;
+    it.q0 = qp * 2 * BQ;
+    auto blocks_of = [&](int qt) {
+      return qt >= p.S ? 0 : (p.causal ? min(qt / BKV + 1, nkb) : nkb);
+    };
+    it.nkv0 = blocks_of(it.q0);
+    it.nkv1 = blocks_of(it.q0 + BQ);  // 0 = tile beyond the sequence
+    it.tok0 = it.b * p.S;
+    return it;
+  };
 
+  if (threadIdx.x == 0) CTA_TRACE(0);
+  if (threadIdx.x == 0) TRACE(8000);
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
+    mbar_init(q_empty, 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&k_full[i], 1);
       mbar_init(&v_full[i], 1);
@@ -480,6 +528,7 @@ __global__ void __launch_bounds__(FWD2_THREADS, 1)
       mbar_init(&s_full[i], 1);
       mbar_init(&p_full[i], 128);
       mbar_init(&o_done[i], 1);
+      mbar_init(&o_free[i], 128);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     fence_async_smem();
@@ -492,29 +541,37 @@ __global__ void __launch_bounds__(FWD2_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) TRACE(8001);
   if (warp == 0) {
     if (lane == 0) {
-      const int nq = nkv1 > 0 ? 2 : 1;
-      mbar_expect_tx(q_full, nq * TILE_BYTES);
-      for (int t = 0; t < nq; ++t)
+      uint32_t kv = 0;  // K/V blocks loaded so far (ring stage and parity)
+      int n_it = 0;
+      for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++n_it) {
+        const Item I = decode(w);
+        mbar_wait(q_empty, (n_it & 1) ^ 1);
+        const int nq = I.nkv1 > 0 ? 2 : 1;
+        mbar_expect_tx(q_full, nq * TILE_BYTES);
+        for (int t = 0; t < nq; ++t)
 #pragma unroll
-        for (int c = 0; c < D / 64; ++c)
-          tma_load_3d(&mq, q_full, sm + L::Q + t * L::TILE + c * 16384, c * 64, h,
-                      tok0 + q0 + t * BQ);
-      for (int j = 0; j < n_kv; ++j) {
-        const int st = j & 1;
-        mbar_wait(&k_empty[st], ((j >> 1) & 1) ^ 1);
-        mbar_expect_tx(&k_full[st], TILE_BYTES);
+          for (int c = 0; c < D / 64; ++c)
+            tma_load_3d(&mq, q_full, sm + L::Q + t * L::TILE + c * 16384, c * 64, I.h,
+                        I.tok0 + I.q0 + t * BQ);
+        const int n_kv = max(I.nkv0, I.nkv1);
+        for (int j = 0; j < n_kv; ++j, ++kv) {
+          const int st = kv & 1;
+          mbar_wait(&k_empty[st], ((kv >> 1) & 1) ^ 1);
+          mbar_expect_tx(&k_full[st], TILE_BYTES);
 #pragma unroll
-        for (int c = 0; c < D / 64; ++c)
-          tma_load_3d(&mk, &k_full[st], sm + L::K0 + st * L::TILE + c * 16384, c * 64, h,
-                      tok0 + j * BKV);
-        mbar_wait(&v_empty[st], ((j >> 1) & 1) ^ 1);
-        mbar_expect_tx(&v_full[st], TILE_BYTES);
+          for (int c = 0; c < D / 64; ++c)
+            tma_load_3d(&mk, &k_full[st], sm + L::K0 + st * L::TILE + c * 16384, c * 64, I.h,
+                        I.tok0 + j * BKV);
+          mbar_wait(&v_empty[st], ((kv >> 1) & 1) ^ 1);
+          mbar_expect_tx(&v_full[st], TILE_BYTES);
 #pragma unroll
-        for (int c = 0; c < D / 64; ++c)
-          tma_load_3d(&mv, &v_full[st], sm + L::V0 + st * L::TILE + c * 16384, c * 64, h,
-                      tok0 + j * BKV);
+          for (int c = 0; c < D / 64; ++c)
+            tma_load_3d(&mv, &v_full[st], sm + L::V0 + st * L::TILE + c * 16384, c * 64, I.h,
+                        I.tok0 + j * BKV);
+        }
       }
     }
   } else if (warp == 1) {
@@ -523,57 +580,81 @@ __global__ void __launch_bounds__(FWD2_THREADS, 1)
     const uint64_t d_q = sdesc(smem_u32(sm + L::Q), 16, 1024);
     const uint64_t d_k = sdesc(smem_u32(sm + L::K0), 16, 1024);
     const uint64_t d_v = sdesc(smem_u32(sm + L::V0), 16384, 1024);
-    mbar_wait_fast(q_full, 0);
-    auto issue_s = [&](int t, int j) {
-      const int st = j & 1;
-      if (lane == 0) TRACE(4096 + t * 1024 + j * 8 + 0);
-      mbar_wait_fast(&k_full[st], (j >> 1) & 1);
-      tc_fence_after();
-      if (lane == 0) TRACE(4096 + t * 1024 + j * 8 + 1);
-      const uint64_t bk = d_k + (uint64_t)((st * L::TILE) >> 4);
-      const uint64_t bq = d_q + (uint64_t)((t * L::TILE) >> 4);
-      if (elect_one()) {
+    uint32_t kv0 = 0;                        // first K/V block of the item (ring position)
+    uint32_t base0 = 0, base1 = 0;           // blocks of tile 0 / 1 in earlier items
+    uint32_t done0 = 0, done1 = 0;           // earlier items with a tile-0 / tile-1 epilogue
+    int n_it = 0;
+    for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++n_it) {
+      const Item I = decode(w);
+      const int nkv0 = I.nkv0, nkv1 = I.nkv1, n_kv = max(nkv0, nkv1);
+      mbar_wait_fast(q_full, n_it & 1);
+      if (lane == 0) TRACE(8002);
+      // the last S MMA of the item reads Q for the last time (S_1 when tile 1 exists)
+      const int last_t = nkv1 > 0 ? 1 : 0, last_j = (last_t ? nkv1 : nkv0) - 1;
+      auto issue_s = [&](int t, int j) {
+        const uint32_t g = kv0 + j;
+        const int st = g & 1;
+        if (lane == 0) TRACE(4096 + t * 1024 + j * 8 + 0);
+        mbar_wait_fast(&k_full[st], (g >> 1) & 1);
+        tc_fence_after();
+        if (lane == 0) TRACE(4096 + t * 1024 + j * 8 + 1);
+        const uint64_t bk = d_k + (uint64_t)((st * L::TILE) >> 4);
+        const uint64_t bq = d_q + (uint64_t)((t * L::TILE) >> 4);
+        if (elect_one()) {
 #pragma unroll
-        for (int k = 0; k < D / 16; ++k) {
-          const uint64_t off = (uint64_t)(((k >> 2) * 16384 + (k & 3) * 32) >> 4);
-          umma_bf16(tmem + t * 128, bq + off, bk + off, id_s, k != 0);
+          for (int k = 0; k < D / 16; ++k) {
+            const uint64_t off = (uint64_t)(((k >> 2) * 16384 + (k & 3) * 32) >> 4);
+            umma_bf16(tmem + t * 128, bq + off, bk + off, id_s, k != 0);
+          }
+          umma_commit(&s_full[t]);
+          if (t == 1 || j >= nkv1) umma_commit(&k_empty[st]);  // last reader of K_j
+          if (t == last_t && j == last_j) umma_commit(q_empty);
         }
-        umma_commit(&s_full[t]);
-        if (t == 1 || j >= nkv1) umma_commit(&k_empty[st]);  // last reader of K_j
-      }
-      __syncwarp();
-    };
-    auto issue_pv = [&](int t, int j) {
-      const int st = j & 1;
-      if (lane == 0) TRACE(4096 + t * 1024 + j * 8 + 2);
-      mbar_wait_fast(&p_full[t], j & 1);
-      if (lane == 0) TRACE(4096 + t * 1024 + j * 8 + 3);
-      mbar_wait_fast(&v_full[st], (j >> 1) & 1);
-      tc_fence_after();
-      if (lane == 0) TRACE(4096 + t * 1024 + j * 8 + 4);
-      const uint64_t bv = d_v + (uint64_t)((st * L::TILE) >> 4);
-      const uint32_t t_o = tmem + 256 + t * 128, t_p = tmem + t * 128;
-      if (elect_one()) {
+        __syncwarp();
+      };
+      auto issue_pv = [&](int t, int j) {
+        const uint32_t g = kv0 + j;
+        const int st = g & 1;
+        const uint32_t bt = (t ? base1 : base0) + j;
+        if (lane == 0) TRACE(4096 + t * 1024 + j * 8 + 2);
+        if (j == 0) {  // O_t is overwritten: the previous item's epilogue must have read it
+          const uint32_t dn = t ? done1 : done0;
+          if (dn > 0) mbar_wait_fast(&o_free[t], (dn - 1) & 1);
+        }
+        mbar_wait_fast(&p_full[t], bt & 1);
+        if (lane == 0) TRACE(4096 + t * 1024 + j * 8 + 3);
+        mbar_wait_fast(&v_full[st], (g >> 1) & 1);
+        tc_fence_after();
+        if (lane == 0) TRACE(4096 + t * 1024 + j * 8 + 4);
+        const uint64_t bv = d_v + (uint64_t)((st * L::TILE) >> 4);
+        const uint32_t t_o = tmem + 256 + t * 128, t_p = tmem + t * 128;
+        if (elect_one()) {
 #pragma unroll
-        for (int k = 0; k < BKV / 16; ++k)
-          umma_bf16_ts(t_o, t_p + (k >> 2) * 64 + (k & 3) * 8,
-                       bv + (uint64_t)((k * 2048) >> 4), id_o, (j | k) != 0);
-        umma_commit(&o_done[t]);
-        if (t == 1 || j >= nkv1) umma_commit(&v_empty[st]);  // last reader of V_j
+          for (int k = 0; k < BKV / 16; ++k)
+            umma_bf16_ts(t_o, t_p + (k >> 2) * 64 + (k & 3) * 8,
+                         bv + (uint64_t)((k * 2048) >> 4), id_o, (j | k) != 0);
+          umma_commit(&o_done[t]);
+          if (t == 1 || j >= nkv1) umma_commit(&v_empty[st]);  // last reader of V_j
+        }
+        __syncwarp();
+      };
+      if (nkv0 > 0) issue_s(0, 0);
+      if (nkv1 > 0) issue_s(1, 0);
+      for (int j = 0; j < n_kv; ++j) {
+        if (j < nkv0) {
+          issue_pv(0, j);
+          if (j + 1 < nkv0) issue_s(0, j + 1);
+        }
+        if (j < nkv1) {
+          issue_pv(1, j);
+          if (j + 1 < nkv1) issue_s(1, j + 1);
+        }
       }
-      __syncwarp();
-    };
-    if (nkv0 > 0) issue_s(0, 0);
-    if (nkv1 > 0) issue_s(1, 0);
-    for (int j = 0; j < n_kv; ++j) {
-      if (j < nkv0) {
-        issue_pv(0, j);
-        if (j + 1 < nkv0) issue_s(0, j + 1);
-      }
-      if (j < nkv1) {
-        issue_pv(1, j);
-        if (j + 1 < nkv1) issue_s(1, j + 1);
-      }
+      kv0 += n_kv;
+      base0 += nkv0;
+      base1 += nkv1;
+      done0 += nkv0 > 0;
+      done1 += nkv1 > 0;
     }
   } else if (warp >= 4) {
     // softmax: one thread per query row (warp % 4 = TMEM lane quarter), all 128 key columns
@@ -582,125 +663,137 @@ __global__ void __launch_bounds__(FWD2_THREADS, 1)
     const int t = (warp - 4) >> 2;              // tile
     const int q = warp & 3;
     const int r = q * 32 + lane;
-    const int qt = q0 + t * BQ, qi = qt + r;
-    const int n_t = t == 0 ? nkv0 : nkv1;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     const uint32_t t_s = tmem + t * 128, t_o = tmem + 256 + t * 128;
-    float m_used = -INFINITY, l = 0.f;
     const bool tr = (warp == 4 || warp == 8) && lane == 0;
-    for (int j = 0; j < n_t; ++j) {
-      if (tr) TRACE(t * 1024 + j * 8 + 0);
-      mbar_wait(&s_full[t], j & 1);
-      tc_fence_after();
-      if (tr) TRACE(t * 1024 + j * 8 + 1);
-      float s[BKV];
-#pragma unroll
-      for (int c = 0; c < BKV / 32; ++c)
-        tmem_ld32_nowait(t_s + c * 32 + lane_off, reinterpret_cast<uint32_t*>(s) + c * 32);
-      tmem_wait_ld();
-      const int k0 = j * BKV;
-      const bool mask = (k0 + BKV > p.S) || (p.causal && k0 + BKV - 1 > qt);
-      if (mask) {  // diagonal / tail block: keys >= lim are invisible to this row
-        const int lim = (p.causal ? min(p.S, qi + 1) : p.S) - k0;
-#pragma unroll
-        for (int i = 0; i < BKV; ++i) s[i] = i < lim ? s[i] : -INFINITY;
-      }
-      float m8[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) m8[u] = s[u];
-#pragma unroll
-      for (int i = 8; i < BKV; ++i) m8[i & 7] = fmaxf(m8[i & 7], s[i]);
-      float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
-                       fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
-      if (tr) TRACE(t * 1024 + j * 8 + 2);
-      mx *= p.scale_log2;
-      float alpha = 1.f;
-      if ((mx > m_used + RESCALE_THRESHOLD || m_used == -INFINITY) && mx != -INFINITY) {
-        alpha = (m_used == -INFINITY) ? 0.f : exp2f(m_used - mx);
-        m_used = mx;
-      }
-      const float mu = (m_used == -INFINITY) ? 0.f : m_used;
-      float r4[4] = {0.f, 0.f, 0.f, 0.f};
-      // P in chunks of 16 keys -> 8 packed bf16x2 columns, placed where the PV MMA reads
-      // its A operand: keys 16c.. at column 64*(c/4) + 8*(c%4) of the tile's S columns
-#pragma unroll
-      for (int c = 0; c < BKV / 16; ++c) {
-        uint32_t pk[8];
-        uint32_t keep = 0xFFFFu;  // dropout: keep bits of the chunk's 16 keys
-        if constexpr (DROP) {
-          keep = 0;
-#pragma unroll
-          for (int g = 0; g < 4; ++g)
-            keep |= dropout_keep4(p.drop, b, h, qi, k0 + c * 16 + g * 4) << (4 * g);
-        }
-#pragma unroll
-        for (int i = 0; i < 16; i += 2) {
-          const int e = c * 16 + i;
-          // all exponentials on MUFU: moving 1/4 or 1/2 of them to an FMA-pipe polynomial
-          // measured 4-14 % slower (D 64 and 128, two-threads-per-row variant)
-          constexpr int PE = D == 64 ? ATTN_POLY64 : 0;
-          const bool poly = PE > 0 && ((i >> 1) % (PE > 0 ? PE : 1)) == (PE > 0 ? PE : 1) - 1;
-          const float x0 = fmaf(s[e], p.scale_log2, -mu), x1 = fmaf(s[e + 1], p.scale_log2, -mu);
-          const float p0 = poly ? exp2_poly3(x0) : exp2_mufu(x0);
-          const float p1 = poly ? exp2_poly3(x1) : exp2_mufu(x1);
-          r4[(i >> 1) & 3] += p0 + p1;  // the normalizer uses the undropped probabilities
-          if constexpr (DROP)
-            pk[i / 2] = pack2((keep >> i) & 1u ? p0 : 0.f, (keep >> (i + 1)) & 1u ? p1 : 0.f);
-          else
-            pk[i / 2] = pack2(p0, p1);
-        }
-        tmem_st8(t_s + (c >> 2) * 64 + (c & 3) * 8 + lane_off, pk);
-      }
-      l = l * alpha + ((r4[0] + r4[1]) + (r4[2] + r4[3]));
-      tmem_wait_st();
-      if (tr) TRACE(t * 1024 + j * 8 + 4);
-      // lazy rescale of O (after P is out of registers): O must hold PV(j-1) first; o_done
-      // has completed j-1 or j phases here (PV(j) needs this P), so the parity wait is exact
-      if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
-        mbar_wait(&o_done[t], (j - 1) & 1);
+    uint32_t base = 0;  // blocks of this tile in earlier items (barrier parities)
+    for (int w = blockIdx.x; w < n_items; w += gridDim.x) {
+      const Item I = decode(w);
+      const int b = I.b, h = I.h, tok0 = I.tok0;
+      const int qt = I.q0 + t * BQ, qi = qt + r;
+      const int n_t = t == 0 ? I.nkv0 : I.nkv1;
+      float m_used = -INFINITY, l = 0.f;
+      for (int j = 0; j < n_t; ++j) {
+        const uint32_t bt = base + j;
+        if (tr) TRACE(t * 1024 + j * 8 + 0);
+        mbar_wait(&s_full[t], bt & 1);
         tc_fence_after();
+        if (tr) TRACE(t * 1024 + j * 8 + 1);
+        float s[BKV];
+#pragma unroll
+        for (int c = 0; c < BKV / 32; ++c)
+          tmem_ld32_nowait(t_s + c * 32 + lane_off, reinterpret_cast<uint32_t*>(s) + c * 32);
+        tmem_wait_ld();
+        const int k0 = j * BKV;
+        const bool mask = (k0 + BKV > p.S) || (p.causal && k0 + BKV - 1 > qt);
+        if (mask) {  // diagonal / tail block: keys >= lim are invisible to this row
+          const int lim = (p.causal ? min(p.S, qi + 1) : p.S) - k0;
+#pragma unroll
+          for (int i = 0; i < BKV; ++i) s[i] = i < lim ? s[i] : -INFINITY;
+        }
+        float m8[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) m8[u] = s[u];
+#pragma unroll
+        for (int i = 8; i < BKV; ++i) m8[i & 7] = fmaxf(m8[i & 7], s[i]);
+        float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
+                         fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
+        if (tr) TRACE(t * 1024 + j * 8 + 2);
+        mx *= p.scale_log2;
+        float alpha = 1.f;
+        if ((mx > m_used + RESCALE_THRESHOLD || m_used == -INFINITY) && mx != -INFINITY) {
+          alpha = (m_used == -INFINITY) ? 0.f : exp2f(m_used - mx);
+          m_used = mx;
+        }
+        const float mu = (m_used == -INFINITY) ? 0.f : m_used;
+        float r4[4] = {0.f, 0.f, 0.f, 0.f};
+        // P in chunks of 16 keys -> 8 packed bf16x2 columns, placed where the PV MMA reads
+        // its A operand: keys 16c.. at column 64*(c/4) + 8*(c%4) of the tile's S columns
+#pragma unroll
+        for (int c = 0; c < BKV / 16; ++c) {
+          uint32_t pk[8];
+          uint32_t keep = 0xFFFFu;  // dropout: keep bits of the chunk's 16 keys
+          if constexpr (DROP) {
+            keep = 0;
+#pragma unroll
+            for (int g = 0; g < 4; ++g)
+              keep |= dropout_keep4(p.drop, b, h, qi, k0 + c * 16 + g * 4) << (4 * g);
+          }
+#pragma unroll
+          for (int i = 0; i < 16; i += 2) {
+            const int e = c * 16 + i;
+            // all exponentials on MUFU: moving 1/4 or 1/2 of them to an FMA-pipe polynomial
+            // measured 4-14 % slower (D 64 and 128, two-threads-per-row variant)
+            constexpr int PE = D == 64 ? ATTN_POLY64 : 0;
+            const bool poly = PE > 0 && ((i >> 1) % (PE > 0 ? PE : 1)) == (PE > 0 ? PE : 1) - 1;
+            const float x0 = fmaf(s[e], p.scale_log2, -mu), x1 = fmaf(s[e + 1], p.scale_log2, -mu);
+            const float p0 = poly ? exp2_poly3(x0) : exp2_mufu(x0);
+            const float p1 = poly ? exp2_poly3(x1) : exp2_mufu(x1);
+            r4[(i >> 1) & 3] += p0 + p1;  // the normalizer uses the undropped probabilities
+            if constexpr (DROP)
+              pk[i / 2] = pack2((keep >> i) & 1u ? p0 : 0.f, (keep >> (i + 1)) & 1u ? p1 : 0.f);
+            else
+              pk[i / 2] = pack2(p0, p1);
+          }
+          tmem_st8(t_s + (c >> 2) * 64 + (c & 3) * 8 + lane_off, pk);
+        }
+        l = l * alpha + ((r4[0] + r4[1]) + (r4[2] + r4[3]));
+        tmem_wait_st();
+        if (tr) TRACE(t * 1024 + j * 8 + 4);
+        // lazy rescale of O (after P is out of registers): O must hold PV(j-1) first; o_done
+        // has completed j-1 or j phases here (PV(j) needs this P), so the parity wait is exact
+        if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
+          mbar_wait(&o_done[t], (bt - 1) & 1);
+          tc_fence_after();
+#pragma unroll 1
+          for (int c = 0; c < D / 32; ++c) {
+            uint32_t ov[32];
+            const uint32_t ta = t_o + c * 32 + lane_off;
+            tmem_ld32(ta, ov);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * alpha);
+            tmem_st32(ta, ov);
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(&p_full[t]);
+        if (tr) TRACE(t * 1024 + j * 8 + 5);
+      }
+      if (tr) TRACE(8003 + 2 * t);
+      if (n_t > 0) {
+        mbar_wait(&o_done[t], (base + n_t - 1) & 1);
+        tc_fence_after();
+        // dropout: kept probabilities carry 1 / (1 - p)
+        const float inv_l = l > 0.f ? (DROP ? p.drop.inv_keep : 1.f) / l : 0.f;
+        __nv_bfloat16* orow = p.o + (long long)(tok0 + qi) * p.o_st + (long long)h * p.sh;
 #pragma unroll 1
         for (int c = 0; c < D / 32; ++c) {
           uint32_t ov[32];
-          const uint32_t ta = t_o + c * 32 + lane_off;
-          tmem_ld32(ta, ov);
+          tmem_ld32(t_o + c * 32 + lane_off, ov);
+          if (qi < p.S) {
 #pragma unroll
-          for (int i = 0; i < 32; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * alpha);
-          tmem_st32(ta, ov);
-        }
-      }
-      tc_fence_before();
-      mbar_arrive(&p_full[t]);
-      if (tr) TRACE(t * 1024 + j * 8 + 5);
-    }
-    if (n_t > 0) {
-      mbar_wait(&o_done[t], (n_t - 1) & 1);
-      tc_fence_after();
-      // dropout: kept probabilities carry 1 / (1 - p)
-      const float inv_l = l > 0.f ? (DROP ? p.drop.inv_keep : 1.f) / l : 0.f;
-      __nv_bfloat16* orow = p.o + (long long)(tok0 + qi) * p.o_st + (long long)h * p.sh;
-#pragma unroll 1
-      for (int c = 0; c < D / 32; ++c) {
-        uint32_t ov[32];
-        tmem_ld32(t_o + c * 32 + lane_off, ov);
-        if (qi < p.S) {
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            uint4 w;
-            w.x = pack2(__uint_as_float(ov[u * 8 + 0]) * inv_l, __uint_as_float(ov[u * 8 + 1]) * inv_l);
-            w.y = pack2(__uint_as_float(ov[u * 8 + 2]) * inv_l, __uint_as_float(ov[u * 8 + 3]) * inv_l);
-            w.z = pack2(__uint_as_float(ov[u * 8 + 4]) * inv_l, __uint_as_float(ov[u * 8 + 5]) * inv_l);
-            w.w = pack2(__uint_as_float(ov[u * 8 + 6]) * inv_l, __uint_as_float(ov[u * 8 + 7]) * inv_l);
-            *reinterpret_cast<uint4*>(orow + c * 32 + u * 8) = w;
+            for (int u = 0; u < 4; ++u) {
+              uint4 v;
+              v.x = pack2(__uint_as_float(ov[u * 8 + 0]) * inv_l, __uint_as_float(ov[u * 8 + 1]) * inv_l);
+              v.y = pack2(__uint_as_float(ov[u * 8 + 2]) * inv_l, __uint_as_float(ov[u * 8 + 3]) * inv_l);
+              v.z = pack2(__uint_as_float(ov[u * 8 + 4]) * inv_l, __uint_as_float(ov[u * 8 + 5]) * inv_l);
+              v.w = pack2(__uint_as_float(ov[u * 8 + 6]) * inv_l, __uint_as_float(ov[u * 8 + 7]) * inv_l);
+              *reinterpret_cast<uint4*>(orow + c * 32 + u * 8) = v;
+            }
           }
         }
+        tc_fence_before();
+        mbar_arrive(&o_free[t]);  // O_t may now be overwritten by the next item's PV
+        if (qi < p.S)
+          p.lse[((long long)b * p.H + h) * p.S + qi] = (m_used + log2f(l)) * 0.6931471805599453f;
       }
-      if (qi < p.S)
-        p.lse[((long long)b * p.H + h) * p.S + qi] = (m_used + log2f(l)) * 0.6931471805599453f;
+      if (tr) TRACE(8004 + 2 * t);
+      base += n_t;
     }
   }
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) CTA_TRACE(1);
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
@@ -1823,6 +1916,26 @@ static bool fwd_two_tiles() {
   return two;
 }
 
+// Forward CTA count: persistent CTAs (one per SM) for short sequences, one CTA per work item
+// otherwise.  Measured (same box, `profiles/r02/attention/persistent/`): B16 S1024 H16 D64
+// 141 -> 120 us, B8 S2048 H16 D64 190-196 -> 184 us, but B2 S4096 H32 D128 280 -> 292 and
+// B1 S32768 H8 1884 -> 2000+ (the static round-robin of long items balances worse than the
+// hardware block scheduler).  GALV_ATTN_FWD_CTAS overrides (0 = one CTA per item).
+static int fwd_ctas(int64_t S) {
+  static const int env = [] {
+    const char* e = getenv("GALV_ATTN_FWD_CTAS");
+    return e ? atoi(e) : -1;
+  }();
+  if (env >= 0) return env;
+  static const int sms = [] {
+    int dev = 0, n = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n;
+  }();
+  return S <= ATTN_FWD_PERSIST_MAX_S ? sms : 0;
+}
+
 // GALV_ATTN_DKDV=1 selects the 64-query-step dK/dV kernel (bwd_dkdv_tc) for A/B runs
 static bool dkdv_64q_steps() {
   static const bool old = [] {
@@ -1877,7 +1990,10 @@ int32_t attn_fwd_sm100(const void* q, const void* k, const void* v, void* o, flo
   int32_t rc;
   // default: the two-Q-tile kernel (fwd_tc2); dropout is implemented there only
   if (fwd_two_tiles() || p.drop.thresh != 0) {
-    const dim3 grid2((unsigned)(B * H), (unsigned)((p.n_qblocks + 1) / 2));
+    p.bh_total = (int)(B * H);
+    const long long n_items = (long long)p.bh_total * ((p.n_qblocks + 1) / 2);
+    const int ctas = fwd_ctas(S);
+    const dim3 grid2((unsigned)(ctas > 0 ? std::min<long long>(n_items, ctas) : n_items));
     const bool drop = p.drop.thresh != 0;
     auto kern = D == 128 ? (drop ? fwd_tc2<128, true> : fwd_tc2<128, false>)
                          : (drop ? fwd_tc2<64, true> : fwd_tc2<64, false>);
@@ -1902,6 +2018,9 @@ int32_t attn_fwd_sm100(const void* q, const void* k, const void* v, void* o, flo
 #ifdef GALV_ATTN_TRACE
 extern "C" int32_t galv_attn_trace_read(void* host) {
   return (int32_t)cudaMemcpyFromSymbol(host, fa::g_trace, sizeof(fa::g_trace));
+}
+extern "C" int32_t galv_attn_cta_trace_read(void* host) {
+  return (int32_t)cudaMemcpyFromSymbol(host, fa::g_cta, sizeof(fa::g_cta));
 }
 #endif
 
