@@ -811,33 +811,50 @@ __global__ void __launch_bounds__(FWD2_THREADS, 1)
 // lse*log2(e) and D = rowsum(dO*O) come from a padded workspace written by bwd_prep
 // (padded rows: lse2 = +inf so their P is exactly 0).
 
-// one warp handles 2 rows of D <= 128 (16 lanes x 8 elements per row, 16-byte loads)
-__global__ void bwd_prep(const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ dout,
-                         const float* __restrict__ lse, float* __restrict__ lse2,
-                         float* __restrict__ dvec, int S, int S_pad, int H, int D, long long ost,
-                         long long sh) {
-  const int lane = threadIdx.x & 31;
-  const long long row = ((long long)blockIdx.x * 4 + (threadIdx.x >> 5)) * 2 + (lane >> 4);
-  const int sub = lane & 15;
-  const int bh = (int)(row / S_pad), i = (int)(row % S_pad);
-  const int b = bh / H, h = bh % H;
-  float s = 0.f;
-  if (i < S) {
-    const __nv_bfloat16* orow = o + ((long long)b * S + i) * ost + (long long)h * sh;
-    const __nv_bfloat16* drow = dout + ((long long)b * S + i) * ost + (long long)h * sh;
-    for (int d = sub * 8; d < D; d += 128) {
-      float a[8], c[8];
-      load16(orow + d, a);
-      load16(drow + d, c);
+// D = rowsum(dO * O) and lse * log2(e) per (batch*head, query) row into the padded workspace.
+// D/8 lanes per row (one 16-byte load of O and of dO each), 32/(D/8) rows per warp, and
+// PREP_ROWS row groups per warp with every load issued before the first use (HBM-bound:
+// 2*D*2 bytes read per row; the one-group-per-warp version ran at ~2 TB/s at D=64).
+constexpr int PREP_ROWS = 4;
+template <int D>
+__global__ void __launch_bounds__(256) bwd_prep(const __nv_bfloat16* __restrict__ o,
+                                                const __nv_bfloat16* __restrict__ dout,
+                                                const float* __restrict__ lse,
+                                                float* __restrict__ lse2, float* __restrict__ dvec,
+                                                int S, int S_pad, int H, long long n_rows,
+                                                long long ost, long long sh) {
+  constexpr int LPR = D / 8, RPW = 32 / LPR;  // lanes per row, rows per warp
+  const int lane = threadIdx.x & 31, sub = lane % LPR;
+  const long long warp_id = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const long long row0 = warp_id * (RPW * PREP_ROWS) + lane / LPR;
+  float a[PREP_ROWS][8], c[PREP_ROWS][8];
+  bool ok[PREP_ROWS];
 #pragma unroll
-      for (int e = 0; e < 8; ++e) s += a[e] * c[e];
+  for (int u = 0; u < PREP_ROWS; ++u) {
+    const long long row = row0 + u * RPW;
+    const int bh = (int)(row / S_pad), i = (int)(row - (long long)bh * S_pad);
+    ok[u] = row < n_rows && i < S;
+    if (ok[u]) {
+      const long long off = ((long long)(bh / H) * S + i) * ost + (long long)(bh % H) * sh + sub * 8;
+      load16(o + off, a[u]);
+      load16(dout + off, c[u]);
     }
   }
 #pragma unroll
-  for (int off = 8; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-  if (sub == 0) {
-    dvec[row] = i < S ? s : 0.f;
-    lse2[row] = i < S ? lse[(long long)bh * S + i] * LOG2E : INFINITY;
+  for (int u = 0; u < PREP_ROWS; ++u) {
+    const long long row = row0 + u * RPW;
+    float s = 0.f;
+    if (ok[u]) {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) s += a[u][e] * c[u][e];
+    }
+#pragma unroll
+    for (int off = LPR / 2; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    if (sub == 0 && row < n_rows) {
+      const int bh = (int)(row / S_pad), i = (int)(row - (long long)bh * S_pad);
+      dvec[row] = i < S ? s : 0.f;
+      lse2[row] = i < S ? lse[(long long)bh * S + i] * LOG2E : INFINITY;
+    }
   }
 }
 
@@ -859,6 +876,8 @@ struct BwdParams {
   long long st, sh;    // output (q layout) strides
   const float* rope;   // optional fp32 [2][S][D/2] cos|sin planes: inverse RoPE on dq / dk
   DropoutParams drop;  // attention-probability dropout (thresh 0 = off)
+  int bh_total;        // batch * heads (work-item decode)
+  int persist;         // 1: persistent CTAs (heaviest item first, (batch, head) fastest)
 };
 
 template <int D>
@@ -1234,11 +1253,11 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
 // (B2 S4096 H32: 941-958 vs 921 us, B4 S8192 H16: 3785-4110 vs 3627 us): a key (query)
 // block sweeps every query (key) block of its head, and with the blocks of one head running
 // side by side those sweeps share L2.  0 = block index fastest (heaviest-first per head).
-// Two MMA-issuing warps for the dK/dV kernel (see the chain comment in bwd_dkdv2_tc):
-// measured slower (B2 S4096 H32 936 vs 884 us, period 3196 vs ~2730 cycles) -- the tensor
-// pipe then interleaves dP(it+1) ahead of S(it+1) and phase 1 starts later.  Off.
-#ifndef DKDV_TWO_ISSUERS
-#define DKDV_TWO_ISSUERS 0
+// (Two MMA-issuing warps for the dK/dV kernel, chain A = dV, S and chain B = dK, dP on
+// disjoint TMEM, measured slower: 936 vs 884 us at B2 S4096 H32 -- the tensor pipe then runs
+// dP(it+1) ahead of S(it+1).  profiles/r02/attention/bwd2/.)
+#ifndef ATTN_BWD_PERSIST_MAX_S
+#define ATTN_BWD_PERSIST_MAX_S 2048
 #endif
 #ifndef DKDV_GRID_BH_FAST
 #define DKDV_GRID_BH_FAST 0
@@ -1259,50 +1278,78 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
 template <int D>
 struct SmemKV2 {
   static constexpr int NST = 2;
-  static constexpr int KT = D * 128 * 2;  // every tile is 128 rows x D
-  static constexpr int K = 0, V = KT, Q0 = 2 * KT, O0 = Q0 + NST * KT;
+  static constexpr int KVB = D == 64 ? 2 : 1;  // K/V buffers (persistent CTAs prefetch the next item's)
+  static constexpr int KT = D * 128 * 2;       // every tile is 128 rows x D
+  static constexpr int KV = 0, Q0 = KVB * 2 * KT, O0 = Q0 + NST * KT;
   static constexpr int LSE = O0 + NST * KT, DV = LSE + NST * 512;
   static constexpr int BAR = DV + NST * 512;
   static constexpr int BYTES = BAR + 256 + 1024;
 };
 
+// Work items (key block, batch*head): one per CTA, or persistent CTAs looping over items c,
+// c + gridDim.x, ... (short sequences; see bwd_ctas).  Persistent order is heaviest key block
+// first with (batch, head) fastest (balanced round-robin); one-per-CTA order is key block
+// fastest (the head's sweeps share L2, DKDV_GRID_BH_FAST).  Between items, the K/V buffers
+// are handed over by kv_empty / kv_full and the dK/dV accumulators by acc_free (the
+// epilogue has read them); every per-step barrier's parity runs on the CTA's global step count.
 template <int D, bool DROP>
 __global__ void __launch_bounds__(BWD_THREADS, 1)
     bwd_dkdv2_tc(const __grid_constant__ CUtensorMap mq, const __grid_constant__ CUtensorMap mk,
                  const __grid_constant__ CUtensorMap mv, const __grid_constant__ CUtensorMap mdo,
                  const BwdParams p) {
   using L = SmemKV2<D>;
-  constexpr int NST = L::NST;
+  constexpr int NST = L::NST, KVB = L::KVB;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::BAR);
-  uint64_t* kv_full = bar + 0;
-  uint64_t* q_full = bar + 1;         // [NST] Q tile + lse2 / D vectors
-  uint64_t* q_empty = q_full + NST;   // [NST]
-  uint64_t* o_full = q_empty + NST;   // [NST] dO tile
-  uint64_t* o_empty = o_full + NST;   // [NST]
-  uint64_t* s_full = o_empty + NST;   // S^T(it) complete
-  uint64_t* dp_full = s_full + 1;     // dP^T(it) complete
-  uint64_t* p_full = dp_full + 1;     // [2] P^T(it) query half packed (all math threads)
-  uint64_t* ds_full = p_full + 2;     // [2] dS^T(it) query half packed (all math threads)
-  uint64_t* mm_done = ds_full + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mm_done + 1);
+  uint64_t* kv_full = bar + 0;          // [KVB]
+  uint64_t* kv_empty = kv_full + KVB;   // [KVB]
+  uint64_t* q_full = kv_empty + KVB;    // [NST] Q tile + lse2 / D vectors
+  uint64_t* q_empty = q_full + NST;     // [NST]
+  uint64_t* o_full = q_empty + NST;     // [NST] dO tile
+  uint64_t* o_empty = o_full + NST;     // [NST]
+  uint64_t* s_full = o_empty + NST;     // S^T(it) complete
+  uint64_t* dp_full = s_full + 1;       // dP^T(it) complete
+  uint64_t* p_full = dp_full + 1;       // [2] P^T(it) query half packed (all math threads)
+  uint64_t* ds_full = p_full + 2;       // [2] dS^T(it) query half packed (all math threads)
+  uint64_t* mm_done = ds_full + 2;      // the item's last dK / dV MMA complete
+  uint64_t* acc_free = mm_done + 1;     // the item's epilogue has read dK / dV
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_free + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // causal: low key blocks carry the most query blocks (see DKDV_GRID_BH_FAST)
-  const int kb = DKDV_GRID_BH_FAST ? blockIdx.y : blockIdx.x;
-  const int bh = DKDV_GRID_BH_FAST ? blockIdx.x : blockIdx.y, b = bh / p.H, h = bh % p.H;
-  const int k0 = kb * 128, tok0 = b * p.S;
   const int n_qb = (p.S + 127) / 128;
-  const int i0 = p.causal ? kb : 0;
-  const int n_it = n_qb - i0;
+  const int n_items = n_qb * p.bh_total;
+  struct Item {
+    int b, h, bh, k0, i0, n_it, tok0;
+  };
+  auto decode = [&](int w) {
+    Item I;
+    int kb;
+    if (p.persist || DKDV_GRID_BH_FAST) {
+      kb = w / p.bh_total;
+      I.bh = w % p.bh_total;
+    } else {
+      kb = w % n_qb;
+      I.bh = w / n_qb;
+    }
+    I.b = I.bh / p.H;
+    I.h = I.bh % p.H;
+    I.k0 = kb * 128;
+    I.i0 = p.causal ? kb : 0;  // causal: low key blocks carry the most query blocks
+    I.n_it = n_qb - I.i0;
+    I.tok0 = I.b * p.S;
+    return I;
+  };
   if (threadIdx.x == 0) TRACE(4096 + 16 * 64 + 3);
   if (threadIdx.x == 0) {
-    mbar_init(kv_full, 1);
+    for (int i = 0; i < KVB; ++i) {
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+    }
     for (int i = 0; i < NST; ++i) {
       mbar_init(&q_full[i], 1);
       mbar_init(&q_empty[i], 1);
       mbar_init(&o_full[i], 1);
-      mbar_init(&o_empty[i], DKDV_TWO_ISSUERS ? 2 : 1);  // dV(it) [+ dP(it) from warp 2]
+      mbar_init(&o_empty[i], 1);
     }
     mbar_init(s_full, 1);
     mbar_init(dp_full, 1);
@@ -1310,7 +1357,8 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       mbar_init(&p_full[i], 128 * BWD_SPLIT);
       mbar_init(&ds_full[i], 128 * BWD_SPLIT);
     }
-    mbar_init(mm_done, DKDV_TWO_ISSUERS ? 2 : 1);
+    mbar_init(mm_done, 1);
+    mbar_init(acc_free, 128 * BWD_SPLIT);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     fence_async_smem();
   }
@@ -1320,155 +1368,178 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t t_dp = tmem + 128, t_dv = tmem + 256, t_dk = tmem + 256 + D;
-  const float* lse2_g = p.lse2 + (long long)bh * p.S_pad;
-  const float* dv_g = p.dvec + (long long)bh * p.S_pad;
 
-  if (warp == 0) {  // Q ring (+ vectors), then K / V once up front
-    if (lane == 0 && n_it > 0) {
-      mbar_expect_tx(kv_full, 2 * L::KT);
+  if (warp == 0) {  // Q ring (+ vectors)
+    if (lane == 0) {
+      uint32_t g = 0;
+      for (int w = blockIdx.x; w < n_items; w += gridDim.x) {
+        const Item I = decode(w);
+        const float* lse2_g = p.lse2 + (long long)I.bh * p.S_pad;
+        const float* dv_g = p.dvec + (long long)I.bh * p.S_pad;
+        for (int it = 0; it < I.n_it; ++it, ++g) {
+          const int st = g % NST, q0 = (I.i0 + it) * 128;
+          mbar_wait(&q_empty[st], ((g / NST) & 1) ^ 1);
+          mbar_expect_tx(&q_full[st], L::KT + 1024);
 #pragma unroll
-      for (int c = 0; c < D / 64; ++c) {
-        tma_load_3d(&mk, kv_full, sm + L::K + c * 16384, c * 64, h, tok0 + k0);
-        tma_load_3d(&mv, kv_full, sm + L::V + c * 16384, c * 64, h, tok0 + k0);
+          for (int c = 0; c < D / 64; ++c)
+            tma_load_3d(&mq, &q_full[st], sm + L::Q0 + st * L::KT + c * 16384, c * 64, I.h,
+                        I.tok0 + q0);
+          bulk_load(sm + L::LSE + st * 512, lse2_g + q0, 512, &q_full[st]);
+          bulk_load(sm + L::DV + st * 512, dv_g + q0, 512, &q_full[st]);
+        }
       }
-      for (int it = 0; it < n_it; ++it) {
-        const int st = it % NST, q0 = (i0 + it) * 128;
-        mbar_wait(&q_empty[st], ((it / NST) & 1) ^ 1);
-        mbar_expect_tx(&q_full[st], L::KT + 1024);
+    }
+  } else if (warp == 2) {  // K / V per item (after the TMEM allocation)
+    if (lane == 0) {
+      int n = 0;
+      for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++n) {
+        const Item I = decode(w);
+        const int kb = n % KVB;
+        mbar_wait(&kv_empty[kb], ((n / KVB) & 1) ^ 1);
+        mbar_expect_tx(&kv_full[kb], 2 * L::KT);
+        uint8_t* kvs = sm + L::KV + kb * 2 * L::KT;
 #pragma unroll
-        for (int c = 0; c < D / 64; ++c)
-          tma_load_3d(&mq, &q_full[st], sm + L::Q0 + st * L::KT + c * 16384, c * 64, h, tok0 + q0);
-        bulk_load(sm + L::LSE + st * 512, lse2_g + q0, 512, &q_full[st]);
-        bulk_load(sm + L::DV + st * 512, dv_g + q0, 512, &q_full[st]);
+        for (int c = 0; c < D / 64; ++c) {
+          tma_load_3d(&mk, &kv_full[kb], kvs + c * 16384, c * 64, I.h, I.tok0 + I.k0);
+          tma_load_3d(&mv, &kv_full[kb], kvs + L::KT + c * 16384, c * 64, I.h, I.tok0 + I.k0);
+        }
       }
     }
   } else if (warp == 3) {  // dO ring
     if (lane == 0) {
-      for (int it = 0; it < n_it; ++it) {
-        const int st = it % NST, q0 = (i0 + it) * 128;
-        mbar_wait(&o_empty[st], ((it / NST) & 1) ^ 1);
-        mbar_expect_tx(&o_full[st], L::KT);
+      uint32_t g = 0;
+      for (int w = blockIdx.x; w < n_items; w += gridDim.x) {
+        const Item I = decode(w);
+        for (int it = 0; it < I.n_it; ++it, ++g) {
+          const int st = g % NST, q0 = (I.i0 + it) * 128;
+          mbar_wait(&o_empty[st], ((g / NST) & 1) ^ 1);
+          mbar_expect_tx(&o_full[st], L::KT);
 #pragma unroll
-        for (int c = 0; c < D / 64; ++c)
-          tma_load_3d(&mdo, &o_full[st], sm + L::O0 + st * L::KT + c * 16384, c * 64, h,
-                      tok0 + q0);
+          for (int c = 0; c < D / 64; ++c)
+            tma_load_3d(&mdo, &o_full[st], sm + L::O0 + st * L::KT + c * 16384, c * 64, I.h,
+                        I.tok0 + q0);
+        }
       }
     }
-  } else if (warp == 1 || (DKDV_TWO_ISSUERS && warp == 2)) {
-    // chain A (S^T columns): dV(it) then S(it+1); chain B (dP^T columns): dK(it) then dP(it+1).
-    // The chains touch disjoint TMEM, so with DKDV_TWO_ISSUERS warp 1 issues A and warp 2
-    // (after its TMEM allocation) issues B, each waiting only on its own barriers; otherwise
-    // warp 1 issues both in the order dV(it) S(it+1) dK(it) dP(it+1).
-    const bool chain_a = warp == 1, chain_b = !DKDV_TWO_ISSUERS || warp == 2;
-    if (n_it > 0) {  // whole warp; elected lane issues
-      const uint32_t id_s = make_idesc(128, 128, 0, 0);
-      const uint32_t id_g = make_idesc(128, D, 0, 1);
-      const uint64_t d_k = sdesc(smem_u32(sm + L::K), 16, 1024);
-      const uint64_t d_v = sdesc(smem_u32(sm + L::V), 16, 1024);
-      const uint64_t d_q = sdesc(smem_u32(sm + L::Q0), 16, 1024);
-      const uint64_t d_o = sdesc(smem_u32(sm + L::O0), 16, 1024);
-      const uint64_t m_q = sdesc(smem_u32(sm + L::Q0), 16384, 1024);  // MN-major views
-      const uint64_t m_o = sdesc(smem_u32(sm + L::O0), 16384, 1024);
-      auto so = [&](int it) { return (uint64_t)(((it % NST) * L::KT) >> 4); };
-      auto scores = [&](uint32_t dst, uint64_t da, uint64_t db) {
-        if (elect_one()) {
+  } else if (warp == 1) {
+    // issue order dV(it) S(it+1) dK(it) dP(it+1): S(it+1) overwrites the S^T columns dV(it)
+    // has read, dP(it+1) the dP^T columns dK(it) has read (one thread's MMAs run in order)
+    const uint32_t id_s = make_idesc(128, 128, 0, 0);
+    const uint32_t id_g = make_idesc(128, D, 0, 1);
+    const uint64_t d_q = sdesc(smem_u32(sm + L::Q0), 16, 1024);
+    const uint64_t d_o = sdesc(smem_u32(sm + L::O0), 16, 1024);
+    const uint64_t m_q = sdesc(smem_u32(sm + L::Q0), 16384, 1024);  // MN-major views
+    const uint64_t m_o = sdesc(smem_u32(sm + L::O0), 16384, 1024);
+    auto so = [&](uint32_t g) { return (uint64_t)(((g % NST) * L::KT) >> 4); };
+    auto scores = [&](uint32_t dst, uint64_t da, uint64_t db) {
+      if (elect_one()) {
 #pragma unroll
-          for (int k = 0; k < D / 16; ++k) {
-            const uint64_t o = (uint64_t)(((k >> 2) * 16384 + (k & 3) * 32) >> 4);
-            umma_bf16(dst, da + o, db + o, id_s, k != 0);
-          }
+        for (int k = 0; k < D / 16; ++k) {
+          const uint64_t o = (uint64_t)(((k >> 2) * 16384 + (k & 3) * 32) >> 4);
+          umma_bf16(dst, da + o, db + o, id_s, k != 0);
         }
-      };
-      // dst += A^T B over query half hf, A^T packed in TMEM (queries 16k.. at col 16k of src)
-      auto grad = [&](uint32_t dst, uint32_t src, uint64_t mb, int hf, bool acc) {
-        if (elect_one()) {
+      }
+    };
+    // dst += A^T B over query half hf, A^T packed in TMEM (queries 16k.. at col 16k of src)
+    auto grad = [&](uint32_t dst, uint32_t src, uint64_t mb, int hf, bool acc) {
+      if (elect_one()) {
 #pragma unroll
-          for (int k = 4 * hf; k < 4 * hf + 4; ++k)
-            umma_bf16_ts(dst, src + k * 16, mb + (uint64_t)((k * 2048) >> 4), id_g, acc || k != 0);
-        }
-      };
-      auto s_mma = [&](int it) {  // S^T(it)
-        mbar_wait_fast(&q_full[it % NST], (it / NST) & 1);
+        for (int k = 4 * hf; k < 4 * hf + 4; ++k)
+          umma_bf16_ts(dst, src + k * 16, mb + (uint64_t)((k * 2048) >> 4), id_g, acc || k != 0);
+      }
+    };
+    uint32_t g0 = 0;
+    int n = 0;
+    for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++n) {
+      const Item I = decode(w);
+      const int n_it = I.n_it, kb = n % KVB;
+      const uint64_t d_k = sdesc(smem_u32(sm + L::KV + kb * 2 * L::KT), 16, 1024);
+      const uint64_t d_v = sdesc(smem_u32(sm + L::KV + kb * 2 * L::KT + L::KT), 16, 1024);
+      auto s_mma = [&](uint32_t g) {
+        mbar_wait_fast(&q_full[g % NST], (g / NST) & 1);
         tc_fence_after();
-        scores(tmem, d_k, d_q + so(it));
+        scores(tmem, d_k, d_q + so(g));
         if (elect_one()) umma_commit(s_full);
         __syncwarp();
       };
-      auto dp_mma = [&](int it) {  // dP^T(it); with two issuers this warp also frees dO(it)
-        mbar_wait_fast(&o_full[it % NST], (it / NST) & 1);
+      auto dp_mma = [&](uint32_t g) {
+        mbar_wait_fast(&o_full[g % NST], (g / NST) & 1);
         tc_fence_after();
-        scores(t_dp, d_v, d_o + so(it));
-        if (elect_one()) {
-          umma_commit(dp_full);
-          if (DKDV_TWO_ISSUERS) umma_commit(&o_empty[it % NST]);
-        }
+        scores(t_dp, d_v, d_o + so(g));
+        if (elect_one()) umma_commit(dp_full);
         __syncwarp();
       };
-      mbar_wait_fast(kv_full, 0);
-      if (lane == 0) TRACE(4096 + 16 * 64 + 2);
-      if (chain_a) s_mma(0);
-      if (chain_b) dp_mma(0);
+      mbar_wait_fast(&kv_full[kb], (n / KVB) & 1);
+      if (n == 0 && lane == 0) TRACE(4096 + 16 * 64 + 2);
+      s_mma(g0);
+      dp_mma(g0);
+      if (n > 0) mbar_wait_fast(acc_free, (n - 1) & 1);  // dK / dV of the last item read out
       for (int it = 0; it < n_it; ++it) {
-        const int st = it % NST;
+        const uint32_t g = g0 + it;
+        const int st = g % NST;
         const bool more = it + 1 < n_it;
-        if (chain_a) {  // dV += P^T dO, then S(it+1) over the columns dV has just read
-          if (lane == 0) TRACE(4096 + it * 16 + 0);
-          mbar_wait_fast(&p_full[0], it & 1);
-          tc_fence_after();
-          if (lane == 0) TRACE(4096 + it * 16 + 1);
-          grad(t_dv, tmem, m_o + so(it), 0, it != 0);
-          __syncwarp();
-          mbar_wait_fast(&p_full[1], it & 1);
-          tc_fence_after();
-          grad(t_dv, tmem, m_o + so(it), 1, true);
-          if (elect_one()) {
-            umma_commit(&o_empty[st]);
-            if (DKDV_TWO_ISSUERS && !more) umma_commit(mm_done);
+        if (n == 0 && lane == 0) TRACE(4096 + it * 16 + 0);
+        mbar_wait_fast(&p_full[0], g & 1);
+        tc_fence_after();
+        if (n == 0 && lane == 0) TRACE(4096 + it * 16 + 1);
+        grad(t_dv, tmem, m_o + so(g), 0, it != 0);
+        __syncwarp();
+        mbar_wait_fast(&p_full[1], g & 1);
+        tc_fence_after();
+        grad(t_dv, tmem, m_o + so(g), 1, true);
+        if (elect_one()) umma_commit(&o_empty[st]);
+        __syncwarp();
+        if (n == 0 && lane == 0) TRACE(4096 + it * 16 + 2);
+        if (more) s_mma(g + 1);
+        mbar_wait_fast(&ds_full[0], g & 1);
+        tc_fence_after();
+        if (n == 0 && lane == 0) TRACE(4096 + it * 16 + 3);
+        grad(t_dk, t_dp, m_q + so(g), 0, it != 0);
+        __syncwarp();
+        mbar_wait_fast(&ds_full[1], g & 1);
+        tc_fence_after();
+        grad(t_dk, t_dp, m_q + so(g), 1, true);
+        if (elect_one()) {
+          umma_commit(&q_empty[st]);
+          if (!more) {
+            umma_commit(mm_done);
+            umma_commit(&kv_empty[kb]);
           }
-          __syncwarp();
-          if (lane == 0) TRACE(4096 + it * 16 + 2);
-          if (more) s_mma(it + 1);
         }
-        if (chain_b) {  // dK += dS^T Q, then dP(it+1)
-          mbar_wait_fast(&ds_full[0], it & 1);
-          tc_fence_after();
-          if (lane == 0) TRACE(4096 + it * 16 + 3);
-          grad(t_dk, t_dp, m_q + so(it), 0, it != 0);
-          __syncwarp();
-          mbar_wait_fast(&ds_full[1], it & 1);
-          tc_fence_after();
-          grad(t_dk, t_dp, m_q + so(it), 1, true);
-          if (elect_one()) {
-            if (!more) umma_commit(mm_done);
-            umma_commit(&q_empty[st]);
-          }
-          __syncwarp();
-          if (lane == 0) TRACE(4096 + it * 16 + 4);
-          if (more) dp_mma(it + 1);
-        }
+        __syncwarp();
+        if (n == 0 && lane == 0) TRACE(4096 + it * 16 + 4);
+        if (more) dp_mma(g + 1);
       }
+      g0 += n_it;
     }
   } else if (warp >= 4) {
     // part p owns query columns [16p, 16p+16) (half 0) and [64+16p, 64+16p+16) (half 1), so
     // the packed bf16 of query slice k lands on the thread's own columns 16k.. and the dV / dK
     // MMAs of half 0 start while half 1 is still being computed
     const int q = warp & 3, part = (warp - 4) >> 2;
-    const int r = q * 32 + lane, key = k0 + r;
+    const int r = q * 32 + lane;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     const float sl2 = p.scale_log2;
+    uint32_t g0 = 0;
+    int n = 0;
+    for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++n) {
+    const Item I = decode(w);
+    const int b = I.b, h = I.h, tok0 = I.tok0, key = I.k0 + r, n_it = I.n_it;
+    const bool tr = n == 0 && warp == 4 && lane == 0;
     for (int it = 0; it < n_it; ++it) {
-      const int st = it % NST, q0 = (i0 + it) * 128;
+      const uint32_t g = g0 + it;
+      const int st = g % NST, q0 = (I.i0 + it) * 128;
       const float* l2 = reinterpret_cast<const float*>(sm + L::LSE + st * 512) + part * 16;
       const float* dd = reinterpret_cast<const float*>(sm + L::DV + st * 512) + part * 16;
       // ---- phase 1: P^T
-      mbar_wait(s_full, it & 1);
+      mbar_wait(s_full, g & 1);
       tc_fence_after();
-      if (warp == 4 && lane == 0) TRACE(4096 + it * 16 + 8);
+      if (tr) TRACE(4096 + it * 16 + 8);
       float pv[32];
       tmem_ld16_nowait(tmem + part * 16 + lane_off, reinterpret_cast<uint32_t*>(pv));
       tmem_ld16_nowait(tmem + 64 + part * 16 + lane_off, reinterpret_cast<uint32_t*>(pv + 16));
       tmem_wait_ld();
-      if (warp == 4 && lane == 0) TRACE(4096 + it * 16 + 13);
+      if (tr) TRACE(4096 + it * 16 + 13);
       uint32_t keep = 0xffffffffu;
       if constexpr (DROP) {
         keep = 0;
@@ -1513,18 +1584,18 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         tmem_wait_st();
         tc_fence_before();
         mbar_arrive(&p_full[hf]);
-        if (warp == 4 && lane == 0) TRACE(4096 + it * 16 + 9 + hf);
+        if (tr) TRACE(4096 + it * 16 + 9 + hf);
       }
       // ---- phase 2: dS^T = P^T (dP^T * mask / (1-p) - D)
-      mbar_wait(dp_full, it & 1);
+      mbar_wait(dp_full, g & 1);
       tc_fence_after();
-      if (warp == 4 && lane == 0) TRACE(4096 + it * 16 + 11);
+      if (tr) TRACE(4096 + it * 16 + 11);
 #pragma unroll
       for (int hf = 0; hf < 2; ++hf) {
         float dp[16];
         tmem_ld16_nowait(t_dp + hf * 64 + part * 16 + lane_off, reinterpret_cast<uint32_t*>(dp));
         tmem_wait_ld();
-        if (warp == 4 && lane == 0 && hf == 0) TRACE(4096 + it * 16 + 14);
+        if (tr && hf == 0) TRACE(4096 + it * 16 + 14);
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
           const int c = hf * 16 + i;
@@ -1539,12 +1610,12 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         tc_fence_before();
         mbar_arrive(&ds_full[hf]);
       }
-      if (warp == 4 && lane == 0) TRACE(4096 + it * 16 + 12);
+      if (tr) TRACE(4096 + it * 16 + 12);
     }
-    if (n_it > 0) {
-      mbar_wait(mm_done, 0);
+    {
+      mbar_wait(mm_done, n & 1);
       tc_fence_after();
-      if (warp == 4 && lane == 0) TRACE(4096 + 16 * 64 + 0);
+      if (tr) TRACE(4096 + 16 * 64 + 0);
       const bool ok = key < p.S;
       constexpr int OC = D / BWD_SPLIT;  // output columns per warp
       const long long off =
@@ -1565,7 +1636,11 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         store_row_out16(p.g1 + off, t_dv + part * OC + lane_off, 1.f, ok);
         store_row_out16(p.g0 + off, t_dk + part * OC + lane_off, p.scale, ok);
       }
-      if (warp == 4 && lane == 0) TRACE(4096 + 16 * 64 + 1);
+      if (tr) TRACE(4096 + 16 * 64 + 1);
+      tc_fence_before();
+      mbar_arrive(acc_free);  // dK / dV are out of TMEM: the next item may overwrite them
+    }
+    g0 += n_it;
     }
   }
   tc_fence_before();
@@ -1936,6 +2011,23 @@ static int fwd_ctas(int64_t S) {
   return S <= ATTN_FWD_PERSIST_MAX_S ? sms : 0;
 }
 
+// Backward CTA count (dK/dV kernel): persistent CTAs for short sequences as in the forward.
+// GALV_ATTN_BWD_CTAS overrides (0 = one CTA per item).
+static int bwd_ctas(int64_t S) {
+  static const int env = [] {
+    const char* e = getenv("GALV_ATTN_BWD_CTAS");
+    return e ? atoi(e) : -1;
+  }();
+  if (env >= 0) return env;
+  static const int sms = [] {
+    int dev = 0, n = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n;
+  }();
+  return S <= ATTN_BWD_PERSIST_MAX_S ? sms : 0;
+}
+
 // GALV_ATTN_DKDV=1 selects the 64-query-step dK/dV kernel (bwd_dkdv_tc) for A/B runs
 static bool dkdv_64q_steps() {
   static const bool old = [] {
@@ -2038,9 +2130,14 @@ int32_t attn_bwd_sm100(const void* q, const void* k, const void* v, const void* 
   const int64_t S_pad = (S + 127) / 128 * 128;
   float* lse2 = reinterpret_cast<float*>(ws);
   float* dvec = lse2 + B * H * S_pad;
-  bwd_prep<<<(unsigned)(B * H * S_pad / 8), 128, 0, stream>>>(
-      (const __nv_bfloat16*)o, (const __nv_bfloat16*)dout, lse, lse2, dvec, (int)S, (int)S_pad,
-      (int)H, (int)D, ost, sh);
+  {
+    const long long n_rows = B * H * S_pad;
+    const int rows_per_block = 8 * (32 / (int)(D / 8)) * PREP_ROWS;  // 8 warps
+    const unsigned blocks = (unsigned)((n_rows + rows_per_block - 1) / rows_per_block);
+    auto prep = D == 128 ? bwd_prep<128> : bwd_prep<64>;
+    prep<<<blocks, 256, 0, stream>>>((const __nv_bfloat16*)o, (const __nv_bfloat16*)dout, lse,
+                                     lse2, dvec, (int)S, (int)S_pad, (int)H, n_rows, ost, sh);
+  }
   GALV_LAUNCH_CHECK();
   const int64_t tokens = B * S;
   CUtensorMap mq64, mdo64, mk128, mv128, mq128, mdo128;
@@ -2067,7 +2164,11 @@ int32_t attn_bwd_sm100(const void* q, const void* k, const void* v, const void* 
   GALV_CHECK_ARG(rope_table == nullptr || D == 128, "fused inverse RoPE needs head_dim 128");
   const dim3 g_kv((unsigned)((S + 127) / 128), (unsigned)(B * H));
   const dim3 g_q = DQ_GRID_BH_FAST ? dim3((unsigned)(B * H), (unsigned)((S + 127) / 128)) : g_kv;
-  const dim3 g_kv2 = DKDV_GRID_BH_FAST ? dim3((unsigned)(B * H), (unsigned)((S + 127) / 128)) : g_kv;
+  p.bh_total = (int)(B * H);
+  const long long bwd_items = (long long)p.bh_total * ((S + 127) / 128);
+  const int bctas = bwd_ctas(S);
+  p.persist = bctas > 0;
+  const dim3 g_kv2((unsigned)(bctas > 0 ? std::min<long long>(bwd_items, bctas) : bwd_items));
 #define GALV_FA_BWD(DD, DR)                                                                      \
   do {                                                                                           \
     static bool set = false;                                                                     \
