@@ -1265,16 +1265,6 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
 #ifndef DQ_GRID_BH_FAST
 #define DQ_GRID_BH_FAST 0
 #endif
-// dq kernel MMA issuers: 0 = one warp issuing S(it), dP(it), dQ(it-1) per step (dP(it) queues
-// behind the waits for S's buffer); 2 (default) = warp 1 issues S(it), dQ(it-1) and warp 2
-// issues dP(it) as soon as dP(it-1) is loaded.  Measured B2 S4096 H32 912-913 -> 895 us
-// (whole backward; period 2080 -> 1860 cycles per 128-key step, where the step's smem
-// traffic -- S and dP read A and B from smem, dQ reads B, TMA writes K and V, 224 KB -- is
-// 1750 cycles at 128 B/clk).  Issuing dQ(it-2) before dP(it) and S(it) from one warp
-// measured neutral (911-912 us).
-#ifndef DQ_ISSUE_ORDER
-#define DQ_ISSUE_ORDER 2
-#endif
 template <int D>
 struct SmemKV2 {
   static constexpr int NST = 2;
@@ -1659,44 +1649,77 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
 template <int D>
 struct SmemQ {
   // K is used by S(it) and dQ(it) (released late), V only by dP(it): separate rings, K one
-  // stage deeper so its TMA load for step it+2 starts a full step before S(it+2) needs it
-  static constexpr int NK = 3, NV = 2;
+  // stage deeper so its TMA load for step it+2 starts a full step before S(it+2) needs it.
+  // Q / dO: QOB buffers (persistent CTAs load the next item's while this one runs; D=64 only,
+  // D=128 has no shared memory left for a second pair)
+  static constexpr int NK = 3, NV = 2, QOB = D == 64 ? 2 : 1;
   static constexpr int QT = D * 128 * 2, KT = D * 128 * 2;
-  static constexpr int Q = 0, O = QT, K0 = 2 * QT, V0 = K0 + NK * KT;
+  static constexpr int QO = 0, K0 = QOB * 2 * QT, V0 = K0 + NK * KT;
   static constexpr int BAR = V0 + NV * KT;
   static constexpr int BYTES = BAR + 256 + 1024;
 };
 
+// Work items (query block, batch*head): one per CTA (query block fastest, heaviest first per
+// head, DQ_GRID_BH_FAST) or persistent CTAs for short sequences (heaviest block first over the
+// whole grid, (batch, head) fastest).  Q/dO buffers are handed over by qo_empty (the item's
+// last S and dP done: one commit from each issuing warp) and the dQ accumulator by acc_free.
+// MMA issuers: warp 1 issues S(it) and dQ(it-1); warp 2 issues dP(it) as soon as the math
+// warps have loaded dP(it-1), so it never queues behind warp 1's waits for dS (measured B2
+// S4096 H32 whole backward 912 -> 895 us, period 2080 -> 1860 cycles per 128-key step, where
+// the step's smem traffic -- 224 KB: S and dP read A and B, dQ reads B, TMA writes K and V --
+// is 1750 cycles at 128 B/clk; issuing dQ(it-2), dP(it), S(it) from one warp was neutral).
 template <int D, bool DROP>
 __global__ void __launch_bounds__(BWD_THREADS, 1)
     bwd_dq_tc(const __grid_constant__ CUtensorMap mq, const __grid_constant__ CUtensorMap mk,
               const __grid_constant__ CUtensorMap mv, const __grid_constant__ CUtensorMap mdo,
               const BwdParams p) {
   using L = SmemQ<D>;
+  constexpr int QOB = L::QOB;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // keeps the shared window
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::BAR);
-  uint64_t* qo_full = bar + 0;
-  uint64_t* k_full = bar + 1;           // [NK]
+  uint64_t* qo_full = bar + 0;          // [QOB]
+  uint64_t* qo_empty = qo_full + QOB;   // [QOB]
+  uint64_t* k_full = qo_empty + QOB;    // [NK]
   uint64_t* k_empty = k_full + L::NK;   // [NK]
   uint64_t* v_full = k_empty + L::NK;   // [NV]
   uint64_t* v_empty = v_full + L::NV;   // [NV]
-  uint64_t* st_full = v_empty + L::NV;  // [2]  S (buffer sb) and dP computed
-  uint64_t* s_free = st_full + 2;       // [2]  dQ MMA of the buffer's step done
-  uint64_t* ds_full = s_free + 2;       // [2]  dS packed into the S buffer
+  uint64_t* st_full = v_empty + L::NV;  // [2]  S (buffer sb) computed
+  uint64_t* ds_full = st_full + 2;      // [2]  dS packed into the S buffer
   uint64_t* dp_free = ds_full + 2;      // dP loaded by every math thread
-  uint64_t* dq_done = dp_free + 1;
-  uint64_t* dp_full = dq_done + 1;      // dP(it) complete (DQ_ISSUE_ORDER 2: own issuing warp)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dp_full + 1);
+  uint64_t* dq_done = dp_free + 1;      // the item's last dQ MMA complete
+  uint64_t* dp_full = dq_done + 1;      // dP(it) complete
+  uint64_t* acc_free = dp_full + 1;     // the item's epilogue has read dQ
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_free + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_q = (p.S + 127) / 128;
-  const int qb = n_q - 1 - (DQ_GRID_BH_FAST ? blockIdx.y : blockIdx.x);  // heavy blocks first
-  const int bh = DQ_GRID_BH_FAST ? blockIdx.x : blockIdx.y, b = bh / p.H, h = bh % p.H;
-  const int q0 = qb * 128, tok0 = b * p.S;
-  const int n_kb = (p.S + 127) / 128;
-  const int n_it = p.causal ? min(n_kb, qb + 1) : n_kb;
+  const int n_kb = n_q;
+  const int n_items = n_q * p.bh_total;
+  struct Item {
+    int b, h, bh, q0, n_it, tok0;
+  };
+  auto decode = [&](int w) {
+    Item I;
+    int qb;
+    if (p.persist || DQ_GRID_BH_FAST) {
+      qb = n_q - 1 - w / p.bh_total;
+      I.bh = w % p.bh_total;
+    } else {
+      qb = n_q - 1 - w % n_q;
+      I.bh = w / n_q;
+    }
+    I.b = I.bh / p.H;
+    I.h = I.bh % p.H;
+    I.q0 = qb * 128;
+    I.n_it = p.causal ? min(n_kb, qb + 1) : n_kb;
+    I.tok0 = I.b * p.S;
+    return I;
+  };
   if (threadIdx.x == 0) {
-    mbar_init(qo_full, 1);
+    for (int i = 0; i < QOB; ++i) {
+      mbar_init(&qo_full[i], 1);
+      mbar_init(&qo_empty[i], 2);  // last S (warp 1) + last dP (warp 2)
+    }
     for (int i = 0; i < L::NK; ++i) {
       mbar_init(&k_full[i], 1);
       mbar_init(&k_empty[i], 1);
@@ -1707,12 +1730,12 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&st_full[i], 1);
-      mbar_init(&s_free[i], 1);
       mbar_init(&ds_full[i], 128 * BWD_SPLIT);
     }
     mbar_init(dp_free, 128 * BWD_SPLIT);
     mbar_init(dq_done, 1);
     mbar_init(dp_full, 1);
+    mbar_init(acc_free, 128 * BWD_SPLIT);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     fence_async_smem();
   }
@@ -1723,166 +1746,165 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
   const uint32_t tmem = *tmem_slot;
   const uint32_t t_dp = tmem + 256, t_dq = tmem + 384;
 
-  if (warp == 0) {
+  if (warp == 0) {  // Q / dO per item, K ring
     if (lane == 0) {
-      mbar_expect_tx(qo_full, 2 * L::QT);
+      uint32_t g = 0;
+      int n = 0;
+      for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++n) {
+        const Item I = decode(w);
+        const int qb = n % QOB;
+        mbar_wait(&qo_empty[qb], ((n / QOB) & 1) ^ 1);
+        mbar_expect_tx(&qo_full[qb], 2 * L::QT);
+        uint8_t* qo = sm + L::QO + qb * 2 * L::QT;
 #pragma unroll
-      for (int c = 0; c < D / 64; ++c) {
-        tma_load_3d(&mq, qo_full, sm + L::Q + c * 16384, c * 64, h, tok0 + q0);
-        tma_load_3d(&mdo, qo_full, sm + L::O + c * 16384, c * 64, h, tok0 + q0);
-      }
-      for (int it = 0; it < n_it; ++it) {  // K ring
-        const int st = it % L::NK;
-        mbar_wait(&k_empty[st], ((it / L::NK) & 1) ^ 1);
-        mbar_expect_tx(&k_full[st], L::KT);
-#pragma unroll
-        for (int c = 0; c < D / 64; ++c)
-          tma_load_3d(&mk, &k_full[st], sm + L::K0 + st * L::KT + c * 16384, c * 64, h,
-                      tok0 + it * 128);
-      }
-    }
-  } else if (warp == 3) {
-    if (lane == 0) {
-      for (int it = 0; it < n_it; ++it) {  // V ring
-        const int st = it % L::NV;
-        mbar_wait(&v_empty[st], ((it / L::NV) & 1) ^ 1);
-        mbar_expect_tx(&v_full[st], L::KT);
-#pragma unroll
-        for (int c = 0; c < D / 64; ++c)
-          tma_load_3d(&mv, &v_full[st], sm + L::V0 + st * L::KT + c * 16384, c * 64, h,
-                      tok0 + it * 128);
-      }
-    }
-  } else if (warp == 2 && DQ_ISSUE_ORDER == 2) {  // dP issuer (after the TMEM allocation)
-    const uint32_t id_s = make_idesc(128, 128, 0, 0);
-    const uint64_t d_o = sdesc(smem_u32(sm + L::O), 16, 1024);
-    const uint64_t d_v = sdesc(smem_u32(sm + L::V0), 16, 1024);
-    mbar_wait_fast(qo_full, 0);
-    for (int it = 0; it < n_it; ++it) {
-      const int sv = it % L::NV;
-      mbar_wait_fast(&v_full[sv], (it / L::NV) & 1);
-      if (it > 0) mbar_wait_fast(dp_free, (it - 1) & 1);
-      tc_fence_after();
-      if (lane == 0) TRACE(it * 8 + 2);
-      const uint64_t ov = (uint64_t)((sv * L::KT) >> 4);
-      if (elect_one()) {
-#pragma unroll
-        for (int k = 0; k < D / 16; ++k) {
-          const uint64_t o = (uint64_t)(((k >> 2) * 16384 + (k & 3) * 32) >> 4);
-          umma_bf16(t_dp, d_o + o, d_v + ov + o, id_s, k != 0);
+        for (int c = 0; c < D / 64; ++c) {
+          tma_load_3d(&mq, &qo_full[qb], qo + c * 16384, c * 64, I.h, I.tok0 + I.q0);
+          tma_load_3d(&mdo, &qo_full[qb], qo + L::QT + c * 16384, c * 64, I.h, I.tok0 + I.q0);
         }
-        umma_commit(dp_full);
-        umma_commit(&v_empty[sv]);
+        for (int it = 0; it < I.n_it; ++it, ++g) {
+          const int st = g % L::NK;
+          mbar_wait(&k_empty[st], ((g / L::NK) & 1) ^ 1);
+          mbar_expect_tx(&k_full[st], L::KT);
+#pragma unroll
+          for (int c = 0; c < D / 64; ++c)
+            tma_load_3d(&mk, &k_full[st], sm + L::K0 + st * L::KT + c * 16384, c * 64, I.h,
+                        I.tok0 + it * 128);
+        }
       }
-      __syncwarp();
     }
-  } else if (warp == 1) {  // whole warp; elected lane issues (see fwd_tc)
+  } else if (warp == 3) {  // V ring
+    if (lane == 0) {
+      uint32_t g = 0;
+      for (int w = blockIdx.x; w < n_items; w += gridDim.x) {
+        const Item I = decode(w);
+        for (int it = 0; it < I.n_it; ++it, ++g) {
+          const int st = g % L::NV;
+          mbar_wait(&v_empty[st], ((g / L::NV) & 1) ^ 1);
+          mbar_expect_tx(&v_full[st], L::KT);
+#pragma unroll
+          for (int c = 0; c < D / 64; ++c)
+            tma_load_3d(&mv, &v_full[st], sm + L::V0 + st * L::KT + c * 16384, c * 64, I.h,
+                        I.tok0 + it * 128);
+        }
+      }
+    }
+  } else if (warp == 2) {  // dP issuer (after the TMEM allocation)
+    const uint32_t id_s = make_idesc(128, 128, 0, 0);
+    const uint64_t d_v = sdesc(smem_u32(sm + L::V0), 16, 1024);
+    uint32_t g = 0;
+    int n = 0;
+    for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++n) {
+      const Item I = decode(w);
+      const int qb = n % QOB;
+      const uint64_t d_o = sdesc(smem_u32(sm + L::QO + qb * 2 * L::QT + L::QT), 16, 1024);
+      mbar_wait_fast(&qo_full[qb], (n / QOB) & 1);
+      for (int it = 0; it < I.n_it; ++it, ++g) {
+        const int sv = g % L::NV;
+        mbar_wait_fast(&v_full[sv], (g / L::NV) & 1);
+        if (g > 0) mbar_wait_fast(dp_free, (g - 1) & 1);
+        tc_fence_after();
+        if (n == 0 && lane == 0) TRACE(it * 8 + 2);
+        const uint64_t ov = (uint64_t)((sv * L::KT) >> 4);
+        if (elect_one()) {
+#pragma unroll
+          for (int k = 0; k < D / 16; ++k) {
+            const uint64_t o = (uint64_t)(((k >> 2) * 16384 + (k & 3) * 32) >> 4);
+            umma_bf16(t_dp, d_o + o, d_v + ov + o, id_s, k != 0);
+          }
+          umma_commit(dp_full);
+          umma_commit(&v_empty[sv]);
+          if (it == I.n_it - 1) umma_commit(&qo_empty[qb]);
+        }
+        __syncwarp();
+      }
+    }
+  } else if (warp == 1) {  // S and dQ issuer
     const uint32_t id_s = make_idesc(128, 128, 0, 0);
     const uint32_t id_g = make_idesc(128, D, 0, 1);
-    const uint64_t d_q = sdesc(smem_u32(sm + L::Q), 16, 1024);
-    const uint64_t d_o = sdesc(smem_u32(sm + L::O), 16, 1024);
     const uint64_t d_k = sdesc(smem_u32(sm + L::K0), 16, 1024);
-    const uint64_t d_v = sdesc(smem_u32(sm + L::V0), 16, 1024);
     const uint64_t m_k = sdesc(smem_u32(sm + L::K0), 16384, 1024);  // K as MN-major B
-    mbar_wait_fast(qo_full, 0);
-    // dQ += dS K: A = dS from TMEM (keys 16k.. packed at col 32*(k/2) + 8*(k%2) of the S
-    // buffer), B = the K tile as an MN-major operand (same smem bytes as the S GEMM's B)
-    auto grads = [&](int it) {
-      const int st = it % L::NK, sb = it & 1;
-      mbar_wait_fast(&ds_full[sb], (it >> 1) & 1);
-      tc_fence_after();
-      if (lane == 0) TRACE(it * 8 + 3);
-      const uint64_t so = (uint64_t)((st * L::KT) >> 4);
-      if (elect_one()) {
+    uint32_t g0 = 0;
+    int n = 0;
+    for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++n) {
+      const Item I = decode(w);
+      const int n_it = I.n_it, qb = n % QOB;
+      const uint64_t d_q = sdesc(smem_u32(sm + L::QO + qb * 2 * L::QT), 16, 1024);
+      mbar_wait_fast(&qo_full[qb], (n / QOB) & 1);
+      // dQ += dS K: A = dS from TMEM (keys 16k.. packed at col 32*(k/2) + 8*(k%2) of the S
+      // buffer), B = the K tile as an MN-major operand (same smem bytes as the S GEMM's B)
+      auto grads = [&](int it) {
+        const uint32_t g = g0 + it;
+        const int st = g % L::NK, sb = g & 1;
+        if (it == 0 && n > 0) mbar_wait_fast(acc_free, (n - 1) & 1);  // last item's dQ read
+        mbar_wait_fast(&ds_full[sb], (g >> 1) & 1);
+        tc_fence_after();
+        if (n == 0 && lane == 0) TRACE(it * 8 + 3);
+        const uint64_t so = (uint64_t)((st * L::KT) >> 4);
+        if (elect_one()) {
 #pragma unroll
-        for (int k = 0; k < 8; ++k)
-          umma_bf16_ts(t_dq, tmem + sb * 128 + (k >> 1) * 32 + (k & 1) * 8,
-                       m_k + so + (uint64_t)((k * 2048) >> 4), id_g, (it | k) != 0);
-        if (it == n_it - 1) umma_commit(dq_done);  // single phase: final dQ complete
-        umma_commit(&s_free[sb]);
-        umma_commit(&k_empty[st]);
-      }
-      __syncwarp();
-    };
-    auto s_mma = [&](int it) {  // S(it) = Q K^T into buffer it&1
-      const int sk = it % L::NK, sb = it & 1;
-      mbar_wait_fast(&k_full[sk], (it / L::NK) & 1);
-      // order 2: this warp issued dQ(it-2) (the last reader of buffer sb) before S(it), and
-      // one thread's MMAs execute in issue order -- no completion wait needed
-      if constexpr (DQ_ISSUE_ORDER != 2) mbar_wait_fast(&s_free[sb], ((it >> 1) & 1) ^ 1);
-      tc_fence_after();
-      if (lane == 0) TRACE(it * 8 + 1);
-      const uint64_t ok = (uint64_t)((sk * L::KT) >> 4);
-      if (elect_one()) {
-#pragma unroll
-        for (int k = 0; k < D / 16; ++k) {
-          const uint64_t o = (uint64_t)(((k >> 2) * 16384 + (k & 3) * 32) >> 4);
-          umma_bf16(tmem + sb * 128, d_q + o, d_k + ok + o, id_s, k != 0);
+          for (int k = 0; k < 8; ++k)
+            umma_bf16_ts(t_dq, tmem + sb * 128 + (k >> 1) * 32 + (k & 1) * 8,
+                         m_k + so + (uint64_t)((k * 2048) >> 4), id_g, (it | k) != 0);
+          if (it == n_it - 1) umma_commit(dq_done);
+          umma_commit(&k_empty[st]);
         }
-      }
-      __syncwarp();
-    };
-    auto dp_mma = [&](int it) {  // dP(it) = dO V^T (single buffer)
-      const int sv = it % L::NV;
-      mbar_wait_fast(&v_full[sv], (it / L::NV) & 1);
-      if (it > 0) mbar_wait_fast(dp_free, (it - 1) & 1);
-      tc_fence_after();
-      if (lane == 0) TRACE(it * 8 + 2);
-      const uint64_t ov = (uint64_t)((sv * L::KT) >> 4);
-      if (elect_one()) {
+        __syncwarp();
+      };
+      // S(it) into buffer g&1: this warp issued dQ(g-2), the buffer's last reader, before it
+      // (one thread's MMAs execute in issue order), so no completion wait is needed
+      auto s_mma = [&](int it) {
+        const uint32_t g = g0 + it;
+        const int sk = g % L::NK, sb = g & 1;
+        mbar_wait_fast(&k_full[sk], (g / L::NK) & 1);
+        tc_fence_after();
+        if (n == 0 && lane == 0) TRACE(it * 8 + 1);
+        const uint64_t ok = (uint64_t)((sk * L::KT) >> 4);
+        if (elect_one()) {
 #pragma unroll
-        for (int k = 0; k < D / 16; ++k) {
-          const uint64_t o = (uint64_t)(((k >> 2) * 16384 + (k & 3) * 32) >> 4);
-          umma_bf16(t_dp, d_o + o, d_v + ov + o, id_s, k != 0);
+          for (int k = 0; k < D / 16; ++k) {
+            const uint64_t o = (uint64_t)(((k >> 2) * 16384 + (k & 3) * 32) >> 4);
+            umma_bf16(tmem + sb * 128, d_q + o, d_k + ok + o, id_s, k != 0);
+          }
+          umma_commit(&st_full[sb]);
+          if (it == n_it - 1) umma_commit(&qo_empty[qb]);
         }
-        umma_commit(&v_empty[sv]);
-      }
-      __syncwarp();
-    };
-    auto st_commit = [&](int it) {  // S(it) and dP(it) both complete
-      if (elect_one()) umma_commit(&st_full[it & 1]);
-      __syncwarp();
-    };
-    if constexpr (DQ_ISSUE_ORDER == 2) {
-      // S and dQ only; dP(it) is issued by warp 2 as soon as the math warps have loaded
-      // dP(it-1), so it never queues behind this warp's waits for dS
+        __syncwarp();
+      };
       for (int it = 0; it < n_it; ++it) {
-        if (lane == 0) TRACE(it * 8 + 0);
+        if (n == 0 && lane == 0) TRACE(it * 8 + 0);
         s_mma(it);
-        st_commit(it);
         if (it > 0) grads(it - 1);
       }
       grads(n_it - 1);
-    } else {
-      for (int it = 0; it < n_it; ++it) {
-        if (lane == 0) TRACE(it * 8 + 0);
-        s_mma(it);
-        dp_mma(it);
-        st_commit(it);
-        if (it > 0) grads(it - 1);
-      }
-      grads(n_it - 1);
+      g0 += n_it;
     }
   } else if (warp >= 4) {
     const int q = warp & 3, part = (warp - 4) >> 2;  // part: keys [32 part, 32 part + 32)
-    const int r = q * 32 + lane, qi = q0 + r;
+    const int r = q * 32 + lane;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-    const float l2 = p.lse2[(long long)bh * p.S_pad + qi];
-    const float dd = p.dvec[(long long)bh * p.S_pad + qi];
     const float sl2 = p.scale_log2;
+    uint32_t g0 = 0;
+    int n = 0;
+    for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++n) {
+    const Item I = decode(w);
+    const int b = I.b, h = I.h, tok0 = I.tok0, qi = I.q0 + r, n_it = I.n_it;
+    const float l2 = p.lse2[(long long)I.bh * p.S_pad + qi];
+    const float dd = p.dvec[(long long)I.bh * p.S_pad + qi];
+    const bool tr = n == 0 && warp == 4 && lane == 0;
     for (int it = 0; it < n_it; ++it) {
-      const int sb = it & 1;
-      mbar_wait(&st_full[sb], (it >> 1) & 1);
-      if constexpr (DQ_ISSUE_ORDER == 2) mbar_wait(dp_full, it & 1);
+      const uint32_t g = g0 + it;
+      const int sb = g & 1;
+      mbar_wait(&st_full[sb], (g >> 1) & 1);
+      mbar_wait(dp_full, g & 1);
       tc_fence_after();
-      if (warp == 4 && lane == 0) TRACE(it * 8 + 4);
+      if (tr) TRACE(it * 8 + 4);
       float s[32], dp[32];
       tmem_ld32_nowait(tmem + sb * 128 + part * 32 + lane_off, reinterpret_cast<uint32_t*>(s));
       tmem_ld32_nowait(t_dp + part * 32 + lane_off, reinterpret_cast<uint32_t*>(dp));
       tmem_wait_ld();
       tc_fence_before();
       mbar_arrive(dp_free);
-      if (warp == 4 && lane == 0) TRACE(it * 8 + 5);
+      if (tr) TRACE(it * 8 + 5);
       const int kbase = it * 128 + part * 32;
       if constexpr (DROP) {
         const int lim = (p.causal ? min(p.S, qi + 1) : p.S) - kbase;
@@ -1914,15 +1936,15 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       uint32_t pk[16];
 #pragma unroll
       for (int i = 0; i < 16; ++i) pk[i] = pack2(dp[2 * i], dp[2 * i + 1]);
-      if (warp == 4 && lane == 0) TRACE(it * 8 + 6);
+      if (tr) TRACE(it * 8 + 6);
       tmem_st8(tmem + sb * 128 + part * 32 + lane_off, pk);
       tmem_st8(tmem + sb * 128 + part * 32 + 8 + lane_off, pk + 8);
       tmem_wait_st();
       tc_fence_before();
       mbar_arrive(&ds_full[sb]);
-      if (warp == 4 && lane == 0) TRACE(it * 8 + 7);
+      if (tr) TRACE(it * 8 + 7);
     }
-    mbar_wait(dq_done, 0);
+    mbar_wait(dq_done, n & 1);
     tc_fence_after();
     const bool ok = qi < p.S;
     constexpr int OC = D / BWD_SPLIT;
@@ -1941,6 +1963,10 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       }
     } else {
       store_row_out16(p.g0 + off, t_dq + part * OC + lane_off, p.scale, ok);
+    }
+    tc_fence_before();
+    mbar_arrive(acc_free);  // dQ is out of TMEM: the next item may overwrite it
+    g0 += n_it;
     }
   }
   tc_fence_before();
@@ -2163,12 +2189,12 @@ int32_t attn_bwd_sm100(const void* q, const void* k, const void* v, const void* 
   p.drop = drop;
   GALV_CHECK_ARG(rope_table == nullptr || D == 128, "fused inverse RoPE needs head_dim 128");
   const dim3 g_kv((unsigned)((S + 127) / 128), (unsigned)(B * H));
-  const dim3 g_q = DQ_GRID_BH_FAST ? dim3((unsigned)(B * H), (unsigned)((S + 127) / 128)) : g_kv;
   p.bh_total = (int)(B * H);
   const long long bwd_items = (long long)p.bh_total * ((S + 127) / 128);
   const int bctas = bwd_ctas(S);
   p.persist = bctas > 0;
   const dim3 g_kv2((unsigned)(bctas > 0 ? std::min<long long>(bwd_items, bctas) : bwd_items));
+  const dim3 g_q = g_kv2;  // same item count and CTA policy for the dq kernel
 #define GALV_FA_BWD(DD, DR)                                                                      \
   do {                                                                                           \
     static bool set = false;                                                                     \
