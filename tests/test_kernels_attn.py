@@ -27,7 +27,7 @@ def ref_attn(q, k, v, causal):
 
 @pytest.mark.parametrize("dt", [torch.bfloat16, torch.float32])
 @pytest.mark.parametrize("D", [64, 128])
-@pytest.mark.parametrize("S", [128, 200, 512])
+@pytest.mark.parametrize("S", [128, 200, 300, 512])
 @pytest.mark.parametrize("causal", [True, False])
 def test_attention(dt, D, S, causal):
     if dt == torch.float32 and D != 64:
@@ -278,3 +278,49 @@ def test_attention_dropout_fwd_bwd(dt, D, S):
                scale=scale, causal=True, dropout=drop)
     for i, want in enumerate((qr.grad, kr.grad, vr.grad)):
         assert rel(d[:, :, i], want) < (1e-5 if dt == torch.float32 else 2e-2), i
+
+
+@pytest.mark.parametrize("D", [64, 128])
+@pytest.mark.parametrize("causal", [True, False])
+def test_attention_short_sequence_many_items(D, causal):
+    """S <= 2048 runs persistent CTAs (one per SM looping over work items): at B4 S1024 H16
+    there are 256 forward and 512 backward items for 148 CTAs, so every CTA hands Q, O, K/V
+    and the dK/dV / dQ accumulators over between items."""
+    from paper_2504_21411_b200 import kernels as K
+    torch.manual_seed(11)
+    B, S, H = 4, 1024, 16
+    qkv = torch.randn(B, S, 3, H, D, device="cuda").bfloat16()
+    q, k, v = qkv[:, :, 0], qkv[:, :, 1], qkv[:, :, 2]
+    o = torch.empty(B, S, H, D, device="cuda", dtype=torch.bfloat16)
+    lse = torch.empty(B, H, S, device="cuda")
+    scale = 1 / math.sqrt(D)
+    K.attn_fwd(q, k, v, o, lse, scale=scale, causal=causal)
+    qr, kr, vr = (t.float().clone().requires_grad_(True) for t in (q, k, v))
+    o_ref, lse_ref = ref_attn(qr, kr, vr, causal)
+    assert rel(o, o_ref) < 1e-2
+    assert rel(lse, lse_ref) < 1e-3
+    do = torch.randn_like(o_ref)
+    o_ref.backward(do)
+    d = torch.empty_like(qkv)
+    K.attn_bwd(q, k, v, o, do.bfloat16().contiguous(), lse, d[:, :, 0], d[:, :, 1], d[:, :, 2],
+               scale=scale, causal=causal)
+    for i, want in enumerate((qr.grad, kr.grad, vr.grad)):
+        assert rel(d[:, :, i], want) < 2e-2, i
+
+
+def test_attention_persistent_few_ctas():
+    """The attention tests above with 3 persistent CTAs for the forward and the backward
+    (GALV_ATTN_FWD_CTAS / GALV_ATTN_BWD_CTAS, read once per process, hence a subprocess):
+    every CTA then runs many items -- including items whose second query tile lies beyond
+    the sequence (S=300), tails, dropout and the fused inverse RoPE."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, GALV_ATTN_FWD_CTAS="3", GALV_ATTN_BWD_CTAS="3")
+    sel = ("(test_attention and not production and not persistent and not many_items) "
+           "or test_attention_dropout_fwd_bwd or test_attention_bwd_fused_inverse_rope")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+                        os.path.join(root, "tests", "test_kernels_attn.py"), "-k", sel],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
