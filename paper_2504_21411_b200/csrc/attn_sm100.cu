@@ -114,7 +114,14 @@ __device__ __forceinline__ float exp2_poly3(float x) {
   return __int_as_float(__float_as_int(q) + (static_cast<int>(n) << 23));
 }
 // head_dim 64 forward: the exp work is 2x the MMA work per block (MUFU-bound); every
-// ATTN_POLY64-th exponential pair goes to the FMA pipe (0 = all on MUFU)
+// ATTN_POLY64-th exponential pair goes to the FMA pipe (0 = all on MUFU); ATTN_POLY128 the
+// same at head_dim 128 -- measured slower at every fraction for both (fwd_poly/)
+#ifndef ATTN_POLY128
+#define ATTN_POLY128 0
+#endif
+#ifndef ATTN_POLY_FN
+#define ATTN_POLY_FN exp2_poly3
+#endif
 #ifndef ATTN_POLY64
 #define ATTN_POLY64 0
 #endif
@@ -724,11 +731,11 @@ __global__ void __launch_bounds__(FWD2_THREADS, 1)
             const int e = c * 16 + i;
             // all exponentials on MUFU: moving 1/4 or 1/2 of them to an FMA-pipe polynomial
             // measured 4-14 % slower (D 64 and 128, two-threads-per-row variant)
-            constexpr int PE = D == 64 ? ATTN_POLY64 : 0;
+            constexpr int PE = D == 64 ? ATTN_POLY64 : ATTN_POLY128;
             const bool poly = PE > 0 && ((i >> 1) % (PE > 0 ? PE : 1)) == (PE > 0 ? PE : 1) - 1;
             const float x0 = fmaf(s[e], p.scale_log2, -mu), x1 = fmaf(s[e + 1], p.scale_log2, -mu);
-            const float p0 = poly ? exp2_poly3(x0) : exp2_mufu(x0);
-            const float p1 = poly ? exp2_poly3(x1) : exp2_mufu(x1);
+            const float p0 = poly ? ATTN_POLY_FN(x0) : exp2_mufu(x0);
+            const float p1 = poly ? ATTN_POLY_FN(x1) : exp2_mufu(x1);
             r4[(i >> 1) & 3] += p0 + p1;  // the normalizer uses the undropped probabilities
             if constexpr (DROP)
               pk[i / 2] = pack2((keep >> i) & 1u ? p0 : 0.f, (keep >> (i + 1)) & 1u ? p1 : 0.f);
