@@ -489,11 +489,11 @@ __global__ void __launch_bounds__(FWD2_THREADS, 1)
   uint64_t* k_empty = bar + 5;   // [2]
   uint64_t* v_empty = bar + 7;   // [2]
   uint64_t* s_full = bar + 9;    // [tile]
-  uint64_t* p_full = bar + 11;   // [tile]
-  uint64_t* o_done = bar + 13;   // [tile]
-  uint64_t* q_empty = bar + 15;  // the item's last S MMA done: Q tiles reusable
-  uint64_t* o_free = bar + 16;   // [tile] the item's epilogue has read O_t out of TMEM
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 18);
+  uint64_t* p_full = bar + 11;   // [tile][key half] P_t of keys [64 hf, 64 hf + 64) stored
+  uint64_t* o_done = bar + 15;   // [tile]
+  uint64_t* q_empty = bar + 17;  // the item's last S MMA done: Q tiles reusable
+  uint64_t* o_free = bar + 18;   // [tile] the item's epilogue has read O_t out of TMEM
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 20);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_pairs = (p.n_qblocks + 1) / 2;
@@ -533,7 +533,8 @@ __global__ void __launch_bounds__(FWD2_THREADS, 1)
       mbar_init(&k_empty[i], 1);
       mbar_init(&v_empty[i], 1);
       mbar_init(&s_full[i], 1);
-      mbar_init(&p_full[i], 128);
+      mbar_init(&p_full[2 * i], 128);
+      mbar_init(&p_full[2 * i + 1], 128);
       mbar_init(&o_done[i], 1);
       mbar_init(&o_free[i], 128);
     }
@@ -628,18 +629,27 @@ __global__ void __launch_bounds__(FWD2_THREADS, 1)
           const uint32_t dn = t ? done1 : done0;
           if (dn > 0) mbar_wait_fast(&o_free[t], (dn - 1) & 1);
         }
-        mbar_wait_fast(&p_full[t], bt & 1);
+        mbar_wait_fast(&p_full[2 * t], bt & 1);
         if (lane == 0) TRACE(4096 + t * 1024 + j * 8 + 3);
         mbar_wait_fast(&v_full[st], (g >> 1) & 1);
         tc_fence_after();
         if (lane == 0) TRACE(4096 + t * 1024 + j * 8 + 4);
         const uint64_t bv = d_v + (uint64_t)((st * L::TILE) >> 4);
         const uint32_t t_o = tmem + 256 + t * 128, t_p = tmem + t * 128;
+        // PV over keys 0-63 as soon as that half of P is stored; the softmax finishes the
+        // other half meanwhile (P of keys 16k.. at column 64*(k/4) + 8*(k%4))
         if (elect_one()) {
 #pragma unroll
-          for (int k = 0; k < BKV / 16; ++k)
-            umma_bf16_ts(t_o, t_p + (k >> 2) * 64 + (k & 3) * 8,
-                         bv + (uint64_t)((k * 2048) >> 4), id_o, (j | k) != 0);
+          for (int k = 0; k < 4; ++k)
+            umma_bf16_ts(t_o, t_p + k * 8, bv + (uint64_t)((k * 2048) >> 4), id_o, (j | k) != 0);
+        }
+        __syncwarp();
+        mbar_wait_fast(&p_full[2 * t + 1], bt & 1);
+        tc_fence_after();
+        if (elect_one()) {
+#pragma unroll
+          for (int k = 4; k < BKV / 16; ++k)
+            umma_bf16_ts(t_o, t_p + 64 + (k & 3) * 8, bv + (uint64_t)((k * 2048) >> 4), id_o, true);
           umma_commit(&o_done[t]);
           if (t == 1 || j >= nkv1) umma_commit(&v_empty[st]);  // last reader of V_j
         }
@@ -743,27 +753,34 @@ __global__ void __launch_bounds__(FWD2_THREADS, 1)
               pk[i / 2] = pack2(p0, p1);
           }
           tmem_st8(t_s + (c >> 2) * 64 + (c & 3) * 8 + lane_off, pk);
+          if (c == BKV / 32 - 1) {  // keys 0-63 stored: PV over them may start
+            tmem_wait_st();
+            if (tr) TRACE(t * 1024 + j * 8 + 4);
+            // lazy rescale of O (after half of P is out of registers): O must hold PV(j-1)
+            // first; o_done has completed j-1 phases here (PV(j) needs this P), so the
+            // parity wait is exact
+            if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
+              mbar_wait(&o_done[t], (bt - 1) & 1);
+              tc_fence_after();
+#pragma unroll 1
+              for (int cc = 0; cc < D / 32; ++cc) {
+                uint32_t ov[32];
+                const uint32_t ta = t_o + cc * 32 + lane_off;
+                tmem_ld32(ta, ov);
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                  ov[i] = __float_as_uint(__uint_as_float(ov[i]) * alpha);
+                tmem_st32(ta, ov);
+              }
+            }
+            tc_fence_before();
+            mbar_arrive(&p_full[2 * t]);
+          }
         }
         l = l * alpha + ((r4[0] + r4[1]) + (r4[2] + r4[3]));
         tmem_wait_st();
-        if (tr) TRACE(t * 1024 + j * 8 + 4);
-        // lazy rescale of O (after P is out of registers): O must hold PV(j-1) first; o_done
-        // has completed j-1 or j phases here (PV(j) needs this P), so the parity wait is exact
-        if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
-          mbar_wait(&o_done[t], (bt - 1) & 1);
-          tc_fence_after();
-#pragma unroll 1
-          for (int c = 0; c < D / 32; ++c) {
-            uint32_t ov[32];
-            const uint32_t ta = t_o + c * 32 + lane_off;
-            tmem_ld32(ta, ov);
-#pragma unroll
-            for (int i = 0; i < 32; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * alpha);
-            tmem_st32(ta, ov);
-          }
-        }
         tc_fence_before();
-        mbar_arrive(&p_full[t]);
+        mbar_arrive(&p_full[2 * t + 1]);
         if (tr) TRACE(t * 1024 + j * 8 + 5);
       }
       if (tr) TRACE(8003 + 2 * t);
