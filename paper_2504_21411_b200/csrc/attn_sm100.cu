@@ -471,6 +471,9 @@ struct Smem2 {
   static constexpr int BYTES = XCH + 2 * 768 * 4 + 1024;
 };
 constexpr int FWD2_THREADS = 384;
+#ifndef FWD_PSPLIT
+#define FWD_PSPLIT 2  // parts of P per tile and block handed to PV separately (1, 2, 4, 8)
+#endif
 #ifndef ATTN_FWD_PERSIST_MAX_S
 #define ATTN_FWD_PERSIST_MAX_S 2048
 #endif
@@ -489,11 +492,13 @@ __global__ void __launch_bounds__(FWD2_THREADS, 1)
   uint64_t* k_empty = bar + 5;   // [2]
   uint64_t* v_empty = bar + 7;   // [2]
   uint64_t* s_full = bar + 9;    // [tile]
-  uint64_t* p_full = bar + 11;   // [tile][key half] P_t of keys [64 hf, 64 hf + 64) stored
-  uint64_t* o_done = bar + 15;   // [tile]
-  uint64_t* q_empty = bar + 17;  // the item's last S MMA done: Q tiles reusable
-  uint64_t* o_free = bar + 18;   // [tile] the item's epilogue has read O_t out of TMEM
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 20);
+  constexpr int NP = FWD_PSPLIT;  // P parts per tile (PV over part q starts once it is stored)
+  static_assert(NP >= 2 && NP <= 8 && (NP & (NP - 1)) == 0, "FWD_PSPLIT: 2, 4 or 8");
+  uint64_t* p_full = bar + 11;        // [tile][part] P_t of keys [128 q / NP, ...) stored
+  uint64_t* o_done = p_full + 2 * NP; // [tile]
+  uint64_t* q_empty = o_done + 2;     // the item's last S MMA done: Q tiles reusable
+  uint64_t* o_free = q_empty + 1;     // [tile] the item's epilogue has read O_t out of TMEM
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_free + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_pairs = (p.n_qblocks + 1) / 2;
@@ -533,8 +538,7 @@ __global__ void __launch_bounds__(FWD2_THREADS, 1)
       mbar_init(&k_empty[i], 1);
       mbar_init(&v_empty[i], 1);
       mbar_init(&s_full[i], 1);
-      mbar_init(&p_full[2 * i], 128);
-      mbar_init(&p_full[2 * i + 1], 128);
+      for (int q = 0; q < NP; ++q) mbar_init(&p_full[NP * i + q], 128);
       mbar_init(&o_done[i], 1);
       mbar_init(&o_free[i], 128);
     }
@@ -629,27 +633,31 @@ __global__ void __launch_bounds__(FWD2_THREADS, 1)
           const uint32_t dn = t ? done1 : done0;
           if (dn > 0) mbar_wait_fast(&o_free[t], (dn - 1) & 1);
         }
-        mbar_wait_fast(&p_full[2 * t], bt & 1);
+        mbar_wait_fast(&p_full[NP * t], bt & 1);
         if (lane == 0) TRACE(4096 + t * 1024 + j * 8 + 3);
         mbar_wait_fast(&v_full[st], (g >> 1) & 1);
         tc_fence_after();
         if (lane == 0) TRACE(4096 + t * 1024 + j * 8 + 4);
         const uint64_t bv = d_v + (uint64_t)((st * L::TILE) >> 4);
         const uint32_t t_o = tmem + 256 + t * 128, t_p = tmem + t * 128;
-        // PV over keys 0-63 as soon as that half of P is stored; the softmax finishes the
-        // other half meanwhile (P of keys 16k.. at column 64*(k/4) + 8*(k%4))
-        if (elect_one()) {
+        // PV over each part of the keys as soon as that part of P is stored; the softmax
+        // computes the next part meanwhile (P of keys 16k.. at column 64*(k/4) + 8*(k%4))
+        constexpr int KP = BKV / 16 / NP;  // K-steps per part
 #pragma unroll
-          for (int k = 0; k < 4; ++k)
-            umma_bf16_ts(t_o, t_p + k * 8, bv + (uint64_t)((k * 2048) >> 4), id_o, (j | k) != 0);
+        for (int q = 0; q < NP; ++q) {
+          if (q > 0) {
+            mbar_wait_fast(&p_full[NP * t + q], bt & 1);
+            tc_fence_after();
+          }
+          if (elect_one()) {
+#pragma unroll
+            for (int k = q * KP; k < (q + 1) * KP; ++k)
+              umma_bf16_ts(t_o, t_p + (k >> 2) * 64 + (k & 3) * 8,
+                           bv + (uint64_t)((k * 2048) >> 4), id_o, (j | k) != 0);
+          }
+          __syncwarp();
         }
-        __syncwarp();
-        mbar_wait_fast(&p_full[2 * t + 1], bt & 1);
-        tc_fence_after();
         if (elect_one()) {
-#pragma unroll
-          for (int k = 4; k < BKV / 16; ++k)
-            umma_bf16_ts(t_o, t_p + 64 + (k & 3) * 8, bv + (uint64_t)((k * 2048) >> 4), id_o, true);
           umma_commit(&o_done[t]);
           if (t == 1 || j >= nkv1) umma_commit(&v_empty[st]);  // last reader of V_j
         }
@@ -753,13 +761,14 @@ __global__ void __launch_bounds__(FWD2_THREADS, 1)
               pk[i / 2] = pack2(p0, p1);
           }
           tmem_st8(t_s + (c >> 2) * 64 + (c & 3) * 8 + lane_off, pk);
-          if (c == BKV / 32 - 1) {  // keys 0-63 stored: PV over them may start
+          constexpr int CP = BKV / 16 / NP;  // 16-key chunks per part
+          if (c % CP == CP - 1 && c != BKV / 16 - 1) {  // a part stored: PV over it may start
             tmem_wait_st();
             if (tr) TRACE(t * 1024 + j * 8 + 4);
             // lazy rescale of O (after half of P is out of registers): O must hold PV(j-1)
             // first; o_done has completed j-1 phases here (PV(j) needs this P), so the
             // parity wait is exact
-            if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
+            if (c == CP - 1 && j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
               mbar_wait(&o_done[t], (bt - 1) & 1);
               tc_fence_after();
 #pragma unroll 1
@@ -774,13 +783,13 @@ __global__ void __launch_bounds__(FWD2_THREADS, 1)
               }
             }
             tc_fence_before();
-            mbar_arrive(&p_full[2 * t]);
+            mbar_arrive(&p_full[NP * t + c / CP]);
           }
         }
         l = l * alpha + ((r4[0] + r4[1]) + (r4[2] + r4[3]));
         tmem_wait_st();
         tc_fence_before();
-        mbar_arrive(&p_full[2 * t + 1]);
+        mbar_arrive(&p_full[NP * t + NP - 1]);
         if (tr) TRACE(t * 1024 + j * 8 + 5);
       }
       if (tr) TRACE(8003 + 2 * t);
