@@ -33,9 +33,10 @@ def main():
     args = ap.parse_args()
     from paper_2504_21411_b200 import kernels as K
     bf = torch.bfloat16
-    res = {"env": {k: os.environ.get(k) for k in ("GALV_NORM_WARP", "GALV_NORM_UNFUSED")}}
+    res = {"env": {k: os.environ.get(k) for k in ("GALV_NORM_WARP", "GALV_NORM_UNFUSED",
+                                                  "GALV_NORM_NARROW")}}
     for rows, cols, layer in [(16384, 1024, True), (16384, 1024, False), (8192, 4096, False),
-                              (16384, 2048, True)]:
+                              (16384, 2048, True), (16384, 768, True), (16384, 512, True)]:
         x = torch.randn(rows, cols, device="cuda", dtype=bf)
         g = torch.randn(cols, device="cuda", dtype=bf)
         b = torch.randn(cols, device="cuda", dtype=bf)
