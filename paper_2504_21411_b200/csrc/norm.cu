@@ -217,6 +217,9 @@ __global__ void __launch_bounds__(128) bwd_dx_row(
 // registers to the in-flight x / dy vectors, and are flushed once per CTA with 16-byte
 // atomics.
 // Per row: 2 reads (x, dy) [+ dres] + 1 write of rows*cols*sizeof(T).
+#ifndef NORM_FUSED_PREFETCH
+#define NORM_FUSED_PREFETCH 1
+#endif
 template <typename T, bool LAYER, int NV, int NT>
 __global__ void __launch_bounds__(NT) bwd_fused_rows(
     const T* __restrict__ x, const T* __restrict__ gamma, const float* __restrict__ mean,
@@ -243,18 +246,39 @@ __global__ void __launch_bounds__(NT) bwd_fused_rows(
     }
   }
   int parity = 0;
-  for (int64_t row = blockIdx.x; row < rows; row += gridDim.x, parity ^= 1) {
-    const T* xr = x + row * cols;
-    const T* dyr = dy + row * cols;
-    const float mu = LAYER ? mean[row] : 0.f, rs = rstd[row];
-    uint4 xv[NV], dv[NV];
+  // the next row's x / dy (and mean / rstd) are loaded before this row's barrier and
+  // arithmetic (NORM_FUSED_PREFETCH): two rows in flight per CTA
+  uint4 xv[NV], dv[NV], xn[NV], dn[NV];
+  float mun = 0.f, rsn = 0.f;
+  auto fetch = [&](int64_t r, uint4* xo, uint4* doo, float& m, float& q) {
+    if (r >= rows) return;
+    const T* xr = x + r * cols;
+    const T* dyr = dy + r * cols;
+    m = LAYER ? mean[r] : 0.f;
+    q = rstd[r];
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
       const int c = (j * NT + threadIdx.x) * V;
       if (c < cols) {
-        xv[j] = __ldcs(reinterpret_cast<const uint4*>(xr + c));
-        dv[j] = __ldcs(reinterpret_cast<const uint4*>(dyr + c));
+        xo[j] = __ldcs(reinterpret_cast<const uint4*>(xr + c));
+        doo[j] = __ldcs(reinterpret_cast<const uint4*>(dyr + c));
       }
+    }
+  };
+  if (NORM_FUSED_PREFETCH) fetch(blockIdx.x, xn, dn, mun, rsn);
+  for (int64_t row = blockIdx.x; row < rows; row += gridDim.x, parity ^= 1) {
+    float mu, rs;
+    if (NORM_FUSED_PREFETCH) {
+#pragma unroll
+      for (int j = 0; j < NV; ++j) {
+        xv[j] = xn[j];
+        dv[j] = dn[j];
+      }
+      mu = mun;
+      rs = rsn;
+      fetch(row + gridDim.x, xn, dn, mun, rsn);
+    } else {
+      fetch(row, xv, dv, mu, rs);
     }
     float a1 = 0.f, a2 = 0.f;
 #pragma unroll
