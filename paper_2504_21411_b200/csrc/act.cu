@@ -377,6 +377,9 @@ int32_t galv_bias_gelu_bwd_colsum(const void* x, const void* bias, const void* d
   return 0;
 }
 
+#ifndef COLSUM_CTAS_PER_SM
+#define COLSUM_CTAS_PER_SM 4  // 8 or 16 measured the same (11-16 us at 16384x1024, noise)
+#endif
 int32_t galv_colsum(const void* x, float* out, int64_t rows, int64_t cols, int32_t accumulate,
                     int32_t dtype, void* ws, void* stream) {
   (void)ws;
@@ -388,7 +391,7 @@ int32_t galv_colsum(const void* x, float* out, int64_t rows, int64_t cols, int32
     const int64_t per = 8 * (16 / esz);  // columns per CTA
     const int64_t strips_v = (cols + per - 1) / per;
     const int64_t ych = std::max<int64_t>(
-        1, std::min<int64_t>((rows + 31) / 32, (int64_t)sm_count() * 4 / strips_v));
+        1, std::min<int64_t>((rows + 31) / 32, (int64_t)sm_count() * COLSUM_CTAS_PER_SM / strips_v));
     const int64_t rpc_v = (rows + ych - 1) / ych;
     dim3 g((unsigned)strips_v, (unsigned)ych);
     GALV_DISPATCH(dtype, T, {
